@@ -1,0 +1,108 @@
+// internal.h -- plan state and kernel launchers shared by plan.cpp and kernels.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/wdd.h"
+
+namespace wdd {
+
+enum ProfSlot { kSlotProject = 0, kSlotRowDft = 1, kSlotFlush = 2, kSlotReadout = 3, kSlotFinalize = 4, kNumSlots = 5 };
+
+// Rows of one ingest chunk handed to the row-DFT kernel.  Contiguous chunks (scan indices
+// s0, s0+1, ..., s0+n-1) are described arithmetically; anything else by a device table.
+struct RowSource {
+  int contiguous;   // 1: rows derived from s0/n
+  int s0;           // first scan index (contiguous)
+  int n;            // frames in the chunk
+  int n_rows;       // rows touched
+  int mode_first;   // 0 = write (row staging was clean), 1 = accumulate (contiguous only)
+  int mode_last;
+  const int2* ent;  // general: (batch position, sx) sorted by row
+  const int4* rows; // general: (sy, first entry, entry count, mode)
+};
+
+struct Plan {
+  // geometry
+  int Sy = 0, Sx = 0, Q = 0, L = 0, K = 0, dtype = 0, normalize = 0, device = 0, combine = 0;
+  int64_t S = 0, n_act = 0;
+  int n_vx = 0;
+  double step = 0, lambda = 0, alpha = 0, defocus = 0, eps = 0, dq = 0, qa = 0, R = 0, sigma = 0;
+  double b_scale = 1.0;  // power-of-two prescale of the fp16 basis operand
+  int sm_count = 148;
+
+  // host tables
+  std::vector<double> basis;          // Q*L, Psi[m][n]
+  std::vector<int32_t> active_v;      // n_act, accumulator order (vx-major, vy ascending)
+  std::vector<int32_t> col_vx;        // n_vx
+  std::vector<int32_t> col_off;       // n_vx + 1
+  std::vector<int32_t> act_vy;        // n_act
+  std::vector<int2> flush_tiles;      // (column j, first row i0) of 32-row tiles
+  std::vector<uint64_t> seen;         // S bits
+  std::vector<uint8_t> row_dirty;     // Sy
+  int64_t frames_ingested = 0;
+
+  // device buffers
+  void* d_Bpack = nullptr;            // fp16 [Psi_hi | Psi_lo] B operand, smem image
+  float* d_psi = nullptr;             // Q*L f32
+  float2* d_Fx = nullptr;             // n_vx * Sx
+  float2* d_Fy = nullptr;             // Sy * Sy
+  float2* d_W = nullptr;              // n_act * K
+  float2* d_G = nullptr;              // n_act * K
+  float2* d_Gsum = nullptr;           // n_act * K (combine = 1 only)
+  float2* d_R = nullptr;              // n_vx * Sy * K   R[j][sy][k]
+  float* d_C = nullptr;               // chunk_cap * K
+  int32_t* d_act_vy = nullptr;
+  int32_t* d_col_off = nullptr;
+  int32_t* d_vpos = nullptr;          // n_act flattened v (scatter positions)
+  int2* d_flush_tiles = nullptr;
+  float2* d_o = nullptr;              // n_act
+  float2* d_spec = nullptr;           // Sy*Sx
+  void* d_meta = nullptr;             // per-chunk row tables
+  void* h_meta = nullptr;             // pinned host mirror of d_meta (2 slots)
+  cudaEvent_t meta_ev[2] = {nullptr, nullptr};
+  int meta_slot = 0;
+  size_t meta_slot_bytes = 0;
+  int64_t chunk_cap = 0;
+  void* d_stage[2] = {nullptr, nullptr};  // host-ingest staging
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;
+  cufftHandle fft = 0;
+  bool fft_ok = false;
+  cudaStream_t stream = nullptr;      // plan stream (last ingest)
+
+  // multi-rank
+  void* nccl = nullptr;
+  int nranks = 1, rank = 0;
+
+  // graph capture
+  bool capturing = false;
+  void* cap_host = nullptr;           // pinned arena for captured metadata copies
+  void* cap_dev = nullptr;            // device arena (same offsets)
+  size_t cap_bytes = 0, cap_used = 0;
+  std::vector<cudaGraphExec_t> graphs;
+
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<int, size_t>> prof_marks;  // (slot, index of start event)
+  int64_t launches = 0;
+};
+
+// ---- kernel launchers (kernels.cu); return cudaError_t of the launch
+cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* C, cudaStream_t st);
+cudaError_t launch_rowdft(const Plan& p, const float* C, const RowSource& rs, cudaStream_t st);
+cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st);
+cudaError_t launch_readout(const Plan& p, const float2* G, bool scatter, cudaStream_t st);
+cudaError_t launch_scatter(const Plan& p, cudaStream_t st);
+cudaError_t launch_finalize(const Plan& p, float2* out, cudaStream_t st);
+// host helper: pack the fp16 B operand image of the projection kernel
+void pack_basis_fp16(const Plan& p, std::vector<uint16_t>& out, double& scale);
+size_t project_smem_bytes(int Q, int L);
+
+}  // namespace wdd

@@ -1,0 +1,853 @@
+// plan.cpp -- host side of libwdd: plan-time float64 math (basis, twiddles, exact active set,
+// Wiener bank; Algorithm 1), buffer management, ingest
+// bookkeeping (range / duplicate checks, row grouping, staging policy), readout orchestration
+// and the NCCL combine.  No step of the per-frame path runs here: it only launches kernels.
+//
+// Compiled with -ffp-contract=off so the aperture tests round exactly like the float64 oracle
+// reading R10.
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "internal.h"
+
+using namespace wdd;
+
+namespace {
+
+thread_local std::string g_err = "no error";
+
+wdd_status fail(wdd_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+  do {                                                                                          \
+    cudaError_t e_ = (expr);                                                                    \
+    if (e_ != cudaSuccess)                                                                      \
+      return fail(e_ == cudaErrorMemoryAllocation ? WDD_E_NOMEM : WDD_E_CUDA, "%s: %s (%s:%d)", \
+                  #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                           \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                     \
+  do {                                                                                     \
+    ncclResult_t r_ = (expr);                                                              \
+    if (r_ != ncclSuccess) return fail(WDD_E_NCCL, "%s: %s", #expr, ncclGetErrorString(r_)); \
+  } while (0)
+
+constexpr double kPi = 3.14159265358979323846;
+
+// ------------------------------------------------------------------ plan math (float64)
+// Normalised Hermite functions by the three-term recurrence (R3).
+void hermite_basis(int Q, int L, double sigma, std::vector<double>& Psi) {
+  Psi.assign((size_t)Q * L, 0.0);
+  const int c = Q / 2;
+  const double norm = 1.0 / std::sqrt(sigma), p0 = std::pow(kPi, -0.25);
+  for (int m = 0; m < Q; ++m) {
+    const double u = (m - c) / sigma;
+    double pm2 = 0, pm1 = p0 * std::exp(-0.5 * u * u);
+    Psi[(size_t)m * L] = pm1 * norm;
+    if (L > 1) {
+      double p1 = std::sqrt(2.0) * u * pm1;
+      Psi[(size_t)m * L + 1] = p1 * norm;
+      pm2 = pm1;
+      pm1 = p1;
+    }
+    for (int n = 2; n < L; ++n) {
+      const double pn = std::sqrt(2.0 / n) * u * pm1 - std::sqrt((n - 1.0) / n) * pm2;
+      Psi[(size_t)m * L + n] = pn * norm;
+      pm2 = pm1;
+      pm1 = pn;
+    }
+  }
+}
+
+int64_t signed_freq(int64_t v, int64_t S) { return v < (S + 1) / 2 ? v : v - S; }  // fftfreq (R15)
+
+struct ApertureRows {
+  std::vector<int> row_begin;  // Q + 1
+  std::vector<int> mx;         // pixels inside the aperture, row-major
+};
+
+ApertureRows aperture(const Plan& p, const std::vector<double>& q) {
+  ApertureRows a;
+  a.row_begin.assign(p.Q + 1, 0);
+  const double qa2 = p.qa * p.qa;
+  for (int my = 0; my < p.Q; ++my) {
+    a.row_begin[my] = (int)a.mx.size();
+    for (int mx = 0; mx < p.Q; ++mx)
+      if (q[my] * q[my] + q[mx] * q[mx] <= qa2) a.mx.push_back(mx);
+  }
+  a.row_begin[p.Q] = (int)a.mx.size();
+  return a;
+}
+
+// Exact discrete active set (R9, R10): v active iff some aperture pixel q also has
+// |q + q_hat_v|^2 <= q_alpha^2.  Candidates need |q_hat_v| <= 2 q_alpha (triangle inequality).
+void active_set(const Plan& p, const std::vector<double>& q, const ApertureRows& ap, std::vector<int32_t>& act) {
+  const double qa2 = p.qa * p.qa, lim = 2.0 * p.qa * (1.0 + 1e-9);
+  std::vector<double> fy(p.Sy), fx(p.Sx);
+  for (int v = 0; v < p.Sy; ++v) fy[v] = (double)signed_freq(v, p.Sy) / ((double)p.Sy * p.step);
+  for (int v = 0; v < p.Sx; ++v) fx[v] = (double)signed_freq(v, p.Sx) / ((double)p.Sx * p.step);
+  std::vector<std::pair<int, int>> cand;
+  for (int vy = 0; vy < p.Sy; ++vy) {
+    if (std::fabs(fy[vy]) > lim) continue;
+    for (int vx = 0; vx < p.Sx; ++vx)
+      if (fy[vy] * fy[vy] + fx[vx] * fx[vx] <= lim * lim) cand.emplace_back(vy, vx);
+  }
+  std::vector<uint8_t> on(cand.size(), 0);
+  const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  std::atomic<size_t> next(0);
+  auto work = [&]() {
+    for (;;) {
+      const size_t i0 = next.fetch_add(256);
+      if (i0 >= cand.size()) break;
+      for (size_t i = i0; i < std::min(cand.size(), i0 + 256); ++i) {
+        const double sy = fy[cand[i].first], sx = fx[cand[i].second];
+        bool hit = false;
+        for (int my = 0; my < p.Q && !hit; ++my) {
+          const double a = q[my] + sy;
+          for (int e = ap.row_begin[my]; e < ap.row_begin[my + 1]; ++e) {
+            const double b = q[ap.mx[e]] + sx;
+            if (a * a + b * b <= qa2) { hit = true; break; }
+          }
+        }
+        on[i] = hit;
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t) th.emplace_back(work);
+  for (auto& t : th) t.join();
+  act.clear();
+  for (size_t i = 0; i < cand.size(); ++i)
+    if (on[i]) act.push_back(cand[i].first * p.Sx + cand[i].second);
+}
+
+// Wiener bank K_v = conj(H(Y_v)) / (|H(Y_v)|^2 + eps) (Algorithm 1), Y_v evaluated
+// on the lens of the two apertures only (Y_v is 0 elsewhere).  Output in accumulator order.
+template <typename OutT>
+void wiener_bank(const Plan& p, const std::vector<double>& q, const ApertureRows& ap, OutT* W) {
+  const int L = p.L, K = p.K;
+  const double qa2 = p.qa * p.qa, c0 = -kPi * p.lambda * p.defocus;
+  const unsigned nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  std::atomic<int64_t> next(0);
+  auto work = [&]() {
+    std::vector<std::complex<double>> H((size_t)K), T((size_t)L);
+    for (;;) {
+      const int64_t g0 = next.fetch_add(16);
+      if (g0 >= p.n_act) break;
+      for (int64_t g = g0; g < std::min<int64_t>(p.n_act, g0 + 16); ++g) {
+        const int v = p.active_v[g];
+        const int vy = v / p.Sx, vx = v % p.Sx;
+        const double sy = (double)signed_freq(vy, p.Sy) / ((double)p.Sy * p.step);
+        const double sx = (double)signed_freq(vx, p.Sx) / ((double)p.Sx * p.step);
+        std::fill(H.begin(), H.end(), 0.0);
+        for (int my = 0; my < p.Q; ++my) {
+          const double a = q[my] + sy;
+          bool any = false;
+          std::fill(T.begin(), T.end(), 0.0);
+          for (int e = ap.row_begin[my]; e < ap.row_begin[my + 1]; ++e) {
+            const int mx = ap.mx[e];
+            const double b = q[mx] + sx;
+            const double s2 = a * a + b * b;
+            if (!(s2 <= qa2)) continue;
+            any = true;
+            const double u2 = q[my] * q[my] + q[mx] * q[mx];
+            // p_hat(q) * conj(p_hat(q + q_hat)), p_hat = exp(-i pi lambda df |q|^2) inside
+            const std::complex<double> y = std::complex<double>(std::cos(c0 * u2), std::sin(c0 * u2)) *
+                                           std::complex<double>(std::cos(c0 * s2), -std::sin(c0 * s2));
+            const double* px = &p.basis[(size_t)mx * L];
+            for (int aa = 0; aa < L; ++aa) T[aa] += px[aa] * y;
+          }
+          if (!any) continue;
+          const double* py = &p.basis[(size_t)my * L];
+          for (int aa = 0; aa < L; ++aa)
+            for (int bb = 0; bb < L; ++bb) H[(size_t)aa * L + bb] += py[bb] * T[aa];
+        }
+        for (int k = 0; k < K; ++k) {
+          const std::complex<double> w = std::conj(H[k]) / (std::norm(H[k]) + p.eps);
+          W[g * K + k] = OutT{(decltype(OutT{}.x))w.real(), (decltype(OutT{}.x))w.imag()};
+        }
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t) th.emplace_back(work);
+  for (auto& t : th) t.join();
+}
+
+struct d2 { double x, y; };
+
+void twiddles(int n_out, const int32_t* freqs, int S, std::vector<float2>& F) {
+  // F[j][s] = exp(-2 pi i ((f_j * s) mod S) / S) / sqrt(S)  (integer angle reduction)
+  F.resize((size_t)n_out * S);
+  const double inv = 1.0 / std::sqrt((double)S);
+  for (int j = 0; j < n_out; ++j)
+    for (int s = 0; s < S; ++s) {
+      const int64_t r = ((int64_t)freqs[j] * s) % S;
+      const double ang = -2.0 * kPi * (double)r / (double)S;
+      F[(size_t)j * S + s] = make_float2((float)(std::cos(ang) * inv), (float)(std::sin(ang) * inv));
+    }
+}
+
+// ------------------------------------------------------------------ launch helpers
+struct Prof {
+  Plan& p;
+  cudaStream_t st;
+  int slot;
+  size_t i0 = 0;
+  Prof(Plan& pp, int s, cudaStream_t stream) : p(pp), st(stream), slot(s) {
+    p.launches++;
+    if (!p.prof || p.capturing) return;
+    if (p.ev_used + 2 > p.ev_pool.size()) {
+      for (int k = 0; k < 64; ++k) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        p.ev_pool.push_back(e);
+      }
+    }
+    i0 = p.ev_used;
+    p.ev_used += 2;
+    cudaEventRecord(p.ev_pool[i0], st);
+  }
+  ~Prof() {
+    if (!p.prof || p.capturing) return;
+    cudaEventRecord(p.ev_pool[i0 + 1], st);
+    p.prof_marks.emplace_back(slot, i0);
+  }
+};
+
+wdd_status check_plan(wdd_plan_t plan) {
+  if (!plan) return fail(WDD_E_ARG, "plan is NULL");
+  return WDD_OK;
+}
+
+Plan* P(wdd_plan_t h) { return reinterpret_cast<Plan*>(h); }
+
+void use_stream(Plan& p, cudaStream_t st) {
+  if (st == p.stream || p.capturing) return;
+  // keep the plan's own work ordered across a stream switch
+  cudaEvent_t e;
+  if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+    cudaEventRecord(e, p.stream);
+    cudaStreamWaitEvent(st, e, 0);
+    cudaEventDestroy(e);
+  }
+  p.stream = st;
+}
+
+wdd_status upload_meta(Plan& p, const void* host, size_t bytes, void** dev_out) {
+  if (bytes > p.meta_slot_bytes) return fail(WDD_E_ARG, "metadata too large");
+  if (p.capturing) {
+    // captured copies read a host block that outlives every replay: bump-allocate from the
+    // pinned / device capture arenas reserved by wdd_capture_begin (owned until destroy)
+    const size_t off = (p.cap_used + 255) / 256 * 256;
+    if (off + bytes > p.cap_bytes) return fail(WDD_E_NOMEM, "capture metadata arena exhausted");
+    uint8_t* h = static_cast<uint8_t*>(p.cap_host) + off;
+    uint8_t* d = static_cast<uint8_t*>(p.cap_dev) + off;
+    std::memcpy(h, host, bytes);
+    CUDA_TRY(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, p.stream));
+    p.cap_used = off + bytes;
+    *dev_out = d;
+    return WDD_OK;
+  }
+  const int s = p.meta_slot;
+  p.meta_slot ^= 1;
+  CUDA_TRY(cudaEventSynchronize(p.meta_ev[s]));
+  uint8_t* h = static_cast<uint8_t*>(p.h_meta) + s * p.meta_slot_bytes;
+  uint8_t* d = static_cast<uint8_t*>(p.d_meta) + s * p.meta_slot_bytes;
+  std::memcpy(h, host, bytes);
+  CUDA_TRY(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, p.stream));
+  CUDA_TRY(cudaEventRecord(p.meta_ev[s], p.stream));
+  *dev_out = d;
+  return WDD_OK;
+}
+
+// Validate a whole call (range, duplicates within the call and against the seen set) before
+// anything is enqueued.  On success the indices are marked seen.
+wdd_status validate_and_mark(Plan& p, const int32_t* idx, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    if (idx[i] < 0 || (int64_t)idx[i] >= p.S)
+      return fail(WDD_E_RANGE, "scan index %d at position %lld outside [0, %lld)", idx[i], (long long)i,
+                  (long long)p.S);
+  std::vector<int32_t> marked;
+  marked.reserve((size_t)n);
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t s = idx[i];
+    uint64_t& w = p.seen[(size_t)s >> 6];
+    const uint64_t bit = 1ull << (s & 63);
+    if (w & bit) {
+      for (int32_t m : marked) p.seen[(size_t)m >> 6] &= ~(1ull << (m & 63));
+      return fail(WDD_E_DUP, "scan index %d (position %lld) already ingested or repeated", s, (long long)i);
+    }
+    w |= bit;
+    marked.push_back(s);
+  }
+  return WDD_OK;
+}
+
+// Enqueue projection + row DFT for one chunk of already-validated frames.
+wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, int64_t nc) {
+  cudaStream_t st = p.stream;
+  {
+    Prof pr(p, kSlotProject, st);
+    CUDA_TRY(launch_project(p, frames_dev, nc, p.d_C, st));
+  }
+  bool contiguous = true;
+  for (int64_t i = 1; i < nc && contiguous; ++i) contiguous = idx[i] == idx[0] + i;
+  RowSource rs{};
+  rs.n = (int)nc;
+  if (contiguous) {
+    rs.contiguous = 1;
+    rs.s0 = idx[0];
+    const int sy0 = idx[0] / p.Sx, sy1 = idx[nc - 1] / p.Sx;
+    rs.n_rows = sy1 - sy0 + 1;
+    rs.mode_first = p.row_dirty[sy0];
+    rs.mode_last = p.row_dirty[sy1];
+    for (int sy = sy0; sy <= sy1; ++sy) p.row_dirty[sy] = 1;
+  } else {
+    // counting sort of chunk positions by scan row
+    std::vector<int> cnt(p.Sy + 1, 0);
+    for (int64_t i = 0; i < nc; ++i) cnt[idx[i] / p.Sx + 1]++;
+    for (int r = 0; r < p.Sy; ++r) cnt[r + 1] += cnt[r];
+    // device table: rows (int4, 16-byte aligned) first, then the entries (int2)
+    std::vector<int4> rows;
+    std::vector<int2> ent((size_t)nc);
+    std::vector<int> fillp(cnt.begin(), cnt.end() - 1);
+    for (int64_t i = 0; i < nc; ++i) {
+      const int sy = idx[i] / p.Sx;
+      ent[fillp[sy]++] = make_int2((int)i, idx[i] % p.Sx);
+    }
+    for (int sy = 0; sy < p.Sy; ++sy) {
+      const int c = cnt[sy + 1] - cnt[sy];
+      if (!c) continue;
+      rows.push_back(make_int4(sy, cnt[sy], c, p.row_dirty[sy]));
+      p.row_dirty[sy] = 1;
+    }
+    const size_t rb = rows.size() * sizeof(int4), eb = ent.size() * sizeof(int2);
+    std::vector<uint8_t> buf(rb + eb);
+    std::memcpy(buf.data(), rows.data(), rb);
+    std::memcpy(buf.data() + rb, ent.data(), eb);
+    void* d = nullptr;
+    wdd_status s = upload_meta(p, buf.data(), buf.size(), &d);
+    if (s != WDD_OK) return s;
+    const int nr = (int)rows.size();
+    rs.contiguous = 0;
+    rs.n_rows = nr;
+    rs.rows = reinterpret_cast<const int4*>(d);
+    rs.ent = reinterpret_cast<const int2*>(static_cast<uint8_t*>(d) + rb);
+  }
+  {
+    Prof pr(p, kSlotRowDft, st);
+    CUDA_TRY(launch_rowdft(p, p.d_C, rs, st));
+  }
+  return WDD_OK;
+}
+
+size_t frame_bytes(const Plan& p) { return (size_t)p.Q * p.Q * (p.dtype == 0 ? 2 : 4); }
+
+// Flush staged rows into G (a5).
+wdd_status flush(Plan& p) {
+  std::vector<int32_t> rows;
+  for (int sy = 0; sy < p.Sy; ++sy)
+    if (p.row_dirty[sy]) rows.push_back(sy);
+  if (rows.empty()) return WDD_OK;
+  void* d = nullptr;
+  wdd_status s = upload_meta(p, rows.data(), rows.size() * sizeof(int32_t), &d);
+  if (s != WDD_OK) return s;
+  {
+    Prof pr(p, kSlotFlush, p.stream);
+    CUDA_TRY(launch_flush(p, static_cast<const int32_t*>(d), (int)rows.size(), p.stream));
+  }
+  for (int32_t sy : rows) p.row_dirty[sy] = 0;
+  return WDD_OK;
+}
+
+void free_plan(Plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  cudaDeviceSynchronize();
+  if (p->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(p->nccl));
+  void* bufs[] = {p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_C,
+                  p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec,
+                  p->d_meta, p->d_stage[0], p->d_stage[1]};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (p->h_meta) cudaFreeHost(p->h_meta);
+  for (auto g : p->graphs) cudaGraphExecDestroy(g);
+  if (p->cap_host) cudaFreeHost(p->cap_host);
+  if (p->cap_dev) cudaFree(p->cap_dev);
+  for (auto& e : p->meta_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : p->stage_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : p->ev_pool) cudaEventDestroy(e);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->fft_ok) cufftDestroy(p->fft);
+  delete p;
+}
+
+}  // namespace
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+extern "C" {
+
+const char* wdd_last_error(void) { return g_err.c_str(); }
+
+wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int32_t det_shape[2], int32_t K,
+                           const wdd_probe* probe, double wiener_eps, const wdd_plan_opts* opts, wdd_plan_t* out) {
+  if (!out) return fail(WDD_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (!scan_shape || !det_shape || !probe) return fail(WDD_E_ARG, "NULL shape or probe");
+  wdd_plan_opts o{};
+  if (opts) o = *opts;
+  for (int r : o.reserved)
+    if (r) return fail(WDD_E_ARG, "opts.reserved must be zero");
+  const int Sy = scan_shape[0], Sx = scan_shape[1], Q = det_shape[0];
+  if (Sy < 2 || Sx < 2 || (int64_t)Sy * Sx > (1ll << 30)) return fail(WDD_E_ARG, "scan shape %d x %d unsupported", Sy, Sx);
+  if (det_shape[1] != Q || !(Q == 32 || Q == 64 || Q == 128 || Q == 256))
+    return fail(WDD_E_ARG, "detector must be square with Q in {32,64,128,256}, got %d x %d", det_shape[0], det_shape[1]);
+  const int L = (int)std::lround(std::sqrt((double)K));
+  if (K <= 0 || L * L != K) return fail(WDD_E_ARG, "K = %d is not a perfect square", K);
+  if (L % 8 != 0 || L < 8 || L > 32 || L > Q) return fail(WDD_E_ARG, "L = %d must be a multiple of 8 in [8, 32] and <= Q", L);
+  if (!(wiener_eps > 0)) return fail(WDD_E_ARG, "wiener_eps must be > 0");
+  if (!(step_A > 0) || !(probe->wavelength_A > 0) || !(probe->semiangle_rad > 0))
+    return fail(WDD_E_ARG, "step, wavelength and semi-angle must be > 0");
+  if (o.dtype != 0 && o.dtype != 1) return fail(WDD_E_ARG, "dtype must be 0 (u16) or 1 (f32)");
+  if (o.combine != 0 && o.combine != 1) return fail(WDD_E_ARG, "combine must be 0 or 1");
+
+  Plan* p = new Plan();
+  p->Sy = Sy; p->Sx = Sx; p->Q = Q; p->L = L; p->K = K; p->S = (int64_t)Sy * Sx;
+  p->dtype = o.dtype; p->normalize = o.normalize ? 1 : 0; p->device = o.device; p->combine = o.combine;
+  p->step = step_A; p->lambda = probe->wavelength_A; p->alpha = probe->semiangle_rad; p->defocus = probe->defocus_A;
+  p->eps = wiener_eps;
+  p->dq = o.det_px_rad > 0 ? o.det_px_rad / p->lambda : 1.0 / (Q * step_A);  // R17
+  p->qa = p->alpha / p->lambda;                                               // R7
+  p->R = p->qa / p->dq;
+  p->sigma = o.sigma_px > 0 ? o.sigma_px : std::sqrt(Q / (2.0 * kPi));        // R1
+
+  auto bail = [&](wdd_status s) { free_plan(p); return s; };
+  if (cudaSetDevice(p->device) != cudaSuccess) return bail(fail(WDD_E_CUDA, "cudaSetDevice(%d) failed", p->device));
+  {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device) == cudaSuccess && sms > 0) p->sm_count = sms;
+  }
+
+  // basis + Gram check
+  hermite_basis(Q, L, p->sigma, p->basis);
+  double gram = 0;
+  for (int a = 0; a < L; ++a)
+    for (int b = 0; b < L; ++b) {
+      double s = 0;
+      for (int m = 0; m < Q; ++m) s += p->basis[(size_t)m * L + a] * p->basis[(size_t)m * L + b];
+      gram = std::max(gram, std::fabs(s - (a == b ? 1.0 : 0.0)));
+    }
+  if (gram > 1e-10) return bail(fail(WDD_E_ARG, "basis Gram error %.3g > 1e-10 (sigma %.4g px)", gram, p->sigma));
+
+  // detector grid, aperture, active set in accumulator order
+  std::vector<double> q(Q);
+  for (int m = 0; m < Q; ++m) q[m] = (double)(m - Q / 2) * p->dq;
+  ApertureRows ap = aperture(*p, q);
+  std::vector<int32_t> act;
+  active_set(*p, q, ap, act);
+  std::sort(act.begin(), act.end(), [&](int32_t a, int32_t b) {
+    const int ax = a % Sx, bx = b % Sx;
+    return ax != bx ? ax < bx : a < b;
+  });
+  p->active_v = act;
+  p->n_act = (int64_t)act.size();
+  if (p->n_act == 0) return bail(fail(WDD_E_ARG, "empty active set"));
+  p->act_vy.resize(act.size());
+  for (size_t g = 0; g < act.size(); ++g) {
+    const int vx = act[g] % Sx;
+    p->act_vy[g] = act[g] / Sx;
+    if (p->col_vx.empty() || p->col_vx.back() != vx) {
+      p->col_vx.push_back(vx);
+      p->col_off.push_back((int32_t)g);
+    }
+  }
+  p->col_off.push_back((int32_t)act.size());
+  p->n_vx = (int)p->col_vx.size();
+  for (int j = 0; j < p->n_vx; ++j)
+    for (int i0 = 0; i0 < p->col_off[j + 1] - p->col_off[j]; i0 += 32) p->flush_tiles.push_back(make_int2(j, i0));
+
+  // twiddles
+  std::vector<float2> Fx, Fy;
+  twiddles(p->n_vx, p->col_vx.data(), Sx, Fx);
+  std::vector<int32_t> ally(Sy);
+  for (int v = 0; v < Sy; ++v) ally[v] = v;
+  twiddles(Sy, ally.data(), Sy, Fy);
+
+  // bank
+  std::vector<float2> W((size_t)p->n_act * K);
+  wiener_bank<float2>(*p, q, ap, W.data());
+
+  // device buffers
+  std::vector<uint16_t> bpack;
+  pack_basis_fp16(*p, bpack, p->b_scale);
+  std::vector<float> psi32(p->basis.begin(), p->basis.end());
+  std::vector<int32_t> vpos(act.begin(), act.end());
+  p->chunk_cap = 8192;
+  p->meta_slot_bytes = std::max((size_t)p->chunk_cap * (sizeof(int2) + sizeof(int4)), (size_t)Sy * 4);
+  p->seen.assign((size_t)(p->S + 63) / 64, 0);
+  p->row_dirty.assign(Sy, 0);
+
+#define ALLOC(ptr, bytes)                                                                           \
+  if (cudaMalloc((void**)&(ptr), (bytes)) != cudaSuccess)                                           \
+    return bail(fail(WDD_E_NOMEM, "cudaMalloc(%s, %zu bytes) failed", #ptr, (size_t)(bytes)));
+  ALLOC(p->d_Bpack, bpack.size() * 2);
+  ALLOC(p->d_psi, psi32.size() * 4);
+  ALLOC(p->d_Fx, Fx.size() * sizeof(float2));
+  ALLOC(p->d_Fy, Fy.size() * sizeof(float2));
+  ALLOC(p->d_W, W.size() * sizeof(float2));
+  ALLOC(p->d_G, W.size() * sizeof(float2));
+  if (p->combine == 1) ALLOC(p->d_Gsum, W.size() * sizeof(float2));
+  ALLOC(p->d_R, (size_t)p->n_vx * Sy * K * sizeof(float2));
+  ALLOC(p->d_C, (size_t)p->chunk_cap * K * sizeof(float));
+  ALLOC(p->d_act_vy, act.size() * 4);
+  ALLOC(p->d_col_off, p->col_off.size() * 4);
+  ALLOC(p->d_vpos, act.size() * 4);
+  ALLOC(p->d_flush_tiles, p->flush_tiles.size() * sizeof(int2));
+  ALLOC(p->d_o, act.size() * sizeof(float2));
+  ALLOC(p->d_spec, (size_t)p->S * sizeof(float2));
+  ALLOC(p->d_meta, 2 * p->meta_slot_bytes);
+#undef ALLOC
+  if (cudaMallocHost(&p->h_meta, 2 * p->meta_slot_bytes) != cudaSuccess)
+    return bail(fail(WDD_E_NOMEM, "pinned metadata buffer"));
+  for (auto& e : p->meta_ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(fail(WDD_E_CUDA, "event"));
+  for (auto& e : p->stage_ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(fail(WDD_E_CUDA, "event"));
+  auto up = [&](void* d, const void* h, size_t b) { return cudaMemcpy(d, h, b, cudaMemcpyHostToDevice) == cudaSuccess; };
+  bool ok = up(p->d_Bpack, bpack.data(), bpack.size() * 2) && up(p->d_psi, psi32.data(), psi32.size() * 4) &&
+            up(p->d_Fx, Fx.data(), Fx.size() * sizeof(float2)) && up(p->d_Fy, Fy.data(), Fy.size() * sizeof(float2)) &&
+            up(p->d_W, W.data(), W.size() * sizeof(float2)) && up(p->d_act_vy, p->act_vy.data(), act.size() * 4) &&
+            up(p->d_col_off, p->col_off.data(), p->col_off.size() * 4) && up(p->d_vpos, vpos.data(), act.size() * 4) &&
+            up(p->d_flush_tiles, p->flush_tiles.data(), p->flush_tiles.size() * sizeof(int2));
+  ok = ok && cudaMemset(p->d_G, 0, W.size() * sizeof(float2)) == cudaSuccess &&
+       cudaMemset(p->d_spec, 0, (size_t)p->S * sizeof(float2)) == cudaSuccess;
+  if (!ok) return bail(fail(WDD_E_CUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError())));
+  if (cufftPlan2d(&p->fft, Sy, Sx, CUFFT_C2C) != CUFFT_SUCCESS) return bail(fail(WDD_E_CUDA, "cufftPlan2d failed"));
+  p->fft_ok = true;
+  if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(WDD_E_CUDA, "plan upload sync failed"));
+  *out = reinterpret_cast<wdd_plan_t>(p);
+  return WDD_OK;
+}
+
+wdd_status wdd_destroy(wdd_plan_t plan) {
+  free_plan(P(plan));
+  return WDD_OK;
+}
+
+wdd_status wdd_ingest(wdd_plan_t plan, const void* frames_dev, const int32_t* scan_idx_host, int64_t n, void* stream) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (n < 0) return fail(WDD_E_ARG, "n < 0");
+  if (n == 0) return WDD_OK;
+  if (!frames_dev || !scan_idx_host) return fail(WDD_E_ARG, "NULL frames or indices");
+  CUDA_TRY(cudaSetDevice(p.device));
+  wdd_status s = validate_and_mark(p, scan_idx_host, n);
+  if (s != WDD_OK) return s;
+  use_stream(p, reinterpret_cast<cudaStream_t>(stream));
+  const size_t fb = frame_bytes(p);
+  for (int64_t c0 = 0; c0 < n; c0 += p.chunk_cap) {
+    const int64_t nc = std::min<int64_t>(p.chunk_cap, n - c0);
+    s = enqueue_chunk(p, static_cast<const uint8_t*>(frames_dev) + (size_t)c0 * fb, scan_idx_host + c0, nc);
+    if (s != WDD_OK) return s;
+  }
+  p.frames_ingested += n;
+  return WDD_OK;
+}
+
+wdd_status wdd_ingest_host(wdd_plan_t plan, const void* frames_host, const int32_t* scan_idx_host, int64_t n,
+                           void* stream) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (n < 0) return fail(WDD_E_ARG, "n < 0");
+  if (n == 0) return WDD_OK;
+  if (!frames_host || !scan_idx_host) return fail(WDD_E_ARG, "NULL frames or indices");
+  if (p.capturing) return fail(WDD_E_STATE, "wdd_ingest_host cannot be captured");
+  CUDA_TRY(cudaSetDevice(p.device));
+  wdd_status s = validate_and_mark(p, scan_idx_host, n);
+  if (s != WDD_OK) return s;
+  use_stream(p, reinterpret_cast<cudaStream_t>(stream));
+  const size_t fb = frame_bytes(p);
+  const int64_t stage_frames = std::max<int64_t>(1, std::min<int64_t>(p.chunk_cap, (64ll << 20) / (int64_t)fb));
+  if (!p.d_stage[0]) {
+    CUDA_TRY(cudaMalloc(&p.d_stage[0], stage_frames * fb));
+    CUDA_TRY(cudaMalloc(&p.d_stage[1], stage_frames * fb));
+    CUDA_TRY(cudaStreamCreateWithFlags(&p.copy_stream, cudaStreamNonBlocking));
+  }
+  cudaEvent_t copied[2];
+  CUDA_TRY(cudaEventCreateWithFlags(&copied[0], cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&copied[1], cudaEventDisableTiming));
+  int slot = 0;
+  for (int64_t c0 = 0; c0 < n; c0 += stage_frames, slot ^= 1) {
+    const int64_t nc = std::min<int64_t>(stage_frames, n - c0);
+    CUDA_TRY(cudaStreamWaitEvent(p.copy_stream, p.stage_ev[slot], 0));  // previous user of the slot done
+    CUDA_TRY(cudaMemcpyAsync(p.d_stage[slot], static_cast<const uint8_t*>(frames_host) + (size_t)c0 * fb, nc * fb,
+                             cudaMemcpyHostToDevice, p.copy_stream));
+    CUDA_TRY(cudaEventRecord(copied[slot], p.copy_stream));
+    CUDA_TRY(cudaStreamWaitEvent(p.stream, copied[slot], 0));
+    s = enqueue_chunk(p, p.d_stage[slot], scan_idx_host + c0, nc);
+    if (s != WDD_OK) return s;
+    CUDA_TRY(cudaEventRecord(p.stage_ev[slot], p.stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(p.copy_stream));
+  cudaEventDestroy(copied[0]);
+  cudaEventDestroy(copied[1]);
+  p.frames_ingested += n;
+  return WDD_OK;
+}
+
+wdd_status wdd_readout(wdd_plan_t plan, void* complex_out_dev) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (!complex_out_dev) return fail(WDD_E_ARG, "NULL output");
+  CUDA_TRY(cudaSetDevice(p.device));
+  wdd_status s = flush(p);
+  if (s != WDD_OK) return s;
+  const float2* G = p.d_G;
+  const bool multi = p.nranks > 1;
+  if (multi && p.combine == 1) {
+    NCCL_TRY(ncclAllReduce(p.d_G, p.d_Gsum, (size_t)p.n_act * p.K * 2, ncclFloat, ncclSum,
+                           reinterpret_cast<ncclComm_t>(p.nccl), p.stream));
+    G = p.d_Gsum;
+  }
+  {
+    Prof pr(p, kSlotReadout, p.stream);
+    CUDA_TRY(launch_readout(p, G, !multi || p.combine == 1, p.stream));
+  }
+  if (multi && p.combine == 0) {
+    NCCL_TRY(ncclAllReduce(p.d_o, p.d_o, (size_t)p.n_act * 2, ncclFloat, ncclSum, reinterpret_cast<ncclComm_t>(p.nccl),
+                           p.stream));
+    Prof pr(p, kSlotReadout, p.stream);
+    CUDA_TRY(launch_scatter(p, p.stream));
+  }
+  {
+    Prof pr(p, kSlotFinalize, p.stream);
+    CUDA_TRY(launch_finalize(p, static_cast<float2*>(complex_out_dev), p.stream));
+  }
+  return WDD_OK;
+}
+
+wdd_status wdd_readout_host(wdd_plan_t plan, void* complex_out_host) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (!complex_out_host) return fail(WDD_E_ARG, "NULL output");
+  if (p.capturing) return fail(WDD_E_STATE, "wdd_readout_host cannot be captured");
+  CUDA_TRY(cudaSetDevice(p.device));
+  void* d = nullptr;
+  CUDA_TRY(cudaMallocAsync(&d, (size_t)p.S * sizeof(float2), p.stream));
+  wdd_status s = wdd_readout(plan, d);
+  if (s == WDD_OK) {
+    CUDA_TRY(cudaMemcpyAsync(complex_out_host, d, (size_t)p.S * sizeof(float2), cudaMemcpyDeviceToHost, p.stream));
+  }
+  cudaFreeAsync(d, p.stream);
+  CUDA_TRY(cudaStreamSynchronize(p.stream));
+  return s;
+}
+
+wdd_status wdd_get_accumulator(wdd_plan_t plan, void* G_out_dev, int32_t* active_v_host, int64_t* n_act) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  CUDA_TRY(cudaSetDevice(p.device));
+  if (n_act) *n_act = p.n_act;
+  if (active_v_host) std::memcpy(active_v_host, p.active_v.data(), p.active_v.size() * 4);
+  if (G_out_dev) {
+    wdd_status s = flush(p);
+    if (s != WDD_OK) return s;
+    CUDA_TRY(cudaMemcpyAsync(G_out_dev, p.d_G, (size_t)p.n_act * p.K * sizeof(float2), cudaMemcpyDeviceToDevice, p.stream));
+  }
+  return WDD_OK;
+}
+
+wdd_status wdd_reset(wdd_plan_t plan) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  CUDA_TRY(cudaSetDevice(p.device));
+  CUDA_TRY(cudaMemsetAsync(p.d_G, 0, (size_t)p.n_act * p.K * sizeof(float2), p.stream));
+  std::fill(p.seen.begin(), p.seen.end(), 0);
+  std::fill(p.row_dirty.begin(), p.row_dirty.end(), 0);  // staged R rows are overwritten on next use
+  p.frames_ingested = 0;
+  return WDD_OK;
+}
+
+wdd_status wdd_nccl_get_unique_id(uint8_t id[128]) {
+  if (!id) return fail(WDD_E_ARG, "NULL id");
+  ncclUniqueId u;
+  NCCL_TRY(ncclGetUniqueId(&u));
+  static_assert(sizeof(u) == 128, "ncclUniqueId size");
+  std::memcpy(id, &u, 128);
+  return WDD_OK;
+}
+
+wdd_status wdd_set_comm(wdd_plan_t plan, int32_t nranks, int32_t rank, const uint8_t id[128]) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (nranks < 1 || rank < 0 || rank >= nranks || !id) return fail(WDD_E_ARG, "bad nranks/rank/id");
+  CUDA_TRY(cudaSetDevice(p.device));
+  if (p.nccl) {
+    ncclCommDestroy(reinterpret_cast<ncclComm_t>(p.nccl));
+    p.nccl = nullptr;
+  }
+  p.nranks = nranks;
+  p.rank = rank;
+  if (nranks == 1) return WDD_OK;
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  ncclComm_t c;
+  NCCL_TRY(ncclCommInitRank(&c, nranks, u, rank));
+  p.nccl = c;
+  return WDD_OK;
+}
+
+wdd_status wdd_get_info(wdd_plan_t plan, wdd_plan_info* info) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  if (!info) return fail(WDD_E_ARG, "NULL info");
+  const Plan& p = *P(plan);
+  wdd_plan_info i{};
+  i.Sy = p.Sy; i.Sx = p.Sx; i.Q = p.Q; i.L = p.L; i.K = p.K; i.n_vx = p.n_vx; i.dtype = p.dtype;
+  i.normalize = p.normalize; i.n_act = p.n_act; i.dq = p.dq; i.q_alpha = p.qa; i.R_px = p.R;
+  i.sigma_px = p.sigma; i.wavelength_A = p.lambda; i.step_A = p.step; i.eps = p.eps;
+  i.bytes_G = p.n_act * p.K * 8; i.bytes_bank = i.bytes_G; i.bytes_R = (int64_t)p.n_vx * p.Sy * p.K * 8;
+  i.bytes_C = p.chunk_cap * p.K * 4; i.frames_ingested = p.frames_ingested; i.nranks = p.nranks; i.rank = p.rank;
+  *info = i;
+  return WDD_OK;
+}
+
+wdd_status wdd_get_tables(wdd_plan_t plan, double* basis, double* bank, int32_t* active_v) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  const Plan& p = *P(plan);
+  if (basis) std::memcpy(basis, p.basis.data(), p.basis.size() * sizeof(double));
+  if (active_v) std::memcpy(active_v, p.active_v.data(), p.active_v.size() * 4);
+  if (bank) {
+    std::vector<double> q(p.Q);
+    for (int m = 0; m < p.Q; ++m) q[m] = (double)(m - p.Q / 2) * p.dq;
+    ApertureRows ap = aperture(p, q);
+    wiener_bank<d2>(p, q, ap, reinterpret_cast<d2*>(bank));
+  }
+  return WDD_OK;
+}
+
+wdd_status wdd_project(wdd_plan_t plan, const void* frames_dev, int64_t n, void* C_out_dev, void* stream) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (n < 0 || (n > 0 && (!frames_dev || !C_out_dev))) return fail(WDD_E_ARG, "bad arguments");
+  CUDA_TRY(cudaSetDevice(p.device));
+  Prof pr(p, kSlotProject, reinterpret_cast<cudaStream_t>(stream));
+  CUDA_TRY(launch_project(p, frames_dev, n, static_cast<float*>(C_out_dev), reinterpret_cast<cudaStream_t>(stream)));
+  return WDD_OK;
+}
+
+wdd_status wdd_profile_enable(wdd_plan_t plan, int32_t enable) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  p.prof = enable != 0;
+  p.prof_marks.clear();
+  p.ev_used = 0;
+  return WDD_OK;
+}
+
+wdd_status wdd_profile_read(wdd_plan_t plan, int32_t slot, double* ms_total, int64_t* count) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (slot < 0 || slot >= kNumSlots) return fail(WDD_E_ARG, "bad slot");
+  double ms = 0;
+  int64_t c = 0;
+  for (auto& m : p.prof_marks) {
+    if (m.first != slot) continue;
+    CUDA_TRY(cudaEventSynchronize(p.ev_pool[m.second + 1]));
+    float t = 0;
+    CUDA_TRY(cudaEventElapsedTime(&t, p.ev_pool[m.second], p.ev_pool[m.second + 1]));
+    ms += t;
+    ++c;
+  }
+  if (ms_total) *ms_total = ms;
+  if (count) *count = c;
+  return WDD_OK;
+}
+
+wdd_status wdd_launch_count(wdd_plan_t plan, int64_t* count, int32_t reset) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (count) *count = p.launches;
+  if (reset) p.launches = 0;
+  return WDD_OK;
+}
+
+wdd_status wdd_capture_begin(wdd_plan_t plan, void* stream) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (p.capturing) return fail(WDD_E_STATE, "already capturing");
+  CUDA_TRY(cudaSetDevice(p.device));
+  if (!p.cap_host) {
+    p.cap_bytes = 16u << 20;
+    CUDA_TRY(cudaMallocHost(&p.cap_host, p.cap_bytes));
+    CUDA_TRY(cudaMalloc(&p.cap_dev, p.cap_bytes));
+  }
+  use_stream(p, reinterpret_cast<cudaStream_t>(stream));
+  CUDA_TRY(cudaStreamSynchronize(p.stream));
+  CUDA_TRY(cudaStreamBeginCapture(p.stream, cudaStreamCaptureModeThreadLocal));
+  p.capturing = true;
+  return WDD_OK;
+}
+
+wdd_status wdd_capture_end(wdd_plan_t plan, int64_t* graph_handle) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (!p.capturing) return fail(WDD_E_STATE, "not capturing");
+  p.capturing = false;
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(cudaStreamEndCapture(p.stream, &g));
+  cudaGraphExec_t ex = nullptr;
+  cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  CUDA_TRY(e);
+  p.graphs.push_back(ex);
+  if (graph_handle) *graph_handle = (int64_t)p.graphs.size() - 1;
+  return WDD_OK;
+}
+
+wdd_status wdd_graph_launch(wdd_plan_t plan, int64_t graph_handle, void* stream) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (p.capturing) return fail(WDD_E_STATE, "graph launch while capturing");
+  if (graph_handle < 0 || graph_handle >= (int64_t)p.graphs.size()) return fail(WDD_E_ARG, "bad graph handle");
+  CUDA_TRY(cudaSetDevice(p.device));
+  use_stream(p, reinterpret_cast<cudaStream_t>(stream));
+  CUDA_TRY(cudaGraphLaunch(p.graphs[(size_t)graph_handle], p.stream));
+  return WDD_OK;
+}
+
+wdd_status wdd_sync(wdd_plan_t plan) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  CUDA_TRY(cudaSetDevice(p.device));
+  CUDA_TRY(cudaStreamSynchronize(p.stream));
+  if (p.copy_stream) CUDA_TRY(cudaStreamSynchronize(p.copy_stream));
+  return WDD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle on the same seeded
+inputs.  Tolerance (BASELINE.json north star): relative L2 <= 1e-4 on G and on the complex
+image; integer work (active set, accumulator order) bit-exact."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from synth import CONFIGS, Acquisition
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    return torch
+
+
+@pytest.fixture(scope="module")
+def wdd():
+    from paper_2212_01309_b200 import build
+    build.build()
+    import paper_2212_01309_b200 as w
+    return w
+
+
+def _frames(cfg, idx, noise=True):
+    return Acquisition(cfg, noise=noise).frames_parallel(np.asarray(idx))
+
+
+def _to_dev(torch, fr):
+    t = torch.from_numpy(np.ascontiguousarray(fr))
+    if t.dtype == torch.uint16:
+        pass
+    return t.cuda()
+
+
+@pytest.mark.parametrize("name", ["tiny", "medium"])
+def test_plan_tables(wdd, torch_cuda, name):
+    cfg = CONFIGS[name]
+    plan = wdd.Plan.from_config(cfg)
+    g = O.geometry(cfg)
+    basis, _, act = plan.tables()
+    assert np.max(np.abs(basis - O.hg_basis(cfg.Q, cfg.L, g.sigma))) < 1e-13
+    oact = O.active_set(g, cfg.Sy, cfg.Sx)
+    assert np.array_equal(np.sort(act), oact)                    # bit-exact set
+    key = (act % cfg.Sx).astype(np.int64) * cfg.S + act           # accumulator order (vx, vy)
+    assert np.all(np.diff(key) > 0)
+    info = plan.info()
+    assert info["n_act"] == len(oact)
+    assert info["n_vx"] == len(np.unique(oact % cfg.Sx))
+
+
+@pytest.mark.parametrize("name", ["tiny", "medium"])
+def test_bank_matches_oracle(wdd, torch_cuda, name):
+    cfg = CONFIGS[name]
+    plan = wdd.Plan.from_config(cfg)
+    g = O.geometry(cfg)
+    _, W, act = plan.tables(bank=True)
+    rng = np.random.default_rng(0)
+    sel = np.sort(rng.choice(len(act), size=min(len(act), 300), replace=False))
+    Wo = O.wiener_bank(g, O.hg_basis(cfg.Q, cfg.L, g.sigma), act[sel], cfg.Sy, cfg.Sx, cfg.eps)
+    assert rel(W[sel], Wo) < 1e-10
+
+
+def _check_project(wdd, torch, cfg, fr):
+    plan = wdd.Plan.from_config(cfg)
+    C = plan.project(_to_dev(torch, fr)).cpu().numpy()
+    g = O.geometry(cfg)
+    Co = O.vec(O.project(fr.astype(np.float64), O.hg_basis(cfg.Q, cfg.L, g.sigma)))
+    return rel(C, Co), np.max(np.abs(C - Co)) / np.max(np.abs(Co))
+
+
+@pytest.mark.parametrize("name,n", [("tiny", 37), ("tiny", 1024), ("medium", 515), ("large", 130), ("live", 33),
+                                    ("box", 17)])
+def test_projection_parity(wdd, torch_cuda, name, n):
+    cfg = CONFIGS[name]
+    fr = _frames(cfg, np.arange(n) * 7 % cfg.S)
+    r, mx = _check_project(wdd, torch_cuda, cfg, fr)
+    assert r < 1e-5 and mx < 1e-5, (r, mx)
+
+
+@pytest.mark.parametrize("Q,L", [(32, 8), (64, 16), (128, 16), (128, 32), (256, 32), (256, 24)])
+def test_projection_high_counts_and_float(wdd, torch_cuda, Q, L):
+    # counts >= 1024 exercise the second (high-bit) plane; float frames the fp16 residual plane.
+    base = CONFIGS["medium"].with_(Q=Q, L=L, Sy=16, Sx=16)
+    rng = np.random.default_rng(Q + L)
+    fr16 = rng.integers(0, 65535, size=(9, Q, Q), dtype=np.uint16)
+    r, mx = _check_project(wdd, torch_cuda, base, fr16)
+    assert r < 1e-5 and mx < 1e-5, (r, mx)
+    fr32 = (rng.random((9, Q, Q)) * 1000.0).astype(np.float32)
+    r, mx = _check_project(wdd, torch_cuda, base.with_(dtype="f32"), fr32)
+    assert r < 1e-5 and mx < 1e-5, (r, mx)
+
+
+def _ingest_batches(torch, plan, fr_dev, idx, batch):
+    for a in range(0, len(idx), batch):
+        plan.ingest(fr_dev[a:a + batch], idx[a:a + batch])
+
+
+def _oracle_all(cfg, fr, idx):
+    g = O.geometry(cfg)
+    return O.reduced_wdd(fr, idx, g, cfg.Sy, cfg.Sx, cfg.L, cfg.eps, return_all=True)
+
+
+@pytest.mark.parametrize("name", ["tiny", "medium"])
+def test_full_scan_parity(wdd, torch_cuda, name):
+    torch = torch_cuda
+    cfg = CONFIGS[name]
+    idx = np.arange(cfg.S)
+    fr = _frames(cfg, idx)
+    ref = _oracle_all(cfg, fr, idx)
+    plan = wdd.Plan.from_config(cfg)
+    fr_dev = _to_dev(torch, fr)
+    _ingest_batches(torch, plan, fr_dev, idx, cfg.batch or cfg.S)
+    G, act = plan.get_accumulator()
+    G = G.cpu().numpy()
+    assert rel(G, ref["G"][act]) < TOL
+    out = plan.readout()
+    torch.cuda.synchronize()
+    Oimg = out.cpu().numpy()
+    assert rel(Oimg, ref["O"]) < TOL
+    # non-mutating: a second readout is bit-identical
+    out2 = plan.readout()
+    torch.cuda.synchronize()
+    assert np.array_equal(out2.cpu().numpy(), Oimg)
+
+
+def test_live_equals_offline_random_partitions(wdd, torch_cuda):
+    torch = torch_cuda
+    cfg = CONFIGS["tiny"]
+    idx = np.arange(cfg.S)
+    fr = _frames(cfg, idx)
+    fr_dev = _to_dev(torch, fr)
+    off = wdd.Plan.from_config(cfg)
+    off.ingest(fr_dev, idx)
+    G_off, _ = off.get_accumulator()
+    rng = np.random.default_rng(3)
+    perm = rng.permutation(cfg.S)
+    live = wdd.Plan.from_config(cfg)
+    cuts = np.sort(rng.choice(np.arange(1, cfg.S), size=9, replace=False))
+    for k, part in enumerate(np.split(perm, cuts)):
+        live.ingest(fr_dev[torch.from_numpy(part).cuda()].contiguous(), part)
+        if k == 4:  # a readout in the middle must not disturb the running sum
+            live.readout()
+    G_live, _ = live.get_accumulator()
+    assert rel(G_live.cpu().numpy(), G_off.cpu().numpy()) < 1e-5
+    ref = _oracle_all(cfg, fr, idx)
+    out = live.readout()
+    torch.cuda.synchronize()
+    assert rel(out.cpu().numpy(), ref["O"]) < TOL
+
+
+def test_partial_rows_and_partial_readout(wdd, torch_cuda):
+    # contiguous chunks that split scan rows, read out at 10 % and 55 % of the scan
+    torch = torch_cuda
+    cfg = CONFIGS["tiny"]
+    idx = np.arange(cfg.S)
+    fr = _frames(cfg, idx)
+    fr_dev = _to_dev(torch, fr)
+    plan = wdd.Plan.from_config(cfg)
+    bounds = [0, 45, 102, 563, cfg.S]
+    for a, b in zip(bounds, bounds[1:]):
+        plan.ingest(fr_dev[a:b], idx[a:b])
+        ref = _oracle_all(cfg, fr[:b], idx[:b])
+        out = plan.readout()
+        torch.cuda.synchronize()
+        assert rel(out.cpu().numpy(), ref["O"]) < TOL, b
+
+
+def test_rejects_duplicates_and_range_without_effect(wdd, torch_cuda):
+    torch = torch_cuda
+    cfg = CONFIGS["tiny"]
+    fr = _frames(cfg, np.arange(8))
+    fr_dev = _to_dev(torch, fr)
+    plan = wdd.Plan.from_config(cfg)
+    plan.ingest(fr_dev[:4], np.arange(4))
+    G0, _ = plan.get_accumulator()
+    with pytest.raises(wdd.WddError) as e:
+        plan.ingest(fr_dev[4:8], [4, 5, 6, 4])
+    assert e.value.name == "WDD_E_DUP"
+    with pytest.raises(wdd.WddError) as e:
+        plan.ingest(fr_dev[4:8], [4, 5, 2, 7])
+    assert e.value.name == "WDD_E_DUP"
+    with pytest.raises(wdd.WddError) as e:
+        plan.ingest(fr_dev[4:8], [4, 5, 6, cfg.S])
+    assert e.value.name == "WDD_E_RANGE"
+    plan.ingest(fr_dev[:0], [])
+    G1, _ = plan.get_accumulator()
+    assert torch.equal(G0, G1)
+    plan.ingest(fr_dev[4:8], [4, 5, 6, 7])  # the rejected indices are still available
+    assert plan.info()["frames_ingested"] == 8
+    plan.reset()
+    G2, _ = plan.get_accumulator()
+    assert float(G2.abs().max()) == 0.0
+    plan.ingest(fr_dev[:4], np.arange(4))
+
+
+def test_normalize_flag(wdd, torch_cuda):
+    torch = torch_cuda
+    cfg = CONFIGS["tiny"]
+    idx = np.arange(cfg.S)
+    fr = _frames(cfg, idx)
+    plan = wdd.Plan.from_config(cfg, normalize=True)
+    plan.ingest(_to_dev(torch, fr), idx)
+    out = plan.readout()
+    torch.cuda.synchronize()
+    ref = O.reduced_wdd(fr, idx, O.geometry(cfg), cfg.Sy, cfg.Sx, cfg.L, cfg.eps, normalize=True)
+    assert rel(out.cpu().numpy(), ref) < TOL
+
+
+def test_host_ingest_equals_device_ingest(wdd, torch_cuda):
+    torch = torch_cuda
+    cfg = CONFIGS["medium"]
+    idx = np.arange(4096)
+    fr = _frames(cfg, idx)
+    a = wdd.Plan.from_config(cfg)
+    a.ingest(_to_dev(torch, fr), idx)
+    b = wdd.Plan.from_config(cfg)
+    pinned = torch.from_numpy(fr).pin_memory()
+    for s in range(0, len(idx), 512):
+        b.ingest_host(pinned[s:s + 512], idx[s:s + 512])
+    Ga, _ = a.get_accumulator()
+    Gb, _ = b.get_accumulator()
+    torch.cuda.synchronize()
+    assert torch.equal(Ga, Gb)
+    host = b.readout_host()
+    dev = a.readout()
+    torch.cuda.synchronize()
+    assert np.array_equal(host, dev.cpu().numpy())
+
+
+def test_phase_recovery_medium(wdd, torch_cuda):
+    torch = torch_cuda
+    cfg = CONFIGS["medium"]
+    acq = Acquisition(cfg)
+    idx = np.arange(cfg.S)
+    fr = acq.frames_parallel(idx)
+    plan = wdd.Plan.from_config(cfg)
+    _ingest_batches(torch, plan, _to_dev(torch, fr), idx, cfg.batch)
+    out = plan.readout().cpu().numpy()
+    ph = np.angle(out * np.conj(out.mean()))
+    assert np.corrcoef(ph.ravel(), acq.phase().ravel())[0, 1] > 0.94
