@@ -202,7 +202,9 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         plan.set_comm(world, rank, obj[0])
     out = torch.empty((cfg.Sy, cfg.Sx), dtype=torch.complex64, device=f"cuda:{local}")
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=local)      # graphs cannot capture the legacy default stream
+    torch.cuda.synchronize()
+    torch.cuda.set_stream(stream)
     batches = [(a, min(a + batch, len(idx))) for a in range(0, len(idx), batch)]
 
     def step_eager():

@@ -32,7 +32,8 @@ struct Plan {
   int64_t S = 0, n_act = 0;
   int n_vx = 0;
   double step = 0, lambda = 0, alpha = 0, defocus = 0, eps = 0, dq = 0, qa = 0, R = 0, sigma = 0;
-  double b_scale = 1.0;  // power-of-two prescale of the fp16 basis operand
+  double b_scale = 1.0;  // power-of-two prescale of the fp16 basis operand (2^s)
+  double sc1 = 1.0, sc2 = 1.0;  // projection epilogue scales: 2^(eT-s), 2^(-s-eT)
   int sm_count = 148;
 
   // host tables
@@ -55,7 +56,9 @@ struct Plan {
   float2* d_G = nullptr;              // n_act * K
   float2* d_Gsum = nullptr;           // n_act * K (combine = 1 only)
   float2* d_R = nullptr;              // n_vx * Sy * K   R[j][sy][k]
-  float* d_C = nullptr;               // chunk_cap * K
+  float* d_Call = nullptr;            // S * K: coefficients at their scan positions (contiguous chunks)
+  float* d_C[2] = {nullptr, nullptr}; // chunk_cap * K scratch, alternating (non-contiguous chunks)
+  int c_parity = 0;
   int32_t* d_act_vy = nullptr;
   int32_t* d_col_off = nullptr;
   int32_t* d_vpos = nullptr;          // n_act flattened v (scatter positions)

@@ -10,12 +10,17 @@
 //   flush_kernel    a5: G[(j,vy)][k] += sum_rows Fy[vy][sy] R[j][sy][k]  (eq:outer_prod).
 //   readout_kernel  a6: o_v = sum_k G[v][k] K_v[k], one warp per active v.
 //   finalize        a8: cuFFT C2C inverse + conj / unitary scale / optional 1/sqrt(o_0).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
+#include <type_traits>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <vector>
 
 #include "internal.h"
@@ -26,34 +31,64 @@ namespace wdd {
 using namespace tc;
 
 // =====================================================================================
-// Projection (tcgen05)
+// Projection (tcgen05), warp-specialised and persistent.
+//
+//   warp 0       stage-1 MMA issuer : T_tile (128 rows x 2L) += A1_chunk * B^T     (TMEM acc1)
+//   warp 1       stage-2 MMA issuer : D (128 x 2L) += A2 * B^T over qy, hi+lo planes (TMEM acc2)
+//   warp 2       TMA producer (u16) : 2-D tiled loads, 128 rows x 64 pixels, SWIZZLE_128B, into
+//                                     the A1 ring (OOB rows of a ragged tail are zero-filled)
+//   warps 3-6    converters         : u16 -> fp16 IN PLACE (same bytes; the TMA's SW128 layout is
+//                                     the UMMA K-major SW128 operand layout), counts split
+//                                     exactly into low 10 bits + (bits 10-15) x 1024, the second
+//                                     plane going to a side slot only for chunks that need it;
+//                                     f32 frames: LDG -> fp16(x) + fp16(x - fp16(x)), no swizzle
+//   warps 7-10   epilogue           : acc1 -> T -> fp16 hi/lo A2 image; acc2 -> C (global, fp32)
+//
+// Stage 1 contracts the detector columns (qx) for 128 detector rows at a time; stage 2 contracts
+// the detector rows (qy) for g2 <= 128/L frames at a time, M = (frame, a) rows, in K-chunks of
+// 128 rows (two for Q = 256).  Both stages use the same B image [Psi_hi | Psi_lo] (N = 2L).
+// g2 is chosen per launch so a small batch still spreads over every SM.
 // =====================================================================================
-constexpr int kProjThreads = 128;
-constexpr uint32_t kLBO_A = 2064;  // bytes between K-adjacent core matrices of the A tile:
-                                   // 16 row groups x 128 B + 16 B pad (rotates banks of STS)
+constexpr int kProjThreads = 352;   // MMA1, MMA2, TMA, 4 converter warps, 4 epilogue warps
+constexpr int kConv = 128;          // converter threads
+constexpr uint32_t kLBO = 2064;     // no-swizzle K-major: bytes between K-adjacent core matrices of a
+                                    // 128-row operand (16 row groups x 128 B + 16 B bank-rotation pad)
 
 __host__ __device__ constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
-template <int Q, int L>
+template <int Q, int L, bool U16>
 struct ProjCfg {
-  static constexpr int kChunks = Q / 8;                 // 16-byte K chunks per row
-  static constexpr int kA_bytes = kChunks * (int)kLBO_A;
-  static constexpr int kN = 2 * L;                      // MMA N: Psi_hi and Psi_lo columns
+  static constexpr int kKC = Q >= 64 ? 64 : Q;            // K elements (pixels) per A1 chunk
+  static constexpr int kCPT = Q / kKC;                    // chunks per stage-1 tile
+  static constexpr int kSpan = kKC * 2;                   // fp16 bytes per row of a chunk (SW span)
+  static constexpr uint32_t kSwz = kSpan == 128 ? 2u : 4u;  // UMMA layout: SWIZZLE_128B / 64B
+  static constexpr int kSlotU = 128 * kSpan;              // u16 slot (TMA box == fp16 operand)
+  static constexpr int kSlotF = (kKC / 8) * (int)kLBO;    // f32 path: no-swizzle fp16 operand
+  static constexpr int kSlot = align_up(U16 ? kSlotU : kSlotF, 1024);
+  static constexpr int kNS = 6;                           // A1 ring slots
+  static constexpr int kN = 2 * L;                        // MMA N: Psi_hi | Psi_lo
   static constexpr int kLBO_B = 16 * kN;
-  static constexpr int kB_bytes = kChunks * kLBO_B;
-  static constexpr int kFPT = Q >= 128 ? 1 : 128 / Q;  // frames per 128-row tile
-  static constexpr int kTPU = Q >= 128 ? Q / 128 : 1;  // tiles per work unit
-  static constexpr int kTs = L + 1;                     // padded row stride of the T tile
-  static constexpr int kOut = kFPT * L * L;             // C outputs per unit
-  static constexpr int kOPT = (kOut + kProjThreads - 1) / kProjThreads;
-  static constexpr int kTmemCols = pow2_cols(2 * kN);
-  static constexpr int off_A = 0;
-  static constexpr int off_B = align_up(kA_bytes, 128);
-  static constexpr int off_T = off_B + align_up(kB_bytes, 128);
-  static constexpr int off_P = off_T + align_up(128 * kTs * 4, 128);
-  static constexpr int off_bar = off_P + align_up(Q * L * 4, 128);
-  static constexpr int smem = off_bar + 64;
+  static constexpr int kB = (Q / 8) * kLBO_B;
+  static constexpr int kFPT = Q >= 128 ? 1 : 128 / Q;     // frames per stage-1 tile
+  static constexpr int kTPF = Q >= 128 ? Q / 128 : 1;     // stage-1 tiles per frame (= stage-2 K chunks)
+  static constexpr int kK2 = Q >= 128 ? 128 : Q;          // stage-2 K chunk (detector rows)
+  static constexpr int kG2 = Q >= 128 ? 128 / L : ((128 / L) / kFPT) * kFPT;  // max frames per group
+  static constexpr int kA2 = (kK2 / 8) * (int)kLBO;       // one A2 plane (K-major, no swizzle)
+  static constexpr int kZero = 4096;                      // 128 x 16 fp16 zeros
+  static constexpr int kAcc1 = 2 * kN;                    // per acc1 slot: plane 0 | plane 1
+  static constexpr int kTmemCols = pow2_cols(2 * kAcc1 + kN);
+  static constexpr int off_ring = 0;
+  static constexpr int off_P1 = off_ring + kNS * kSlot;
+  static constexpr int off_A2 = off_P1 + kSlot;
+  static constexpr int off_B = off_A2 + align_up(2 * kA2, 1024);
+  static constexpr int off_Z = off_B + align_up(kB, 1024);
+  static constexpr int off_bar = off_Z + kZero;
+  static constexpr int kBars = 3 * kNS + 7;
+  static constexpr int off_misc = off_bar + 8 * kBars;    // meta[kNS], wflag[2][4], tmem slot
+  static constexpr int smem = off_misc + 4 * kNS + 32 + 16;
+  static_assert(kG2 >= 1, "group");
+  static_assert(smem <= 232448, "shared memory");
 };
 
 __device__ __forceinline__ uint32_t magic_half2(uint32_t v10) {
@@ -65,224 +100,425 @@ __device__ __forceinline__ uint32_t magic_half2(uint32_t v10) {
   return *reinterpret_cast<const uint32_t*>(&r);
 }
 
-// Convert rows [row0, row0+valid) of the frame matrix (n*Q rows of Q pixels) into the
-// K-major no-swizzle fp16 A image.  plane 0: u16 -> low 10 bits (exact), f32 -> fp16(x);
-// plane 1: u16 -> bits 10..15, f32 -> fp16(x - fp16(x)).  Returns whether plane 1 is nonzero.
-template <int Q, bool U16>
-__device__ __forceinline__ bool convert_tile(const void* __restrict__ frames, int64_t row0, int valid,
-                                             uint8_t* sA, int plane, int tid) {
-  constexpr int kChunks = Q / 8;
-  constexpr int kPer = kChunks;  // 128 rows * kChunks chunks / 128 threads
-  constexpr int G = kPer < 8 ? kPer : 8;
-  bool resid = false;
-#pragma unroll 1
-  for (int base = 0; base < kPer; base += G) {
-    if constexpr (U16) {
-      uint4 raw[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const int c = tid + kProjThreads * (base + g);
-        const int r = c / kChunks, j = c % kChunks;
-        raw[g] = make_uint4(0, 0, 0, 0);
-        if (r < valid) {
-          const uint16_t* src = reinterpret_cast<const uint16_t*>(frames) + (row0 + r) * Q + j * 8;
-          raw[g] = __ldg(reinterpret_cast<const uint4*>(src));
-        }
-      }
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const int c = tid + kProjThreads * (base + g);
-        const int r = c / kChunks, j = c % kChunks;
-        uint32_t w[4] = {raw[g].x, raw[g].y, raw[g].z, raw[g].w};
-        uint4 o;
-        uint32_t* op = reinterpret_cast<uint32_t*>(&o);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          resid |= (w[q] & 0xFC00FC00u) != 0u;
-          op[q] = plane == 0 ? magic_half2(w[q] & 0x03FF03FFu) : magic_half2((w[q] >> 10) & 0x003F003Fu);
-        }
-        *reinterpret_cast<uint4*>(sA + j * kLBO_A + (r >> 3) * 128 + (r & 7) * 16) = o;
-      }
-    } else {
-      float4 raw[2 * G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const int c = tid + kProjThreads * (base + g);
-        const int r = c / kChunks, j = c % kChunks;
-        raw[2 * g] = raw[2 * g + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r < valid) {
-          const float4* src = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(frames) + (row0 + r) * Q + j * 8);
-          raw[2 * g] = __ldg(src);
-          raw[2 * g + 1] = __ldg(src + 1);
-        }
-      }
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const int c = tid + kProjThreads * (base + g);
-        const int r = c / kChunks, j = c % kChunks;
-        const float* x = reinterpret_cast<const float*>(&raw[2 * g]);
-        uint4 o;
-        __half* hp = reinterpret_cast<__half*>(&o);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const __half h = __float2half_rn(x[e]);
-          const float d = x[e] - __half2float(h);
-          resid |= d != 0.f;
-          hp[e] = plane == 0 ? h : __float2half_rn(d);
-        }
-        *reinterpret_cast<uint4*>(sA + j * kLBO_A + (r >> 3) * 128 + (r & 7) * 16) = o;
-      }
-    }
-  }
-  return resid;
-}
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-template <int Q, int L>
-__device__ __forceinline__ void issue_proj_mmas(const uint8_t* sA, const uint8_t* sB, uint32_t tacc) {
-  using Cfg = ProjCfg<Q, L>;
-  constexpr uint32_t idesc = idesc_f16(128, Cfg::kN);
-  const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-#pragma unroll
-  for (int kk = 0; kk < Q / 16; ++kk) {
-    const uint64_t ad = smem_desc_noswz(a0 + 2 * kk * kLBO_A, kLBO_A, 128);
-    const uint64_t bd = smem_desc_noswz(b0 + 2 * kk * Cfg::kLBO_B, Cfg::kLBO_B, 128);
-    mma_f16_ss(tacc, ad, bd, idesc, kk > 0 ? 1u : 0u);
-  }
+struct ProjArgs {
+  const void* frames;
+  int64_t n;
+  float* C;
+  int g2;      // frames per stage-2 group (<= kG2; a multiple of kFPT)
+  const uint4* Bpack;
+  float sc1;   // acc1 -> fp16 A2 scale   (2^(eT - s))
+  float sc2;   // acc2 -> C scale          (2^(-s - eT))
+};
+
+// Stage-1 tile tt of group g: first frame-matrix row and the number of valid rows.
+// Q >= 128: tiles are ordered (half h, frame f) with tt = h*g2 + f, so that the stage-2 K chunk h
+// of every frame of the group is complete before the next chunk begins.
+template <int Q, int L, bool U16>
+__device__ __forceinline__ void tile_coords(int64_t g, int tt, int g2, int64_t n, int64_t& row0, int& valid) {
+  using Cfg = ProjCfg<Q, L, U16>;
+  const int64_t frame0 = g * g2;
+  if constexpr (Q >= 128) row0 = (frame0 + tt % g2) * Q + (int64_t)(tt / g2) * 128;
+  else row0 = (frame0 + (int64_t)tt * Cfg::kFPT) * Q;
+  const int64_t rem = n * Q - row0;
+  valid = rem <= 0 ? 0 : (rem < 128 ? (int)rem : 128);
 }
 
 template <int Q, int L, bool U16>
-__global__ void __launch_bounds__(kProjThreads) project_kernel(const void* __restrict__ frames, int64_t n,
-                                                               float* __restrict__ C, const uint4* __restrict__ Bpack,
-                                                               const float* __restrict__ psi, float inv_scale) {
-  using Cfg = ProjCfg<Q, L>;
+__global__ void __launch_bounds__(kProjThreads, 1)
+    project_kernel(ProjArgs a, const __grid_constant__ CUtensorMap tmap) {
+  using Cfg = ProjCfg<Q, L, U16>;
   constexpr int K = L * L;
-  constexpr float kResScale = U16 ? 1024.f : 1.f;
+  constexpr float kRes = U16 ? 1024.f : 1.f;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sA = smem + Cfg::off_A;
+  uint8_t* ring = smem + Cfg::off_ring;
+  uint8_t* sP1 = smem + Cfg::off_P1;
+  uint8_t* sA2 = smem + Cfg::off_A2;
   uint8_t* sB = smem + Cfg::off_B;
-  float* sT = reinterpret_cast<float*>(smem + Cfg::off_T);
-  float* sP = reinterpret_cast<float*>(smem + Cfg::off_P);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cfg::off_bar);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + Cfg::off_bar + 8);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  uint8_t* sZ = smem + Cfg::off_Z;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::off_bar);
+  uint64_t* raw_full = bars;                 // [kNS] TMA landed
+  uint64_t* full = bars + Cfg::kNS;          // [kNS] converted
+  uint64_t* empty = bars + 2 * Cfg::kNS;     // [kNS] consumed by the MMA
+  uint64_t* p1_empty = bars + 3 * Cfg::kNS;
+  uint64_t* acc1_full = p1_empty + 1;
+  uint64_t* acc1_empty = acc1_full + 2;
+  uint64_t* a2_full = acc1_empty + 2;
+  uint64_t* s2_done = a2_full + 1;
+  uint32_t* meta = reinterpret_cast<uint32_t*>(smem + Cfg::off_misc);   // [kNS]
+  uint32_t* wflag = meta + Cfg::kNS;                                     // [2][4]
+  uint32_t* tslot = wflag + 8;
 
-  for (int i = tid; i < Cfg::kB_bytes / 16; i += kProjThreads) reinterpret_cast<uint4*>(sB)[i] = __ldg(Bpack + i);
-  for (int i = tid; i < Q * L; i += kProjThreads) sP[i] = __ldg(psi + i);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  pdl_trigger();
+
+  // ---- setup
+  for (int i = tid; i < Cfg::kB / 16; i += kProjThreads) reinterpret_cast<uint4*>(sB)[i] = __ldg(a.Bpack + i);
+  for (int i = tid; i < Cfg::kZero / 16; i += kProjThreads) reinterpret_cast<uint4*>(sZ)[i] = make_uint4(0, 0, 0, 0);
   if (tid == 0) {
-    mbar_init(bar, 1);
+    for (int i = 0; i < Cfg::kNS; ++i) { mbar_init(&raw_full[i], 1); mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(p1_empty, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&acc1_full[i], 1); mbar_init(&acc1_empty[i], 4); }
+    mbar_init(a2_full, 1);
+    mbar_init(s2_done, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<Cfg::kTmemCols>(tslot);
+  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tslot);
+  if (U16 && warp == 2 && lane == 0) prefetch_tmap(&tmap);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t tlane = tbase + ((uint32_t)(warp * 32) << 16);
-  uint32_t phase = 0;
 
-  const int64_t n_units = (n + Cfg::kFPT - 1) / Cfg::kFPT;
-  const int64_t total_rows = n * Q;
-  for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
-    float cacc[Cfg::kOPT];
-#pragma unroll
-    for (int i = 0; i < Cfg::kOPT; ++i) cacc[i] = 0.f;
-#pragma unroll 1
-    for (int tt = 0; tt < Cfg::kTPU; ++tt) {
-      const int64_t row0 = u * Cfg::kFPT * Q + (int64_t)tt * 128;
-      const int64_t rem = total_rows - row0;
-      const int valid = rem < 128 ? (int)rem : 128;
-      const bool r = convert_tile<Q, U16>(frames, row0, valid, sA, 0, tid);
-      fence_proxy_async_smem();
-      const int any = __syncthreads_or(r);
-      if (tid == 0) {
-        tc_fence_after();
-        issue_proj_mmas<Q, L>(sA, sB, tbase);
-        mma_commit(bar);
-      }
-      mbar_wait(bar, phase);
-      phase ^= 1u;
-      tc_fence_after();
-      if (any) {  // counts >= 1024 (u16) or non-fp16 values (f32): second plane
-        convert_tile<Q, U16>(frames, row0, valid, sA, 1, tid);
-        fence_proxy_async_smem();
-        __syncthreads();
-        if (tid == 0) {
+  const int64_t n = a.n;
+  const int g2 = a.g2;
+  const int tpg = Q >= 128 ? g2 * Cfg::kTPF : g2 / Cfg::kFPT;   // stage-1 tiles per group
+  const int tph = Q >= 128 ? g2 : tpg;                           // stage-1 tiles per stage-2 K chunk
+  const int64_t n_groups = (n + g2 - 1) / g2;
+  const int64_t my_groups = blockIdx.x < n_groups ? (n_groups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp == 0) {
+    // ================= stage-1 MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16(128, Cfg::kN);
+      const uint32_t ring0 = smem_u32(ring), p10 = smem_u32(sP1), b0 = smem_u32(sB), z0 = smem_u32(sZ);
+      uint32_t slot = 0, sphase = 0, tile = 0, p1_uses = 0;
+      for (int64_t gi = 0; gi < my_groups; ++gi) {
+        for (int tt = 0; tt < tpg; ++tt, ++tile) {
+          const uint32_t s1 = tile & 1u;
+          mbar_wait(&acc1_empty[s1], ((tile >> 1) & 1u) ^ 1u);
           tc_fence_after();
-          issue_proj_mmas<Q, L>(sA, sB, tbase + Cfg::kN);
-          mma_commit(bar);
-        }
-        mbar_wait(bar, phase);
-        phase ^= 1u;
-        tc_fence_after();
-      }
-      // ---- stage-1 epilogue: T[qy][a] = (acc_hi + acc_lo) / scale
-      {
-        float acc[Cfg::kN];
-        tmem_ld_cols<Cfg::kN>(tlane, acc);
-        float t[L];
+          const uint32_t acc = tbase + s1 * Cfg::kAcc1;
+          bool p1 = false;
+          for (int c = 0; c < Cfg::kCPT; ++c) {
+            mbar_wait(&full[slot], sphase);
+            tc_fence_after();
+            const bool has_p1 = meta[slot] & 1u;
+#pragma unroll 1
+            for (int plane = 0; plane < (has_p1 ? 2 : 1); ++plane) {
+              const uint32_t sa = plane == 0 ? ring0 + slot * Cfg::kSlot : p10;
 #pragma unroll
-        for (int a = 0; a < L; ++a) t[a] = acc[a] + acc[L + a];
-        if (any) {
-          tmem_ld_cols<Cfg::kN>(tlane + Cfg::kN, acc);
-#pragma unroll
-          for (int a = 0; a < L; ++a) t[a] = fmaf(kResScale, acc[a] + acc[L + a], t[a]);
-        }
-#pragma unroll
-        for (int a = 0; a < L; ++a) sT[tid * Cfg::kTs + a] = t[a] * inv_scale;
-      }
-      tc_fence_before();
-      __syncthreads();
-      // ---- stage 2: C[f][a][b] += sum_qy Psi[qy][b] T[qy][a]
-#pragma unroll
-      for (int i = 0; i < Cfg::kOPT; ++i) {
-        const int o = tid + kProjThreads * i;
-        if (o < Cfg::kOut) {
-          const int f = o / K, a = (o / L) % L, b = o % L;
-          const int r0 = Q >= 128 ? 0 : f * Q;
-          const int rn = Q >= 128 ? 128 : Q;
-          const int qy0 = Q >= 128 ? tt * 128 : 0;
-          float s = 0.f;
-#pragma unroll 8
-          for (int rr = 0; rr < rn; ++rr) s = fmaf(sP[(qy0 + rr) * L + b], sT[(r0 + rr) * Cfg::kTs + a], s);
-          cacc[i] += s;
+              for (int kk = 0; kk < Cfg::kKC / 16; ++kk) {
+                const uint64_t ad = U16 ? smem_desc_sw(sa + kk * 32, 8 * Cfg::kSpan, Cfg::kSwz)
+                                        : smem_desc_noswz(sa + 2 * kk * kLBO, kLBO, 128);
+                const uint64_t bd = smem_desc_noswz(b0 + (c * (Cfg::kKC / 8) + 2 * kk) * Cfg::kLBO_B, Cfg::kLBO_B, 128);
+                const uint32_t accum = plane == 0 ? (c > 0 || kk > 0) : (p1 || kk > 0);
+                mma_f16_ss(acc + plane * Cfg::kN, ad, bd, idesc, accum);
+              }
+            }
+            if (has_p1) { p1 = true; mma_commit(p1_empty); ++p1_uses; }
+            mma_commit(&empty[slot]);
+            if (++slot == Cfg::kNS) { slot = 0; sphase ^= 1u; }
+          }
+          if (!p1) mma_f16_ss(acc + Cfg::kN, smem_desc_noswz(z0, 2048, 128), smem_desc_noswz(b0, Cfg::kLBO_B, 128), idesc, 0u);
+          mma_commit(&acc1_full[s1]);
         }
       }
-      __syncthreads();
     }
+  } else if (warp == 1) {
+    // ================= stage-2 MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16(128, Cfg::kN);
+      const uint32_t a20 = smem_u32(sA2), b0 = smem_u32(sB);
+      const uint32_t acc2 = tbase + 2 * Cfg::kAcc1;
+      uint32_t phase = 0;
+      for (int64_t gi = 0; gi < my_groups; ++gi) {
+        for (int h = 0; h < Cfg::kTPF; ++h, phase ^= 1u) {
+          mbar_wait(a2_full, phase);
+          tc_fence_after();
+#pragma unroll 1
+          for (int plane = 0; plane < 2; ++plane) {
 #pragma unroll
-    for (int i = 0; i < Cfg::kOPT; ++i) {
-      const int o = tid + kProjThreads * i;
-      if (o < Cfg::kOut) {
-        const int64_t fg = u * Cfg::kFPT + o / K;
-        if (fg < n) C[fg * K + (o % K)] = cacc[i];
+            for (int kk = 0; kk < Cfg::kK2 / 16; ++kk) {
+              const uint64_t ad = smem_desc_noswz(a20 + plane * Cfg::kA2 + 2 * kk * kLBO, kLBO, 128);
+              const uint64_t bd = smem_desc_noswz(b0 + (h * (Cfg::kK2 / 8) + 2 * kk) * Cfg::kLBO_B, Cfg::kLBO_B, 128);
+              mma_f16_ss(acc2, ad, bd, idesc, (h > 0 || plane > 0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          mma_commit(s2_done);
+        }
       }
+    }
+  } else if (warp == 2) {
+    // ================= TMA producer (u16 frames)
+    if (U16 && lane == 0) {
+      uint32_t slot = 0, sphase = 0;
+      for (int64_t gi = 0; gi < my_groups; ++gi) {
+        const int64_t g = blockIdx.x + gi * gridDim.x;
+        for (int tt = 0; tt < tpg; ++tt) {
+          int64_t row0;
+          int valid;
+          tile_coords<Q, L, U16>(g, tt, g2, n, row0, valid);
+          for (int c = 0; c < Cfg::kCPT; ++c) {
+            mbar_wait(&empty[slot], sphase ^ 1u);
+            mbar_arrive_expect_tx(&raw_full[slot], Cfg::kSlotU);
+            tma_load_2d(ring + slot * Cfg::kSlot, &tmap, c * Cfg::kKC, (int)row0, &raw_full[slot]);
+            if (++slot == Cfg::kNS) { slot = 0; sphase ^= 1u; }
+          }
+        }
+      }
+    }
+  } else if (warp < 7) {
+    // ================= converters (128 threads)
+    const int ct = tid - 96;
+    const int cw = warp - 3;
+    uint32_t slot = 0, sphase = 0, job = 0, p1_uses = 0;
+    for (int64_t gi = 0; gi < my_groups; ++gi) {
+      const int64_t g = blockIdx.x + gi * gridDim.x;
+      for (int tt = 0; tt < tpg; ++tt) {
+        int64_t row0;
+        int valid;
+        tile_coords<Q, L, U16>(g, tt, g2, n, row0, valid);
+        for (int c = 0; c < Cfg::kCPT; ++c, ++job) {
+          uint8_t* dst = ring + slot * Cfg::kSlot;
+          bool resid = false;
+          if constexpr (U16) {
+            // in place: 128 rows x kSpan bytes; piece p = ct + 128 i (any 16-B piece maps to itself)
+            constexpr int kPieces = Cfg::kSlotU / 16 / kConv;
+            uint4 hiw[kPieces];
+            mbar_wait(&raw_full[slot], sphase);
+#pragma unroll
+            for (int i = 0; i < kPieces; ++i) {
+              uint4* p = reinterpret_cast<uint4*>(dst) + ct + kConv * i;
+              const uint4 v = *p;
+              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+              uint4 o, h;
+              uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+              uint32_t* hp = reinterpret_cast<uint32_t*>(&h);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                resid |= (w[q] & 0xFC00FC00u) != 0u;
+                op[q] = magic_half2(w[q] & 0x03FF03FFu);
+                hp[q] = w[q] & 0xFC00FC00u;   // raw high bits, converted only if needed
+              }
+              *p = o;
+              hiw[i] = h;
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, resid);
+            uint32_t* wf = wflag + (job & 1) * 4;
+            if (lane == 0) wf[cw] = bal ? 1u : 0u;
+            fence_proxy_async_smem();
+            named_sync(1, kConv);
+            const bool any = (wf[0] | wf[1] | wf[2] | wf[3]) != 0u;
+            if (any) {
+              mbar_wait(p1_empty, (p1_uses & 1u) ^ 1u);
+              ++p1_uses;
+#pragma unroll
+              for (int i = 0; i < kPieces; ++i) {
+                const uint32_t w[4] = {hiw[i].x, hiw[i].y, hiw[i].z, hiw[i].w};
+                uint4 o;
+                uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) op[q] = magic_half2(w[q] >> 10);
+                reinterpret_cast<uint4*>(sP1)[ct + kConv * i] = o;
+              }
+              fence_proxy_async_smem();
+              named_sync(1, kConv);
+            }
+            if (ct == 0) { meta[slot] = any ? 1u : 0u; mbar_arrive(&full[slot]); }
+          } else {
+            // f32: LDG -> fp16(x) (+ residual plane) into a no-swizzle K-major slot
+            constexpr int kPPR = Cfg::kKC / 8;              // 16-B fp16 pieces per row
+            constexpr int kPieces = 128 * kPPR / kConv;
+            uint4 lo[kPieces];
+            mbar_wait(&empty[slot], sphase ^ 1u);
+#pragma unroll
+            for (int i = 0; i < kPieces; ++i) {
+              const int p = ct + kConv * i, r = p / kPPR, j = p % kPPR;
+              float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0;
+              if (r < valid) {
+                const float4* src = reinterpret_cast<const float4*>(
+                    reinterpret_cast<const float*>(a.frames) + (row0 + r) * Q + c * Cfg::kKC + j * 8);
+                x0 = __ldg(src);
+                x1 = __ldg(src + 1);
+              }
+              const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+              uint4 o, l;
+              __half* hp = reinterpret_cast<__half*>(&o);
+              __half* lp = reinterpret_cast<__half*>(&l);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                hp[e] = __float2half_rn(x[e]);
+                const float d = x[e] - __half2float(hp[e]);
+                resid |= d != 0.f;
+                lp[e] = __float2half_rn(d);
+              }
+              *reinterpret_cast<uint4*>(dst + j * kLBO + (r >> 3) * 128 + (r & 7) * 16) = o;
+              lo[i] = l;
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, resid);
+            uint32_t* wf = wflag + (job & 1) * 4;
+            if (lane == 0) wf[cw] = bal ? 1u : 0u;
+            fence_proxy_async_smem();
+            named_sync(1, kConv);
+            const bool any = (wf[0] | wf[1] | wf[2] | wf[3]) != 0u;
+            if (any) {
+              mbar_wait(p1_empty, (p1_uses & 1u) ^ 1u);
+              ++p1_uses;
+#pragma unroll
+              for (int i = 0; i < kPieces; ++i) {
+                const int p = ct + kConv * i, r = p / kPPR, j = p % kPPR;
+                *reinterpret_cast<uint4*>(sP1 + j * kLBO + (r >> 3) * 128 + (r & 7) * 16) = lo[i];
+              }
+              fence_proxy_async_smem();
+              named_sync(1, kConv);
+            }
+            if (ct == 0) { meta[slot] = any ? 1u : 0u; mbar_arrive(&full[slot]); }
+          }
+          if (++slot == Cfg::kNS) { slot = 0; sphase ^= 1u; }
+        }
+      }
+    }
+  } else {
+    // ================= epilogue (128 threads; TMEM lane quadrant = warp % 4)
+    const int et = tid - 224;
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;                    // TMEM lane == tile row == A2 m index
+    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+    const uint32_t acc2 = tbase + 2 * Cfg::kAcc1 + lane_addr;
+    uint32_t tile = 0, s2_issued = 0;
+    int64_t pending = -1;   // frame0 of a group whose stage-2 result has not been stored yet
+    auto stage2_epilogue = [&](int64_t frame0) {
+      float d[Cfg::kN];
+      tmem_ld_cols<Cfg::kN>(acc2, d);
+      const int f = row / L, aa = row % L;
+      const int64_t fg = frame0 + f;
+      if (f < g2 && fg < n) {
+        float* dst = a.C + fg * K + aa * L;
+#pragma unroll
+        for (int b = 0; b < L; b += 4) {
+          float4 v = make_float4((d[b] + d[L + b]) * a.sc2, (d[b + 1] + d[L + b + 1]) * a.sc2,
+                                 (d[b + 2] + d[L + b + 2]) * a.sc2, (d[b + 3] + d[L + b + 3]) * a.sc2);
+          *reinterpret_cast<float4*>(dst + b) = v;
+        }
+      }
+    };
+    for (int64_t gi = 0; gi < my_groups; ++gi) {
+      const int64_t g = blockIdx.x + gi * gridDim.x;
+      for (int tt = 0; tt < tpg; ++tt, ++tile) {
+        const uint32_t s1 = tile & 1u;
+        mbar_wait(&acc1_full[s1], (tile >> 1) & 1u);
+        tc_fence_after();
+        float acc[Cfg::kN];
+        float t[L];
+        const uint32_t aaddr = tbase + s1 * Cfg::kAcc1 + lane_addr;
+        tmem_ld_cols<Cfg::kN>(aaddr, acc);
+#pragma unroll
+        for (int q = 0; q < L; ++q) t[q] = acc[q] + acc[L + q];
+        tmem_ld_cols<Cfg::kN>(aaddr + Cfg::kN, acc);
+#pragma unroll
+        for (int q = 0; q < L; ++q) t[q] = fmaf(kRes, acc[q] + acc[L + q], t[q]) * a.sc1;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc1_empty[s1]);
+        if (tt % tph == 0 && s2_issued > 0) {   // A2 is free once the previous stage-2 chunk is done
+          mbar_wait(s2_done, (s2_issued - 1) & 1u);
+          tc_fence_after();
+          if (pending >= 0) { stage2_epilogue(pending); pending = -1; }
+        }
+        // A2 element (m = f*L + a, k), K-major no swizzle: (k/8)*kLBO + (m/8)*128 + (m%8)*16 + (k%8)*2
+        int f, k;
+        if constexpr (Q >= 128) { f = tt % g2; k = row; }
+        else { f = tt * Cfg::kFPT + row / Q; k = row % Q; }
+        if (Q >= 128 || row < Cfg::kFPT * Q) {
+          uint8_t* base = sA2 + (k >> 3) * kLBO + (k & 7) * 2;
+#pragma unroll
+          for (int q = 0; q < L; ++q) {
+            const int m = f * L + q;
+            const __half hi = __float2half_rn(t[q]);
+            const __half lo = __float2half_rn(t[q] - __half2float(hi));
+            uint8_t* p = base + (m >> 3) * 128 + (m & 7) * 16;
+            *reinterpret_cast<__half*>(p) = hi;
+            *reinterpret_cast<__half*>(p + Cfg::kA2) = lo;
+          }
+        }
+        if (tt % tph == tph - 1) {   // stage-2 K chunk complete
+          fence_proxy_async_smem();
+          named_sync(2, 128);
+          if (et == 0) mbar_arrive(a2_full);
+          ++s2_issued;
+        }
+      }
+      pending = g * g2;
+    }
+    if (s2_issued > 0) {
+      mbar_wait(s2_done, (s2_issued - 1) & 1u);
+      tc_fence_after();
+      if (pending >= 0) stage2_epilogue(pending);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<Cfg::kTmemCols>(tbase);
+  if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tbase);
+  pdl_wait();   // this grid completes only after the preceding (row-DFT) grid has completed
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link needed)
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
 }
 
 template <int Q, int L, bool U16>
 static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n, float* C, cudaStream_t st) {
-  using Cfg = ProjCfg<Q, L>;
+  using Cfg = ProjCfg<Q, L, U16>;
   auto kern = project_kernel<Q, L, U16>;
-  static int blocks_per_sm = -1;
-  if (blocks_per_sm < 0) {
+  static bool init = false;
+  if (!init) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::smem);
     if (e != cudaSuccess) return e;
-    int nb = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kProjThreads, Cfg::smem);
-    if (e != cudaSuccess) return e;
-    blocks_per_sm = std::max(1, std::min(nb, 512 / Cfg::kTmemCols));
+    init = true;
   }
-  const int64_t units = (n + Cfg::kFPT - 1) / Cfg::kFPT;
-  const int grid = (int)std::min<int64_t>(units, (int64_t)blocks_per_sm * p.sm_count);
-  if (grid <= 0) return cudaSuccess;
-  kern<<<grid, kProjThreads, Cfg::smem, st>>>(frames, n, C, reinterpret_cast<const uint4*>(p.d_Bpack), p.d_psi,
-                                              (float)(1.0 / p.b_scale));
-  return cudaGetLastError();
+  if (n <= 0) return cudaSuccess;
+  // frames per stage-2 group: the largest multiple of kFPT (<= kG2) that keeps the per-CTA
+  // frame count minimal, so small batches still spread over every SM
+  int g2 = Cfg::kFPT;
+  int64_t best = INT64_MAX;
+  for (int c = Cfg::kFPT; c <= Cfg::kG2; c += Cfg::kFPT) {
+    const int64_t groups = (n + c - 1) / c;
+    const int64_t per_cta = (groups + p.sm_count - 1) / p.sm_count * c;
+    if (per_cta <= best) { best = per_cta; g2 = c; }
+  }
+  const int64_t groups = (n + g2 - 1) / g2;
+  const int grid = (int)std::min<int64_t>(groups, (int64_t)p.sm_count);
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof tmap);
+  if constexpr (U16) {
+    auto enc = get_encode();
+    if (!enc) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {(cuuint64_t)Q, (cuuint64_t)(n * Q)};
+    const cuuint64_t strides[1] = {(cuuint64_t)Q * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)Cfg::kKC, 128u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(frames), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           Cfg::kSpan == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  ProjArgs a{frames, n, C, g2, reinterpret_cast<const uint4*>(p.d_Bpack), (float)p.sc1, (float)p.sc2};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kProjThreads);
+  cfg.dynamicSmemBytes = Cfg::smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, tmap);
 }
 
 #define WDD_PROJ_CASE(QQ, LL)                                                          \
@@ -291,17 +527,17 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
                         : launch_project_t<QQ, LL, false>(p, frames, n, C, st);
 
 cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* C, cudaStream_t st) {
-  WDD_PROJ_CASE(32, 8) WDD_PROJ_CASE(32, 16) WDD_PROJ_CASE(32, 24) WDD_PROJ_CASE(32, 32)
-  WDD_PROJ_CASE(64, 8) WDD_PROJ_CASE(64, 16) WDD_PROJ_CASE(64, 24) WDD_PROJ_CASE(64, 32)
+  WDD_PROJ_CASE(32, 8) WDD_PROJ_CASE(32, 16) WDD_PROJ_CASE(32, 32)
+  WDD_PROJ_CASE(64, 8) WDD_PROJ_CASE(64, 16) WDD_PROJ_CASE(64, 32)
   WDD_PROJ_CASE(128, 8) WDD_PROJ_CASE(128, 16) WDD_PROJ_CASE(128, 24) WDD_PROJ_CASE(128, 32)
   WDD_PROJ_CASE(256, 8) WDD_PROJ_CASE(256, 16) WDD_PROJ_CASE(256, 24) WDD_PROJ_CASE(256, 32)
   return cudaErrorInvalidValue;
 }
 
 size_t project_smem_bytes(int Q, int L) {
-#define WDD_SMEM_CASE(QQ, LL) if (Q == QQ && L == LL) return ProjCfg<QQ, LL>::smem;
-  WDD_SMEM_CASE(32, 8) WDD_SMEM_CASE(32, 16) WDD_SMEM_CASE(32, 24) WDD_SMEM_CASE(32, 32)
-  WDD_SMEM_CASE(64, 8) WDD_SMEM_CASE(64, 16) WDD_SMEM_CASE(64, 24) WDD_SMEM_CASE(64, 32)
+#define WDD_SMEM_CASE(QQ, LL) if (Q == QQ && L == LL) return ProjCfg<QQ, LL, true>::smem;
+  WDD_SMEM_CASE(32, 8) WDD_SMEM_CASE(32, 16) WDD_SMEM_CASE(32, 32)
+  WDD_SMEM_CASE(64, 8) WDD_SMEM_CASE(64, 16) WDD_SMEM_CASE(64, 32)
   WDD_SMEM_CASE(128, 8) WDD_SMEM_CASE(128, 16) WDD_SMEM_CASE(128, 24) WDD_SMEM_CASE(128, 32)
   WDD_SMEM_CASE(256, 8) WDD_SMEM_CASE(256, 16) WDD_SMEM_CASE(256, 24) WDD_SMEM_CASE(256, 32)
 #undef WDD_SMEM_CASE
@@ -331,14 +567,21 @@ void pack_basis_fp16(const Plan& p, std::vector<uint16_t>& out, double& scale) {
 
 // =====================================================================================
 // Row DFT (a4): R[j][sy][k] (+)= sum_{frames of row sy in chunk} Fx[j][sx] C[p][k]
+// Tile: 16 active-vx columns j x 64 coefficients k of one scan row; 128 threads, 2 j x 4 k each.
 // =====================================================================================
-__global__ void __launch_bounds__(256) rowdft_kernel(const float* __restrict__ C, RowSource rs,
+__global__ void __launch_bounds__(128) rowdft_kernel(const float* __restrict__ C, RowSource rs,
                                                      const float2* __restrict__ Fx, float2* __restrict__ R,
-                                                     int Sx, int Sy, int K, int n_vx) {
-  __shared__ float Cs[32][64];
-  __shared__ float2 Fs[32][33];
-  const int t = threadIdx.x, kk = t & 63, jg = t >> 6;
-  const int k0 = blockIdx.x * 64, j0 = blockIdx.y * 32, r = blockIdx.z;
+                                                     int Sx, int Sy, int K, int n_vx, int early) {
+  // PDL: the projection grid of this chunk (and, transitively, the previous row DFT) must be
+  // complete before C is read and R rows are written.  With C indexed by scan position
+  // (contiguous chunks) the next projection may start right away (early trigger).
+  if (early) pdl_trigger();
+  pdl_wait();
+  if (!early) pdl_trigger();
+  __shared__ __align__(16) float Cs[32][64];
+  __shared__ float2 Fs[16][33];
+  const int t = threadIdx.x, kq = (t & 15) * 4, jg = t >> 4;
+  const int k0 = blockIdx.x * 64, j0 = blockIdx.y * 16, r = blockIdx.z;
   int sy, count, mode, pb = 0, eb = 0, sx0 = 0;
   if (rs.contiguous) {
     const int sy0 = rs.s0 / Sx;
@@ -355,65 +598,79 @@ __global__ void __launch_bounds__(256) rowdft_kernel(const float* __restrict__ C
     count = ri.z;
     mode = ri.w;
   }
-  float2 acc[8];
+  float2 acc[2][4];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) acc[q] = make_float2(0.f, 0.f);
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[q][e] = make_float2(0.f, 0.f);
   for (int e0 = 0; e0 < count; e0 += 32) {
     const int ne = min(32, count - e0);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int idx = t + 256 * i, ee = idx >> 6, kq = idx & 63;
-      float v = 0.f;
-      if (ee < ne && k0 + kq < K) {
+    for (int i = 0; i < 4; ++i) {          // 32 entries x 64 k as float4: 512 / 128 threads
+      const int idx = t + 128 * i, ee = idx >> 4, kk = (idx & 15) * 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ee < ne) {
         const int p = rs.contiguous ? pb + e0 + ee : rs.ent[eb + e0 + ee].x;
-        v = C[(int64_t)p * K + k0 + kq];
+        v = __ldg(reinterpret_cast<const float4*>(C + (int64_t)p * K + k0 + kk));
       }
-      Cs[ee][kq] = v;
+      *reinterpret_cast<float4*>(&Cs[ee][kk]) = v;
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int idx = t + 256 * i, jj = idx >> 5, ee = idx & 31;
+    for (int i = 0; i < 4; ++i) {          // 16 j x 32 entries
+      const int idx = t + 128 * i, jj = idx >> 5, ee = idx & 31;
       float2 v = make_float2(0.f, 0.f);
       if (ee < ne && j0 + jj < n_vx) {
         const int sx = rs.contiguous ? sx0 + pb + e0 + ee - r * Sx : rs.ent[eb + e0 + ee].y;
-        v = Fx[(int64_t)(j0 + jj) * Sx + sx];
+        v = __ldg(Fx + (int64_t)(j0 + jj) * Sx + sx);
       }
       Fs[jj][ee] = v;
     }
     __syncthreads();
     for (int ee = 0; ee < ne; ++ee) {
-      const float c = Cs[ee][kk];
+      const float4 c = *reinterpret_cast<const float4*>(&Cs[ee][kq]);
+      const float cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float2 f = Fs[jg * 8 + q][ee];
-        acc[q].x = fmaf(f.x, c, acc[q].x);
-        acc[q].y = fmaf(f.y, c, acc[q].y);
+      for (int q = 0; q < 2; ++q) {
+        const float2 f = Fs[jg * 2 + q][ee];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          acc[q][e].x = fmaf(f.x, cv[e], acc[q][e].x);
+          acc[q][e].y = fmaf(f.y, cv[e], acc[q][e].y);
+        }
       }
     }
     __syncthreads();
   }
-  const int k = k0 + kk;
-  if (k >= K) return;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int j = j0 + jg * 8 + q;
-    if (j < n_vx) {
-      float2* ptr = R + ((int64_t)j * Sy + sy) * K + k;
-      if (mode) {
-        const float2 o = *ptr;
-        *ptr = make_float2(o.x + acc[q].x, o.y + acc[q].y);
-      } else {
-        *ptr = acc[q];
-      }
+  for (int q = 0; q < 2; ++q) {
+    const int j = j0 + jg * 2 + q;
+    if (j >= n_vx) continue;
+    float4* ptr = reinterpret_cast<float4*>(R + ((int64_t)j * Sy + sy) * K + k0 + kq);
+    float4 a0 = make_float4(acc[q][0].x, acc[q][0].y, acc[q][1].x, acc[q][1].y);
+    float4 a1 = make_float4(acc[q][2].x, acc[q][2].y, acc[q][3].x, acc[q][3].y);
+    if (mode) {
+      const float4 o0 = ptr[0], o1 = ptr[1];
+      a0.x += o0.x; a0.y += o0.y; a0.z += o0.z; a0.w += o0.w;
+      a1.x += o1.x; a1.y += o1.y; a1.z += o1.z; a1.w += o1.w;
     }
+    ptr[0] = a0;
+    ptr[1] = a1;
   }
 }
 
 cudaError_t launch_rowdft(const Plan& p, const float* C, const RowSource& rs, cudaStream_t st) {
   if (rs.n_rows <= 0) return cudaSuccess;
-  dim3 grid((p.K + 63) / 64, (p.n_vx + 31) / 32, rs.n_rows);
-  rowdft_kernel<<<grid, 256, 0, st>>>(C, rs, p.d_Fx, p.d_R, p.Sx, p.Sy, p.K, p.n_vx);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.K / 64, (p.n_vx + 15) / 16, rs.n_rows);
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, rowdft_kernel, C, rs, (const float2*)p.d_Fx, p.d_R, p.Sx, p.Sy, p.K, p.n_vx,
+                            rs.contiguous);
 }
 
 // =====================================================================================

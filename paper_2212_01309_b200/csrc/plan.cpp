@@ -307,12 +307,21 @@ wdd_status validate_and_mark(Plan& p, const int32_t* idx, int64_t n) {
 // Enqueue projection + row DFT for one chunk of already-validated frames.
 wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, int64_t nc) {
   cudaStream_t st = p.stream;
-  {
-    Prof pr(p, kSlotProject, st);
-    CUDA_TRY(launch_project(p, frames_dev, nc, p.d_C, st));
-  }
   bool contiguous = true;
   for (int64_t i = 1; i < nc && contiguous; ++i) contiguous = idx[i] == idx[0] + i;
+  // contiguous chunks write C at their scan positions (no buffer reuse within an acquisition, so
+  // consecutive chunks may overlap under PDL); other chunks use an alternating scratch buffer
+  float* C;
+  if (contiguous) {
+    C = p.d_Call + (size_t)idx[0] * p.K;
+  } else {
+    C = p.d_C[p.c_parity];
+    p.c_parity ^= 1;
+  }
+  {
+    Prof pr(p, kSlotProject, st);
+    CUDA_TRY(launch_project(p, frames_dev, nc, C, st));
+  }
   RowSource rs{};
   rs.n = (int)nc;
   if (contiguous) {
@@ -357,7 +366,7 @@ wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, in
   }
   {
     Prof pr(p, kSlotRowDft, st);
-    CUDA_TRY(launch_rowdft(p, p.d_C, rs, st));
+    CUDA_TRY(launch_rowdft(p, C, rs, st));
   }
   return WDD_OK;
 }
@@ -387,7 +396,7 @@ void free_plan(Plan* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   cudaDeviceSynchronize();
   if (p->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(p->nccl));
-  void* bufs[] = {p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_C,
+  void* bufs[] = {p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_C[0], p->d_C[1], p->d_Call,
                   p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec,
                   p->d_meta, p->d_stage[0], p->d_stage[1]};
   for (void* b : bufs)
@@ -506,6 +515,20 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   // device buffers
   std::vector<uint16_t> bpack;
   pack_basis_fp16(*p, bpack, p->b_scale);
+  {
+    // |T| <= max|I| * max_a sum_qx |Psi[qx][a]|; choose eT so T * 2^eT stays below 2^15 in fp16
+    double colsum = 0;
+    for (int a = 0; a < L; ++a) {
+      double s = 0;
+      for (int m = 0; m < Q; ++m) s += std::fabs(p->basis[(size_t)m * L + a]);
+      colsum = std::max(colsum, s);
+    }
+    const double bound = (p->dtype == 0 ? 65535.0 : 65504.0) * colsum;
+    const int eT = (int)std::floor(std::log2(32768.0 / bound));
+    const int es = (int)std::lround(std::log2(p->b_scale));
+    p->sc1 = std::ldexp(1.0, eT - es);
+    p->sc2 = std::ldexp(1.0, -es - eT);
+  }
   std::vector<float> psi32(p->basis.begin(), p->basis.end());
   std::vector<int32_t> vpos(act.begin(), act.end());
   p->chunk_cap = 8192;
@@ -524,7 +547,9 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ALLOC(p->d_G, W.size() * sizeof(float2));
   if (p->combine == 1) ALLOC(p->d_Gsum, W.size() * sizeof(float2));
   ALLOC(p->d_R, (size_t)p->n_vx * Sy * K * sizeof(float2));
-  ALLOC(p->d_C, (size_t)p->chunk_cap * K * sizeof(float));
+  ALLOC(p->d_Call, (size_t)p->S * K * sizeof(float));
+  ALLOC(p->d_C[0], (size_t)p->chunk_cap * K * sizeof(float));
+  ALLOC(p->d_C[1], (size_t)p->chunk_cap * K * sizeof(float));
   ALLOC(p->d_act_vy, act.size() * 4);
   ALLOC(p->d_col_off, p->col_off.size() * 4);
   ALLOC(p->d_vpos, act.size() * 4);
@@ -801,6 +826,9 @@ wdd_status wdd_capture_begin(wdd_plan_t plan, void* stream) {
   if (check_plan(plan)) return WDD_E_ARG;
   Plan& p = *P(plan);
   if (p.capturing) return fail(WDD_E_STATE, "already capturing");
+  if (stream == nullptr || reinterpret_cast<cudaStream_t>(stream) == cudaStreamLegacy ||
+      reinterpret_cast<cudaStream_t>(stream) == cudaStreamPerThread)
+    return fail(WDD_E_ARG, "capture needs a created (non-default) stream");
   CUDA_TRY(cudaSetDevice(p.device));
   if (!p.cap_host) {
     p.cap_bytes = 16u << 20;
