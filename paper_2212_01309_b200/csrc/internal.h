@@ -13,19 +13,6 @@ namespace wdd {
 
 enum ProfSlot { kSlotProject = 0, kSlotRowDft = 1, kSlotFlush = 2, kSlotReadout = 3, kSlotFinalize = 4, kNumSlots = 5 };
 
-// Rows of one ingest chunk handed to the row-DFT kernel.  Contiguous chunks (scan indices
-// s0, s0+1, ..., s0+n-1) are described arithmetically; anything else by a device table.
-struct RowSource {
-  int contiguous;   // 1: rows derived from s0/n
-  int s0;           // first scan index (contiguous)
-  int n;            // frames in the chunk
-  int n_rows;       // rows touched
-  int mode_first;   // 0 = write (row staging was clean), 1 = accumulate (contiguous only)
-  int mode_last;
-  const int2* ent;  // general: (batch position, sx) sorted by row
-  const int4* rows; // general: (sy, first entry, entry count, mode)
-};
-
 struct Plan {
   // geometry
   int Sy = 0, Sx = 0, Q = 0, L = 0, K = 0, dtype = 0, normalize = 0, device = 0, combine = 0;
@@ -44,7 +31,7 @@ struct Plan {
   std::vector<int32_t> act_vy;        // n_act
   std::vector<int2> flush_tiles;      // (column j, first row i0) of 32-row tiles
   std::vector<uint64_t> seen;         // S bits
-  std::vector<uint8_t> row_dirty;     // Sy
+  std::vector<uint8_t> row_dirty;     // Sy: row has coefficients in d_Call not yet flushed into G
   int64_t frames_ingested = 0;
 
   // device buffers
@@ -56,9 +43,8 @@ struct Plan {
   float2* d_G = nullptr;              // n_act * K
   float2* d_Gsum = nullptr;           // n_act * K (combine = 1 only)
   float2* d_R = nullptr;              // n_vx * Sy * K   R[j][sy][k]
-  float* d_Call = nullptr;            // S * K: coefficients at their scan positions (contiguous chunks)
-  float* d_C[2] = {nullptr, nullptr}; // chunk_cap * K scratch, alternating (non-contiguous chunks)
-  int c_parity = 0;
+  float* d_Call = nullptr;            // S * K: coefficients of ingested, not yet flushed frames at
+                                      // their scan positions (zero elsewhere)
   int32_t* d_act_vy = nullptr;
   int32_t* d_col_off = nullptr;
   int32_t* d_vpos = nullptr;          // n_act flattened v (scatter positions)
@@ -98,8 +84,12 @@ struct Plan {
 };
 
 // ---- kernel launchers (kernels.cu); return cudaError_t of the launch
-cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* C, cudaStream_t st);
-cudaError_t launch_rowdft(const Plan& p, const float* C, const RowSource& rs, cudaStream_t st);
+// projection of n frames; C row of frame f = idx ? idx[f] : f (idx: device array or null)
+cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* C, const int32_t* idx,
+                           cudaStream_t st);
+// row DFT of the listed scan rows from d_Call into R, then zero those rows of d_Call
+cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st);
+cudaError_t launch_zero_rows(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st);
 cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st);
 cudaError_t launch_readout(const Plan& p, const float2* G, bool scatter, cudaStream_t st);
 cudaError_t launch_scatter(const Plan& p, cudaStream_t st);

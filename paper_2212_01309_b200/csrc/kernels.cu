@@ -33,24 +33,43 @@ using namespace tc;
 // =====================================================================================
 // Projection (tcgen05), warp-specialised and persistent.
 //
-//   warp 0       stage-1 MMA issuer : T_tile (128 rows x 2L) += A1_chunk * B^T     (TMEM acc1)
+//   warp 0       stage-1 MMA issuer : T_tile (128 rows x 2L) += A1 * B^T            (TMEM acc1)
 //   warp 1       stage-2 MMA issuer : D (128 x 2L) += A2 * B^T over qy, hi+lo planes (TMEM acc2)
-//   warp 2       TMA producer (u16) : 2-D tiled loads, 128 rows x 64 pixels, SWIZZLE_128B, into
-//                                     the A1 ring (OOB rows of a ragged tail are zero-filled)
-//   warps 3-6    converters         : u16 -> fp16 IN PLACE (same bytes; the TMA's SW128 layout is
-//                                     the UMMA K-major SW128 operand layout), counts split
-//                                     exactly into low 10 bits + (bits 10-15) x 1024, the second
-//                                     plane going to a side slot only for chunks that need it;
-//                                     f32 frames: LDG -> fp16(x) + fp16(x - fp16(x)), no swizzle
-//   warps 7-10   epilogue           : acc1 -> T -> fp16 hi/lo A2 image; acc2 -> C (global, fp32)
+//   warp 2       TMA producer (u16) : 2-D tiled loads of 128 detector rows x 64 pixels with hardware
+//                                     swizzle into a shared-memory ring (ragged tails zero-filled)
+//   warps 3-10   converters (2 groups of 4 warps, even / odd chunks)
+//                                   : one detector row per thread: swizzled LDS -> exact fp16 in
+//                                     registers (counts split into low 10 bits + bits 10-15 x 1024)
+//                                     -> tcgen05.st into a TMEM A ring; the raw slot is released as
+//                                     soon as it has been read.  f32 frames: LDG -> fp16(x) +
+//                                     fp16(x - fp16(x)) into shared-memory operand slots instead.
+//   warps 11-14  epilogue           : acc1 -> T -> fp16 hi/lo A2 image (smem); acc2 -> C (global)
 //
 // Stage 1 contracts the detector columns (qx) for 128 detector rows at a time; stage 2 contracts
 // the detector rows (qy) for g2 <= 128/L frames at a time, M = (frame, a) rows, in K-chunks of
 // 128 rows (two for Q = 256).  Both stages use the same B image [Psi_hi | Psi_lo] (N = 2L).
 // g2 is chosen per launch so a small batch still spreads over every SM.
 // =====================================================================================
-constexpr int kProjThreads = 352;   // MMA1, MMA2, TMA, 4 converter warps, 4 epilogue warps
-constexpr int kConv = 128;          // converter threads
+#ifdef WDD_TRACE
+__device__ unsigned long long g_trace[16 * 4096];
+__device__ __forceinline__ void trace_rec(int code, unsigned& cnt, int j) {
+  if (blockIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_trace[code * 4096 + (cnt++ & 4095)] = (t << 16) | ((unsigned long long)(code & 0xff) << 8) | (unsigned long long)(j & 0xff);
+}
+#define TRACE(c, j) trace_rec(c, trc[c], j)
+#define TRACE_DECL unsigned trc[16] = {0};
+#else
+#define TRACE(c, j)
+#define TRACE_DECL
+#endif
+#ifndef WDD_NS
+#define WDD_NS 8
+#endif
+constexpr int kProjThreads = 480;   // MMA1, MMA2, TMA, 2 x 4 converter warps, 4 epilogue warps
+constexpr int kConv = 128;          // threads per converter group (2 groups: even / odd chunks)
+constexpr int kNA = 4;              // TMEM A-operand ring (u16 path)
 constexpr uint32_t kLBO = 2064;     // no-swizzle K-major: bytes between K-adjacent core matrices of a
                                     // 128-row operand (16 row groups x 128 B + 16 B bank-rotation pad)
 
@@ -61,12 +80,11 @@ template <int Q, int L, bool U16>
 struct ProjCfg {
   static constexpr int kKC = Q >= 64 ? 64 : Q;            // K elements (pixels) per A1 chunk
   static constexpr int kCPT = Q / kKC;                    // chunks per stage-1 tile
-  static constexpr int kSpan = kKC * 2;                   // fp16 bytes per row of a chunk (SW span)
-  static constexpr uint32_t kSwz = kSpan == 128 ? 2u : 4u;  // UMMA layout: SWIZZLE_128B / 64B
-  static constexpr int kSlotU = 128 * kSpan;              // u16 slot (TMA box == fp16 operand)
+  static constexpr int kSpan = kKC * 2;                   // bytes per row of a raw u16 chunk (swizzle span)
+  static constexpr int kSwzMask = kSpan == 128 ? 7 : 3;   // TMA SWIZZLE_128B / 64B address XOR mask
+  static constexpr int kSlotU = 128 * kSpan;              // u16 slot == TMA box
   static constexpr int kSlotF = (kKC / 8) * (int)kLBO;    // f32 path: no-swizzle fp16 operand
   static constexpr int kSlot = align_up(U16 ? kSlotU : kSlotF, 1024);
-  static constexpr int kNS = 6;                           // A1 ring slots
   static constexpr int kN = 2 * L;                        // MMA N: Psi_hi | Psi_lo
   static constexpr int kLBO_B = 16 * kN;
   static constexpr int kB = (Q / 8) * kLBO_B;
@@ -75,18 +93,27 @@ struct ProjCfg {
   static constexpr int kK2 = Q >= 128 ? 128 : Q;          // stage-2 K chunk (detector rows)
   static constexpr int kG2 = Q >= 128 ? 128 / L : ((128 / L) / kFPT) * kFPT;  // max frames per group
   static constexpr int kA2 = (kK2 / 8) * (int)kLBO;       // one A2 plane (K-major, no swizzle)
-  static constexpr int kZero = 4096;                      // 128 x 16 fp16 zeros
-  static constexpr int kAcc1 = 2 * kN;                    // per acc1 slot: plane 0 | plane 1
-  static constexpr int kTmemCols = pow2_cols(2 * kAcc1 + kN);
+  static constexpr int kAcc1 = kN;                        // per acc1 slot (both count planes accumulate here)
+  static constexpr int kNAcc = 4;                         // acc1 ring
+  static constexpr int kACols = kKC / 2;                  // TMEM columns of one A1 chunk (fp16 pairs)
+  static constexpr int tA = 0;                            // TMEM column map
+  static constexpr int tP1 = tA + kNA * kACols;          // one plane-1 buffer per converter group
+  static constexpr int tAcc1 = tP1 + 2 * kACols;
+  static constexpr int tAcc2 = tAcc1 + kNAcc * kAcc1;
+  static constexpr int kTmemCols = pow2_cols(tAcc2 + kN);
+  static_assert(tAcc2 + kN <= 512, "TMEM");
+  static constexpr int kFixed = (U16 ? 0 : 2 * kSlot) + align_up(2 * kA2, 1024) + align_up(kB, 1024) + 512;
+  static constexpr int kNSfit = ((232448 - kFixed) / kSlot) & ~1;
+  static constexpr int kNS = kNSfit < WDD_NS ? kNSfit : WDD_NS;  // raw ring (even: group = job parity)
   static constexpr int off_ring = 0;
-  static constexpr int off_P1 = off_ring + kNS * kSlot;
-  static constexpr int off_A2 = off_P1 + kSlot;
+  static constexpr int off_P1 = off_ring + kNS * kSlot;   // f32 path only
+  static constexpr int off_A2 = off_P1 + (U16 ? 0 : 2 * kSlot);
   static constexpr int off_B = off_A2 + align_up(2 * kA2, 1024);
-  static constexpr int off_Z = off_B + align_up(kB, 1024);
-  static constexpr int off_bar = off_Z + kZero;
-  static constexpr int kBars = 3 * kNS + 7;
-  static constexpr int off_misc = off_bar + 8 * kBars;    // meta[kNS], wflag[2][4], tmem slot
-  static constexpr int smem = off_misc + 4 * kNS + 32 + 16;
+  static constexpr int off_bar = off_B + align_up(kB, 1024);
+  static constexpr int kBars = 2 * kNS + 2 * kNA + 2 * kNAcc + 4;
+  static constexpr int off_misc = off_bar + 8 * kBars;    // meta[kNS+kNA], wflag[2 groups][2][4], tmem slot
+  static constexpr int smem = off_misc + 4 * (kNS + kNA) + 64 + 16;
+  static_assert(kNS % 2 == 0 && kNA % 2 == 0, "even rings: converter group = job parity");
   static_assert(kG2 >= 1, "group");
   static_assert(smem <= 232448, "shared memory");
 };
@@ -100,6 +127,14 @@ __device__ __forceinline__ uint32_t magic_half2(uint32_t v10) {
   return *reinterpret_cast<const uint32_t*>(&r);
 }
 
+// Second count plane of a u16 pair: (x >> 10) * 1024 = x & 0xFC00, exact in fp16.
+__device__ __forceinline__ uint32_t hi_plane(uint32_t w) {
+  const uint32_t v = magic_half2((w >> 10) & 0x003F003Fu);
+  const __half2 h = *reinterpret_cast<const __half2*>(&v);
+  const __half2 r = __hmul2(h, __half2half2(__ushort_as_half((unsigned short)0x6400)));
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
+
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -108,6 +143,7 @@ struct ProjArgs {
   const void* frames;
   int64_t n;
   float* C;
+  const int32_t* idx;   // C row of frame f: idx ? idx[f] : f
   int g2;      // frames per stage-2 group (<= kG2; a multiple of kFPT)
   const uint4* Bpack;
   float sc1;   // acc1 -> fp16 A2 scale   (2^(eT - s))
@@ -132,36 +168,37 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     project_kernel(ProjArgs a, const __grid_constant__ CUtensorMap tmap) {
   using Cfg = ProjCfg<Q, L, U16>;
   constexpr int K = L * L;
-  constexpr float kRes = U16 ? 1024.f : 1.f;
+  TRACE_DECL
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem + Cfg::off_ring;
   uint8_t* sP1 = smem + Cfg::off_P1;
   uint8_t* sA2 = smem + Cfg::off_A2;
   uint8_t* sB = smem + Cfg::off_B;
-  uint8_t* sZ = smem + Cfg::off_Z;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::off_bar);
-  uint64_t* raw_full = bars;                 // [kNS] TMA landed
-  uint64_t* full = bars + Cfg::kNS;          // [kNS] converted
-  uint64_t* empty = bars + 2 * Cfg::kNS;     // [kNS] consumed by the MMA
-  uint64_t* p1_empty = bars + 3 * Cfg::kNS;
-  uint64_t* acc1_full = p1_empty + 1;
-  uint64_t* acc1_empty = acc1_full + 2;
-  uint64_t* a2_full = acc1_empty + 2;
+  uint64_t* raw_full = bars;                   // [kNS] slot filled (TMA tx / f32 converter)
+  uint64_t* raw_empty = bars + Cfg::kNS;       // [kNS] slot free   (u16 converter / f32 MMA commit)
+  uint64_t* a_full = bars + 2 * Cfg::kNS;      // [kNA] TMEM A chunk written (u16)
+  uint64_t* a_empty = a_full + kNA;            // [kNA] TMEM A chunk consumed (u16)
+  uint64_t* p1_empty = a_empty + kNA;          // [2] per converter group
+  uint64_t* acc1_full = p1_empty + 2;          // [kNAcc]
+  uint64_t* acc1_empty = acc1_full + Cfg::kNAcc;
+  uint64_t* a2_full = acc1_empty + Cfg::kNAcc;
   uint64_t* s2_done = a2_full + 1;
-  uint32_t* meta = reinterpret_cast<uint32_t*>(smem + Cfg::off_misc);   // [kNS]
-  uint32_t* wflag = meta + Cfg::kNS;                                     // [2][4]
-  uint32_t* tslot = wflag + 8;
+  uint32_t* meta = reinterpret_cast<uint32_t*>(smem + Cfg::off_misc);   // [kNS + kNA]
+  uint32_t* wflag = meta + Cfg::kNS + kNA;                               // [2][2][4]
+  uint32_t* tslot = wflag + 16;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   pdl_trigger();
 
   // ---- setup
   for (int i = tid; i < Cfg::kB / 16; i += kProjThreads) reinterpret_cast<uint4*>(sB)[i] = __ldg(a.Bpack + i);
-  for (int i = tid; i < Cfg::kZero / 16; i += kProjThreads) reinterpret_cast<uint4*>(sZ)[i] = make_uint4(0, 0, 0, 0);
   if (tid == 0) {
-    for (int i = 0; i < Cfg::kNS; ++i) { mbar_init(&raw_full[i], 1); mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    mbar_init(p1_empty, 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(&acc1_full[i], 1); mbar_init(&acc1_empty[i], 4); }
+    for (int i = 0; i < Cfg::kNS; ++i) { mbar_init(&raw_full[i], 1); mbar_init(&raw_empty[i], 1); }
+    for (int i = 0; i < kNA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
+    mbar_init(&p1_empty[0], 1);
+    mbar_init(&p1_empty[1], 1);
+    for (int i = 0; i < Cfg::kNAcc; ++i) { mbar_init(&acc1_full[i], 1); mbar_init(&acc1_empty[i], 4); }
     mbar_init(a2_full, 1);
     mbar_init(s2_done, 1);
     fence_mbar_init();
@@ -185,36 +222,40 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     // ================= stage-1 MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_f16(128, Cfg::kN);
-      const uint32_t ring0 = smem_u32(ring), p10 = smem_u32(sP1), b0 = smem_u32(sB), z0 = smem_u32(sZ);
-      uint32_t slot = 0, sphase = 0, tile = 0, p1_uses = 0;
+      const uint32_t ring0 = smem_u32(ring), p10 = smem_u32(sP1), b0 = smem_u32(sB);
+      uint32_t slot = 0, sphase = 0, tile = 0, job = 0;
       for (int64_t gi = 0; gi < my_groups; ++gi) {
         for (int tt = 0; tt < tpg; ++tt, ++tile) {
-          const uint32_t s1 = tile & 1u;
-          mbar_wait(&acc1_empty[s1], ((tile >> 1) & 1u) ^ 1u);
+          const uint32_t s1 = tile % Cfg::kNAcc;
+          mbar_wait(&acc1_empty[s1], ((tile / Cfg::kNAcc) & 1u) ^ 1u);
+          TRACE(6, tile);
           tc_fence_after();
-          const uint32_t acc = tbase + s1 * Cfg::kAcc1;
-          bool p1 = false;
-          for (int c = 0; c < Cfg::kCPT; ++c) {
-            mbar_wait(&full[slot], sphase);
+          const uint32_t acc = tbase + Cfg::tAcc1 + s1 * Cfg::kAcc1;
+          for (int c = 0; c < Cfg::kCPT; ++c, ++job) {
+            const uint32_t grp = job & 1u;
+            mbar_wait(U16 ? &a_full[slot] : &raw_full[slot], sphase);
+            TRACE(5, slot);
             tc_fence_after();
             const bool has_p1 = meta[slot] & 1u;
-#pragma unroll 1
-            for (int plane = 0; plane < (has_p1 ? 2 : 1); ++plane) {
-              const uint32_t sa = plane == 0 ? ring0 + slot * Cfg::kSlot : p10;
+#pragma unroll
+            for (int kk = 0; kk < Cfg::kKC / 16; ++kk) {
+              const uint64_t bd = smem_desc_noswz(b0 + (c * (Cfg::kKC / 8) + 2 * kk) * Cfg::kLBO_B, Cfg::kLBO_B, 128);
+              const uint32_t accum = (c > 0 || kk > 0) ? 1u : 0u;
+              if constexpr (U16) mma_f16_ts(acc, tbase + Cfg::tA + slot * Cfg::kACols + kk * 8, bd, idesc, accum);
+              else mma_f16_ss(acc, smem_desc_noswz(ring0 + slot * Cfg::kSlot + 2 * kk * kLBO, kLBO, 128), bd, idesc, accum);
+            }
+            if (has_p1) {
 #pragma unroll
               for (int kk = 0; kk < Cfg::kKC / 16; ++kk) {
-                const uint64_t ad = U16 ? smem_desc_sw(sa + kk * 32, 8 * Cfg::kSpan, Cfg::kSwz)
-                                        : smem_desc_noswz(sa + 2 * kk * kLBO, kLBO, 128);
                 const uint64_t bd = smem_desc_noswz(b0 + (c * (Cfg::kKC / 8) + 2 * kk) * Cfg::kLBO_B, Cfg::kLBO_B, 128);
-                const uint32_t accum = plane == 0 ? (c > 0 || kk > 0) : (p1 || kk > 0);
-                mma_f16_ss(acc + plane * Cfg::kN, ad, bd, idesc, accum);
+                if constexpr (U16) mma_f16_ts(acc, tbase + Cfg::tP1 + grp * Cfg::kACols + kk * 8, bd, idesc, 1u);
+                else mma_f16_ss(acc, smem_desc_noswz(p10 + grp * Cfg::kSlot + 2 * kk * kLBO, kLBO, 128), bd, idesc, 1u);
               }
+              mma_commit(&p1_empty[grp]);
             }
-            if (has_p1) { p1 = true; mma_commit(p1_empty); ++p1_uses; }
-            mma_commit(&empty[slot]);
-            if (++slot == Cfg::kNS) { slot = 0; sphase ^= 1u; }
+            mma_commit(U16 ? &a_empty[slot] : &raw_empty[slot]);
+            if (++slot == (U16 ? kNA : Cfg::kNS)) { slot = 0; sphase ^= 1u; }
           }
-          if (!p1) mma_f16_ss(acc + Cfg::kN, smem_desc_noswz(z0, 2048, 128), smem_desc_noswz(b0, Cfg::kLBO_B, 128), idesc, 0u);
           mma_commit(&acc1_full[s1]);
         }
       }
@@ -224,11 +265,12 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_f16(128, Cfg::kN);
       const uint32_t a20 = smem_u32(sA2), b0 = smem_u32(sB);
-      const uint32_t acc2 = tbase + 2 * Cfg::kAcc1;
+      const uint32_t acc2 = tbase + Cfg::tAcc2;
       uint32_t phase = 0;
       for (int64_t gi = 0; gi < my_groups; ++gi) {
         for (int h = 0; h < Cfg::kTPF; ++h, phase ^= 1u) {
           mbar_wait(a2_full, phase);
+          TRACE(12, h);
           tc_fence_after();
 #pragma unroll 1
           for (int plane = 0; plane < 2; ++plane) {
@@ -254,7 +296,8 @@ __global__ void __launch_bounds__(kProjThreads, 1)
           int valid;
           tile_coords<Q, L, U16>(g, tt, g2, n, row0, valid);
           for (int c = 0; c < Cfg::kCPT; ++c) {
-            mbar_wait(&empty[slot], sphase ^ 1u);
+            mbar_wait(&raw_empty[slot], sphase ^ 1u);
+            TRACE(2, slot);
             mbar_arrive_expect_tx(&raw_full[slot], Cfg::kSlotU);
             tma_load_2d(ring + slot * Cfg::kSlot, &tmap, c * Cfg::kKC, (int)row0, &raw_full[slot]);
             if (++slot == Cfg::kNS) { slot = 0; sphase ^= 1u; }
@@ -262,11 +305,16 @@ __global__ void __launch_bounds__(kProjThreads, 1)
         }
       }
     }
-  } else if (warp < 7) {
-    // ================= converters (128 threads)
-    const int ct = tid - 96;
-    const int cw = warp - 3;
-    uint32_t slot = 0, sphase = 0, job = 0, p1_uses = 0;
+  } else if (warp < 11) {
+    // ================= converters: group cg handles the jobs (chunks) with job % 2 == cg
+    const int cg = (warp - 3) >> 2;
+    const int ct = tid - 96 - cg * kConv;
+    const int cw = (warp - 3) & 3;
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;                     // detector row of the tile == TMEM lane
+    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+    const int bar_id = 1 + 2 * cg;                        // named barriers 1 and 3 (2 = epilogue)
+    uint32_t p1_uses = 0, job = 0;
     for (int64_t gi = 0; gi < my_groups; ++gi) {
       const int64_t g = blockIdx.x + gi * gridDim.x;
       for (int tt = 0; tt < tpg; ++tt) {
@@ -274,58 +322,74 @@ __global__ void __launch_bounds__(kProjThreads, 1)
         int valid;
         tile_coords<Q, L, U16>(g, tt, g2, n, row0, valid);
         for (int c = 0; c < Cfg::kCPT; ++c, ++job) {
-          uint8_t* dst = ring + slot * Cfg::kSlot;
+          if ((job & 1u) != (uint32_t)cg) continue;
+          const uint32_t slot = job % Cfg::kNS, sphase = (job / Cfg::kNS) & 1u;
+          const uint32_t aslot = job % kNA, aphase = (job / kNA) & 1u;
           bool resid = false;
+          uint32_t* wf = wflag + cg * 8 + ((job >> 1) & 1) * 4;
           if constexpr (U16) {
-            // in place: 128 rows x kSpan bytes; piece p = ct + 128 i (any 16-B piece maps to itself)
-            constexpr int kPieces = Cfg::kSlotU / 16 / kConv;
-            uint4 hiw[kPieces];
+            constexpr int kW = Cfg::kACols;               // 32-bit words of this row in the chunk
+            const uint8_t* src = ring + slot * Cfg::kSlot;
+            uint32_t w[kW];
             mbar_wait(&raw_full[slot], sphase);
+            if (ct == 0) TRACE(3, slot);
 #pragma unroll
-            for (int i = 0; i < kPieces; ++i) {
-              uint4* p = reinterpret_cast<uint4*>(dst) + ct + kConv * i;
-              const uint4 v = *p;
-              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-              uint4 o, h;
-              uint32_t* op = reinterpret_cast<uint32_t*>(&o);
-              uint32_t* hp = reinterpret_cast<uint32_t*>(&h);
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                resid |= (w[q] & 0xFC00FC00u) != 0u;
-                op[q] = magic_half2(w[q] & 0x03FF03FFu);
-                hp[q] = w[q] & 0xFC00FC00u;   // raw high bits, converted only if needed
-              }
-              *p = o;
-              hiw[i] = h;
+            for (int j = 0; j < kW / 4; ++j) {           // swizzled 16-byte pieces of row `row`
+              int off = row * Cfg::kSpan + j * 16;
+              off ^= ((off >> 7) & Cfg::kSwzMask) << 4;
+              const uint4 v = *reinterpret_cast<const uint4*>(src + off);
+              w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
             }
+            uint32_t hi_or = 0;
+#pragma unroll
+            for (int q = 0; q < kW; ++q) hi_or |= w[q];
+            resid = (hi_or & 0xFC00FC00u) != 0u;
+#pragma unroll
+            for (int q = 0; q < kW; ++q) w[q] = magic_half2(w[q] & 0x03FF03FFu) | 0u;
+            mbar_wait(&a_empty[aslot], aphase ^ 1u);
+            tc_fence_after();
+#pragma unroll
+            for (int q = 0; q < kW; q += 16) tmem_st16(tbase + lane_addr + Cfg::tA + aslot * Cfg::kACols + q, w + q);
+            tmem_st_wait();
             const uint32_t bal = __ballot_sync(0xffffffffu, resid);
-            uint32_t* wf = wflag + (job & 1) * 4;
             if (lane == 0) wf[cw] = bal ? 1u : 0u;
-            fence_proxy_async_smem();
-            named_sync(1, kConv);
+            tc_fence_before();
+            named_sync(bar_id, kConv);
             const bool any = (wf[0] | wf[1] | wf[2] | wf[3]) != 0u;
-            if (any) {
-              mbar_wait(p1_empty, (p1_uses & 1u) ^ 1u);
+            if (any) {  // bits 10-15 of the counts: second plane
+              mbar_wait(&p1_empty[cg], (p1_uses & 1u) ^ 1u);
               ++p1_uses;
+              tc_fence_after();
 #pragma unroll
-              for (int i = 0; i < kPieces; ++i) {
-                const uint32_t w[4] = {hiw[i].x, hiw[i].y, hiw[i].z, hiw[i].w};
-                uint4 o;
-                uint32_t* op = reinterpret_cast<uint32_t*>(&o);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) op[q] = magic_half2(w[q] >> 10);
-                reinterpret_cast<uint4*>(sP1)[ct + kConv * i] = o;
+              for (int j = 0; j < kW / 4; ++j) {
+                int off = row * Cfg::kSpan + j * 16;
+                off ^= ((off >> 7) & Cfg::kSwzMask) << 4;
+                const uint4 v = *reinterpret_cast<const uint4*>(src + off);
+                // (bits 10-15) * 1024 is exact in fp16 (<= 64512): accumulates into the same acc
+                w[4 * j] = hi_plane(v.x);
+                w[4 * j + 1] = hi_plane(v.y);
+                w[4 * j + 2] = hi_plane(v.z);
+                w[4 * j + 3] = hi_plane(v.w);
               }
-              fence_proxy_async_smem();
-              named_sync(1, kConv);
+#pragma unroll
+              for (int q = 0; q < kW; q += 16) tmem_st16(tbase + lane_addr + Cfg::tP1 + cg * Cfg::kACols + q, w + q);
+              tmem_st_wait();
+              tc_fence_before();
+              named_sync(bar_id, kConv);
             }
-            if (ct == 0) { meta[slot] = any ? 1u : 0u; mbar_arrive(&full[slot]); }
+            if (ct == 0) {
+              mbar_arrive(&raw_empty[slot]);            // raw slot fully read
+              meta[aslot] = any ? 1u : 0u;
+              mbar_arrive(&a_full[aslot]);
+              TRACE(4, aslot);
+            }
           } else {
-            // f32: LDG -> fp16(x) (+ residual plane) into a no-swizzle K-major slot
+            // f32: LDG -> fp16(x) (+ residual plane) into a no-swizzle K-major smem slot
             constexpr int kPPR = Cfg::kKC / 8;              // 16-B fp16 pieces per row
             constexpr int kPieces = 128 * kPPR / kConv;
+            uint8_t* dst = ring + slot * Cfg::kSlot;
             uint4 lo[kPieces];
-            mbar_wait(&empty[slot], sphase ^ 1u);
+            mbar_wait(&raw_empty[slot], sphase ^ 1u);
 #pragma unroll
             for (int i = 0; i < kPieces; ++i) {
               const int p = ct + kConv * i, r = p / kPPR, j = p % kPPR;
@@ -351,35 +415,33 @@ __global__ void __launch_bounds__(kProjThreads, 1)
               lo[i] = l;
             }
             const uint32_t bal = __ballot_sync(0xffffffffu, resid);
-            uint32_t* wf = wflag + (job & 1) * 4;
             if (lane == 0) wf[cw] = bal ? 1u : 0u;
             fence_proxy_async_smem();
-            named_sync(1, kConv);
+            named_sync(bar_id, kConv);
             const bool any = (wf[0] | wf[1] | wf[2] | wf[3]) != 0u;
             if (any) {
-              mbar_wait(p1_empty, (p1_uses & 1u) ^ 1u);
+              mbar_wait(&p1_empty[cg], (p1_uses & 1u) ^ 1u);
               ++p1_uses;
 #pragma unroll
               for (int i = 0; i < kPieces; ++i) {
                 const int p = ct + kConv * i, r = p / kPPR, j = p % kPPR;
-                *reinterpret_cast<uint4*>(sP1 + j * kLBO + (r >> 3) * 128 + (r & 7) * 16) = lo[i];
+                *reinterpret_cast<uint4*>(sP1 + cg * Cfg::kSlot + j * kLBO + (r >> 3) * 128 + (r & 7) * 16) = lo[i];
               }
               fence_proxy_async_smem();
-              named_sync(1, kConv);
+              named_sync(bar_id, kConv);
             }
-            if (ct == 0) { meta[slot] = any ? 1u : 0u; mbar_arrive(&full[slot]); }
+            if (ct == 0) { meta[slot] = any ? 1u : 0u; mbar_arrive(&raw_full[slot]); }
           }
-          if (++slot == Cfg::kNS) { slot = 0; sphase ^= 1u; }
         }
       }
     }
   } else {
     // ================= epilogue (128 threads; TMEM lane quadrant = warp % 4)
-    const int et = tid - 224;
+    const int et = tid - 352;
     const int quad = warp & 3;
     const int row = quad * 32 + lane;                    // TMEM lane == tile row == A2 m index
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    const uint32_t acc2 = tbase + 2 * Cfg::kAcc1 + lane_addr;
+    const uint32_t acc2 = tbase + Cfg::tAcc2 + lane_addr;
     uint32_t tile = 0, s2_issued = 0;
     int64_t pending = -1;   // frame0 of a group whose stage-2 result has not been stored yet
     auto stage2_epilogue = [&](int64_t frame0) {
@@ -388,7 +450,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
       const int f = row / L, aa = row % L;
       const int64_t fg = frame0 + f;
       if (f < g2 && fg < n) {
-        float* dst = a.C + fg * K + aa * L;
+        float* dst = a.C + (a.idx ? (int64_t)__ldg(a.idx + fg) : fg) * K + aa * L;
 #pragma unroll
         for (int b = 0; b < L; b += 4) {
           float4 v = make_float4((d[b] + d[L + b]) * a.sc2, (d[b + 1] + d[L + b + 1]) * a.sc2,
@@ -400,18 +462,15 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     for (int64_t gi = 0; gi < my_groups; ++gi) {
       const int64_t g = blockIdx.x + gi * gridDim.x;
       for (int tt = 0; tt < tpg; ++tt, ++tile) {
-        const uint32_t s1 = tile & 1u;
-        mbar_wait(&acc1_full[s1], (tile >> 1) & 1u);
+        const uint32_t s1 = tile % Cfg::kNAcc;
+        mbar_wait(&acc1_full[s1], (tile / Cfg::kNAcc) & 1u);
+        if (et == 0) TRACE(8, tile);
         tc_fence_after();
         float acc[Cfg::kN];
         float t[L];
-        const uint32_t aaddr = tbase + s1 * Cfg::kAcc1 + lane_addr;
-        tmem_ld_cols<Cfg::kN>(aaddr, acc);
+        tmem_ld_cols<Cfg::kN>(tbase + Cfg::tAcc1 + s1 * Cfg::kAcc1 + lane_addr, acc);
 #pragma unroll
-        for (int q = 0; q < L; ++q) t[q] = acc[q] + acc[L + q];
-        tmem_ld_cols<Cfg::kN>(aaddr + Cfg::kN, acc);
-#pragma unroll
-        for (int q = 0; q < L; ++q) t[q] = fmaf(kRes, acc[q] + acc[L + q], t[q]) * a.sc1;
+        for (int q = 0; q < L; ++q) t[q] = (acc[q] + acc[L + q]) * a.sc1;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc1_empty[s1]);
@@ -424,7 +483,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
         int f, k;
         if constexpr (Q >= 128) { f = tt % g2; k = row; }
         else { f = tt * Cfg::kFPT + row / Q; k = row % Q; }
-        if (Q >= 128 || row < Cfg::kFPT * Q) {
+        {
           uint8_t* base = sA2 + (k >> 3) * kLBO + (k & 7) * 2;
 #pragma unroll
           for (int q = 0; q < L; ++q) {
@@ -436,10 +495,11 @@ __global__ void __launch_bounds__(kProjThreads, 1)
             *reinterpret_cast<__half*>(p + Cfg::kA2) = lo;
           }
         }
+        if (et == 0) TRACE(10, tile);
         if (tt % tph == tph - 1) {   // stage-2 K chunk complete
           fence_proxy_async_smem();
           named_sync(2, 128);
-          if (et == 0) mbar_arrive(a2_full);
+          if (et == 0) { mbar_arrive(a2_full); TRACE(11, tile); }
           ++s2_issued;
         }
       }
@@ -471,7 +531,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 template <int Q, int L, bool U16>
-static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n, float* C, cudaStream_t st) {
+static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n, float* C, const int32_t* idx,
+                                    cudaStream_t st) {
   using Cfg = ProjCfg<Q, L, U16>;
   auto kern = project_kernel<Q, L, U16>;
   static bool init = false;
@@ -507,7 +568,7 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
-  ProjArgs a{frames, n, C, g2, reinterpret_cast<const uint4*>(p.d_Bpack), (float)p.sc1, (float)p.sc2};
+  ProjArgs a{frames, n, C, idx, g2, reinterpret_cast<const uint4*>(p.d_Bpack), (float)p.sc1, (float)p.sc2};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kProjThreads);
@@ -523,16 +584,28 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
 
 #define WDD_PROJ_CASE(QQ, LL)                                                          \
   if (p.Q == QQ && p.L == LL)                                                          \
-    return p.dtype == 0 ? launch_project_t<QQ, LL, true>(p, frames, n, C, st)          \
-                        : launch_project_t<QQ, LL, false>(p, frames, n, C, st);
+    return p.dtype == 0 ? launch_project_t<QQ, LL, true>(p, frames, n, C, idx, st)     \
+                        : launch_project_t<QQ, LL, false>(p, frames, n, C, idx, st);
 
-cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* C, cudaStream_t st) {
+cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* C, const int32_t* idx,
+                           cudaStream_t st) {
   WDD_PROJ_CASE(32, 8) WDD_PROJ_CASE(32, 16) WDD_PROJ_CASE(32, 32)
   WDD_PROJ_CASE(64, 8) WDD_PROJ_CASE(64, 16) WDD_PROJ_CASE(64, 32)
   WDD_PROJ_CASE(128, 8) WDD_PROJ_CASE(128, 16) WDD_PROJ_CASE(128, 24) WDD_PROJ_CASE(128, 32)
   WDD_PROJ_CASE(256, 8) WDD_PROJ_CASE(256, 16) WDD_PROJ_CASE(256, 24) WDD_PROJ_CASE(256, 32)
   return cudaErrorInvalidValue;
 }
+
+#ifdef WDD_TRACE
+extern "C" int wdd_trace_dump(unsigned long long* host, int max_n) {
+  cudaDeviceSynchronize();
+  const int n = max_n < 16 * 4096 ? max_n : 16 * 4096;
+  cudaMemcpyFromSymbol(host, g_trace, n * sizeof(unsigned long long));
+  static unsigned long long zeros[16 * 4096];
+  cudaMemcpyToSymbol(g_trace, zeros, sizeof zeros);
+  return n;
+}
+#endif
 
 size_t project_smem_bytes(int Q, int L) {
 #define WDD_SMEM_CASE(QQ, LL) if (Q == QQ && L == LL) return ProjCfg<QQ, LL, true>::smem;
@@ -566,111 +639,101 @@ void pack_basis_fp16(const Plan& p, std::vector<uint16_t>& out, double& scale) {
 }
 
 // =====================================================================================
-// Row DFT (a4): R[j][sy][k] (+)= sum_{frames of row sy in chunk} Fx[j][sx] C[p][k]
-// Tile: 16 active-vx columns j x 64 coefficients k of one scan row; 128 threads, 2 j x 4 k each.
+// Row DFT (a4), run at flush time for every scan row with unflushed coefficients:
+//   R[j][sy][k] = sum_sx Fx[j][sx] C[sy*Sx + sx][k]      (zeros stand for frames not ingested)
+// Tile: 16 active-vx columns j x 64 coefficients k of one scan row, 256 threads (2 j x 2 k each).
+// Entries are staged 128 at a time (C 32 KB + twiddles 16 KB of shared memory) with all loads of
+// a stage in flight at once; the next stage is prefetched into registers during the multiply.
 // =====================================================================================
-__global__ void __launch_bounds__(128) rowdft_kernel(const float* __restrict__ C, RowSource rs,
+constexpr int kRdE = 128;                                  // entries per stage
+constexpr int kRdSmem = kRdE * 64 * 4 + 16 * kRdE * 8;     // 48 KB
+
+__global__ void __launch_bounds__(256) rowdft_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
                                                      const float2* __restrict__ Fx, float2* __restrict__ R,
-                                                     int Sx, int Sy, int K, int n_vx, int early) {
-  // PDL: the projection grid of this chunk (and, transitively, the previous row DFT) must be
-  // complete before C is read and R rows are written.  With C indexed by scan position
-  // (contiguous chunks) the next projection may start right away (early trigger).
-  if (early) pdl_trigger();
-  pdl_wait();
-  if (!early) pdl_trigger();
-  __shared__ __align__(16) float Cs[32][64];
-  __shared__ float2 Fs[16][33];
-  const int t = threadIdx.x, kq = (t & 15) * 4, jg = t >> 4;
-  const int k0 = blockIdx.x * 64, j0 = blockIdx.y * 16, r = blockIdx.z;
-  int sy, count, mode, pb = 0, eb = 0, sx0 = 0;
-  if (rs.contiguous) {
-    const int sy0 = rs.s0 / Sx;
-    sx0 = rs.s0 % Sx;
-    sy = sy0 + r;
-    pb = max(0, r * Sx - sx0);
-    const int pe = min(rs.n, (r + 1) * Sx - sx0);
-    count = pe - pb;
-    mode = r == 0 ? rs.mode_first : (r == rs.n_rows - 1 ? rs.mode_last : 0);
-  } else {
-    const int4 ri = rs.rows[r];
-    sy = ri.x;
-    eb = ri.y;
-    count = ri.z;
-    mode = ri.w;
-  }
-  float2 acc[2][4];
+                                                     int Sx, int Sy, int K, int n_vx) {
+  extern __shared__ __align__(16) uint8_t rd_smem[];
+  float* Cs = reinterpret_cast<float*>(rd_smem);                       // [kRdE][64]
+  float2* Fs = reinterpret_cast<float2*>(rd_smem + kRdE * 64 * 4);     // [16][kRdE]
+  const int t = threadIdx.x, kq = (t & 31) * 2, jg = t >> 5;           // k pair, j pair (0..7)
+  const int k0 = blockIdx.x * 64, j0 = blockIdx.y * 16;
+  const int sy = rows[blockIdx.z];
+  const float* Crow = C + (int64_t)sy * Sx * K + k0;
+  float4 cv[8];   // 128 entries x 64 k / 256 threads = 8 float4
+  float2 fv[8];   // 16 j x 128 entries / 256 threads = 8 float2
+  auto load = [&](int e0) {
+    const int ne = min(kRdE, Sx - e0);
 #pragma unroll
-  for (int q = 0; q < 2; ++q)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) acc[q][e] = make_float2(0.f, 0.f);
-  for (int e0 = 0; e0 < count; e0 += 32) {
-    const int ne = min(32, count - e0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {          // 32 entries x 64 k as float4: 512 / 128 threads
-      const int idx = t + 128 * i, ee = idx >> 4, kk = (idx & 15) * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (ee < ne) {
-        const int p = rs.contiguous ? pb + e0 + ee : rs.ent[eb + e0 + ee].x;
-        v = __ldg(reinterpret_cast<const float4*>(C + (int64_t)p * K + k0 + kk));
-      }
-      *reinterpret_cast<float4*>(&Cs[ee][kk]) = v;
+    for (int i = 0; i < 8; ++i) {
+      const int idx = t + 256 * i;
+      const int ee = idx >> 4, kk = (idx & 15) * 4;
+      cv[i] = ee < ne ? __ldg(reinterpret_cast<const float4*>(Crow + (int64_t)(e0 + ee) * K + kk))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int jj = idx >> 7, e2 = idx & (kRdE - 1);
+      fv[i] = (e2 < ne && j0 + jj < n_vx) ? __ldg(Fx + (int64_t)(j0 + jj) * Sx + e0 + e2) : make_float2(0.f, 0.f);
     }
+  };
+  load(0);
+  float2 acc[2][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {          // 16 j x 32 entries
-      const int idx = t + 128 * i, jj = idx >> 5, ee = idx & 31;
-      float2 v = make_float2(0.f, 0.f);
-      if (ee < ne && j0 + jj < n_vx) {
-        const int sx = rs.contiguous ? sx0 + pb + e0 + ee - r * Sx : rs.ent[eb + e0 + ee].y;
-        v = __ldg(Fx + (int64_t)(j0 + jj) * Sx + sx);
-      }
-      Fs[jj][ee] = v;
+  for (int q = 0; q < 2; ++q) acc[q][0] = acc[q][1] = make_float2(0.f, 0.f);
+  for (int e0 = 0; e0 < Sx; e0 += kRdE) {
+    const int ne = min(kRdE, Sx - e0);
+    __syncthreads();   // previous stage fully consumed
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = t + 256 * i;
+      *reinterpret_cast<float4*>(Cs + (idx >> 4) * 64 + (idx & 15) * 4) = cv[i];
+      Fs[(idx >> 7) * kRdE + (idx & (kRdE - 1))] = fv[i];
     }
     __syncthreads();
+    if (e0 + kRdE < Sx) load(e0 + kRdE);   // prefetch while computing
+    const float2* f0 = Fs + (jg * 2) * kRdE;
+    const float2* f1 = f0 + kRdE;
+#pragma unroll 4
     for (int ee = 0; ee < ne; ++ee) {
-      const float4 c = *reinterpret_cast<const float4*>(&Cs[ee][kq]);
-      const float cv[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const float2 f = Fs[jg * 2 + q][ee];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          acc[q][e].x = fmaf(f.x, cv[e], acc[q][e].x);
-          acc[q][e].y = fmaf(f.y, cv[e], acc[q][e].y);
-        }
-      }
+      const float2 c = *reinterpret_cast<const float2*>(Cs + ee * 64 + kq);
+      const float2 a = f0[ee], b = f1[ee];
+      acc[0][0].x = fmaf(a.x, c.x, acc[0][0].x); acc[0][0].y = fmaf(a.y, c.x, acc[0][0].y);
+      acc[0][1].x = fmaf(a.x, c.y, acc[0][1].x); acc[0][1].y = fmaf(a.y, c.y, acc[0][1].y);
+      acc[1][0].x = fmaf(b.x, c.x, acc[1][0].x); acc[1][0].y = fmaf(b.y, c.x, acc[1][0].y);
+      acc[1][1].x = fmaf(b.x, c.y, acc[1][1].x); acc[1][1].y = fmaf(b.y, c.y, acc[1][1].y);
     }
-    __syncthreads();
   }
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int j = j0 + jg * 2 + q;
     if (j >= n_vx) continue;
-    float4* ptr = reinterpret_cast<float4*>(R + ((int64_t)j * Sy + sy) * K + k0 + kq);
-    float4 a0 = make_float4(acc[q][0].x, acc[q][0].y, acc[q][1].x, acc[q][1].y);
-    float4 a1 = make_float4(acc[q][2].x, acc[q][2].y, acc[q][3].x, acc[q][3].y);
-    if (mode) {
-      const float4 o0 = ptr[0], o1 = ptr[1];
-      a0.x += o0.x; a0.y += o0.y; a0.z += o0.z; a0.w += o0.w;
-      a1.x += o1.x; a1.y += o1.y; a1.z += o1.z; a1.w += o1.w;
-    }
-    ptr[0] = a0;
-    ptr[1] = a1;
+    *reinterpret_cast<float4*>(R + ((int64_t)j * Sy + sy) * K + k0 + kq) =
+        make_float4(acc[q][0].x, acc[q][0].y, acc[q][1].x, acc[q][1].y);
   }
 }
 
-cudaError_t launch_rowdft(const Plan& p, const float* C, const RowSource& rs, cudaStream_t st) {
-  if (rs.n_rows <= 0) return cudaSuccess;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.K / 64, (p.n_vx + 15) / 16, rs.n_rows);
-  cfg.blockDim = dim3(128);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, rowdft_kernel, C, rs, (const float2*)p.d_Fx, p.d_R, p.Sx, p.Sy, p.K, p.n_vx,
-                            rs.contiguous);
+cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st) {
+  if (n_rows <= 0) return cudaSuccess;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(rowdft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRdSmem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  dim3 grid(p.K / 64, (p.n_vx + 15) / 16, n_rows);
+  rowdft_kernel<<<grid, 256, kRdSmem, st>>>(p.d_Call, rows, p.d_Fx, p.d_R, p.Sx, p.Sy, p.K, p.n_vx);
+  return cudaGetLastError();
+}
+
+// Zero the listed scan rows of C (their coefficients have been folded into G).
+__global__ void zero_rows_kernel(float* __restrict__ C, const int32_t* __restrict__ rows, int64_t row_floats) {
+  float4* dst = reinterpret_cast<float4*>(C + (int64_t)rows[blockIdx.y] * row_floats);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < row_floats / 4; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+cudaError_t launch_zero_rows(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st) {
+  if (n_rows <= 0) return cudaSuccess;
+  const int64_t rf = (int64_t)p.Sx * p.K;
+  dim3 grid((unsigned)std::min<int64_t>((rf / 4 + 255) / 256, 64), n_rows);
+  zero_rows_kernel<<<grid, 256, 0, st>>>(p.d_Call, rows, rf);
+  return cudaGetLastError();
 }
 
 // =====================================================================================

@@ -304,76 +304,34 @@ wdd_status validate_and_mark(Plan& p, const int32_t* idx, int64_t n) {
   return WDD_OK;
 }
 
-// Enqueue projection + row DFT for one chunk of already-validated frames.
+// Enqueue the projection of one chunk of already-validated frames; its coefficients land in
+// d_Call at their scan positions (the row DFT of completed rows happens at flush time).
 wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, int64_t nc) {
   cudaStream_t st = p.stream;
   bool contiguous = true;
   for (int64_t i = 1; i < nc && contiguous; ++i) contiguous = idx[i] == idx[0] + i;
-  // contiguous chunks write C at their scan positions (no buffer reuse within an acquisition, so
-  // consecutive chunks may overlap under PDL); other chunks use an alternating scratch buffer
-  float* C;
+  float* C = p.d_Call;
+  const int32_t* d_idx = nullptr;
   if (contiguous) {
-    C = p.d_Call + (size_t)idx[0] * p.K;
+    C += (size_t)idx[0] * p.K;
   } else {
-    C = p.d_C[p.c_parity];
-    p.c_parity ^= 1;
+    void* d = nullptr;
+    wdd_status s = upload_meta(p, idx, (size_t)nc * sizeof(int32_t), &d);
+    if (s != WDD_OK) return s;
+    d_idx = static_cast<const int32_t*>(d);
   }
   {
     Prof pr(p, kSlotProject, st);
-    CUDA_TRY(launch_project(p, frames_dev, nc, C, st));
+    CUDA_TRY(launch_project(p, frames_dev, nc, C, d_idx, st));
   }
-  RowSource rs{};
-  rs.n = (int)nc;
-  if (contiguous) {
-    rs.contiguous = 1;
-    rs.s0 = idx[0];
-    const int sy0 = idx[0] / p.Sx, sy1 = idx[nc - 1] / p.Sx;
-    rs.n_rows = sy1 - sy0 + 1;
-    rs.mode_first = p.row_dirty[sy0];
-    rs.mode_last = p.row_dirty[sy1];
-    for (int sy = sy0; sy <= sy1; ++sy) p.row_dirty[sy] = 1;
-  } else {
-    // counting sort of chunk positions by scan row
-    std::vector<int> cnt(p.Sy + 1, 0);
-    for (int64_t i = 0; i < nc; ++i) cnt[idx[i] / p.Sx + 1]++;
-    for (int r = 0; r < p.Sy; ++r) cnt[r + 1] += cnt[r];
-    // device table: rows (int4, 16-byte aligned) first, then the entries (int2)
-    std::vector<int4> rows;
-    std::vector<int2> ent((size_t)nc);
-    std::vector<int> fillp(cnt.begin(), cnt.end() - 1);
-    for (int64_t i = 0; i < nc; ++i) {
-      const int sy = idx[i] / p.Sx;
-      ent[fillp[sy]++] = make_int2((int)i, idx[i] % p.Sx);
-    }
-    for (int sy = 0; sy < p.Sy; ++sy) {
-      const int c = cnt[sy + 1] - cnt[sy];
-      if (!c) continue;
-      rows.push_back(make_int4(sy, cnt[sy], c, p.row_dirty[sy]));
-      p.row_dirty[sy] = 1;
-    }
-    const size_t rb = rows.size() * sizeof(int4), eb = ent.size() * sizeof(int2);
-    std::vector<uint8_t> buf(rb + eb);
-    std::memcpy(buf.data(), rows.data(), rb);
-    std::memcpy(buf.data() + rb, ent.data(), eb);
-    void* d = nullptr;
-    wdd_status s = upload_meta(p, buf.data(), buf.size(), &d);
-    if (s != WDD_OK) return s;
-    const int nr = (int)rows.size();
-    rs.contiguous = 0;
-    rs.n_rows = nr;
-    rs.rows = reinterpret_cast<const int4*>(d);
-    rs.ent = reinterpret_cast<const int2*>(static_cast<uint8_t*>(d) + rb);
-  }
-  {
-    Prof pr(p, kSlotRowDft, st);
-    CUDA_TRY(launch_rowdft(p, C, rs, st));
-  }
+  for (int64_t i = 0; i < nc; ++i) p.row_dirty[idx[i] / p.Sx] = 1;
   return WDD_OK;
 }
 
 size_t frame_bytes(const Plan& p) { return (size_t)p.Q * p.Q * (p.dtype == 0 ? 2 : 4); }
 
-// Flush staged rows into G (a5).
+// Flush: row DFT of every row with unflushed coefficients (a4), zero those coefficient rows,
+// then the phase-weighted rank update of G over the same rows (a5).
 wdd_status flush(Plan& p) {
   std::vector<int32_t> rows;
   for (int sy = 0; sy < p.Sy; ++sy)
@@ -382,9 +340,18 @@ wdd_status flush(Plan& p) {
   void* d = nullptr;
   wdd_status s = upload_meta(p, rows.data(), rows.size() * sizeof(int32_t), &d);
   if (s != WDD_OK) return s;
+  const int32_t* dr = static_cast<const int32_t*>(d);
+  {
+    Prof pr(p, kSlotRowDft, p.stream);
+    CUDA_TRY(launch_rowdft(p, dr, (int)rows.size(), p.stream));
+  }
   {
     Prof pr(p, kSlotFlush, p.stream);
-    CUDA_TRY(launch_flush(p, static_cast<const int32_t*>(d), (int)rows.size(), p.stream));
+    CUDA_TRY(launch_zero_rows(p, dr, (int)rows.size(), p.stream));
+  }
+  {
+    Prof pr(p, kSlotFlush, p.stream);
+    CUDA_TRY(launch_flush(p, dr, (int)rows.size(), p.stream));
   }
   for (int32_t sy : rows) p.row_dirty[sy] = 0;
   return WDD_OK;
@@ -396,7 +363,7 @@ void free_plan(Plan* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   cudaDeviceSynchronize();
   if (p->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(p->nccl));
-  void* bufs[] = {p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_C[0], p->d_C[1], p->d_Call,
+  void* bufs[] = {p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
                   p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec,
                   p->d_meta, p->d_stage[0], p->d_stage[1]};
   for (void* b : bufs)
@@ -532,7 +499,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   std::vector<float> psi32(p->basis.begin(), p->basis.end());
   std::vector<int32_t> vpos(act.begin(), act.end());
   p->chunk_cap = 8192;
-  p->meta_slot_bytes = std::max((size_t)p->chunk_cap * (sizeof(int2) + sizeof(int4)), (size_t)Sy * 4);
+  p->meta_slot_bytes = std::max((size_t)p->chunk_cap, (size_t)Sy) * sizeof(int32_t);
   p->seen.assign((size_t)(p->S + 63) / 64, 0);
   p->row_dirty.assign(Sy, 0);
 
@@ -548,8 +515,6 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   if (p->combine == 1) ALLOC(p->d_Gsum, W.size() * sizeof(float2));
   ALLOC(p->d_R, (size_t)p->n_vx * Sy * K * sizeof(float2));
   ALLOC(p->d_Call, (size_t)p->S * K * sizeof(float));
-  ALLOC(p->d_C[0], (size_t)p->chunk_cap * K * sizeof(float));
-  ALLOC(p->d_C[1], (size_t)p->chunk_cap * K * sizeof(float));
   ALLOC(p->d_act_vy, act.size() * 4);
   ALLOC(p->d_col_off, p->col_off.size() * 4);
   ALLOC(p->d_vpos, act.size() * 4);
@@ -571,6 +536,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
             up(p->d_col_off, p->col_off.data(), p->col_off.size() * 4) && up(p->d_vpos, vpos.data(), act.size() * 4) &&
             up(p->d_flush_tiles, p->flush_tiles.data(), p->flush_tiles.size() * sizeof(int2));
   ok = ok && cudaMemset(p->d_G, 0, W.size() * sizeof(float2)) == cudaSuccess &&
+       cudaMemset(p->d_Call, 0, (size_t)p->S * K * sizeof(float)) == cudaSuccess &&
        cudaMemset(p->d_spec, 0, (size_t)p->S * sizeof(float2)) == cudaSuccess;
   if (!ok) return bail(fail(WDD_E_CUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError())));
   if (cufftPlan2d(&p->fft, Sy, Sx, CUFFT_C2C) != CUFFT_SUCCESS) return bail(fail(WDD_E_CUDA, "cufftPlan2d failed"));
@@ -713,8 +679,18 @@ wdd_status wdd_reset(wdd_plan_t plan) {
   Plan& p = *P(plan);
   CUDA_TRY(cudaSetDevice(p.device));
   CUDA_TRY(cudaMemsetAsync(p.d_G, 0, (size_t)p.n_act * p.K * sizeof(float2), p.stream));
+  std::vector<int32_t> rows;
+  for (int sy = 0; sy < p.Sy; ++sy)
+    if (p.row_dirty[sy]) rows.push_back(sy);
+  if (!rows.empty()) {   // coefficients ingested but never flushed
+    void* d = nullptr;
+    wdd_status s = upload_meta(p, rows.data(), rows.size() * sizeof(int32_t), &d);
+    if (s != WDD_OK) return s;
+    Prof pr(p, kSlotFlush, p.stream);
+    CUDA_TRY(launch_zero_rows(p, static_cast<const int32_t*>(d), (int)rows.size(), p.stream));
+  }
   std::fill(p.seen.begin(), p.seen.end(), 0);
-  std::fill(p.row_dirty.begin(), p.row_dirty.end(), 0);  // staged R rows are overwritten on next use
+  std::fill(p.row_dirty.begin(), p.row_dirty.end(), 0);
   p.frames_ingested = 0;
   return WDD_OK;
 }
@@ -782,7 +758,8 @@ wdd_status wdd_project(wdd_plan_t plan, const void* frames_dev, int64_t n, void*
   if (n < 0 || (n > 0 && (!frames_dev || !C_out_dev))) return fail(WDD_E_ARG, "bad arguments");
   CUDA_TRY(cudaSetDevice(p.device));
   Prof pr(p, kSlotProject, reinterpret_cast<cudaStream_t>(stream));
-  CUDA_TRY(launch_project(p, frames_dev, n, static_cast<float*>(C_out_dev), reinterpret_cast<cudaStream_t>(stream)));
+  CUDA_TRY(launch_project(p, frames_dev, n, static_cast<float*>(C_out_dev), nullptr,
+                          reinterpret_cast<cudaStream_t>(stream)));
   return WDD_OK;
 }
 

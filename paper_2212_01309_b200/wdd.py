@@ -11,7 +11,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libwdd.so")
+LIB_PATH = os.environ.get("WDD_LIB") or os.path.join(_HERE, "_lib", "libwdd.so")
 
 STATUS = {0: "WDD_OK", 1: "WDD_E_ARG", 2: "WDD_E_RANGE", 3: "WDD_E_DUP", 4: "WDD_E_NOMEM",
           5: "WDD_E_CUDA", 6: "WDD_E_NCCL", 7: "WDD_E_STATE"}
