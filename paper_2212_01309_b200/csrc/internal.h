@@ -32,6 +32,8 @@ struct Plan {
   std::vector<int2> flush_tiles;      // (column j, first row i0) of 32-row tiles
   std::vector<uint64_t> seen;         // S bits
   std::vector<uint8_t> row_dirty;     // Sy: row has coefficients in d_Call not yet flushed into G
+  std::vector<uint32_t> pending;      // Sy x mask_words bits: position ingested, not yet flushed
+  int mask_words = 1;                 // ceil(Sx / 32)
   int64_t frames_ingested = 0;
 
   // device buffers
@@ -39,12 +41,15 @@ struct Plan {
   float* d_psi = nullptr;             // Q*L f32
   float2* d_Fx = nullptr;             // n_vx * Sx
   float2* d_Fy = nullptr;             // Sy * Sy
+  float2* d_twx = nullptr;            // Sx/2 FFT twiddles exp(-2 pi i m / Sx) (power-of-two Sx)
+  float2* d_twy = nullptr;            // Sy/2 FFT twiddles exp(-2 pi i m / Sy) (power-of-two Sy)
+  int32_t* d_col_vx = nullptr;        // n_vx active vx, ascending
   float2* d_W = nullptr;              // n_act * K
   float2* d_G = nullptr;              // n_act * K
   float2* d_Gsum = nullptr;           // n_act * K (combine = 1 only)
   float2* d_R = nullptr;              // n_vx * Sy * K   R[j][sy][k]
-  float* d_Call = nullptr;            // S * K: coefficients of ingested, not yet flushed frames at
-                                      // their scan positions (zero elsewhere)
+  float* d_Call = nullptr;            // S * K: coefficients of ingested frames at their scan
+                                      // positions (only the pending ones are ever read)
   int32_t* d_act_vy = nullptr;
   int32_t* d_col_off = nullptr;
   int32_t* d_vpos = nullptr;          // n_act flattened v (scatter positions)
@@ -87,10 +92,12 @@ struct Plan {
 // projection of n frames; C row of frame f = idx ? idx[f] : f (idx: device array or null)
 cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* C, const int32_t* idx,
                            cudaStream_t st);
-// row DFT of the listed scan rows from d_Call into R, then zero those rows of d_Call
-cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st);
-cudaError_t launch_zero_rows(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st);
+// row DFT (a4) of the listed scan rows from the pending positions of d_Call (masks: n_rows x
+// mask_words bits) into R; FFT for power-of-two Sx, DFT matrix otherwise
+cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, cudaStream_t st);
+// rank update (a5) of the listed staged rows of R into G; FFT along y or DFT matrix
 cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st);
+bool flush_uses_fft(const Plan& p, int n_rows);
 cudaError_t launch_readout(const Plan& p, const float2* G, bool scatter, cudaStream_t st);
 cudaError_t launch_scatter(const Plan& p, cudaStream_t st);
 cudaError_t launch_finalize(const Plan& p, float2* out, cudaStream_t st);

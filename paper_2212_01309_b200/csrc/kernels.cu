@@ -4,10 +4,13 @@
 //                   H(I) = psi_x^T I^T psi_y.  Stage 1 (contraction over detector
 //                   columns) runs on the 5th-gen tensor cores: tcgen05.mma kind::f16, A = frame
 //                   rows converted in registers to exact fp16, B = [Psi_hi | Psi_lo] fp16 split,
-//                   fp32 accumulation in TMEM.  Stage 2 (contraction over detector rows) is fp32.
-//   rowdft_kernel   a4: R[j][sy][k] (+)= sum_sx Fx[j][sx] C[(sy,sx)][k]  (F_2D =
-//                   F_y (x) F_x), over the active vx columns j only.
-//   flush_kernel    a5: G[(j,vy)][k] += sum_rows Fy[vy][sy] R[j][sy][k]  (eq:outer_prod).
+//                   fp32 accumulation in TMEM.  Stage 2 (contraction over detector rows) runs on the
+//                   tensor cores too, with T split into fp16 hi/lo planes.
+//   rowfft_kernel   a4: R[j][sy][k] = sum_sx Fx[j][sx] C[(sy,sx)][k]  (F_2D =
+//                   F_y (x) F_x), over the active vx columns j only (radix-2 FFT in
+//                   shared memory; rowdft_kernel is the DFT-matrix form for other row lengths).
+//   colfft_kernel   a5: G[(j,vy)][k] += sum_rows Fy[vy][sy] R[j][sy][k]  (eq:outer_prod)
+//                   (FFT along y; flush_kernel is the DFT-matrix form for a few staged rows).
 //   readout_kernel  a6: o_v = sum_k G[v][k] K_v[k], one warp per active v.
 //   finalize        a8: cuFFT C2C inverse + conj / unitary scale / optional 1/sqrt(o_0).
 #include <cuda.h>
@@ -639,8 +642,120 @@ void pack_basis_fp16(const Plan& p, std::vector<uint16_t>& out, double& scale) {
 }
 
 // =====================================================================================
-// Row DFT (a4), run at flush time for every scan row with unflushed coefficients:
-//   R[j][sy][k] = sum_sx Fx[j][sx] C[sy*Sx + sx][k]      (zeros stand for frames not ingested)
+// Accumulation (a4 + a5): G[v][k] += F_y (x) F_x applied to the pending coefficients C (P:411-414,
+// eq:outer_prod P:424), in the separable form of the north star: a 1-D DFT along each scan row
+// (a4) into the staging R[j][sy][k] (active vx columns j only), then the phase-weighted update
+// along y (a5) into G for the active (vx, vy).  Both transforms are unitary (1/sqrt(S_axis)).
+//
+// Power-of-two scan axes use radix-2 FFTs in shared memory (O(S log S) per coefficient instead
+// of the O(S * n_active) of the DFT-matrix form; both passes are then HBM-bound); other sizes,
+// and flushes of only a few rows along y, use the DFT-matrix kernels further below.  Positions
+// not pending (not ingested, or already folded into G) enter as exact zeros: the host passes a
+// per-row bitmask of pending positions, so the coefficient store never needs to be cleared.
+// =====================================================================================
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+
+// In-place radix-2 DIT FFT of `cnt` sequences of length N = 2^logN stored interleaved as
+// x[n * cnt + c] (sequence index fastest, so a warp touches consecutive c: conflict-free), the
+// input already in bit-reversed order.  tw[m] = exp(-2 pi i m / N), m < N/2.  Ends synchronised.
+__device__ __forceinline__ void fft_stages(float2* x, const float2* tw, int logN, int logc) {
+  const int N = 1 << logN, cnt = 1 << logc, nb = (N >> 1) << logc;
+  for (int s = 1; s <= logN; ++s) {
+    const int half = 1 << (s - 1), tsh = logN - s;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+      const int c = b & (cnt - 1), t = b >> logc;
+      const int pos = t & (half - 1);
+      const int i = ((t >> (s - 1)) << s) + pos;
+      float2* xi = x + (i << logc) + c;
+      float2* xj = xi + (half << logc);
+      const float2 u = *xi, v = cmul(*xj, tw[pos << tsh]);
+      *xi = make_float2(u.x + v.x, u.y + v.y);
+      *xj = make_float2(u.x - v.x, u.y - v.y);
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ int bitrev(int v, int logN) { return logN ? (int)(__brev((unsigned)v) >> (32 - logN)) : 0; }
+
+// a4 by FFT.  CTA = (k-tile of KT coefficients, one pending scan row).  Two real coefficient
+// sequences k, k+1 share one complex FFT (z = C_k + i C_{k+1}); X_k[v] = (Z[v] + conj Z[-v]) / 2,
+// X_{k+1}[v] = (Z[v] - conj Z[-v]) / 2i.
+__global__ void __launch_bounds__(256) rowfft_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
+                                                     const uint32_t* __restrict__ masks, int mask_words,
+                                                     const float2* __restrict__ tw, const int32_t* __restrict__ col_vx,
+                                                     float2* __restrict__ R, int logSx, int logP, int Sy, int K,
+                                                     int n_vx, float scale) {
+  extern __shared__ __align__(16) float2 fsm[];
+  const int Sx = 1 << logSx, P = 1 << logP;
+  float2* x = fsm;                       // [Sx][P]
+  float2* stw = fsm + (Sx << logP);      // [Sx/2]
+  const int r = blockIdx.y, sy = __ldg(rows + r), k0 = blockIdx.x * 2 * P;
+  const uint32_t* mrow = masks + (int64_t)r * mask_words;
+  for (int i = threadIdx.x; i < Sx / 2; i += blockDim.x) stw[i] = __ldg(tw + i);
+  const float* Crow = C + (int64_t)sy * Sx * K + k0;
+  for (int e = threadIdx.x; e < (Sx << logP); e += blockDim.x) {
+    const int sx = e >> logP, pp = e & (P - 1);
+    float2 v = make_float2(0.f, 0.f);
+    if ((__ldg(mrow + (sx >> 5)) >> (sx & 31)) & 1u) v = __ldg(reinterpret_cast<const float2*>(Crow + (int64_t)sx * K) + pp);
+    x[(bitrev(sx, logSx) << logP) + pp] = v;
+  }
+  __syncthreads();
+  fft_stages(x, stw, logSx, logP);
+  const float hs = 0.5f * scale;
+  for (int e = threadIdx.x; e < (n_vx << logP); e += blockDim.x) {
+    const int j = e >> logP, pp = e & (P - 1);
+    const int v = __ldg(col_vx + j), vm = (Sx - v) & (Sx - 1);
+    const float2 z = x[(v << logP) + pp], zm = x[(vm << logP) + pp];
+    const float4 o = make_float4((z.x + zm.x) * hs, (z.y - zm.y) * hs, (z.y + zm.y) * hs, (zm.x - z.x) * hs);
+    *reinterpret_cast<float4*>(R + ((int64_t)j * Sy + sy) * K + k0 + 2 * pp) = o;
+  }
+}
+
+// a5 by FFT.  CTA = (k-tile of KT coefficients, one active vx column j): the length-Sy FFT of the
+// staged rows of R[j][.][k] (rows not staged are zeros), then G[(j, vy)][k] += X[vy] for the
+// active vy of column j.
+__global__ void __launch_bounds__(256) colfft_kernel(const float2* __restrict__ R, const int32_t* __restrict__ rows,
+                                                     int n_rows, const float2* __restrict__ tw,
+                                                     const int32_t* __restrict__ col_off,
+                                                     const int32_t* __restrict__ act_vy, float2* __restrict__ G,
+                                                     int logSy, int logKT, int K, float scale) {
+  extern __shared__ __align__(16) float2 fsm[];
+  const int Sy = 1 << logSy, KT = 1 << logKT;
+  float2* x = fsm;                       // [Sy][KT]
+  float2* stw = fsm + (Sy << logKT);     // [Sy/2]
+  const int j = blockIdx.y, k0 = blockIdx.x * KT;
+  for (int i = threadIdx.x; i < Sy / 2; i += blockDim.x) stw[i] = __ldg(tw + i);
+  if (n_rows < Sy)
+    for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x) x[e] = make_float2(0.f, 0.f);
+  __syncthreads();
+  const float2* Rj = R + (int64_t)j * Sy * K + k0;
+  for (int e = threadIdx.x; e < (n_rows << logKT); e += blockDim.x) {
+    const int rr = e >> logKT, kk = e & (KT - 1);
+    const int sy = __ldg(rows + rr);
+    x[(bitrev(sy, logSy) << logKT) + kk] = __ldg(Rj + (int64_t)sy * K + kk);
+  }
+  __syncthreads();
+  fft_stages(x, stw, logSy, logKT);
+  const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
+  for (int e = threadIdx.x; e < (mj << logKT); e += blockDim.x) {
+    const int i = e >> logKT, kk = e & (KT - 1);
+    const float2 z = x[(__ldg(act_vy + g0 + i) << logKT) + kk];
+    float2* ptr = G + (int64_t)(g0 + i) * K + k0 + kk;
+    const float2 o = *ptr;
+    *ptr = make_float2(fmaf(z.x, scale, o.x), fmaf(z.y, scale, o.y));
+  }
+}
+
+static int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
+static bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+constexpr int kFftSmem = 64 * 1024;   // FFT working set per CTA (the twiddle table is added)
+
+// =====================================================================================
+// a4 by DFT matrix (scan rows whose length is not a power of two):
+//   R[j][sy][k] = sum_sx Fx[j][sx] C[sy*Sx + sx][k]   over pending positions (sx) only
 // Tile: 16 active-vx columns j x 64 coefficients k of one scan row, 256 threads (2 j x 2 k each).
 // Entries are staged 128 at a time (C 32 KB + twiddles 16 KB of shared memory) with all loads of
 // a stage in flight at once; the next stage is prefetched into registers during the multiply.
@@ -649,6 +764,7 @@ constexpr int kRdE = 128;                                  // entries per stage
 constexpr int kRdSmem = kRdE * 64 * 4 + 16 * kRdE * 8;     // 48 KB
 
 __global__ void __launch_bounds__(256) rowdft_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
+                                                     const uint32_t* __restrict__ masks, int mask_words,
                                                      const float2* __restrict__ Fx, float2* __restrict__ R,
                                                      int Sx, int Sy, int K, int n_vx) {
   extern __shared__ __align__(16) uint8_t rd_smem[];
@@ -657,6 +773,7 @@ __global__ void __launch_bounds__(256) rowdft_kernel(const float* __restrict__ C
   const int t = threadIdx.x, kq = (t & 31) * 2, jg = t >> 5;           // k pair, j pair (0..7)
   const int k0 = blockIdx.x * 64, j0 = blockIdx.y * 16;
   const int sy = rows[blockIdx.z];
+  const uint32_t* mrow = masks + (int64_t)blockIdx.z * mask_words;
   const float* Crow = C + (int64_t)sy * Sx * K + k0;
   float4 cv[8];   // 128 entries x 64 k / 256 threads = 8 float4
   float2 fv[8];   // 16 j x 128 entries / 256 threads = 8 float2
@@ -665,9 +782,10 @@ __global__ void __launch_bounds__(256) rowdft_kernel(const float* __restrict__ C
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int idx = t + 256 * i;
-      const int ee = idx >> 4, kk = (idx & 15) * 4;
-      cv[i] = ee < ne ? __ldg(reinterpret_cast<const float4*>(Crow + (int64_t)(e0 + ee) * K + kk))
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int ee = idx >> 4, kk = (idx & 15) * 4, sx = e0 + ee;
+      cv[i] = (ee < ne && ((__ldg(mrow + (sx >> 5)) >> (sx & 31)) & 1u))
+                  ? __ldg(reinterpret_cast<const float4*>(Crow + (int64_t)sx * K + kk))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
       const int jj = idx >> 7, e2 = idx & (kRdE - 1);
       fv[i] = (e2 < ne && j0 + jj < n_vx) ? __ldg(Fx + (int64_t)(j0 + jj) * Sx + e0 + e2) : make_float2(0.f, 0.f);
     }
@@ -708,8 +826,24 @@ __global__ void __launch_bounds__(256) rowdft_kernel(const float* __restrict__ C
   }
 }
 
-cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st) {
+cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, cudaStream_t st) {
   if (n_rows <= 0) return cudaSuccess;
+  if (is_pow2(p.Sx) && p.Sx >= 2) {
+    const int logSx = ilog2(p.Sx);
+    int logP = ilog2(std::max(1, std::min(32, kFftSmem / (8 * p.Sx))));   // k pairs per CTA
+    while ((2 << logP) > p.K || p.K % (2 << logP)) --logP;
+    const size_t smem = ((size_t)p.Sx << logP) * 8 + (size_t)p.Sx / 2 * 8 + 16;
+    static bool init = false;
+    if (!init) {
+      cudaError_t e = cudaFuncSetAttribute(rowfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFftSmem + 8192);
+      if (e != cudaSuccess) return e;
+      init = true;
+    }
+    dim3 grid(p.K / (2 << logP), n_rows);
+    rowfft_kernel<<<grid, 256, smem, st>>>(p.d_Call, rows, masks, p.mask_words, p.d_twx, p.d_col_vx, p.d_R, logSx,
+                                           logP, p.Sy, p.K, p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)));
+    return cudaGetLastError();
+  }
   static bool init = false;
   if (!init) {
     cudaError_t e = cudaFuncSetAttribute(rowdft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRdSmem);
@@ -717,27 +851,14 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, int n_rows, cudaSt
     init = true;
   }
   dim3 grid(p.K / 64, (p.n_vx + 15) / 16, n_rows);
-  rowdft_kernel<<<grid, 256, kRdSmem, st>>>(p.d_Call, rows, p.d_Fx, p.d_R, p.Sx, p.Sy, p.K, p.n_vx);
-  return cudaGetLastError();
-}
-
-// Zero the listed scan rows of C (their coefficients have been folded into G).
-__global__ void zero_rows_kernel(float* __restrict__ C, const int32_t* __restrict__ rows, int64_t row_floats) {
-  float4* dst = reinterpret_cast<float4*>(C + (int64_t)rows[blockIdx.y] * row_floats);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < row_floats / 4; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-}
-
-cudaError_t launch_zero_rows(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st) {
-  if (n_rows <= 0) return cudaSuccess;
-  const int64_t rf = (int64_t)p.Sx * p.K;
-  dim3 grid((unsigned)std::min<int64_t>((rf / 4 + 255) / 256, 64), n_rows);
-  zero_rows_kernel<<<grid, 256, 0, st>>>(p.d_Call, rows, rf);
+  rowdft_kernel<<<grid, 256, kRdSmem, st>>>(p.d_Call, rows, masks, p.mask_words, p.d_Fx, p.d_R, p.Sx, p.Sy, p.K,
+                                            p.n_vx);
   return cudaGetLastError();
 }
 
 // =====================================================================================
-// Flush (a5): G[(j,vy)][k] += sum_{staged rows} Fy[vy][sy] R[j][sy][k]
+// a5 by DFT matrix (flush of a few rows, or Sy not a power of two):
+//   G[(j,vy)][k] += sum_{staged rows} Fy[vy][sy] R[j][sy][k]
 // =====================================================================================
 __global__ void __launch_bounds__(256) flush_kernel(const float2* __restrict__ R, const float2* __restrict__ Fy,
                                                     const int32_t* __restrict__ rows, int n_rows,
@@ -797,8 +918,30 @@ __global__ void __launch_bounds__(256) flush_kernel(const float2* __restrict__ R
   }
 }
 
+bool flush_uses_fft(const Plan& p, int n_rows) {
+  // FFT along y costs ~5 Sy log2(Sy) flops per (column, k) whatever the number of staged rows r;
+  // the DFT-matrix update ~8 r m_j with m_j (active vy of the column) a fraction of Sy.
+  return is_pow2(p.Sy) && p.Sy >= 2 && n_rows >= std::max(4, ilog2(p.Sy));
+}
+
 cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st) {
   if (n_rows <= 0) return cudaSuccess;
+  if (flush_uses_fft(p, n_rows)) {
+    const int logSy = ilog2(p.Sy);
+    int logKT = ilog2(std::max(1, std::min(32, kFftSmem / (8 * p.Sy))));
+    while ((1 << logKT) > p.K || p.K % (1 << logKT)) --logKT;
+    const size_t smem = ((size_t)p.Sy << logKT) * 8 + (size_t)p.Sy / 2 * 8 + 16;
+    static bool init = false;
+    if (!init) {
+      cudaError_t e = cudaFuncSetAttribute(colfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFftSmem + 8192);
+      if (e != cudaSuccess) return e;
+      init = true;
+    }
+    dim3 grid(p.K >> logKT, p.n_vx);
+    colfft_kernel<<<grid, 256, smem, st>>>(p.d_R, rows, n_rows, p.d_twy, p.d_col_off, p.d_act_vy, p.d_G, logSy, logKT,
+                                           p.K, (float)(1.0 / std::sqrt((double)p.Sy)));
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)p.flush_tiles.size(), (p.K + 63) / 64);
   flush_kernel<<<grid, 256, 0, st>>>(p.d_R, p.d_Fy, rows, n_rows, p.d_flush_tiles, p.d_col_off, p.d_act_vy,
                                      p.d_G, p.Sy, p.K);

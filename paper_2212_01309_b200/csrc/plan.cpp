@@ -208,6 +208,15 @@ void twiddles(int n_out, const int32_t* freqs, int S, std::vector<float2>& F) {
     }
 }
 
+// FFT twiddles tw[m] = exp(-2 pi i m / N), m < N/2 (unscaled; the kernels apply 1/sqrt(N))
+void fft_twiddles(int N, std::vector<float2>& tw) {
+  tw.resize(std::max(1, N / 2));
+  for (int m = 0; m < (int)tw.size(); ++m) {
+    const double ang = -2.0 * kPi * (double)m / (double)N;
+    tw[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
+}
+
 // ------------------------------------------------------------------ launch helpers
 struct Prof {
   Plan& p;
@@ -324,36 +333,49 @@ wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, in
     Prof pr(p, kSlotProject, st);
     CUDA_TRY(launch_project(p, frames_dev, nc, C, d_idx, st));
   }
-  for (int64_t i = 0; i < nc; ++i) p.row_dirty[idx[i] / p.Sx] = 1;
+  for (int64_t i = 0; i < nc; ++i) {
+    const int sy = idx[i] / p.Sx, sx = idx[i] % p.Sx;
+    p.row_dirty[sy] = 1;
+    p.pending[(size_t)sy * p.mask_words + (sx >> 5)] |= 1u << (sx & 31);
+  }
   return WDD_OK;
 }
 
 size_t frame_bytes(const Plan& p) { return (size_t)p.Q * p.Q * (p.dtype == 0 ? 2 : 4); }
 
-// Flush: row DFT of every row with unflushed coefficients (a4), zero those coefficient rows,
-// then the phase-weighted rank update of G over the same rows (a5).
+// Flush: row DFT of the pending positions of every row that has any (a4), then the
+// phase-weighted rank update of G over the same rows (a5).  The metadata block is the row list
+// followed by one pending bitmask per row; positions outside the mask are read as zeros, so the
+// coefficient store never needs clearing (each scan position is ingested at most once per reset).
 wdd_status flush(Plan& p) {
-  std::vector<int32_t> rows;
+  std::vector<int32_t> blob;
+  int n_rows = 0;
   for (int sy = 0; sy < p.Sy; ++sy)
-    if (p.row_dirty[sy]) rows.push_back(sy);
-  if (rows.empty()) return WDD_OK;
+    if (p.row_dirty[sy]) { blob.push_back(sy); ++n_rows; }
+  if (n_rows == 0) return WDD_OK;
+  const size_t mask_off = ((size_t)n_rows + 3) / 4 * 4;
+  blob.resize(mask_off + (size_t)n_rows * p.mask_words, 0);
+  for (int r = 0; r < n_rows; ++r) {
+    const int sy = blob[r];
+    for (int w = 0; w < p.mask_words; ++w) {
+      uint32_t& m = p.pending[(size_t)sy * p.mask_words + w];
+      blob[mask_off + (size_t)r * p.mask_words + w] = (int32_t)m;
+      m = 0;
+    }
+    p.row_dirty[sy] = 0;
+  }
   void* d = nullptr;
-  wdd_status s = upload_meta(p, rows.data(), rows.size() * sizeof(int32_t), &d);
+  wdd_status s = upload_meta(p, blob.data(), blob.size() * sizeof(int32_t), &d);
   if (s != WDD_OK) return s;
   const int32_t* dr = static_cast<const int32_t*>(d);
   {
     Prof pr(p, kSlotRowDft, p.stream);
-    CUDA_TRY(launch_rowdft(p, dr, (int)rows.size(), p.stream));
+    CUDA_TRY(launch_rowdft(p, dr, reinterpret_cast<const uint32_t*>(dr + mask_off), n_rows, p.stream));
   }
   {
     Prof pr(p, kSlotFlush, p.stream);
-    CUDA_TRY(launch_zero_rows(p, dr, (int)rows.size(), p.stream));
+    CUDA_TRY(launch_flush(p, dr, n_rows, p.stream));
   }
-  {
-    Prof pr(p, kSlotFlush, p.stream);
-    CUDA_TRY(launch_flush(p, dr, (int)rows.size(), p.stream));
-  }
-  for (int32_t sy : rows) p.row_dirty[sy] = 0;
   return WDD_OK;
 }
 
@@ -363,7 +385,7 @@ void free_plan(Plan* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   cudaDeviceSynchronize();
   if (p->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(p->nccl));
-  void* bufs[] = {p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
+  void* bufs[] = {p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
                   p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec,
                   p->d_meta, p->d_stage[0], p->d_stage[1]};
   for (void* b : bufs)
@@ -474,6 +496,9 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   std::vector<int32_t> ally(Sy);
   for (int v = 0; v < Sy; ++v) ally[v] = v;
   twiddles(Sy, ally.data(), Sy, Fy);
+  std::vector<float2> twx, twy;
+  fft_twiddles(Sx, twx);
+  fft_twiddles(Sy, twy);
 
   // bank
   std::vector<float2> W((size_t)p->n_act * K);
@@ -499,9 +524,11 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   std::vector<float> psi32(p->basis.begin(), p->basis.end());
   std::vector<int32_t> vpos(act.begin(), act.end());
   p->chunk_cap = 8192;
-  p->meta_slot_bytes = std::max((size_t)p->chunk_cap, (size_t)Sy) * sizeof(int32_t);
+  p->mask_words = (Sx + 31) / 32;
+  p->meta_slot_bytes = std::max((size_t)p->chunk_cap, (size_t)Sy * (1 + p->mask_words) + 4) * sizeof(int32_t);
   p->seen.assign((size_t)(p->S + 63) / 64, 0);
   p->row_dirty.assign(Sy, 0);
+  p->pending.assign((size_t)Sy * p->mask_words, 0);
 
 #define ALLOC(ptr, bytes)                                                                           \
   if (cudaMalloc((void**)&(ptr), (bytes)) != cudaSuccess)                                           \
@@ -510,6 +537,9 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ALLOC(p->d_psi, psi32.size() * 4);
   ALLOC(p->d_Fx, Fx.size() * sizeof(float2));
   ALLOC(p->d_Fy, Fy.size() * sizeof(float2));
+  ALLOC(p->d_twx, twx.size() * sizeof(float2));
+  ALLOC(p->d_twy, twy.size() * sizeof(float2));
+  ALLOC(p->d_col_vx, p->col_vx.size() * sizeof(int32_t));
   ALLOC(p->d_W, W.size() * sizeof(float2));
   ALLOC(p->d_G, W.size() * sizeof(float2));
   if (p->combine == 1) ALLOC(p->d_Gsum, W.size() * sizeof(float2));
@@ -532,6 +562,8 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   auto up = [&](void* d, const void* h, size_t b) { return cudaMemcpy(d, h, b, cudaMemcpyHostToDevice) == cudaSuccess; };
   bool ok = up(p->d_Bpack, bpack.data(), bpack.size() * 2) && up(p->d_psi, psi32.data(), psi32.size() * 4) &&
             up(p->d_Fx, Fx.data(), Fx.size() * sizeof(float2)) && up(p->d_Fy, Fy.data(), Fy.size() * sizeof(float2)) &&
+            up(p->d_twx, twx.data(), twx.size() * sizeof(float2)) && up(p->d_twy, twy.data(), twy.size() * sizeof(float2)) &&
+            up(p->d_col_vx, p->col_vx.data(), p->col_vx.size() * sizeof(int32_t)) &&
             up(p->d_W, W.data(), W.size() * sizeof(float2)) && up(p->d_act_vy, p->act_vy.data(), act.size() * 4) &&
             up(p->d_col_off, p->col_off.data(), p->col_off.size() * 4) && up(p->d_vpos, vpos.data(), act.size() * 4) &&
             up(p->d_flush_tiles, p->flush_tiles.data(), p->flush_tiles.size() * sizeof(int2));
@@ -679,18 +711,11 @@ wdd_status wdd_reset(wdd_plan_t plan) {
   Plan& p = *P(plan);
   CUDA_TRY(cudaSetDevice(p.device));
   CUDA_TRY(cudaMemsetAsync(p.d_G, 0, (size_t)p.n_act * p.K * sizeof(float2), p.stream));
-  std::vector<int32_t> rows;
-  for (int sy = 0; sy < p.Sy; ++sy)
-    if (p.row_dirty[sy]) rows.push_back(sy);
-  if (!rows.empty()) {   // coefficients ingested but never flushed
-    void* d = nullptr;
-    wdd_status s = upload_meta(p, rows.data(), rows.size() * sizeof(int32_t), &d);
-    if (s != WDD_OK) return s;
-    Prof pr(p, kSlotFlush, p.stream);
-    CUDA_TRY(launch_zero_rows(p, static_cast<const int32_t*>(d), (int)rows.size(), p.stream));
-  }
+  // coefficients of frames ingested but never flushed are simply forgotten: only pending
+  // positions are ever read from the coefficient store
   std::fill(p.seen.begin(), p.seen.end(), 0);
   std::fill(p.row_dirty.begin(), p.row_dirty.end(), 0);
+  std::fill(p.pending.begin(), p.pending.end(), 0u);
   p.frames_ingested = 0;
   return WDD_OK;
 }

@@ -251,3 +251,44 @@ def test_phase_recovery_medium(wdd, torch_cuda):
     out = plan.readout().cpu().numpy()
     ph = np.angle(out * np.conj(out.mean()))
     assert np.corrcoef(ph.ravel(), acq.phase().ravel())[0, 1] > 0.94
+
+
+@pytest.mark.parametrize("Sy,Sx", [(24, 40), (32, 20), (20, 32)])
+def test_non_power_of_two_scan(wdd, torch_cuda, Sy, Sx):
+    # non-power-of-two scan axes take the DFT-matrix kernels for that axis (rowdft / flush)
+    torch = torch_cuda
+    cfg = CONFIGS["tiny"].with_(Sy=Sy, Sx=Sx)
+    idx = np.arange(cfg.S)
+    fr = _frames(cfg, idx)
+    ref = _oracle_all(cfg, fr, idx)
+    plan = wdd.Plan.from_config(cfg)
+    _ingest_batches(torch, plan, _to_dev(torch, fr), idx, 100)
+    G, act = plan.get_accumulator()
+    assert rel(G.cpu().numpy(), ref["G"][act]) < TOL
+    out = plan.readout()
+    torch.cuda.synchronize()
+    assert rel(out.cpu().numpy(), ref["O"]) < TOL
+
+
+@pytest.mark.parametrize("rows_per_readout", [1, 2, 5, 8])
+def test_live_readout_cadence(wdd, torch_cuda, rows_per_readout):
+    # frames arrive in scan order; a readout every r rows flushes r staged rows into G (few rows:
+    # DFT-matrix rank update; more: FFT along y with the missing rows as zeros).  Every readout
+    # must equal the oracle on the frames ingested so far.
+    torch = torch_cuda
+    cfg = CONFIGS["tiny"]
+    idx = np.arange(cfg.S)
+    fr = _frames(cfg, idx)
+    fr_dev = _to_dev(torch, fr)
+    plan = wdd.Plan.from_config(cfg)
+    step = rows_per_readout * cfg.Sx
+    for a in range(0, cfg.S, step):
+        b = min(cfg.S, a + step)
+        plan.ingest(fr_dev[a:b], idx[a:b])
+        out = plan.readout()
+        torch.cuda.synchronize()
+        if (a // step) % 3 == 0 or b == cfg.S:
+            ref = _oracle_all(cfg, fr[:b], idx[:b])
+            assert rel(out.cpu().numpy(), ref["O"]) < TOL, b
+    G, act = plan.get_accumulator()
+    assert rel(G.cpu().numpy(), _oracle_all(cfg, fr, idx)["G"][act]) < TOL
