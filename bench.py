@@ -45,6 +45,16 @@ def _peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def _traffic(workload):
+    """DRAM bytes (read + write) per projection launch from the committed ncu --set full capture
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f).get(workload, {}).get("project_kernel_bytes_per_launch")
+
+
 class ClockSampler:
     """NVML sampling of SM clock and throttle reasons during the timed region."""
 
@@ -172,6 +182,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-frames", type=int, default=2048)
     ap.add_argument("--e2e-steps", type=int, default=5)
+
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -253,7 +264,30 @@ def main():
     ms_step = ms / args.steps
     value = cfg.S * args.steps / (ms / 1e3)
 
-    # ---- per-kernel device times (eager pass with event pairs around every launch)
+    # ---- projection stage alone: a second graph with the same reset + ingests and no readout
+    # (the flush runs at readout), replayed and timed with events on the plan stream.  Batches
+    # overlap on the GPU (PDL), so the stage time, not an isolated launch, is what the kernel costs.
+    plan.capture_begin(stream)
+    plan.reset()
+    for a, b in batches:
+        plan.ingest(dev[a:b], idx[a:b], stream)
+    h_ing = plan.capture_end()
+    for _ in range(3):
+        plan.graph_launch(h_ing, stream)
+    plan.reset()
+    torch.cuda.synchronize()
+    reps = max(10, min(args.steps, 100))
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(reps):
+        plan.graph_launch(h_ing, stream)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    plan.reset()
+    proj_ms_step = p0.elapsed_time(p1) / reps
+
+    # ---- per-kernel device times (eager pass with event pairs around every launch; batches do
+    # not overlap here, so these are isolated-launch costs)
     prof_steps = min(args.steps, 20)
     plan.profile_enable(True)
     for _ in range(prof_steps):
@@ -265,11 +299,19 @@ def main():
         kern[name] = {"ms_total": tot, "launches": cnt, "ms_per_launch": tot / cnt if cnt else None}
     plan.profile_enable(False)
     peaks, peak_src = _peaks()
-    proj = kern["project"]
-    frames_per_launch = len(idx) * prof_steps / max(1, proj["launches"])
+    info = plan.info()
+    n_launch = len(batches)
+    frames_per_launch = len(idx) / n_launch
     bytes_per_launch = frames_per_launch * (frame_bytes + cfg.K * 4)   # frames read + C written
-    achieved = bytes_per_launch / (proj["ms_per_launch"] * 1e-3) / 1e9
-    share = proj["ms_total"] / sum(v["ms_total"] for v in kern.values())
+    proj_ms_launch = proj_ms_step / n_launch
+    achieved = bytes_per_launch / (proj_ms_launch * 1e-3) / 1e9
+    share = proj_ms_step / ms_step
+    # whole-step algorithmic roofline (SURVEY §8(d) bytes per frame; every stage is HBM-bound):
+    # frame + C write/read (8K) + row staging R write/read (16 n_vx K / Sx) + G written once and
+    # the bank read once by the fused readout (2 x 8 n_act K / S)
+    b_step = (frame_bytes + 8 * cfg.K + 16 * info["n_vx"] * cfg.K / cfg.Sx
+              + 16 * info["n_act"] * cfg.K / cfg.S)
+    roof_fps = peaks["hbm_gbs"] * 1e9 / b_step
 
     # ---- end to end through the public API from pinned host memory (H2D + compute + D2H)
     out_host = np.empty((cfg.Sy, cfg.Sx), dtype=np.complex64)
@@ -314,12 +356,14 @@ def main():
                        "l2": "inputs larger than L2 (537 MB of frames per step)",
                        "graph": not args.no_graph},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": "project",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": _traffic(cfg.name), "kernel": "project_kernel",
                          "peak_source": peak_src, "bytes_per_launch": bytes_per_launch,
-                         "ms_per_launch": proj["ms_per_launch"], "share_of_step": share},
-            "kernels": kern,
-            "step_roofline": {"frames_per_s_at_hbm": peaks["hbm_gbs"] * 1e9 / (frame_bytes + 8 * cfg.K),
-                              "frac": value / (peaks["hbm_gbs"] * 1e9 / (frame_bytes + 8 * cfg.K))},
+                         "ms_per_launch": proj_ms_launch, "launches_per_step": n_launch,
+                         "share_of_step": share},
+            "kernels_isolated": kern,
+            "step_roofline": {"bytes_per_frame": b_step, "frames_per_s_at_hbm": roof_fps,
+                              "frac": value / roof_fps,
+                              "frame_bytes_only_frames_per_s": peaks["hbm_gbs"] * 1e9 / frame_bytes},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(len(idx) * frame_bytes),
                     "d2h_bytes_per_step": int(cfg.S * 8)},
             "gpu_launches": int(launches_per_step * args.steps),

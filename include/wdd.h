@@ -91,10 +91,10 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
 wdd_status wdd_ingest(wdd_plan_t plan, const void* frames_dev, const int32_t* scan_idx_host,
                       int64_t n, void* stream);
 
-/* Same as wdd_ingest for frames in HOST memory (pinned or pageable): the library copies them
- * through double-buffered device staging on its own copy stream, overlapping the H2D copy of
- * chunk i+1 with the compute of chunk i.  Returns when the frames have been copied (the host
- * buffer may then be reused); the compute is still asynchronous on `stream`. */
+/* Same as wdd_ingest for frames in HOST memory (pinned for asynchronous copies): the library
+ * copies them through double-buffered device staging on its own copy stream, so the H2D copy of
+ * one chunk overlaps the projection of the previous one.  Stream-ordered like wdd_ingest: the
+ * host buffer must stay valid (and unmodified) until `stream` has passed this call. */
 wdd_status wdd_ingest_host(wdd_plan_t plan, const void* frames_host, const int32_t* scan_idx_host,
                            int64_t n, void* stream);
 

@@ -17,7 +17,7 @@ __all__ = [
     "signed_freq", "probe_hat", "autocorrelation", "project", "vec",
     "accumulate_fft", "accumulate_stream", "active_set", "wiener_bank",
     "readout_spectrum", "image_from_spectrum", "reduced_wdd", "full_wdd",
-    "pruning_bound_paper", "cdft2", "cidft2",
+    "pruning_bound_paper", "cdft2", "cidft2", "project_events", "scan_phase", "accumulate_at",
 ]
 
 
@@ -176,6 +176,35 @@ def accumulate_stream(C, idx, Sy, Sx):
         f = np.exp(-2j * math.pi * (vy * sy / Sy + vx * sx / Sx)) / math.sqrt(Sy * Sx)
         G += np.outer(f.reshape(-1), c)
     return G
+
+
+def project_events(pix, cnt, Psi):
+    """H(I_s) of P:361 evaluated directly on a sparse frame given as events (pixel my*Q + mx,
+    count): entry [a, b] = sum_events count * Psi[mx, a] * Psi[my, b] -- the same double sum
+    as project(), restricted to the nonzero pixels.  Returns vec(H) per frame, shape (n, L*L)."""
+    Q, L = Psi.shape
+    pix = np.asarray(pix, dtype=np.int64)
+    w = np.asarray(cnt, dtype=np.float64)
+    my, mx = pix // Q, pix % Q
+    H = np.einsum("ne,nea,neb->nab", w, Psi[mx], Psi[my], optimize=True)
+    return vec(H)
+
+
+def scan_phase(v_list, idx, Sy, Sx):
+    """f_s[v] = exp(-2 pi i (vy*sy/Sy + vx*sx/Sx)) / sqrt(Sy*Sx) for the listed v
+    (rows) and scan positions idx (columns).  The angle is reduced exactly in integers
+    ((vy*sy) mod Sy, (vx*sx) mod Sx) before the float64 cos/sin."""
+    v = np.asarray(v_list, dtype=np.int64)[:, None]
+    s = np.asarray(idx, dtype=np.int64)[None, :]
+    vy, vx, sy, sx = v // Sx, v % Sx, s // Sx, s % Sx
+    ang = 2.0 * math.pi * (((vy * sy) % Sy) / Sy + ((vx * sx) % Sx) / Sx)
+    return (np.cos(ang) - 1j * np.sin(ang)) / math.sqrt(Sy * Sx)
+
+
+def accumulate_at(C, idx, v_list, Sy, Sx):
+    """Rows v_list of G = sum_s f_s c_s^T (eq:outer_prod) for coefficient vectors C (n, K)
+    at scan positions idx: G[v, :] = sum_s f_s[v] C[s, :]."""
+    return scan_phase(v_list, idx, Sy, Sx) @ np.asarray(C, dtype=np.float64)
 
 
 # ---------------------------------------------------------------------------------------

@@ -11,9 +11,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "_lib", "libwdd.so")
+LIB = os.environ.get("WDD_LIB_OUT") or os.path.join(HERE, "_lib", "libwdd.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "plan.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("internal.h", "tc.cuh")] + [os.path.join(ROOT, "include", "wdd.h")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("internal.h", "tc.cuh", "fft.cuh")] + [os.path.join(ROOT, "include", "wdd.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

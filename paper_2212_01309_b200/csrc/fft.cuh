@@ -1,0 +1,115 @@
+// fft.cuh -- shared-memory FFTs for the scan-frequency transforms of the Live-WDD path.
+//
+// The unitary scan DFT F_2D = F_y (x) F_x is applied along one scan axis at
+// a time to many independent sequences (one per coefficient k, or per image column).  For a
+// power-of-two length N = N1 * N2 this is the four-step (Cooley-Tukey) factorisation:
+//   step 1  for each n2 < N2:  y[n2][k1] = W_N^{n2 k1} * sum_{n1} x[N2 n1 + n2] W_N1^{n1 k1}
+//   step 2  for each k1 < N1:  X[k1 + N1 k2] = sum_{n2} y[n2][k1] W_N2^{n2 k2}
+// Each thread owns one short DFT (N1 or N2 <= 32 points) held entirely in registers (radix-2
+// DIT, compile-time unrolled), so a length-N transform costs two register passes and one
+// shared-memory exchange instead of log2(N) synchronised shared-memory passes.
+#pragma once
+#include <cstdint>
+
+namespace wdd {
+namespace fft {
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+
+__host__ __device__ constexpr int brev_c(int v, int bits) {
+  int r = 0;
+  for (int i = 0; i < bits; ++i) r |= ((v >> i) & 1) << (bits - 1 - i);
+  return r;
+}
+
+// W_N^m for 0 <= m < N from the half table tw[m] = exp(-2 pi i m / N), m < N/2.
+__device__ __forceinline__ float2 twiddle(const float2* tw, int m, int half_n) {
+  const float2 w = tw[m < half_n ? m : m - half_n];
+  return m < half_n ? w : make_float2(-w.x, -w.y);
+}
+
+// One radix-2 DIT stage (butterfly span LEN) of an in-register DFT of R points; recursion over
+// LEN keeps every register index a compile-time constant.
+template <int R, int LEN>
+__device__ __forceinline__ void dft_stage(float2 (&v)[R], const float2* tw, int stride) {
+  if constexpr (LEN <= R) {
+#pragma unroll
+    for (int i = 0; i < R; i += LEN) {
+#pragma unroll
+      for (int j = 0; j < LEN / 2; ++j) {
+        const float2 a = v[i + j];
+        const float2 b = j == 0 ? v[i + j + LEN / 2] : cmul(v[i + j + LEN / 2], tw[j * (R / LEN) * stride]);
+        v[i + j] = make_float2(a.x + b.x, a.y + b.y);
+        v[i + j + LEN / 2] = make_float2(a.x - b.x, a.y - b.y);
+      }
+    }
+    dft_stage<R, 2 * LEN>(v, tw, stride);
+  }
+}
+
+// In-register forward DFT of R = 2^LR points (natural order in and out).  W_R^j is read from
+// the length-N half table as tw[j * stride] with stride = N / R (a warp-uniform broadcast).
+template <int LR>
+__device__ __forceinline__ void dft_reg(float2 (&v)[1 << LR], const float2* tw, int stride) {
+  constexpr int R = 1 << LR;
+  float2 u[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) u[i] = v[brev_c(i, LR)];
+  dft_stage<R, 2>(u, tw, stride);
+#pragma unroll
+  for (int i = 0; i < R; ++i) v[i] = u[i];
+}
+
+template <int LOGN> struct Split {
+  static constexpr int L1 = (LOGN + 1) / 2, L2 = LOGN - L1;
+  static constexpr int N1 = 1 << L1, N2 = 1 << L2;
+};
+
+// Slot holding frequency f after fft_seq<LOGN>.
+template <int LOGN>
+__device__ __forceinline__ int fslot(int f) {
+  using S = Split<LOGN>;
+  return S::N2 * (f & (S::N1 - 1)) + (f >> S::L1);
+}
+
+// Forward DFT (unnormalised, e^{-2 pi i}) of 2^logc interleaved sequences of length N = 2^LOGN
+// stored in shared memory as x[n * cnt + c] (sequence index fastest: a warp touches consecutive
+// addresses).  Input in natural order; frequency f ends at slot fslot<LOGN>(f).  tw = the N/2
+// half table in shared memory.  Starts and ends with the block synchronised.
+template <int LOGN>
+__device__ __forceinline__ void fft_seq(float2* x, const float2* tw, int logc) {
+  using S = Split<LOGN>;
+  constexpr int N1 = S::N1, N2 = S::N2, HN = (1 << LOGN) / 2;
+  const int cnt = 1 << logc;
+  for (int t = threadIdx.x; t < (N2 << logc); t += blockDim.x) {
+    const int c = t & (cnt - 1), n2 = t >> logc;
+    float2 v[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = x[((N2 * n1 + n2) << logc) + c];
+    dft_reg<S::L1>(v, tw, N2);
+    if (N2 > 1) {
+#pragma unroll
+      for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], twiddle(tw, n2 * k1, HN));
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < N1; ++k1) x[((N2 * k1 + n2) << logc) + c] = v[k1];
+  }
+  __syncthreads();
+  if (N2 > 1) {
+    for (int t = threadIdx.x; t < (N1 << logc); t += blockDim.x) {
+      const int c = t & (cnt - 1), k1 = t >> logc;
+      float2 v[N2];
+#pragma unroll
+      for (int n2 = 0; n2 < N2; ++n2) v[n2] = x[((N2 * k1 + n2) << logc) + c];
+      dft_reg<S::L2>(v, tw, N1);
+#pragma unroll
+      for (int k2 = 0; k2 < N2; ++k2) x[((N2 * k1 + k2) << logc) + c] = v[k2];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace fft
+}  // namespace wdd

@@ -54,8 +54,15 @@ struct Plan {
   int32_t* d_col_off = nullptr;
   int32_t* d_vpos = nullptr;          // n_act flattened v (scatter positions)
   int2* d_flush_tiles = nullptr;
-  float2* d_o = nullptr;              // n_act
+  float2* d_o = nullptr;              // n_act (multi-rank combine of o)
+  float2* d_opart = nullptr;          // opart_cap x n_act partial readouts (per colfft k-tile)
+  int32_t* d_gidx = nullptr;          // S: accumulator row of v, or -1 (inactive)
+  int64_t g_dc = 0;                   // accumulator row of v = 0
+  int opart_cap = 1;                  // rows of d_opart
+  int opart_tiles = 0;                // valid partial-readout rows for the current G (0: stale)
+  bool G_zero = true;                 // G is logically zero (reset); its memory may be stale
   float2* d_spec = nullptr;           // Sy*Sx
+  float2* d_img_tmp = nullptr;        // Sy*Sx scratch of the image transform (row pass)
   void* d_meta = nullptr;             // per-chunk row tables
   void* h_meta = nullptr;             // pinned host mirror of d_meta (2 slots)
   cudaEvent_t meta_ev[2] = {nullptr, nullptr};
@@ -63,7 +70,9 @@ struct Plan {
   size_t meta_slot_bytes = 0;
   int64_t chunk_cap = 0;
   void* d_stage[2] = {nullptr, nullptr};  // host-ingest staging
-  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};   // staging slot consumed by the projection
+  cudaEvent_t copy_ev[2] = {nullptr, nullptr};    // staging slot filled by the H2D copy
+  int stage_slot = 0;
   cudaStream_t copy_stream = nullptr;
   cufftHandle fft = 0;
   bool fft_ok = false;
@@ -96,11 +105,16 @@ cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* 
 // mask_words bits) into R; FFT for power-of-two Sx, DFT matrix otherwise
 cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, cudaStream_t st);
 // rank update (a5) of the listed staged rows of R into G; FFT along y or DFT matrix
-cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st);
+// (overwrite: G is logically zero, write instead of accumulate).  The FFT form also writes the
+// per-k-tile partial Wiener readout d_opart[colfft_tiles][n_act].
+cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st);
 bool flush_uses_fft(const Plan& p, int n_rows);
-cudaError_t launch_readout(const Plan& p, const float2* G, bool scatter, cudaStream_t st);
-cudaError_t launch_scatter(const Plan& p, cudaStream_t st);
-cudaError_t launch_finalize(const Plan& p, float2* out, cudaStream_t st);
+int colfft_tiles(const Plan& p);
+bool finalize_uses_fft(const Plan& p);
+// o[g] = sum_k G[g][k] W[g][k] (one warp per active v)
+cudaError_t launch_readout(const Plan& p, const float2* G, float2* o, cudaStream_t st);
+// image from the partial readouts op[tiles][n_act] (summed over tiles in order)
+cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st);
 // host helper: pack the fp16 B operand image of the projection kernel
 void pack_basis_fp16(const Plan& p, std::vector<uint16_t>& out, double& scale);
 size_t project_smem_bytes(int Q, int L);

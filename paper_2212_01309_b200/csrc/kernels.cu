@@ -23,11 +23,13 @@
 #include <type_traits>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "internal.h"
 #include "tc.cuh"
+#include "fft.cuh"
 
 namespace wdd {
 
@@ -113,7 +115,7 @@ struct ProjCfg {
   static constexpr int off_A2 = off_P1 + (U16 ? 0 : 2 * kSlot);
   static constexpr int off_B = off_A2 + align_up(2 * kA2, 1024);
   static constexpr int off_bar = off_B + align_up(kB, 1024);
-  static constexpr int kBars = 2 * kNS + 2 * kNA + 2 * kNAcc + 4;
+  static constexpr int kBars = 2 * kNS + 2 * kNA + 2 * kNAcc + 5;
   static constexpr int off_misc = off_bar + 8 * kBars;    // meta[kNS+kNA], wflag[2 groups][2][4], tmem slot
   static constexpr int smem = off_misc + 4 * (kNS + kNA) + 64 + 16;
   static_assert(kNS % 2 == 0 && kNA % 2 == 0, "even rings: converter group = job parity");
@@ -187,6 +189,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   uint64_t* acc1_empty = acc1_full + Cfg::kNAcc;
   uint64_t* a2_full = acc1_empty + Cfg::kNAcc;
   uint64_t* s2_done = a2_full + 1;
+  uint64_t* b_full = s2_done + 1;               // basis operand image landed (bulk copy)
   uint32_t* meta = reinterpret_cast<uint32_t*>(smem + Cfg::off_misc);   // [kNS + kNA]
   uint32_t* wflag = meta + Cfg::kNS + kNA;                               // [2][2][4]
   uint32_t* tslot = wflag + 16;
@@ -194,8 +197,8 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   pdl_trigger();
 
-  // ---- setup
-  for (int i = tid; i < Cfg::kB / 16; i += kProjThreads) reinterpret_cast<uint4*>(sB)[i] = __ldg(a.Bpack + i);
+  // ---- setup: barriers and TMEM only, so the TMA producer can start streaming at once; the basis
+  // operand image arrives by one bulk copy that only the MMA issuers wait for
   if (tid == 0) {
     for (int i = 0; i < Cfg::kNS; ++i) { mbar_init(&raw_full[i], 1); mbar_init(&raw_empty[i], 1); }
     for (int i = 0; i < kNA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
@@ -204,11 +207,13 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     for (int i = 0; i < Cfg::kNAcc; ++i) { mbar_init(&acc1_full[i], 1); mbar_init(&acc1_empty[i], 4); }
     mbar_init(a2_full, 1);
     mbar_init(s2_done, 1);
+    mbar_init(b_full, 1);
     fence_mbar_init();
+    mbar_arrive_expect_tx(b_full, Cfg::kB);
+    bulk_load(sB, a.Bpack, Cfg::kB, b_full);
   }
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tslot);
   if (U16 && warp == 2 && lane == 0) prefetch_tmap(&tmap);
-  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -226,6 +231,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_f16(128, Cfg::kN);
       const uint32_t ring0 = smem_u32(ring), p10 = smem_u32(sP1), b0 = smem_u32(sB);
+      mbar_wait(b_full, 0);
       uint32_t slot = 0, sphase = 0, tile = 0, job = 0;
       for (int64_t gi = 0; gi < my_groups; ++gi) {
         for (int tt = 0; tt < tpg; ++tt, ++tile) {
@@ -269,6 +275,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
       constexpr uint32_t idesc = idesc_f16(128, Cfg::kN);
       const uint32_t a20 = smem_u32(sA2), b0 = smem_u32(sB);
       const uint32_t acc2 = tbase + Cfg::tAcc2;
+      mbar_wait(b_full, 0);
       uint32_t phase = 0;
       for (int64_t gi = 0; gi < my_groups; ++gi) {
         for (int h = 0; h < Cfg::kTPF; ++h, phase ^= 1u) {
@@ -554,8 +561,16 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
     const int64_t per_cta = (groups + p.sm_count - 1) / p.sm_count * c;
     if (per_cta <= best) { best = per_cta; g2 = c; }
   }
+  // Frames per CTA: about 1 MiB of frame data per CTA, so that a small batch occupies only part
+  // of the GPU and consecutive (PDL-chained) batches stream concurrently on the other SMs instead
+  // of each batch paying its own pipeline fill and drain on every SM.  WDD_PROJ_MIN_FRAMES
+  // overrides (0 = spread every batch over all SMs).
+  static const int env_frames = [] { const char* e = std::getenv("WDD_PROJ_MIN_FRAMES"); return e ? std::atoi(e) : -1; }();
+  const int min_frames = env_frames >= 0 ? env_frames : std::max(4, (1 << 20) / (Q * Q * (U16 ? 2 : 4)));
+  if (min_frames > 0) g2 = Cfg::kG2;
   const int64_t groups = (n + g2 - 1) / g2;
-  const int grid = (int)std::min<int64_t>(groups, (int64_t)p.sm_count);
+  int grid = (int)std::min<int64_t>(groups, (int64_t)p.sm_count);
+  if (min_frames > 0) grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, (n + min_frames - 1) / min_frames));
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof tmap);
   if constexpr (U16) {
@@ -653,77 +668,75 @@ void pack_basis_fp16(const Plan& p, std::vector<uint16_t>& out, double& scale) {
 // not pending (not ingested, or already folded into G) enter as exact zeros: the host passes a
 // per-row bitmask of pending positions, so the coefficient store never needs to be cleared.
 // =====================================================================================
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
-}
+using fft::cmul;
+constexpr int kU = 8;   // loads in flight per thread in the FFT kernels' staging loops
+constexpr int kFftMaxLog = 10;   // FFT path for scan axes up to 1024 (DFT-matrix kernels beyond)
 
-// In-place radix-2 DIT FFT of `cnt` sequences of length N = 2^logN stored interleaved as
-// x[n * cnt + c] (sequence index fastest, so a warp touches consecutive c: conflict-free), the
-// input already in bit-reversed order.  tw[m] = exp(-2 pi i m / N), m < N/2.  Ends synchronised.
-__device__ __forceinline__ void fft_stages(float2* x, const float2* tw, int logN, int logc) {
-  const int N = 1 << logN, cnt = 1 << logc, nb = (N >> 1) << logc;
-  for (int s = 1; s <= logN; ++s) {
-    const int half = 1 << (s - 1), tsh = logN - s;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-      const int c = b & (cnt - 1), t = b >> logc;
-      const int pos = t & (half - 1);
-      const int i = ((t >> (s - 1)) << s) + pos;
-      float2* xi = x + (i << logc) + c;
-      float2* xj = xi + (half << logc);
-      const float2 u = *xi, v = cmul(*xj, tw[pos << tsh]);
-      *xi = make_float2(u.x + v.x, u.y + v.y);
-      *xj = make_float2(u.x - v.x, u.y - v.y);
-    }
-    __syncthreads();
-  }
-}
-
-__device__ __forceinline__ int bitrev(int v, int logN) { return logN ? (int)(__brev((unsigned)v) >> (32 - logN)) : 0; }
-
-// a4 by FFT.  CTA = (k-tile of KT coefficients, one pending scan row).  Two real coefficient
+// a4 by FFT.  CTA = (k-tile of 2P coefficients, one pending scan row).  Two real coefficient
 // sequences k, k+1 share one complex FFT (z = C_k + i C_{k+1}); X_k[v] = (Z[v] + conj Z[-v]) / 2,
-// X_{k+1}[v] = (Z[v] - conj Z[-v]) / 2i.
-__global__ void __launch_bounds__(256) rowfft_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
+// X_{k+1}[v] = (Z[v] - conj Z[-v]) / 2i.  Non-pending positions enter as zeros.
+template <int LOGN>
+__global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) rowfft_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
                                                      const uint32_t* __restrict__ masks, int mask_words,
                                                      const float2* __restrict__ tw, const int32_t* __restrict__ col_vx,
-                                                     float2* __restrict__ R, int logSx, int logP, int Sy, int K,
-                                                     int n_vx, float scale) {
+                                                     float2* __restrict__ R, int logP, int Sy, int K, int n_vx,
+                                                     float scale) {
+  constexpr int Sx = 1 << LOGN;
   extern __shared__ __align__(16) float2 fsm[];
-  const int Sx = 1 << logSx, P = 1 << logP;
+  __shared__ uint32_t smask[(Sx + 31) / 32];
+  const int P = 1 << logP;
   float2* x = fsm;                       // [Sx][P]
   float2* stw = fsm + (Sx << logP);      // [Sx/2]
   const int r = blockIdx.y, sy = __ldg(rows + r), k0 = blockIdx.x * 2 * P;
-  const uint32_t* mrow = masks + (int64_t)r * mask_words;
   for (int i = threadIdx.x; i < Sx / 2; i += blockDim.x) stw[i] = __ldg(tw + i);
-  const float* Crow = C + (int64_t)sy * Sx * K + k0;
-  for (int e = threadIdx.x; e < (Sx << logP); e += blockDim.x) {
-    const int sx = e >> logP, pp = e & (P - 1);
-    float2 v = make_float2(0.f, 0.f);
-    if ((__ldg(mrow + (sx >> 5)) >> (sx & 31)) & 1u) v = __ldg(reinterpret_cast<const float2*>(Crow + (int64_t)sx * K) + pp);
-    x[(bitrev(sx, logSx) << logP) + pp] = v;
+  if (threadIdx.x < mask_words) smask[threadIdx.x] = __ldg(masks + (int64_t)r * mask_words + threadIdx.x);
+  __syncthreads();
+  const float2* Crow = reinterpret_cast<const float2*>(C + (int64_t)sy * Sx * K + k0);
+  const int total = Sx << logP;
+  for (int base = 0; base < total; base += kU * 256) {
+    float2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = base + u * 256 + threadIdx.x;
+      v[u] = e < total ? __ldg(Crow + (int64_t)(e >> logP) * (K >> 1) + (e & (P - 1))) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = base + u * 256 + threadIdx.x;
+      if (e < total) {
+        const int sx = e >> logP;
+        x[e] = ((smask[sx >> 5] >> (sx & 31)) & 1u) ? v[u] : make_float2(0.f, 0.f);
+      }
+    }
   }
   __syncthreads();
-  fft_stages(x, stw, logSx, logP);
+  fft::fft_seq<LOGN>(x, stw, logP);
   const float hs = 0.5f * scale;
   for (int e = threadIdx.x; e < (n_vx << logP); e += blockDim.x) {
     const int j = e >> logP, pp = e & (P - 1);
     const int v = __ldg(col_vx + j), vm = (Sx - v) & (Sx - 1);
-    const float2 z = x[(v << logP) + pp], zm = x[(vm << logP) + pp];
+    const float2 z = x[(fft::fslot<LOGN>(v) << logP) + pp], zm = x[(fft::fslot<LOGN>(vm) << logP) + pp];
     const float4 o = make_float4((z.x + zm.x) * hs, (z.y - zm.y) * hs, (z.y + zm.y) * hs, (zm.x - z.x) * hs);
     *reinterpret_cast<float4*>(R + ((int64_t)j * Sy + sy) * K + k0 + 2 * pp) = o;
   }
 }
 
-// a5 by FFT.  CTA = (k-tile of KT coefficients, one active vx column j): the length-Sy FFT of the
-// staged rows of R[j][.][k] (rows not staged are zeros), then G[(j, vy)][k] += X[vy] for the
-// active vy of column j.
-__global__ void __launch_bounds__(256) colfft_kernel(const float2* __restrict__ R, const int32_t* __restrict__ rows,
+// a5 by FFT, fused with the first half of a6.  CTA = (k-tile t of KT coefficients, one active vx
+// column j): the length-Sy FFT of the staged rows of R[j][.][k] (rows not staged are zeros), then
+// G[(j, vy)][k] (+)= X[vy] for the active vy of column j (overwrite: the first flush after a
+// reset, G is logically zero), and, with the updated G still in registers, the tile's share of the
+// Wiener readout  opart[t][g] = sum_{k in tile t} G[g][k] K_g[k], so a readout never
+// re-reads G.  The partial sums are combined over tiles in a fixed order by the image transform.
+template <int LOGN>
+__global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) colfft_kernel(const float2* __restrict__ R, const int32_t* __restrict__ rows,
                                                      int n_rows, const float2* __restrict__ tw,
                                                      const int32_t* __restrict__ col_off,
                                                      const int32_t* __restrict__ act_vy, float2* __restrict__ G,
-                                                     int logSy, int logKT, int K, float scale) {
+                                                     const float2* __restrict__ W, float2* __restrict__ opart,
+                                                     int64_t n_act, int logKT, int K, float scale, int overwrite) {
+  constexpr int Sy = 1 << LOGN;
   extern __shared__ __align__(16) float2 fsm[];
-  const int Sy = 1 << logSy, KT = 1 << logKT;
+  const int KT = 1 << logKT;
   float2* x = fsm;                       // [Sy][KT]
   float2* stw = fsm + (Sy << logKT);     // [Sy/2]
   const int j = blockIdx.y, k0 = blockIdx.x * KT;
@@ -732,26 +745,77 @@ __global__ void __launch_bounds__(256) colfft_kernel(const float2* __restrict__ 
     for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x) x[e] = make_float2(0.f, 0.f);
   __syncthreads();
   const float2* Rj = R + (int64_t)j * Sy * K + k0;
-  for (int e = threadIdx.x; e < (n_rows << logKT); e += blockDim.x) {
-    const int rr = e >> logKT, kk = e & (KT - 1);
-    const int sy = __ldg(rows + rr);
-    x[(bitrev(sy, logSy) << logKT) + kk] = __ldg(Rj + (int64_t)sy * K + kk);
+  const int total = n_rows << logKT;
+  for (int base = 0; base < total; base += kU * 256) {
+    float2 v[kU];
+    int dst[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = base + u * 256 + threadIdx.x;
+      const int rr = e >> logKT, kk = e & (KT - 1);
+      const int sy = e < total ? __ldg(rows + rr) : 0;
+      dst[u] = e < total ? (sy << logKT) + kk : -1;
+      v[u] = e < total ? __ldg(Rj + (int64_t)sy * K + kk) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (dst[u] >= 0) x[dst[u]] = v[u];
   }
   __syncthreads();
-  fft_stages(x, stw, logSy, logKT);
+  fft::fft_seq<LOGN>(x, stw, logKT);
   const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
-  for (int e = threadIdx.x; e < (mj << logKT); e += blockDim.x) {
-    const int i = e >> logKT, kk = e & (KT - 1);
-    const float2 z = x[(__ldg(act_vy + g0 + i) << logKT) + kk];
-    float2* ptr = G + (int64_t)(g0 + i) * K + k0 + kk;
-    const float2 o = *ptr;
-    *ptr = make_float2(fmaf(z.x, scale, o.x), fmaf(z.y, scale, o.y));
+  const int tout = mj << logKT;
+  for (int base = 0; base < tout; base += kU * 256) {   // warp-uniform trip count (shuffles below)
+    float2 o[kU], w[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = base + u * 256 + threadIdx.x;
+      const int64_t gi = (int64_t)(g0 + (e >> logKT)) * K + k0 + (e & (KT - 1));
+      o[u] = (e < tout && !overwrite) ? G[gi] : make_float2(0.f, 0.f);
+      w[u] = e < tout ? __ldg(W + gi) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int e = base + u * 256 + threadIdx.x;
+      const int i = e >> logKT, kk = e & (KT - 1);
+      float2 d = make_float2(0.f, 0.f);
+      if (e < tout) {
+        const float2 z = x[(fft::fslot<LOGN>(__ldg(act_vy + g0 + i)) << logKT) + kk];
+        const float2 gn = make_float2(fmaf(z.x, scale, o[u].x), fmaf(z.y, scale, o[u].y));
+        G[(int64_t)(g0 + i) * K + k0 + kk] = gn;
+        d = cmul(gn, w[u]);
+      }
+      if (base + u * 256 < tout) {            // some lane of this block-row holds data
+        for (int off = KT >> 1; off > 0; off >>= 1) {
+          d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
+          d.y += __shfl_xor_sync(0xffffffffu, d.y, off);
+        }
+        if (kk == 0 && e < tout) opart[(int64_t)blockIdx.x * n_act + g0 + i] = d;
+      }
+    }
   }
 }
 
 static int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
 static bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 constexpr int kFftSmem = 64 * 1024;   // FFT working set per CTA (the twiddle table is added)
+
+template <typename F>
+static cudaError_t with_log(int logn, F&& f) {
+  switch (logn) {
+    case 1: return f(std::integral_constant<int, 1>{});
+    case 2: return f(std::integral_constant<int, 2>{});
+    case 3: return f(std::integral_constant<int, 3>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 5: return f(std::integral_constant<int, 5>{});
+    case 6: return f(std::integral_constant<int, 6>{});
+    case 7: return f(std::integral_constant<int, 7>{});
+    case 8: return f(std::integral_constant<int, 8>{});
+    case 9: return f(std::integral_constant<int, 9>{});
+    case 10: return f(std::integral_constant<int, 10>{});
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 // =====================================================================================
 // a4 by DFT matrix (scan rows whose length is not a power of two):
@@ -828,21 +892,25 @@ __global__ void __launch_bounds__(256) rowdft_kernel(const float* __restrict__ C
 
 cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, cudaStream_t st) {
   if (n_rows <= 0) return cudaSuccess;
-  if (is_pow2(p.Sx) && p.Sx >= 2) {
+  if (is_pow2(p.Sx) && p.Sx >= 2 && p.Sx <= (1 << kFftMaxLog)) {
     const int logSx = ilog2(p.Sx);
     int logP = ilog2(std::max(1, std::min(32, kFftSmem / (8 * p.Sx))));   // k pairs per CTA
     while ((2 << logP) > p.K || p.K % (2 << logP)) --logP;
     const size_t smem = ((size_t)p.Sx << logP) * 8 + (size_t)p.Sx / 2 * 8 + 16;
-    static bool init = false;
-    if (!init) {
-      cudaError_t e = cudaFuncSetAttribute(rowfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFftSmem + 8192);
-      if (e != cudaSuccess) return e;
-      init = true;
-    }
-    dim3 grid(p.K / (2 << logP), n_rows);
-    rowfft_kernel<<<grid, 256, smem, st>>>(p.d_Call, rows, masks, p.mask_words, p.d_twx, p.d_col_vx, p.d_R, logSx,
-                                           logP, p.Sy, p.K, p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)));
-    return cudaGetLastError();
+    return with_log(logSx, [&](auto LN) {
+      constexpr int LOGN = decltype(LN)::value;
+      static bool init = false;
+      if (!init) {
+        cudaError_t e = cudaFuncSetAttribute(rowfft_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kFftSmem + 8192);
+        if (e != cudaSuccess) return e;
+        init = true;
+      }
+      dim3 grid(p.K / (2 << logP), n_rows);
+      rowfft_kernel<LOGN><<<grid, 256, smem, st>>>(p.d_Call, rows, masks, p.mask_words, p.d_twx, p.d_col_vx, p.d_R,
+                                                   logP, p.Sy, p.K, p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)));
+      return cudaGetLastError();
+    });
   }
   static bool init = false;
   if (!init) {
@@ -864,7 +932,7 @@ __global__ void __launch_bounds__(256) flush_kernel(const float2* __restrict__ R
                                                     const int32_t* __restrict__ rows, int n_rows,
                                                     const int2* __restrict__ tiles, const int32_t* __restrict__ col_off,
                                                     const int32_t* __restrict__ act_vy, float2* __restrict__ G,
-                                                    int Sy, int K) {
+                                                    int Sy, int K, int overwrite) {
   __shared__ float2 Rs[32][64];
   __shared__ float2 Fs[32][33];
   __shared__ int vys[32];
@@ -912,39 +980,51 @@ __global__ void __launch_bounds__(256) flush_kernel(const float2* __restrict__ R
     const int i = i0 + ig * 8 + q;
     if (i < mj) {
       float2* ptr = G + (int64_t)(g0 + i) * K + k;
-      const float2 o = *ptr;
+      const float2 o = overwrite ? make_float2(0.f, 0.f) : *ptr;
       *ptr = make_float2(o.x + acc[q].x, o.y + acc[q].y);
     }
   }
 }
 
+static int colfft_logkt(const Plan& p) {
+  int logKT = ilog2(std::max(1, std::min(32, kFftSmem / (8 * p.Sy))));
+  while ((1 << logKT) > p.K || p.K % (1 << logKT)) --logKT;
+  return logKT;
+}
+
+int colfft_tiles(const Plan& p) { return p.K >> colfft_logkt(p); }
+
 bool flush_uses_fft(const Plan& p, int n_rows) {
   // FFT along y costs ~5 Sy log2(Sy) flops per (column, k) whatever the number of staged rows r;
   // the DFT-matrix update ~8 r m_j with m_j (active vy of the column) a fraction of Sy.
-  return is_pow2(p.Sy) && p.Sy >= 2 && n_rows >= std::max(4, ilog2(p.Sy));
+  return is_pow2(p.Sy) && p.Sy >= 2 && p.Sy <= (1 << kFftMaxLog) && n_rows >= std::max(4, ilog2(p.Sy));
 }
 
-cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, cudaStream_t st) {
+cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st) {
   if (n_rows <= 0) return cudaSuccess;
   if (flush_uses_fft(p, n_rows)) {
     const int logSy = ilog2(p.Sy);
-    int logKT = ilog2(std::max(1, std::min(32, kFftSmem / (8 * p.Sy))));
-    while ((1 << logKT) > p.K || p.K % (1 << logKT)) --logKT;
+    const int logKT = colfft_logkt(p);
     const size_t smem = ((size_t)p.Sy << logKT) * 8 + (size_t)p.Sy / 2 * 8 + 16;
-    static bool init = false;
-    if (!init) {
-      cudaError_t e = cudaFuncSetAttribute(colfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFftSmem + 8192);
-      if (e != cudaSuccess) return e;
-      init = true;
-    }
-    dim3 grid(p.K >> logKT, p.n_vx);
-    colfft_kernel<<<grid, 256, smem, st>>>(p.d_R, rows, n_rows, p.d_twy, p.d_col_off, p.d_act_vy, p.d_G, logSy, logKT,
-                                           p.K, (float)(1.0 / std::sqrt((double)p.Sy)));
-    return cudaGetLastError();
+    return with_log(logSy, [&](auto LN) {
+      constexpr int LOGN = decltype(LN)::value;
+      static bool init = false;
+      if (!init) {
+        cudaError_t e = cudaFuncSetAttribute(colfft_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kFftSmem + 8192);
+        if (e != cudaSuccess) return e;
+        init = true;
+      }
+      dim3 grid(p.K >> logKT, p.n_vx);
+      colfft_kernel<LOGN><<<grid, 256, smem, st>>>(p.d_R, rows, n_rows, p.d_twy, p.d_col_off, p.d_act_vy, p.d_G,
+                                                   p.d_W, p.d_opart, p.n_act, logKT, p.K,
+                                                   (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0);
+      return cudaGetLastError();
+    });
   }
   dim3 grid((unsigned)p.flush_tiles.size(), (p.K + 63) / 64);
   flush_kernel<<<grid, 256, 0, st>>>(p.d_R, p.d_Fy, rows, n_rows, p.d_flush_tiles, p.d_col_off, p.d_act_vy,
-                                     p.d_G, p.Sy, p.K);
+                                     p.d_G, p.Sy, p.K, overwrite ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -952,14 +1032,14 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, cudaStr
 // Readout (a6): o_v = sum_k G[v][k] W[v][k], one warp per active v
 // =====================================================================================
 __global__ void __launch_bounds__(256) readout_kernel(const float2* __restrict__ G, const float2* __restrict__ W,
-                                                      int64_t n_act, int K, float2* __restrict__ o,
-                                                      const int32_t* __restrict__ vpos, float2* __restrict__ spec) {
+                                                      int64_t n_act, int K, float2* __restrict__ o) {
   const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (g >= n_act) return;
   const float4* Gr = reinterpret_cast<const float4*>(G + g * K);
   const float4* Wr = reinterpret_cast<const float4*>(W + g * K);
   float re = 0.f, im = 0.f;
+#pragma unroll 4
   for (int i = lane; i < K / 2; i += 32) {
     const float4 a = __ldg(Gr + i), b = __ldg(Wr + i);
     re = fmaf(a.x, b.x, fmaf(-a.y, b.y, re));
@@ -972,32 +1052,36 @@ __global__ void __launch_bounds__(256) readout_kernel(const float2* __restrict__
     re += __shfl_xor_sync(0xffffffffu, re, s);
     im += __shfl_xor_sync(0xffffffffu, im, s);
   }
-  if (lane == 0) {
-    o[g] = make_float2(re, im);
-    if (spec) spec[vpos[g]] = make_float2(re, im);
-  }
+  if (lane == 0) o[g] = make_float2(re, im);
 }
 
-cudaError_t launch_readout(const Plan& p, const float2* G, bool scatter, cudaStream_t st) {
+cudaError_t launch_readout(const Plan& p, const float2* G, float2* o, cudaStream_t st) {
   const int64_t threads = p.n_act * 32;
   const unsigned blocks = (unsigned)((threads + 255) / 256);
-  readout_kernel<<<blocks, 256, 0, st>>>(G, p.d_W, p.n_act, p.K, p.d_o, p.d_vpos, scatter ? p.d_spec : nullptr);
+  readout_kernel<<<blocks, 256, 0, st>>>(G, p.d_W, p.n_act, p.K, o);
   return cudaGetLastError();
 }
 
-__global__ void scatter_kernel(const float2* __restrict__ o, const int32_t* __restrict__ vpos, int64_t n_act,
-                               float2* __restrict__ spec) {
+// o_v = sum over the `tiles` partial sums (fixed order), scattered to the dense spectrum
+__device__ __forceinline__ float2 sum_tiles(const float2* __restrict__ op, int tiles, int64_t n_act, int64_t g) {
+  float2 acc = __ldg(op + g);
+  for (int t = 1; t < tiles; ++t) {
+    const float2 v = __ldg(op + (int64_t)t * n_act + g);
+    acc.x += v.x;
+    acc.y += v.y;
+  }
+  return acc;
+}
+
+__global__ void scatter_kernel(const float2* __restrict__ op, int tiles, const int32_t* __restrict__ vpos,
+                               int64_t n_act, float2* __restrict__ spec) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < n_act) spec[vpos[g]] = o[g];
-}
-
-cudaError_t launch_scatter(const Plan& p, cudaStream_t st) {
-  scatter_kernel<<<(unsigned)((p.n_act + 255) / 256), 256, 0, st>>>(p.d_o, p.d_vpos, p.n_act, p.d_spec);
-  return cudaGetLastError();
+  if (g < n_act) spec[vpos[g]] = sum_tiles(op, tiles, n_act, g);
 }
 
 // =====================================================================================
-// Finalize (a8): out = conj(IDFT2(o)) / sqrt(S) [/ sqrt(o_0)]; the IDFT itself is cuFFT.
+// Finalize (a8): out = conj(IDFT2(o)) / sqrt(S) [/ sqrt(o_0)]; cuFFT for scans that are not
+// powers of two, else the two-pass shared-memory FFT below.
 // =====================================================================================
 __global__ void conj_scale_kernel(float2* __restrict__ out, int64_t S, double inv_sqrt_s,
                                   const float2* __restrict__ spec, int normalize) {
@@ -1024,12 +1108,106 @@ __global__ void conj_scale_kernel(float2* __restrict__ out, int64_t S, double in
   out[i] = make_float2((float)xr, (float)xi);
 }
 
-cudaError_t launch_finalize(const Plan& p, float2* out, cudaStream_t st) {
+// a8 on power-of-two scans without cuFFT.  O = conj(IDFT2_unitary(o)) = DFT2(conj o) / sqrt(S),
+// as two passes of the shared-memory FFT: rows (A[vy][x] = sum_vx conj o[vy][vx] W_Sx^{vx x})
+// into a scratch image, then columns with the unitary scale and the optional 1/sqrt(o_0).
+template <int LOGN>
+__global__ void __launch_bounds__(256) img_rows_kernel(const float2* __restrict__ op, int tiles, int64_t n_act,
+                                                       const int32_t* __restrict__ gidx, const float2* __restrict__ tw,
+                                                       float2* __restrict__ A, int logc) {
+  constexpr int N = 1 << LOGN;
+  extern __shared__ __align__(16) float2 fsm[];
+  float2* x = fsm;                 // [N][cnt]: x[vx * cnt + c] = conj o[vy0 + c][vx]
+  float2* stw = fsm + (N << logc);
+  const int vy0 = blockIdx.x << logc;
+  for (int i = threadIdx.x; i < N / 2; i += blockDim.x) stw[i] = __ldg(tw + i);
+  for (int e = threadIdx.x; e < (N << logc); e += blockDim.x) {
+    const int c = e >> LOGN, vx = e & (N - 1);
+    const int g = __ldg(gidx + (int64_t)(vy0 + c) * N + vx);
+    const float2 v = g >= 0 ? sum_tiles(op, tiles, n_act, g) : make_float2(0.f, 0.f);
+    x[(vx << logc) + c] = make_float2(v.x, -v.y);
+  }
+  __syncthreads();
+  fft::fft_seq<LOGN>(x, stw, logc);
+  for (int e = threadIdx.x; e < (N << logc); e += blockDim.x) {
+    const int c = e >> LOGN, xx = e & (N - 1);
+    A[(int64_t)(vy0 + c) * N + xx] = x[(fft::fslot<LOGN>(xx) << logc) + c];
+  }
+}
+
+__device__ __forceinline__ float2 inv_principal_sqrt(float2 o0) {
+  // 1 / sqrt(o_0), principal branch (eq:extract; R13); 1 if o_0 == 0
+  const double a = o0.x, b = o0.y, r = hypot(a, b);
+  if (!(r > 0)) return make_float2(1.f, 0.f);
+  const double s = sqrt(0.5 * (r + fabs(a)));
+  double wr, wi;
+  if (a >= 0) { wr = s; wi = b / (2 * s); } else { wr = fabs(b) / (2 * s); wi = copysign(s, b); }
+  const double d = wr * wr + wi * wi;
+  return make_float2((float)(wr / d), (float)(-wi / d));
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(256) img_cols_kernel(const float2* __restrict__ A, const float2* __restrict__ tw,
+                                                       float2* __restrict__ out, int Sx, int logc, float scale,
+                                                       const float2* __restrict__ op, int tiles, int64_t n_act,
+                                                       int64_t g_dc, int normalize) {
+  constexpr int N = 1 << LOGN;     // Sy
+  extern __shared__ __align__(16) float2 fsm[];
+  const int cnt = 1 << logc;
+  float2* x = fsm;                 // [N][cnt]: x[vy * cnt + c] = A[vy][x0 + c]
+  float2* stw = fsm + (N << logc);
+  const int x0 = blockIdx.x << logc;
+  for (int i = threadIdx.x; i < N / 2; i += blockDim.x) stw[i] = __ldg(tw + i);
+  for (int e = threadIdx.x; e < (N << logc); e += blockDim.x) {
+    const int vy = e >> logc, c = e & (cnt - 1);
+    x[e] = __ldg(A + (int64_t)vy * Sx + x0 + c);
+  }
+  __syncthreads();
+  fft::fft_seq<LOGN>(x, stw, logc);
+  float2 f = make_float2(scale, 0.f);
+  if (normalize) {
+    const float2 w = inv_principal_sqrt(sum_tiles(op, tiles, n_act, g_dc));
+    f = make_float2(w.x * scale, w.y * scale);
+  }
+  for (int e = threadIdx.x; e < (N << logc); e += blockDim.x) {
+    const int y = e >> logc, c = e & (cnt - 1);
+    out[(int64_t)y * Sx + x0 + c] = cmul(x[(fft::fslot<LOGN>(y) << logc) + c], f);
+  }
+}
+
+bool finalize_uses_fft(const Plan& p) {
+  return is_pow2(p.Sx) && is_pow2(p.Sy) && p.Sx >= 2 && p.Sy >= 2 && p.Sx <= (1 << kFftMaxLog) &&
+         p.Sy <= (1 << kFftMaxLog);
+}
+
+cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st) {
+  const int64_t S = p.S;
+  if (finalize_uses_fft(p)) {
+    // rows: 2^lr rows per CTA (<= 32 KB of shared memory, at least 16 CTAs when the image allows)
+    const int lx = ilog2(p.Sx), ly = ilog2(p.Sy);
+    int lr = std::max(0, std::min(ilog2(std::max(1, 4096 / p.Sx)), ly - 4));
+    cudaError_t e = with_log(lx, [&](auto LN) {
+      constexpr int L = decltype(LN)::value;
+      const size_t smem = ((size_t)p.Sx << lr) * 8 + (size_t)p.Sx / 2 * 8 + 16;
+      img_rows_kernel<L><<<p.Sy >> lr, 256, smem, st>>>(op, tiles, p.n_act, p.d_gidx, p.d_twx, p.d_img_tmp, lr);
+      return cudaGetLastError();
+    });
+    if (e != cudaSuccess) return e;
+    int lc = std::max(0, std::min(ilog2(std::max(1, 4096 / p.Sy)), lx - 4));
+    return with_log(ly, [&](auto LN) {
+      constexpr int L = decltype(LN)::value;
+      const size_t smem = ((size_t)p.Sy << lc) * 8 + (size_t)p.Sy / 2 * 8 + 16;
+      img_cols_kernel<L><<<p.Sx >> lc, 256, smem, st>>>(p.d_img_tmp, p.d_twy, out, p.Sx, lc,
+                                                        (float)(1.0 / std::sqrt((double)S)), op, tiles, p.n_act,
+                                                        p.g_dc, p.normalize);
+      return cudaGetLastError();
+    });
+  }
+  scatter_kernel<<<(unsigned)((p.n_act + 255) / 256), 256, 0, st>>>(op, tiles, p.d_vpos, p.n_act, p.d_spec);
   if (cufftSetStream(p.fft, st) != CUFFT_SUCCESS) return cudaErrorUnknown;
   if (cufftExecC2C(p.fft, reinterpret_cast<cufftComplex*>(p.d_spec), reinterpret_cast<cufftComplex*>(out),
                    CUFFT_INVERSE) != CUFFT_SUCCESS)
     return cudaErrorUnknown;
-  const int64_t S = p.S;
   conj_scale_kernel<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(out, S, 1.0 / std::sqrt((double)S), p.d_spec,
                                                                  p.normalize);
   return cudaGetLastError();

@@ -374,7 +374,19 @@ wdd_status flush(Plan& p) {
   }
   {
     Prof pr(p, kSlotFlush, p.stream);
-    CUDA_TRY(launch_flush(p, dr, n_rows, p.stream));
+    CUDA_TRY(launch_flush(p, dr, n_rows, p.G_zero, p.stream));
+  }
+  p.G_zero = false;
+  p.opart_tiles = flush_uses_fft(p, n_rows) ? colfft_tiles(p) : 0;
+  return WDD_OK;
+}
+
+// Make the memory of G hold its logical value (after a reset nothing has been written yet).
+wdd_status materialize_G(Plan& p) {
+  if (p.G_zero) {
+    CUDA_TRY(cudaMemsetAsync(p.d_G, 0, (size_t)p.n_act * p.K * sizeof(float2), p.stream));
+    p.G_zero = false;
+    p.opart_tiles = 0;
   }
   return WDD_OK;
 }
@@ -385,8 +397,8 @@ void free_plan(Plan* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   cudaDeviceSynchronize();
   if (p->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(p->nccl));
-  void* bufs[] = {p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
-                  p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec,
+  void* bufs[] = {p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
+                  p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec, p->d_img_tmp,
                   p->d_meta, p->d_stage[0], p->d_stage[1]};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -397,6 +409,8 @@ void free_plan(Plan* p) {
   for (auto& e : p->meta_ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : p->stage_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : p->copy_ev)
     if (e) cudaEventDestroy(e);
   for (auto e : p->ev_pool) cudaEventDestroy(e);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
@@ -523,6 +537,10 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   }
   std::vector<float> psi32(p->basis.begin(), p->basis.end());
   std::vector<int32_t> vpos(act.begin(), act.end());
+  std::vector<int32_t> gidx((size_t)p->S, -1);
+  for (size_t g = 0; g < act.size(); ++g) gidx[(size_t)act[g]] = (int32_t)g;
+  if (gidx[0] < 0) return bail(fail(WDD_E_ARG, "v = 0 is not active (empty aperture?)"));
+  p->g_dc = gidx[0];
   p->chunk_cap = 8192;
   p->mask_words = (Sx + 31) / 32;
   p->meta_slot_bytes = std::max((size_t)p->chunk_cap, (size_t)Sy * (1 + p->mask_words) + 4) * sizeof(int32_t);
@@ -550,7 +568,11 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ALLOC(p->d_vpos, act.size() * 4);
   ALLOC(p->d_flush_tiles, p->flush_tiles.size() * sizeof(int2));
   ALLOC(p->d_o, act.size() * sizeof(float2));
+  p->opart_cap = std::max(1, colfft_tiles(*p));
+  ALLOC(p->d_opart, (size_t)p->opart_cap * act.size() * sizeof(float2));
+  ALLOC(p->d_gidx, (size_t)p->S * sizeof(int32_t));
   ALLOC(p->d_spec, (size_t)p->S * sizeof(float2));
+  ALLOC(p->d_img_tmp, (size_t)p->S * sizeof(float2));
   ALLOC(p->d_meta, 2 * p->meta_slot_bytes);
 #undef ALLOC
   if (cudaMallocHost(&p->h_meta, 2 * p->meta_slot_bytes) != cudaSuccess)
@@ -559,6 +581,8 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(fail(WDD_E_CUDA, "event"));
   for (auto& e : p->stage_ev)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(fail(WDD_E_CUDA, "event"));
+  for (auto& e : p->copy_ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(fail(WDD_E_CUDA, "event"));
   auto up = [&](void* d, const void* h, size_t b) { return cudaMemcpy(d, h, b, cudaMemcpyHostToDevice) == cudaSuccess; };
   bool ok = up(p->d_Bpack, bpack.data(), bpack.size() * 2) && up(p->d_psi, psi32.data(), psi32.size() * 4) &&
             up(p->d_Fx, Fx.data(), Fx.size() * sizeof(float2)) && up(p->d_Fy, Fy.data(), Fy.size() * sizeof(float2)) &&
@@ -566,6 +590,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
             up(p->d_col_vx, p->col_vx.data(), p->col_vx.size() * sizeof(int32_t)) &&
             up(p->d_W, W.data(), W.size() * sizeof(float2)) && up(p->d_act_vy, p->act_vy.data(), act.size() * 4) &&
             up(p->d_col_off, p->col_off.data(), p->col_off.size() * 4) && up(p->d_vpos, vpos.data(), act.size() * 4) &&
+            up(p->d_gidx, gidx.data(), gidx.size() * 4) &&
             up(p->d_flush_tiles, p->flush_tiles.data(), p->flush_tiles.size() * sizeof(int2));
   ok = ok && cudaMemset(p->d_G, 0, W.size() * sizeof(float2)) == cudaSuccess &&
        cudaMemset(p->d_Call, 0, (size_t)p->S * K * sizeof(float)) == cudaSuccess &&
@@ -622,24 +647,21 @@ wdd_status wdd_ingest_host(wdd_plan_t plan, const void* frames_host, const int32
     CUDA_TRY(cudaMalloc(&p.d_stage[1], stage_frames * fb));
     CUDA_TRY(cudaStreamCreateWithFlags(&p.copy_stream, cudaStreamNonBlocking));
   }
-  cudaEvent_t copied[2];
-  CUDA_TRY(cudaEventCreateWithFlags(&copied[0], cudaEventDisableTiming));
-  CUDA_TRY(cudaEventCreateWithFlags(&copied[1], cudaEventDisableTiming));
-  int slot = 0;
-  for (int64_t c0 = 0; c0 < n; c0 += stage_frames, slot ^= 1) {
+  for (int64_t c0 = 0; c0 < n; c0 += stage_frames) {
+    const int slot = p.stage_slot;
+    p.stage_slot ^= 1;
     const int64_t nc = std::min<int64_t>(stage_frames, n - c0);
     CUDA_TRY(cudaStreamWaitEvent(p.copy_stream, p.stage_ev[slot], 0));  // previous user of the slot done
     CUDA_TRY(cudaMemcpyAsync(p.d_stage[slot], static_cast<const uint8_t*>(frames_host) + (size_t)c0 * fb, nc * fb,
                              cudaMemcpyHostToDevice, p.copy_stream));
-    CUDA_TRY(cudaEventRecord(copied[slot], p.copy_stream));
-    CUDA_TRY(cudaStreamWaitEvent(p.stream, copied[slot], 0));
+    CUDA_TRY(cudaEventRecord(p.copy_ev[slot], p.copy_stream));
+    CUDA_TRY(cudaStreamWaitEvent(p.stream, p.copy_ev[slot], 0));
     s = enqueue_chunk(p, p.d_stage[slot], scan_idx_host + c0, nc);
     if (s != WDD_OK) return s;
     CUDA_TRY(cudaEventRecord(p.stage_ev[slot], p.stream));
   }
-  CUDA_TRY(cudaStreamSynchronize(p.copy_stream));
-  cudaEventDestroy(copied[0]);
-  cudaEventDestroy(copied[1]);
+  // the H2D copies stay asynchronous: the plan stream waits for them, and the caller keeps the
+  // host buffer valid until that stream has passed this call (as for device frames)
   p.frames_ingested += n;
   return WDD_OK;
 }
@@ -651,26 +673,36 @@ wdd_status wdd_readout(wdd_plan_t plan, void* complex_out_dev) {
   CUDA_TRY(cudaSetDevice(p.device));
   wdd_status s = flush(p);
   if (s != WDD_OK) return s;
-  const float2* G = p.d_G;
-  const bool multi = p.nranks > 1;
-  if (multi && p.combine == 1) {
-    NCCL_TRY(ncclAllReduce(p.d_G, p.d_Gsum, (size_t)p.n_act * p.K * 2, ncclFloat, ncclSum,
-                           reinterpret_cast<ncclComm_t>(p.nccl), p.stream));
-    G = p.d_Gsum;
-  }
-  {
+  const float2* op = p.d_opart;
+  int tiles = p.opart_tiles;
+  if (p.nranks > 1) {
+    // multi-rank: every rank reduces its partial accumulator the same way, then NCCL sums
+    if ((s = materialize_G(p)) != WDD_OK) return s;
+    const float2* G = p.d_G;
+    if (p.combine == 1) {
+      NCCL_TRY(ncclAllReduce(p.d_G, p.d_Gsum, (size_t)p.n_act * p.K * 2, ncclFloat, ncclSum,
+                             reinterpret_cast<ncclComm_t>(p.nccl), p.stream));
+      G = p.d_Gsum;
+    }
+    {
+      Prof pr(p, kSlotReadout, p.stream);
+      CUDA_TRY(launch_readout(p, G, p.d_o, p.stream));
+    }
+    if (p.combine == 0)
+      NCCL_TRY(ncclAllReduce(p.d_o, p.d_o, (size_t)p.n_act * 2, ncclFloat, ncclSum,
+                             reinterpret_cast<ncclComm_t>(p.nccl), p.stream));
+    op = p.d_o;
+    tiles = 1;
+  } else if (tiles == 0) {
+    // no fused partial readout for the current G (after a DFT-matrix flush, or nothing flushed)
+    if ((s = materialize_G(p)) != WDD_OK) return s;
     Prof pr(p, kSlotReadout, p.stream);
-    CUDA_TRY(launch_readout(p, G, !multi || p.combine == 1, p.stream));
-  }
-  if (multi && p.combine == 0) {
-    NCCL_TRY(ncclAllReduce(p.d_o, p.d_o, (size_t)p.n_act * 2, ncclFloat, ncclSum, reinterpret_cast<ncclComm_t>(p.nccl),
-                           p.stream));
-    Prof pr(p, kSlotReadout, p.stream);
-    CUDA_TRY(launch_scatter(p, p.stream));
+    CUDA_TRY(launch_readout(p, p.d_G, p.d_opart, p.stream));
+    p.opart_tiles = tiles = 1;
   }
   {
     Prof pr(p, kSlotFinalize, p.stream);
-    CUDA_TRY(launch_finalize(p, static_cast<float2*>(complex_out_dev), p.stream));
+    CUDA_TRY(launch_finalize(p, op, tiles, static_cast<float2*>(complex_out_dev), p.stream));
   }
   return WDD_OK;
 }
@@ -700,6 +732,7 @@ wdd_status wdd_get_accumulator(wdd_plan_t plan, void* G_out_dev, int32_t* active
   if (active_v_host) std::memcpy(active_v_host, p.active_v.data(), p.active_v.size() * 4);
   if (G_out_dev) {
     wdd_status s = flush(p);
+    if (s == WDD_OK) s = materialize_G(p);
     if (s != WDD_OK) return s;
     CUDA_TRY(cudaMemcpyAsync(G_out_dev, p.d_G, (size_t)p.n_act * p.K * sizeof(float2), cudaMemcpyDeviceToDevice, p.stream));
   }
@@ -710,7 +743,8 @@ wdd_status wdd_reset(wdd_plan_t plan) {
   if (check_plan(plan)) return WDD_E_ARG;
   Plan& p = *P(plan);
   CUDA_TRY(cudaSetDevice(p.device));
-  CUDA_TRY(cudaMemsetAsync(p.d_G, 0, (size_t)p.n_act * p.K * sizeof(float2), p.stream));
+  p.G_zero = true;          // the next flush writes G instead of accumulating (no clearing pass)
+  p.opart_tiles = 0;
   // coefficients of frames ingested but never flushed are simply forgotten: only pending
   // positions are ever read from the coefficient store
   std::fill(p.seen.begin(), p.seen.end(), 0);

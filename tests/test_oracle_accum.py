@@ -72,3 +72,38 @@ def test_zero_frame_leaves_accumulator_unchanged():
     a = O.accumulate_fft(C, idx, Sy, Sx)
     b = O.accumulate_fft(np.vstack([C, np.zeros((1, K))]), np.r_[idx, 9], Sy, Sx)
     assert np.array_equal(a, b)
+
+
+def test_accumulate_at_equals_fft_rows():
+    # G at selected frequencies (explicit phase rows, integer angle reduction) == the rows of the
+    # FFT-computed G (a different algorithm) on a non-square scan with a random index subset.
+    rng = np.random.default_rng(11)
+    Sy, Sx, K = 12, 20, 6
+    idx = rng.permutation(Sy * Sx)[:150]
+    C = _rand_C(rng, len(idx), K)
+    v = rng.choice(Sy * Sx, size=17, replace=False)
+    assert np.max(np.abs(O.accumulate_at(C, idx, v, Sy, Sx) - O.accumulate_fft(C, idx, Sy, Sx)[v])) < 1e-12
+
+
+def test_scan_phase_large_indices_exact_reduction():
+    # At 1024 x 1024 the integer-reduced phase must agree with the explicitly reduced angle
+    # (vy*sy mod Sy is exact in int64), and |f_s[v]| = 1/sqrt(S) for every entry.
+    Sy = Sx = 1024
+    v = np.array([1023 * Sx + 1023, 511 * Sx + 3, 0])
+    s = np.array([1023 * Sx + 1022, 7, 1024 * 1024 - 1])
+    f = O.scan_phase(v, s, Sy, Sx)
+    assert np.allclose(np.abs(f), 1.0 / 1024, rtol=0, atol=1e-15)
+    vy, vx, sy, sx = v[:, None] // Sx, v[:, None] % Sx, s[None] // Sx, s[None] % Sx
+    ang = 2 * np.pi * ((vy * sy % Sy) / Sy + (vx * sx % Sx) / Sx)
+    assert np.max(np.abs(f - np.exp(-1j * ang) / 1024)) < 1e-15
+
+
+def test_project_events_equals_dense_projection():
+    # the sparse-event form of H equals the dense projection of the same frames
+    from synth.sparse import dense_frames_numpy, sparse_events
+    Q, L = 32, 8
+    Psi = O.hg_basis(Q, L, math.sqrt(Q / (2 * math.pi)))
+    pix, cnt = sparse_events(5, np.arange(40), Q, events=9)
+    pix[0, 1] = pix[0, 0]                       # a duplicated pixel must add
+    dense = dense_frames_numpy(pix, cnt, Q).astype(np.float64)
+    assert np.max(np.abs(O.project_events(pix, cnt, Psi) - O.vec(O.project(dense, Psi)))) < 1e-10
