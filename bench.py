@@ -178,6 +178,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="wdd", choices=["wdd", "reference"])
     ap.add_argument("--config", default="medium")
+    ap.add_argument("--batch", type=int, default=0, help="override the workload's batch (experiments only)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-frames", type=int, default=2048)
@@ -199,7 +200,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg = CONFIGS[args.config]
-    batch = cfg.batch or cfg.S
+    batch = args.batch or cfg.batch or cfg.S
     rows = np.array_split(np.arange(cfg.Sy), world)[rank]
     idx = (rows[:, None] * cfg.Sx + np.arange(cfg.Sx)[None, :]).reshape(-1).astype(np.int32)
     frames = Acquisition(cfg).frames_parallel(idx)

@@ -24,40 +24,50 @@ __host__ __device__ constexpr int brev_c(int v, int bits) {
   return r;
 }
 
-// W_N^m for 0 <= m < N from the half table tw[m] = exp(-2 pi i m / N), m < N/2.
-__device__ __forceinline__ float2 twiddle(const float2* tw, int m, int half_n) {
-  const float2 w = tw[m < half_n ? m : m - half_n];
-  return m < half_n ? w : make_float2(-w.x, -w.y);
+// cos / sin of 2 pi q / 32, q < 16, as compile-time constants (float-rounded exact values)
+__host__ __device__ constexpr float cos32(int q) {
+  return q == 0 ? 1.f : q == 1 ? 9.807852804e-01f : q == 2 ? 9.238795325e-01f : q == 3 ? 8.314696123e-01f
+       : q == 4 ? 7.071067812e-01f : q == 5 ? 5.555702330e-01f : q == 6 ? 3.826834324e-01f : q == 7 ? 1.950903220e-01f
+       : q == 8 ? 0.f : q == 9 ? -1.950903220e-01f : q == 10 ? -3.826834324e-01f : q == 11 ? -5.555702330e-01f
+       : q == 12 ? -7.071067812e-01f : q == 13 ? -8.314696123e-01f : q == 14 ? -9.238795325e-01f : -9.807852804e-01f;
+}
+// v * W_32^q = v * exp(-2 pi i q / 32) with q a compile-time constant after unrolling
+__device__ __forceinline__ float2 rot32(float2 v, int q) {
+  if (q == 0) return v;
+  if (q == 8) return make_float2(v.y, -v.x);                        // times -i
+  const float c = cos32(q), sn = q < 8 ? cos32(8 - q) : cos32(q - 8);
+  // exp(-i t) = cos t - i sin t; sin(2 pi q/32) = cos(2 pi (8 - q)/32) for q < 8, = cos(2 pi (q - 8)/32) for q >= 8
+  return make_float2(fmaf(v.x, c, v.y * sn), fmaf(v.y, c, -v.x * sn));
 }
 
-// One radix-2 DIT stage (butterfly span LEN) of an in-register DFT of R points; recursion over
-// LEN keeps every register index a compile-time constant.
+// One radix-2 DIT stage (butterfly span LEN) of an in-register DFT of R <= 32 points; recursion
+// over LEN keeps every register index and twiddle a compile-time constant.
 template <int R, int LEN>
-__device__ __forceinline__ void dft_stage(float2 (&v)[R], const float2* tw, int stride) {
+__device__ __forceinline__ void dft_stage(float2 (&v)[R]) {
   if constexpr (LEN <= R) {
 #pragma unroll
     for (int i = 0; i < R; i += LEN) {
 #pragma unroll
       for (int j = 0; j < LEN / 2; ++j) {
         const float2 a = v[i + j];
-        const float2 b = j == 0 ? v[i + j + LEN / 2] : cmul(v[i + j + LEN / 2], tw[j * (R / LEN) * stride]);
+        const float2 b = rot32(v[i + j + LEN / 2], j * (32 / LEN));   // W_LEN^j = W_32^{32 j / LEN}
         v[i + j] = make_float2(a.x + b.x, a.y + b.y);
         v[i + j + LEN / 2] = make_float2(a.x - b.x, a.y - b.y);
       }
     }
-    dft_stage<R, 2 * LEN>(v, tw, stride);
+    dft_stage<R, 2 * LEN>(v);
   }
 }
 
-// In-register forward DFT of R = 2^LR points (natural order in and out).  W_R^j is read from
-// the length-N half table as tw[j * stride] with stride = N / R (a warp-uniform broadcast).
+// In-register forward DFT of R = 2^LR <= 32 points (natural order in and out).
 template <int LR>
-__device__ __forceinline__ void dft_reg(float2 (&v)[1 << LR], const float2* tw, int stride) {
+__device__ __forceinline__ void dft_reg(float2 (&v)[1 << LR]) {
+  static_assert(LR <= 5, "register DFT up to 32 points");
   constexpr int R = 1 << LR;
   float2 u[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) u[i] = v[brev_c(i, LR)];
-  dft_stage<R, 2>(u, tw, stride);
+  dft_stage<R, 2>(u);
 #pragma unroll
   for (int i = 0; i < R; ++i) v[i] = u[i];
 }
@@ -76,22 +86,23 @@ __device__ __forceinline__ int fslot(int f) {
 
 // Forward DFT (unnormalised, e^{-2 pi i}) of 2^logc interleaved sequences of length N = 2^LOGN
 // stored in shared memory as x[n * cnt + c] (sequence index fastest: a warp touches consecutive
-// addresses).  Input in natural order; frequency f ends at slot fslot<LOGN>(f).  tw = the N/2
-// half table in shared memory.  Starts and ends with the block synchronised.
+// addresses).  Input in natural order; frequency f ends at slot fslot<LOGN>(f).  tw = the full
+// table tw[m] = exp(-2 pi i m / N), m < N, in shared memory (only the step-2 twiddles W_N^{n2 k1}
+// read it).  Starts and ends with the block synchronised.
 template <int LOGN>
 __device__ __forceinline__ void fft_seq(float2* x, const float2* tw, int logc) {
   using S = Split<LOGN>;
-  constexpr int N1 = S::N1, N2 = S::N2, HN = (1 << LOGN) / 2;
+  constexpr int N1 = S::N1, N2 = S::N2;
   const int cnt = 1 << logc;
   for (int t = threadIdx.x; t < (N2 << logc); t += blockDim.x) {
     const int c = t & (cnt - 1), n2 = t >> logc;
     float2 v[N1];
 #pragma unroll
     for (int n1 = 0; n1 < N1; ++n1) v[n1] = x[((N2 * n1 + n2) << logc) + c];
-    dft_reg<S::L1>(v, tw, N2);
+    dft_reg<S::L1>(v);
     if (N2 > 1) {
 #pragma unroll
-      for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], twiddle(tw, n2 * k1, HN));
+      for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], tw[n2 * k1]);
     }
 #pragma unroll
     for (int k1 = 0; k1 < N1; ++k1) x[((N2 * k1 + n2) << logc) + c] = v[k1];
@@ -103,7 +114,7 @@ __device__ __forceinline__ void fft_seq(float2* x, const float2* tw, int logc) {
       float2 v[N2];
 #pragma unroll
       for (int n2 = 0; n2 < N2; ++n2) v[n2] = x[((N2 * k1 + n2) << logc) + c];
-      dft_reg<S::L2>(v, tw, N1);
+      dft_reg<S::L2>(v);
 #pragma unroll
       for (int k2 = 0; k2 < N2; ++k2) x[((N2 * k1 + k2) << logc) + c] = v[k2];
     }

@@ -41,8 +41,8 @@ struct Plan {
   float* d_psi = nullptr;             // Q*L f32
   float2* d_Fx = nullptr;             // n_vx * Sx
   float2* d_Fy = nullptr;             // Sy * Sy
-  float2* d_twx = nullptr;            // Sx/2 FFT twiddles exp(-2 pi i m / Sx) (power-of-two Sx)
-  float2* d_twy = nullptr;            // Sy/2 FFT twiddles exp(-2 pi i m / Sy) (power-of-two Sy)
+  float2* d_twx = nullptr;            // Sx FFT twiddles exp(-2 pi i m / Sx), m < Sx
+  float2* d_twy = nullptr;            // Sy FFT twiddles exp(-2 pi i m / Sy), m < Sy
   int32_t* d_col_vx = nullptr;        // n_vx active vx, ascending
   float2* d_W = nullptr;              // n_act * K
   float2* d_G = nullptr;              // n_act * K

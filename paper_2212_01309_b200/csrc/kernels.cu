@@ -23,6 +23,7 @@
 #include <type_traits>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -153,6 +154,7 @@ struct ProjArgs {
   const uint4* Bpack;
   float sc1;   // acc1 -> fp16 A2 scale   (2^(eT - s))
   float sc2;   // acc2 -> C scale          (2^(-s - eT))
+  int pdl_wait_end;   // 1: complete only after the preceding grid (keeps stream order for later launches)
 };
 
 // Stage-1 tile tt of group g: first frame-matrix row and the number of valid rows.
@@ -200,7 +202,9 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   // ---- setup: barriers and TMEM only, so the TMA producer can start streaming at once; the basis
   // operand image arrives by one bulk copy that only the MMA issuers wait for
   if (tid == 0) {
-    for (int i = 0; i < Cfg::kNS; ++i) { mbar_init(&raw_full[i], 1); mbar_init(&raw_empty[i], 1); }
+    // u16: each of the 4 converter warps releases its 32 rows of a raw slot as soon as it has them
+    // in registers (f32: the stage-1 MMA commit releases the slot)
+    for (int i = 0; i < Cfg::kNS; ++i) { mbar_init(&raw_full[i], 1); mbar_init(&raw_empty[i], U16 ? 4 : 1); }
     for (int i = 0; i < kNA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
     mbar_init(&p1_empty[0], 1);
     mbar_init(&p1_empty[1], 1);
@@ -298,6 +302,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   } else if (warp == 2) {
     // ================= TMA producer (u16 frames)
     if (U16 && lane == 0) {
+      const uint64_t pol = policy_evict_first();   // frames are read exactly once
       uint32_t slot = 0, sphase = 0;
       for (int64_t gi = 0; gi < my_groups; ++gi) {
         const int64_t g = blockIdx.x + gi * gridDim.x;
@@ -309,7 +314,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
             mbar_wait(&raw_empty[slot], sphase ^ 1u);
             TRACE(2, slot);
             mbar_arrive_expect_tx(&raw_full[slot], Cfg::kSlotU);
-            tma_load_2d(ring + slot * Cfg::kSlot, &tmap, c * Cfg::kKC, (int)row0, &raw_full[slot]);
+            tma_load_2d_hint(ring + slot * Cfg::kSlot, &tmap, c * Cfg::kKC, (int)row0, &raw_full[slot], pol);
             if (++slot == Cfg::kNS) { slot = 0; sphase ^= 1u; }
           }
         }
@@ -354,6 +359,12 @@ __global__ void __launch_bounds__(kProjThreads, 1)
 #pragma unroll
             for (int q = 0; q < kW; ++q) hi_or |= w[q];
             resid = (hi_or & 0xFC00FC00u) != 0u;
+            // a warp with no count >= 1024 never re-reads its rows: release them now
+            const bool warp_resid = __any_sync(0xffffffffu, resid);
+            if (!warp_resid) {
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&raw_empty[slot]);
+            }
 #pragma unroll
             for (int q = 0; q < kW; ++q) w[q] = magic_half2(w[q] & 0x03FF03FFu) | 0u;
             mbar_wait(&a_empty[aslot], aphase ^ 1u);
@@ -372,14 +383,18 @@ __global__ void __launch_bounds__(kProjThreads, 1)
               tc_fence_after();
 #pragma unroll
               for (int j = 0; j < kW / 4; ++j) {
-                int off = row * Cfg::kSpan + j * 16;
-                off ^= ((off >> 7) & Cfg::kSwzMask) << 4;
-                const uint4 v = *reinterpret_cast<const uint4*>(src + off);
-                // (bits 10-15) * 1024 is exact in fp16 (<= 64512): accumulates into the same acc
-                w[4 * j] = hi_plane(v.x);
-                w[4 * j + 1] = hi_plane(v.y);
-                w[4 * j + 2] = hi_plane(v.z);
-                w[4 * j + 3] = hi_plane(v.w);
+                if (warp_resid) {   // (warps without high bits released their rows: their plane is 0)
+                  int off = row * Cfg::kSpan + j * 16;
+                  off ^= ((off >> 7) & Cfg::kSwzMask) << 4;
+                  const uint4 v = *reinterpret_cast<const uint4*>(src + off);
+                  // (bits 10-15) * 1024 is exact in fp16 (<= 64512): accumulates into the same acc
+                  w[4 * j] = hi_plane(v.x);
+                  w[4 * j + 1] = hi_plane(v.y);
+                  w[4 * j + 2] = hi_plane(v.z);
+                  w[4 * j + 3] = hi_plane(v.w);
+                } else {
+                  w[4 * j] = w[4 * j + 1] = w[4 * j + 2] = w[4 * j + 3] = 0u;
+                }
               }
 #pragma unroll
               for (int q = 0; q < kW; q += 16) tmem_st16(tbase + lane_addr + Cfg::tP1 + cg * Cfg::kACols + q, w + q);
@@ -387,8 +402,11 @@ __global__ void __launch_bounds__(kProjThreads, 1)
               tc_fence_before();
               named_sync(bar_id, kConv);
             }
+            if (warp_resid) {                             // second plane done: release the rows
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&raw_empty[slot]);
+            }
             if (ct == 0) {
-              mbar_arrive(&raw_empty[slot]);            // raw slot fully read
               meta[aslot] = any ? 1u : 0u;
               mbar_arrive(&a_full[aslot]);
               TRACE(4, aslot);
@@ -524,7 +542,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tbase);
-  pdl_wait();   // this grid completes only after the preceding (row-DFT) grid has completed
+  if (a.pdl_wait_end) pdl_wait();   // this grid completes only after the preceding grid has completed
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link needed)
@@ -586,7 +604,9 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
-  ProjArgs a{frames, n, C, idx, g2, reinterpret_cast<const uint4*>(p.d_Bpack), (float)p.sc1, (float)p.sc2};
+  static const int no_wait = [] { const char* e = std::getenv("WDD_PROJ_NO_PDLWAIT"); return e ? std::atoi(e) : 0; }();
+  ProjArgs a{frames, n, C, idx, g2, reinterpret_cast<const uint4*>(p.d_Bpack), (float)p.sc1, (float)p.sc2,
+             no_wait ? 0 : 1};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kProjThreads);
@@ -684,25 +704,30 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) rowfft_kernel(const fl
   constexpr int Sx = 1 << LOGN;
   extern __shared__ __align__(16) float2 fsm[];
   __shared__ uint32_t smask[(Sx + 31) / 32];
+  __shared__ int2 sslot[Sx];             // (slot of v, slot of -v) per active column j
   const int P = 1 << logP;
   float2* x = fsm;                       // [Sx][P]
-  float2* stw = fsm + (Sx << logP);      // [Sx/2]
+  float2* stw = fsm + (Sx << logP);      // [Sx] twiddles
   const int r = blockIdx.y, sy = __ldg(rows + r), k0 = blockIdx.x * 2 * P;
-  for (int i = threadIdx.x; i < Sx / 2; i += blockDim.x) stw[i] = __ldg(tw + i);
+  for (int i = threadIdx.x; i < Sx; i += blockDim.x) stw[i] = __ldg(tw + i);
+  for (int j = threadIdx.x; j < n_vx; j += blockDim.x) {
+    const int v = __ldg(col_vx + j);
+    sslot[j] = make_int2(fft::fslot<LOGN>(v), fft::fslot<LOGN>((Sx - v) & (Sx - 1)));
+  }
   if (threadIdx.x < mask_words) smask[threadIdx.x] = __ldg(masks + (int64_t)r * mask_words + threadIdx.x);
   __syncthreads();
   const float2* Crow = reinterpret_cast<const float2*>(C + (int64_t)sy * Sx * K + k0);
   const int total = Sx << logP;
-  for (int base = 0; base < total; base += kU * 256) {
+  for (int base = 0; base < total; base += kU * (int)blockDim.x) {
     float2 v[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int e = base + u * 256 + threadIdx.x;
+      const int e = base + u * (int)blockDim.x + threadIdx.x;
       v[u] = e < total ? __ldg(Crow + (int64_t)(e >> logP) * (K >> 1) + (e & (P - 1))) : make_float2(0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int e = base + u * 256 + threadIdx.x;
+      const int e = base + u * (int)blockDim.x + threadIdx.x;
       if (e < total) {
         const int sx = e >> logP;
         x[e] = ((smask[sx >> 5] >> (sx & 31)) & 1u) ? v[u] : make_float2(0.f, 0.f);
@@ -714,8 +739,8 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) rowfft_kernel(const fl
   const float hs = 0.5f * scale;
   for (int e = threadIdx.x; e < (n_vx << logP); e += blockDim.x) {
     const int j = e >> logP, pp = e & (P - 1);
-    const int v = __ldg(col_vx + j), vm = (Sx - v) & (Sx - 1);
-    const float2 z = x[(fft::fslot<LOGN>(v) << logP) + pp], zm = x[(fft::fslot<LOGN>(vm) << logP) + pp];
+    const int2 sl = sslot[j];
+    const float2 z = x[(sl.x << logP) + pp], zm = x[(sl.y << logP) + pp];
     const float4 o = make_float4((z.x + zm.x) * hs, (z.y - zm.y) * hs, (z.y + zm.y) * hs, (zm.x - z.x) * hs);
     *reinterpret_cast<float4*>(R + ((int64_t)j * Sy + sy) * K + k0 + 2 * pp) = o;
   }
@@ -728,7 +753,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) rowfft_kernel(const fl
 // Wiener readout  opart[t][g] = sum_{k in tile t} G[g][k] K_g[k], so a readout never
 // re-reads G.  The partial sums are combined over tiles in a fixed order by the image transform.
 template <int LOGN>
-__global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) colfft_kernel(const float2* __restrict__ R, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, LOGN <= 8 ? 3 : 2) colfft_kernel(const float2* __restrict__ R, const int32_t* __restrict__ rows,
                                                      int n_rows, const float2* __restrict__ tw,
                                                      const int32_t* __restrict__ col_off,
                                                      const int32_t* __restrict__ act_vy, float2* __restrict__ G,
@@ -737,23 +762,28 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) colfft_kernel(const fl
   constexpr int Sy = 1 << LOGN;
   extern __shared__ __align__(16) float2 fsm[];
   const int KT = 1 << logKT;
+  __shared__ int srow[Sy];                // staged rows
+  __shared__ int svy[Sy];                 // slot of each active vy of column j
   float2* x = fsm;                       // [Sy][KT]
-  float2* stw = fsm + (Sy << logKT);     // [Sy/2]
+  float2* stw = fsm + (Sy << logKT);     // [Sy] twiddles
   const int j = blockIdx.y, k0 = blockIdx.x * KT;
-  for (int i = threadIdx.x; i < Sy / 2; i += blockDim.x) stw[i] = __ldg(tw + i);
+  const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
+  for (int i = threadIdx.x; i < Sy; i += blockDim.x) stw[i] = __ldg(tw + i);
+  for (int i = threadIdx.x; i < n_rows; i += blockDim.x) srow[i] = __ldg(rows + i);
+  for (int i = threadIdx.x; i < mj; i += blockDim.x) svy[i] = fft::fslot<LOGN>(__ldg(act_vy + g0 + i));
   if (n_rows < Sy)
     for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x) x[e] = make_float2(0.f, 0.f);
   __syncthreads();
   const float2* Rj = R + (int64_t)j * Sy * K + k0;
   const int total = n_rows << logKT;
-  for (int base = 0; base < total; base += kU * 256) {
+  for (int base = 0; base < total; base += kU * (int)blockDim.x) {
     float2 v[kU];
     int dst[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int e = base + u * 256 + threadIdx.x;
+      const int e = base + u * (int)blockDim.x + threadIdx.x;
       const int rr = e >> logKT, kk = e & (KT - 1);
-      const int sy = e < total ? __ldg(rows + rr) : 0;
+      const int sy = e < total ? srow[rr] : 0;
       dst[u] = e < total ? (sy << logKT) + kk : -1;
       v[u] = e < total ? __ldg(Rj + (int64_t)sy * K + kk) : make_float2(0.f, 0.f);
     }
@@ -763,29 +793,28 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) colfft_kernel(const fl
   }
   __syncthreads();
   fft::fft_seq<LOGN>(x, stw, logKT);
-  const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
   const int tout = mj << logKT;
-  for (int base = 0; base < tout; base += kU * 256) {   // warp-uniform trip count (shuffles below)
+  for (int base = 0; base < tout; base += kU * (int)blockDim.x) {   // warp-uniform trip count (shuffles below)
     float2 o[kU], w[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int e = base + u * 256 + threadIdx.x;
+      const int e = base + u * (int)blockDim.x + threadIdx.x;
       const int64_t gi = (int64_t)(g0 + (e >> logKT)) * K + k0 + (e & (KT - 1));
       o[u] = (e < tout && !overwrite) ? G[gi] : make_float2(0.f, 0.f);
       w[u] = e < tout ? __ldg(W + gi) : make_float2(0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int e = base + u * 256 + threadIdx.x;
+      const int e = base + u * (int)blockDim.x + threadIdx.x;
       const int i = e >> logKT, kk = e & (KT - 1);
       float2 d = make_float2(0.f, 0.f);
       if (e < tout) {
-        const float2 z = x[(fft::fslot<LOGN>(__ldg(act_vy + g0 + i)) << logKT) + kk];
+        const float2 z = x[(svy[i] << logKT) + kk];
         const float2 gn = make_float2(fmaf(z.x, scale, o[u].x), fmaf(z.y, scale, o[u].y));
         G[(int64_t)(g0 + i) * K + k0 + kk] = gn;
         d = cmul(gn, w[u]);
       }
-      if (base + u * 256 < tout) {            // some lane of this block-row holds data
+      if (base + u * (int)blockDim.x < tout) {            // some lane of this block-row holds data
         for (int off = KT >> 1; off > 0; off >>= 1) {
           d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
           d.y += __shfl_xor_sync(0xffffffffu, d.y, off);
@@ -797,6 +826,14 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) colfft_kernel(const fl
 }
 
 static int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
+// tuning override "a,b" from the environment (unset: (-1, 0))
+static int2 env_pair(const char* name) {
+  const char* e = std::getenv(name);
+  int2 r = make_int2(-1, 0);
+  if (e) std::sscanf(e, "%d,%d", &r.x, &r.y);
+  return r;
+}
+
 static bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 constexpr int kFftSmem = 64 * 1024;   // FFT working set per CTA (the twiddle table is added)
 
@@ -894,9 +931,12 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
   if (n_rows <= 0) return cudaSuccess;
   if (is_pow2(p.Sx) && p.Sx >= 2 && p.Sx <= (1 << kFftMaxLog)) {
     const int logSx = ilog2(p.Sx);
+    static const int2 knob = env_pair("WDD_ROWFFT");   // (log2 k pairs per CTA, threads) override
     int logP = ilog2(std::max(1, std::min(32, kFftSmem / (8 * p.Sx))));   // k pairs per CTA
+    if (knob.x >= 0) logP = std::min(logP, knob.x);
+    const int nt = knob.y > 0 ? knob.y : 256;
     while ((2 << logP) > p.K || p.K % (2 << logP)) --logP;
-    const size_t smem = ((size_t)p.Sx << logP) * 8 + (size_t)p.Sx / 2 * 8 + 16;
+    const size_t smem = ((size_t)p.Sx << logP) * 8 + (size_t)p.Sx * 8 + 16;
     return with_log(logSx, [&](auto LN) {
       constexpr int LOGN = decltype(LN)::value;
       static bool init = false;
@@ -907,7 +947,7 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
         init = true;
       }
       dim3 grid(p.K / (2 << logP), n_rows);
-      rowfft_kernel<LOGN><<<grid, 256, smem, st>>>(p.d_Call, rows, masks, p.mask_words, p.d_twx, p.d_col_vx, p.d_R,
+      rowfft_kernel<LOGN><<<grid, nt, smem, st>>>(p.d_Call, rows, masks, p.mask_words, p.d_twx, p.d_col_vx, p.d_R,
                                                    logP, p.Sy, p.K, p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)));
       return cudaGetLastError();
     });
@@ -987,7 +1027,9 @@ __global__ void __launch_bounds__(256) flush_kernel(const float2* __restrict__ R
 }
 
 static int colfft_logkt(const Plan& p) {
+  static const int2 knob = env_pair("WDD_COLFFT");   // (log2 k per CTA, threads) override
   int logKT = ilog2(std::max(1, std::min(32, kFftSmem / (8 * p.Sy))));
+  if (knob.x >= 0) logKT = std::min(logKT, knob.x);
   while ((1 << logKT) > p.K || p.K % (1 << logKT)) --logKT;
   return logKT;
 }
@@ -1005,7 +1047,7 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
   if (flush_uses_fft(p, n_rows)) {
     const int logSy = ilog2(p.Sy);
     const int logKT = colfft_logkt(p);
-    const size_t smem = ((size_t)p.Sy << logKT) * 8 + (size_t)p.Sy / 2 * 8 + 16;
+    const size_t smem = ((size_t)p.Sy << logKT) * 8 + (size_t)p.Sy * 8 + 16;
     return with_log(logSy, [&](auto LN) {
       constexpr int LOGN = decltype(LN)::value;
       static bool init = false;
@@ -1016,7 +1058,8 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
         init = true;
       }
       dim3 grid(p.K >> logKT, p.n_vx);
-      colfft_kernel<LOGN><<<grid, 256, smem, st>>>(p.d_R, rows, n_rows, p.d_twy, p.d_col_off, p.d_act_vy, p.d_G,
+      static const int2 knob = env_pair("WDD_COLFFT");
+      colfft_kernel<LOGN><<<grid, knob.y > 0 ? knob.y : 256, smem, st>>>(p.d_R, rows, n_rows, p.d_twy, p.d_col_off, p.d_act_vy, p.d_G,
                                                    p.d_W, p.d_opart, p.n_act, logKT, p.K,
                                                    (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0);
       return cudaGetLastError();
@@ -1064,11 +1107,17 @@ cudaError_t launch_readout(const Plan& p, const float2* G, float2* o, cudaStream
 
 // o_v = sum over the `tiles` partial sums (fixed order), scattered to the dense spectrum
 __device__ __forceinline__ float2 sum_tiles(const float2* __restrict__ op, int tiles, int64_t n_act, int64_t g) {
-  float2 acc = __ldg(op + g);
-  for (int t = 1; t < tiles; ++t) {
-    const float2 v = __ldg(op + (int64_t)t * n_act + g);
-    acc.x += v.x;
-    acc.y += v.y;
+  float2 acc = make_float2(0.f, 0.f);
+  for (int t0 = 0; t0 < tiles; t0 += 8) {      // eight independent loads in flight, summed in order
+    float2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = t0 + u < tiles ? __ldg(op + (int64_t)(t0 + u) * n_act + g) : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc.x += v[u].x;
+      acc.y += v[u].y;
+    }
   }
   return acc;
 }
@@ -1120,7 +1169,7 @@ __global__ void __launch_bounds__(256) img_rows_kernel(const float2* __restrict_
   float2* x = fsm;                 // [N][cnt]: x[vx * cnt + c] = conj o[vy0 + c][vx]
   float2* stw = fsm + (N << logc);
   const int vy0 = blockIdx.x << logc;
-  for (int i = threadIdx.x; i < N / 2; i += blockDim.x) stw[i] = __ldg(tw + i);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) stw[i] = __ldg(tw + i);
   for (int e = threadIdx.x; e < (N << logc); e += blockDim.x) {
     const int c = e >> LOGN, vx = e & (N - 1);
     const int g = __ldg(gidx + (int64_t)(vy0 + c) * N + vx);
@@ -1157,7 +1206,7 @@ __global__ void __launch_bounds__(256) img_cols_kernel(const float2* __restrict_
   float2* x = fsm;                 // [N][cnt]: x[vy * cnt + c] = A[vy][x0 + c]
   float2* stw = fsm + (N << logc);
   const int x0 = blockIdx.x << logc;
-  for (int i = threadIdx.x; i < N / 2; i += blockDim.x) stw[i] = __ldg(tw + i);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) stw[i] = __ldg(tw + i);
   for (int e = threadIdx.x; e < (N << logc); e += blockDim.x) {
     const int vy = e >> logc, c = e & (cnt - 1);
     x[e] = __ldg(A + (int64_t)vy * Sx + x0 + c);
@@ -1188,7 +1237,7 @@ cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* 
     int lr = std::max(0, std::min(ilog2(std::max(1, 4096 / p.Sx)), ly - 4));
     cudaError_t e = with_log(lx, [&](auto LN) {
       constexpr int L = decltype(LN)::value;
-      const size_t smem = ((size_t)p.Sx << lr) * 8 + (size_t)p.Sx / 2 * 8 + 16;
+      const size_t smem = ((size_t)p.Sx << lr) * 8 + (size_t)p.Sx * 8 + 16;
       img_rows_kernel<L><<<p.Sy >> lr, 256, smem, st>>>(op, tiles, p.n_act, p.d_gidx, p.d_twx, p.d_img_tmp, lr);
       return cudaGetLastError();
     });
@@ -1196,7 +1245,7 @@ cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* 
     int lc = std::max(0, std::min(ilog2(std::max(1, 4096 / p.Sy)), lx - 4));
     return with_log(ly, [&](auto LN) {
       constexpr int L = decltype(LN)::value;
-      const size_t smem = ((size_t)p.Sy << lc) * 8 + (size_t)p.Sy / 2 * 8 + 16;
+      const size_t smem = ((size_t)p.Sy << lc) * 8 + (size_t)p.Sy * 8 + 16;
       img_cols_kernel<L><<<p.Sx >> lc, 256, smem, st>>>(p.d_img_tmp, p.d_twy, out, p.Sx, lc,
                                                         (float)(1.0 / std::sqrt((double)S)), op, tiles, p.n_act,
                                                         p.g_dc, p.normalize);

@@ -208,9 +208,9 @@ void twiddles(int n_out, const int32_t* freqs, int S, std::vector<float2>& F) {
     }
 }
 
-// FFT twiddles tw[m] = exp(-2 pi i m / N), m < N/2 (unscaled; the kernels apply 1/sqrt(N))
+// FFT twiddles tw[m] = exp(-2 pi i m / N), m < N (unscaled; the kernels apply 1/sqrt(N))
 void fft_twiddles(int N, std::vector<float2>& tw) {
-  tw.resize(std::max(1, N / 2));
+  tw.resize(std::max(1, N));
   for (int m = 0; m < (int)tw.size(); ++m) {
     const double ang = -2.0 * kPi * (double)m / (double)N;
     tw[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));

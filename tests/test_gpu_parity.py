@@ -103,6 +103,20 @@ def test_projection_high_counts_and_float(wdd, torch_cuda, Q, L):
     assert r < 1e-5 and mx < 1e-5, (r, mx)
 
 
+@pytest.mark.parametrize("Q,L", [(128, 16), (256, 32), (64, 8)])
+def test_projection_sparse_high_counts(wdd, torch_cuda, Q, L):
+    # counts >= 1024 in only a few detector rows: some converter warps need the second count
+    # plane while others have already released their rows (mixed per-warp paths)
+    base = CONFIGS["medium"].with_(Q=Q, L=L, Sy=16, Sx=16)
+    rng = np.random.default_rng(7 * Q + L)
+    fr = rng.poisson(3.0, size=(21, Q, Q)).astype(np.uint16)
+    for f in range(fr.shape[0]):
+        for _ in range(3):
+            fr[f, rng.integers(0, Q), rng.integers(0, Q)] = rng.integers(1024, 65535)
+    r, mx = _check_project(wdd, torch_cuda, base, fr)
+    assert r < 1e-5 and mx < 1e-5, (r, mx)
+
+
 def _ingest_batches(torch, plan, fr_dev, idx, batch):
     for a in range(0, len(idx), batch):
         plan.ingest(fr_dev[a:a + batch], idx[a:a + batch])

@@ -49,8 +49,10 @@ __global__ void __launch_bounds__(128, 1) k_tma(const __grid_constant__ CUtensor
   if (acc == 0x12345678u) *sink = acc;
 }
 
+constexpr int NSB = 6;
 __global__ void __launch_bounds__(128, 1) k_bulk(const uint8_t* src, int64_t n_pieces, unsigned long long* sink) {
   extern __shared__ __align__(1024) uint8_t sm[];
+  constexpr int NS = NSB;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + NS * 32768);
   if (threadIdx.x == 0) { for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1); asm volatile("fence.mbarrier_init.release.cluster;"); }
   __syncthreads();
@@ -112,14 +114,14 @@ int main() {
     return 1;
   }
   CK(cudaFuncSetAttribute(k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, NS * 16384 + 1024));
-  CK(cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, NS * 32768 + 1024));
+  CK(cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, NSB * 32768 + 1024));
   for (int grid_mul = 1; grid_mul <= 2; ++grid_mul) {
     for (int variant = 0; variant < 3; ++variant) {
       float best = 1e9;
       for (int r = 0; r < 6; ++r) {
         cudaEventRecord(e0);
         if (variant == 0) k_tma<<<sms * grid_mul, 128, NS * 16384 + 1024>>>(tm, N * Q / 128, 2, sink);
-        if (variant == 1 && grid_mul == 1) k_bulk<<<sms, 128, NS * 32768 + 1024>>>(d, (int64_t)(bytes / 32768), sink);
+        if (variant == 1 && grid_mul == 1) k_bulk<<<sms, 128, NSB * 32768 + 1024>>>(d, (int64_t)(bytes / 32768), sink);
         if (variant == 2) k_ldg<<<sms * 8 * grid_mul, 512>>>(reinterpret_cast<const uint4*>(d), (int64_t)(bytes / 16), sink);
         cudaEventRecord(e1);
         CK(cudaEventSynchronize(e1));
@@ -127,7 +129,7 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         if (r > 0 && ms < best) best = ms;
       }
-      const char* nm[3] = {"tma2d(64px x 128 rows, SW128, 8 x 16KB)", "bulk(32KB, 8 slots)", "ldg128"};
+      const char* nm[3] = {"tma2d(64px x 128 rows, SW128, 8 x 16KB)", "bulk(32KB, 6 slots)", "ldg128"};
       if (!(variant == 1 && grid_mul == 2))
         printf("%-42s grid=%d x SMs: %.1f GB/s (%.1f us for %.0f MB)\n", nm[variant], grid_mul, bytes / (best * 1e-3) / 1e9,
                best * 1e3, bytes / 1e6);
