@@ -767,10 +767,12 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 3 : 2) colfft_kernel(const fl
   float2* x = fsm;                       // [Sy][KT]
   float2* stw = fsm + (Sy << logKT);     // [Sy] twiddles
   const int j = blockIdx.y, k0 = blockIdx.x * KT;
+  pdl_trigger();
   const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
   for (int i = threadIdx.x; i < Sy; i += blockDim.x) stw[i] = __ldg(tw + i);
   for (int i = threadIdx.x; i < n_rows; i += blockDim.x) srow[i] = __ldg(rows + i);
   for (int i = threadIdx.x; i < mj; i += blockDim.x) svy[i] = fft::fslot<LOGN>(__ldg(act_vy + g0 + i));
+  pdl_wait();   // R (row DFT) and G of the preceding kernels
   if (n_rows < Sy)
     for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x) x[e] = make_float2(0.f, 0.f);
   __syncthreads();
@@ -826,6 +828,25 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 3 : 2) colfft_kernel(const fl
 }
 
 static int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
+
+// Launch with programmatic dependent launch: the kernel may start (prologue: twiddles, tables)
+// while the preceding kernel drains; it calls griddepcontrol.wait before touching that kernel's
+// output.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 // tuning override "a,b" from the environment (unset: (-1, 0))
 static int2 env_pair(const char* name) {
   const char* e = std::getenv(name);
@@ -942,7 +963,7 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
       static bool init = false;
       if (!init) {
         cudaError_t e = cudaFuncSetAttribute(rowfft_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kFftSmem + 8192);
+                                             kFftSmem + 16384);
         if (e != cudaSuccess) return e;
         init = true;
       }
@@ -1053,16 +1074,16 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
       static bool init = false;
       if (!init) {
         cudaError_t e = cudaFuncSetAttribute(colfft_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kFftSmem + 8192);
+                                             kFftSmem + 16384);
         if (e != cudaSuccess) return e;
         init = true;
       }
       dim3 grid(p.K >> logKT, p.n_vx);
       static const int2 knob = env_pair("WDD_COLFFT");
-      colfft_kernel<LOGN><<<grid, knob.y > 0 ? knob.y : 256, smem, st>>>(p.d_R, rows, n_rows, p.d_twy, p.d_col_off, p.d_act_vy, p.d_G,
-                                                   p.d_W, p.d_opart, p.n_act, logKT, p.K,
-                                                   (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0);
-      return cudaGetLastError();
+      return launch_pdl(colfft_kernel<LOGN>, grid, dim3(knob.y > 0 ? knob.y : 256), smem, st, p.d_R, rows, n_rows,
+                        (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G,
+                        (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.K,
+                        (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0);
     });
   }
   dim3 grid((unsigned)p.flush_tiles.size(), (p.K + 63) / 64);
@@ -1169,7 +1190,9 @@ __global__ void __launch_bounds__(256) img_rows_kernel(const float2* __restrict_
   float2* x = fsm;                 // [N][cnt]: x[vx * cnt + c] = conj o[vy0 + c][vx]
   float2* stw = fsm + (N << logc);
   const int vy0 = blockIdx.x << logc;
+  pdl_trigger();
   for (int i = threadIdx.x; i < N; i += blockDim.x) stw[i] = __ldg(tw + i);
+  pdl_wait();   // partial readouts of the preceding flush / readout kernel
   for (int e = threadIdx.x; e < (N << logc); e += blockDim.x) {
     const int c = e >> LOGN, vx = e & (N - 1);
     const int g = __ldg(gidx + (int64_t)(vy0 + c) * N + vx);
@@ -1206,7 +1229,9 @@ __global__ void __launch_bounds__(256) img_cols_kernel(const float2* __restrict_
   float2* x = fsm;                 // [N][cnt]: x[vy * cnt + c] = A[vy][x0 + c]
   float2* stw = fsm + (N << logc);
   const int x0 = blockIdx.x << logc;
+  pdl_trigger();
   for (int i = threadIdx.x; i < N; i += blockDim.x) stw[i] = __ldg(tw + i);
+  pdl_wait();   // row pass of the preceding kernel
   for (int e = threadIdx.x; e < (N << logc); e += blockDim.x) {
     const int vy = e >> logc, c = e & (cnt - 1);
     x[e] = __ldg(A + (int64_t)vy * Sx + x0 + c);
@@ -1238,18 +1263,17 @@ cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* 
     cudaError_t e = with_log(lx, [&](auto LN) {
       constexpr int L = decltype(LN)::value;
       const size_t smem = ((size_t)p.Sx << lr) * 8 + (size_t)p.Sx * 8 + 16;
-      img_rows_kernel<L><<<p.Sy >> lr, 256, smem, st>>>(op, tiles, p.n_act, p.d_gidx, p.d_twx, p.d_img_tmp, lr);
-      return cudaGetLastError();
+      return launch_pdl(img_rows_kernel<L>, dim3(p.Sy >> lr), dim3(256), smem, st, op, tiles, (int64_t)p.n_act,
+                        (const int32_t*)p.d_gidx, (const float2*)p.d_twx, p.d_img_tmp, lr);
     });
     if (e != cudaSuccess) return e;
     int lc = std::max(0, std::min(ilog2(std::max(1, 4096 / p.Sy)), lx - 4));
     return with_log(ly, [&](auto LN) {
       constexpr int L = decltype(LN)::value;
       const size_t smem = ((size_t)p.Sy << lc) * 8 + (size_t)p.Sy * 8 + 16;
-      img_cols_kernel<L><<<p.Sx >> lc, 256, smem, st>>>(p.d_img_tmp, p.d_twy, out, p.Sx, lc,
-                                                        (float)(1.0 / std::sqrt((double)S)), op, tiles, p.n_act,
-                                                        p.g_dc, p.normalize);
-      return cudaGetLastError();
+return launch_pdl(img_cols_kernel<L>, dim3(p.Sx >> lc), dim3(256), smem, st, (const float2*)p.d_img_tmp,
+                        (const float2*)p.d_twy, out, p.Sx, lc, (float)(1.0 / std::sqrt((double)S)), op, tiles,
+                        (int64_t)p.n_act, (int64_t)p.g_dc, p.normalize);
     });
   }
   scatter_kernel<<<(unsigned)((p.n_act + 255) / 256), 256, 0, st>>>(op, tiles, p.d_vpos, p.n_act, p.d_spec);
