@@ -716,21 +716,24 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) rowfft_kernel(const fl
   }
   if (threadIdx.x < mask_words) smask[threadIdx.x] = __ldg(masks + (int64_t)r * mask_words + threadIdx.x);
   __syncthreads();
-  const float2* Crow = reinterpret_cast<const float2*>(C + (int64_t)sy * Sx * K + k0);
-  const int total = Sx << logP;
+  // two coefficient pairs (16 bytes) per load; requires P >= 2
+  const float4* Crow = reinterpret_cast<const float4*>(C + (int64_t)sy * Sx * K + k0);
+  const int lq = logP - 1, total = Sx << lq;            // 16-byte pieces
   for (int base = 0; base < total; base += kU * (int)blockDim.x) {
-    float2 v[kU];
+    float4 v[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int e = base + u * (int)blockDim.x + threadIdx.x;
-      v[u] = e < total ? __ldg(Crow + (int64_t)(e >> logP) * (K >> 1) + (e & (P - 1))) : make_float2(0.f, 0.f);
+      v[u] = e < total ? __ldg(Crow + (int64_t)(e >> lq) * (K >> 2) + (e & ((P >> 1) - 1)))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int e = base + u * (int)blockDim.x + threadIdx.x;
       if (e < total) {
-        const int sx = e >> logP;
-        x[e] = ((smask[sx >> 5] >> (sx & 31)) & 1u) ? v[u] : make_float2(0.f, 0.f);
+        const int sx = e >> lq;
+        *reinterpret_cast<float4*>(x + 2 * e) =
+            ((smask[sx >> 5] >> (sx & 31)) & 1u) ? v[u] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
   }
@@ -776,53 +779,59 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 3 : 2) colfft_kernel(const fl
   if (n_rows < Sy)
     for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x) x[e] = make_float2(0.f, 0.f);
   __syncthreads();
-  const float2* Rj = R + (int64_t)j * Sy * K + k0;
-  const int total = n_rows << logKT;
+  // staged rows of R[j] (k0 .. k0+KT), two coefficients (16 bytes) per load, kU loads in flight
+  const float4* Rj = reinterpret_cast<const float4*>(R + (int64_t)j * Sy * K + k0);
+  const int hKT = KT >> 1, lh = logKT - 1;             // 16-byte pieces per row
+  const int total = n_rows << lh;
   for (int base = 0; base < total; base += kU * (int)blockDim.x) {
-    float2 v[kU];
+    float4 v[kU];
     int dst[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int e = base + u * (int)blockDim.x + threadIdx.x;
-      const int rr = e >> logKT, kk = e & (KT - 1);
-      const int sy = e < total ? srow[rr] : 0;
-      dst[u] = e < total ? (sy << logKT) + kk : -1;
-      v[u] = e < total ? __ldg(Rj + (int64_t)sy * K + kk) : make_float2(0.f, 0.f);
+      const int sy = e < total ? srow[e >> lh] : 0, h = e & (hKT - 1);
+      dst[u] = e < total ? (sy << logKT) + 2 * h : -1;
+      v[u] = e < total ? __ldg(Rj + (int64_t)sy * (K >> 1) + h) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u)
-      if (dst[u] >= 0) x[dst[u]] = v[u];
+      if (dst[u] >= 0) *reinterpret_cast<float4*>(x + dst[u]) = v[u];
   }
   __syncthreads();
   fft::fft_seq<LOGN>(x, stw, logKT);
-  const int tout = mj << logKT;
-  for (int base = 0; base < tout; base += kU * (int)blockDim.x) {   // warp-uniform trip count (shuffles below)
-    float2 o[kU], w[kU];
+  // Output: thread = (row slot, coefficient pair p); G (+)= X / sqrt(Sy) for the column's active
+  // vy, and the tile's share of sum_k G K_v reduced over the hKT threads of the row.
+  const int pp = threadIdx.x & (hKT - 1), rs = threadIdx.x >> lh, rpp = (int)blockDim.x >> lh;
+  float4* G4 = reinterpret_cast<float4*>(G);
+  const float4* W4 = reinterpret_cast<const float4*>(W);
+  const int64_t K2 = K >> 1;
+  for (int ib = 0; ib < mj; ib += rpp * 4) {             // block-uniform trip count (shuffles)
+    float4 o[4], w[4];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int e = base + u * (int)blockDim.x + threadIdx.x;
-      const int64_t gi = (int64_t)(g0 + (e >> logKT)) * K + k0 + (e & (KT - 1));
-      o[u] = (e < tout && !overwrite) ? G[gi] : make_float2(0.f, 0.f);
-      w[u] = e < tout ? __ldg(W + gi) : make_float2(0.f, 0.f);
+    for (int u = 0; u < 4; ++u) {
+      const int i = ib + u * rpp + rs;
+      const int64_t gi = (int64_t)(g0 + i) * K2 + (k0 >> 1) + pp;
+      w[u] = i < mj ? __ldg(W4 + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
+      o[u] = (i < mj && !overwrite) ? G4[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int e = base + u * (int)blockDim.x + threadIdx.x;
-      const int i = e >> logKT, kk = e & (KT - 1);
+    for (int u = 0; u < 4; ++u) {
+      if (ib + u * rpp >= mj) break;                     // block-uniform
+      const int i = ib + u * rpp + rs;
       float2 d = make_float2(0.f, 0.f);
-      if (e < tout) {
-        const float2 z = x[(svy[i] << logKT) + kk];
-        const float2 gn = make_float2(fmaf(z.x, scale, o[u].x), fmaf(z.y, scale, o[u].y));
-        G[(int64_t)(g0 + i) * K + k0 + kk] = gn;
-        d = cmul(gn, w[u]);
+      if (i < mj) {
+        const float4 z = *reinterpret_cast<const float4*>(x + (svy[i] << logKT) + 2 * pp);
+        const float4 gn = make_float4(fmaf(z.x, scale, o[u].x), fmaf(z.y, scale, o[u].y), fmaf(z.z, scale, o[u].z),
+                                      fmaf(z.w, scale, o[u].w));
+        G4[(int64_t)(g0 + i) * K2 + (k0 >> 1) + pp] = gn;
+        d.x = fmaf(gn.x, w[u].x, fmaf(-gn.y, w[u].y, fmaf(gn.z, w[u].z, -gn.w * w[u].w)));
+        d.y = fmaf(gn.x, w[u].y, fmaf(gn.y, w[u].x, fmaf(gn.z, w[u].w, gn.w * w[u].z)));
       }
-      if (base + u * (int)blockDim.x < tout) {            // some lane of this block-row holds data
-        for (int off = KT >> 1; off > 0; off >>= 1) {
-          d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
-          d.y += __shfl_xor_sync(0xffffffffu, d.y, off);
-        }
-        if (kk == 0 && e < tout) opart[(int64_t)blockIdx.x * n_act + g0 + i] = d;
+      for (int off = hKT >> 1; off > 0; off >>= 1) {
+        d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
+        d.y += __shfl_xor_sync(0xffffffffu, d.y, off);
       }
+      if (pp == 0 && i < mj) opart[(int64_t)blockIdx.x * n_act + g0 + i] = d;
     }
   }
 }
@@ -953,7 +962,7 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
   if (is_pow2(p.Sx) && p.Sx >= 2 && p.Sx <= (1 << kFftMaxLog)) {
     const int logSx = ilog2(p.Sx);
     static const int2 knob = env_pair("WDD_ROWFFT");   // (log2 k pairs per CTA, threads) override
-    int logP = ilog2(std::max(1, std::min(32, kFftSmem / (8 * p.Sx))));   // k pairs per CTA
+    int logP = ilog2(std::max(2, std::min(32, kFftSmem / (8 * p.Sx))));   // k pairs per CTA (>= 2)
     if (knob.x >= 0) logP = std::min(logP, knob.x);
     const int nt = knob.y > 0 ? knob.y : 256;
     while ((2 << logP) > p.K || p.K % (2 << logP)) --logP;
@@ -1049,7 +1058,7 @@ __global__ void __launch_bounds__(256) flush_kernel(const float2* __restrict__ R
 
 static int colfft_logkt(const Plan& p) {
   static const int2 knob = env_pair("WDD_COLFFT");   // (log2 k per CTA, threads) override
-  int logKT = ilog2(std::max(1, std::min(32, kFftSmem / (8 * p.Sy))));
+  int logKT = ilog2(std::max(2, std::min(32, kFftSmem / (8 * p.Sy))));
   if (knob.x >= 0) logKT = std::min(logKT, knob.x);
   while ((1 << logKT) > p.K || p.K % (1 << logKT)) --logKT;
   return logKT;
