@@ -57,6 +57,8 @@ struct Plan {
   float2* d_o = nullptr;              // n_act (multi-rank combine of o)
   float2* d_opart = nullptr;          // opart_cap x n_act partial readouts (per colfft k-tile)
   int32_t* d_gidx = nullptr;          // S: accumulator row of v, or -1 (inactive)
+  int32_t* d_iota = nullptr;          // Sy: 0, 1, ..., Sy-1 (row list of contiguous flushes)
+  uint32_t* d_ones = nullptr;         // Sy x mask_words all-ones pending masks (complete rows)
   int64_t g_dc = 0;                   // accumulator row of v = 0
   int opart_cap = 1;                  // rows of d_opart
   int opart_tiles = 0;                // valid partial-readout rows for the current G (0: stale)

@@ -66,6 +66,15 @@ __device__ __forceinline__ void trace_rec(int code, unsigned& cnt, int j) {
 }
 #define TRACE(c, j) trace_rec(c, trc[c], j)
 #define TRACE_DECL unsigned trc[16] = {0};
+// per-CTA timeline of every projection CTA: [entry, first TMA issue, last raw landing, exit, smid]
+__device__ unsigned long long g_cta[8192][5];
+__device__ unsigned g_cta_n;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CTA_REC(slot, field) do { if ((slot) < 8192) g_cta[slot][field] = gtime(); } while (0)
 #else
 #define TRACE(c, j)
 #define TRACE_DECL
@@ -198,6 +207,16 @@ __global__ void __launch_bounds__(kProjThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   pdl_trigger();
+#ifdef WDD_TRACE
+  __shared__ unsigned cta_slot;
+  if (tid == 0) {
+    cta_slot = atomicAdd(&g_cta_n, 1u);
+    CTA_REC(cta_slot, 0);
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    if (cta_slot < 8192) g_cta[cta_slot][4] = sm;
+  }
+#endif
 
   // ---- setup: barriers and TMEM only, so the TMA producer can start streaming at once; the basis
   // operand image arrives by one bulk copy that only the MMA issuers wait for
@@ -304,6 +323,10 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     if (U16 && lane == 0) {
       const uint64_t pol = policy_evict_first();   // frames are read exactly once
       uint32_t slot = 0, sphase = 0;
+#ifdef WDD_TRACE
+      __syncwarp(1u);
+      CTA_REC(cta_slot, 1);
+#endif
       for (int64_t gi = 0; gi < my_groups; ++gi) {
         const int64_t g = blockIdx.x + gi * gridDim.x;
         for (int tt = 0; tt < tpg; ++tt) {
@@ -348,6 +371,9 @@ __global__ void __launch_bounds__(kProjThreads, 1)
             uint32_t w[kW];
             mbar_wait(&raw_full[slot], sphase);
             if (ct == 0) TRACE(3, slot);
+#ifdef WDD_TRACE
+            if (ct == 0) CTA_REC(cta_slot, 2);
+#endif
 #pragma unroll
             for (int j = 0; j < kW / 4; ++j) {           // swizzled 16-byte pieces of row `row`
               int off = row * Cfg::kSpan + j * 16;
@@ -542,7 +568,10 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tbase);
-  if (a.pdl_wait_end) pdl_wait();   // this grid completes only after the preceding grid has completed
+  if (a.pdl_wait_end) pdl_wait();
+#ifdef WDD_TRACE
+  if (tid == 0) CTA_REC(cta_slot, 3);
+#endif   // this grid completes only after the preceding grid has completed
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link needed)
@@ -643,6 +672,15 @@ extern "C" int wdd_trace_dump(unsigned long long* host, int max_n) {
   cudaMemcpyToSymbol(g_trace, zeros, sizeof zeros);
   return n;
 }
+extern "C" int wdd_trace_ctas(unsigned long long* host /* 8192 x 5 */) {
+  cudaDeviceSynchronize();
+  unsigned n = 0;
+  cudaMemcpyFromSymbol(&n, g_cta_n, sizeof n);
+  cudaMemcpyFromSymbol(host, g_cta, sizeof(unsigned long long) * 8192 * 5);
+  const unsigned z = 0;
+  cudaMemcpyToSymbol(g_cta_n, &z, sizeof z);
+  return (int)(n < 8192 ? n : 8192);
+}
 #endif
 
 size_t project_smem_bytes(int Q, int L) {
@@ -708,13 +746,16 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) rowfft_kernel(const fl
   const int P = 1 << logP;
   float2* x = fsm;                       // [Sx][P]
   float2* stw = fsm + (Sx << logP);      // [Sx] twiddles
-  const int r = blockIdx.y, sy = __ldg(rows + r), k0 = blockIdx.x * 2 * P;
+  const int r = blockIdx.y, k0 = blockIdx.x * 2 * P;
+  pdl_trigger();
   for (int i = threadIdx.x; i < Sx; i += blockDim.x) stw[i] = __ldg(tw + i);
   for (int j = threadIdx.x; j < n_vx; j += blockDim.x) {
     const int v = __ldg(col_vx + j);
     sslot[j] = make_int2(fft::fslot<LOGN>(v), fft::fslot<LOGN>((Sx - v) & (Sx - 1)));
   }
-  if (threadIdx.x < mask_words) smask[threadIdx.x] = __ldg(masks + (int64_t)r * mask_words + threadIdx.x);
+  pdl_wait();   // C of the projection kernels (and the uploaded row list / masks)
+  const int sy = rows[r];
+  if (threadIdx.x < mask_words) smask[threadIdx.x] = masks[(int64_t)r * mask_words + threadIdx.x];
   __syncthreads();
   // two coefficient pairs (16 bytes) per load; requires P >= 2
   const float4* Crow = reinterpret_cast<const float4*>(C + (int64_t)sy * Sx * K + k0);
@@ -977,9 +1018,9 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
         init = true;
       }
       dim3 grid(p.K / (2 << logP), n_rows);
-      rowfft_kernel<LOGN><<<grid, nt, smem, st>>>(p.d_Call, rows, masks, p.mask_words, p.d_twx, p.d_col_vx, p.d_R,
-                                                   logP, p.Sy, p.K, p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)));
-      return cudaGetLastError();
+      return launch_pdl(rowfft_kernel<LOGN>, grid, dim3(nt), smem, st, (const float*)p.d_Call, rows, masks,
+                        p.mask_words, (const float2*)p.d_twx, (const int32_t*)p.d_col_vx, p.d_R, logP, p.Sy, p.K,
+                        p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)));
     });
   }
   static bool init = false;

@@ -355,22 +355,36 @@ wdd_status flush(Plan& p) {
   if (n_rows == 0) return WDD_OK;
   const size_t mask_off = ((size_t)n_rows + 3) / 4 * 4;
   blob.resize(mask_off + (size_t)n_rows * p.mask_words, 0);
+  // a contiguous range of complete rows (offline scans, live scans in scan order) needs no
+  // metadata upload: the rows are a slice of the plan's device iota and the masks all-ones
+  bool simple = blob[n_rows - 1] - blob[0] == n_rows - 1;
   for (int r = 0; r < n_rows; ++r) {
     const int sy = blob[r];
     for (int w = 0; w < p.mask_words; ++w) {
       uint32_t& m = p.pending[(size_t)sy * p.mask_words + w];
+      const int bits = std::min(32, p.Sx - 32 * w);
+      const uint32_t full = bits == 32 ? 0xFFFFFFFFu : ((1u << bits) - 1u);
+      simple = simple && m == full;
       blob[mask_off + (size_t)r * p.mask_words + w] = (int32_t)m;
       m = 0;
     }
     p.row_dirty[sy] = 0;
   }
-  void* d = nullptr;
-  wdd_status s = upload_meta(p, blob.data(), blob.size() * sizeof(int32_t), &d);
-  if (s != WDD_OK) return s;
-  const int32_t* dr = static_cast<const int32_t*>(d);
+  const int32_t* dr = nullptr;
+  const uint32_t* dm = nullptr;
+  if (simple) {
+    dr = p.d_iota + blob[0];
+    dm = p.d_ones;
+  } else {
+    void* d = nullptr;
+    wdd_status s = upload_meta(p, blob.data(), blob.size() * sizeof(int32_t), &d);
+    if (s != WDD_OK) return s;
+    dr = static_cast<const int32_t*>(d);
+    dm = reinterpret_cast<const uint32_t*>(dr + mask_off);
+  }
   {
     Prof pr(p, kSlotRowDft, p.stream);
-    CUDA_TRY(launch_rowdft(p, dr, reinterpret_cast<const uint32_t*>(dr + mask_off), n_rows, p.stream));
+    CUDA_TRY(launch_rowdft(p, dr, dm, n_rows, p.stream));
   }
   {
     Prof pr(p, kSlotFlush, p.stream);
@@ -397,7 +411,7 @@ void free_plan(Plan* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   cudaDeviceSynchronize();
   if (p->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(p->nccl));
-  void* bufs[] = {p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
+  void* bufs[] = {p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
                   p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec, p->d_img_tmp,
                   p->d_meta, p->d_stage[0], p->d_stage[1]};
   for (void* b : bufs)
@@ -537,6 +551,8 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   }
   std::vector<float> psi32(p->basis.begin(), p->basis.end());
   std::vector<int32_t> vpos(act.begin(), act.end());
+  std::vector<int32_t> iota(Sy);
+  for (int i = 0; i < Sy; ++i) iota[i] = i;
   std::vector<int32_t> gidx((size_t)p->S, -1);
   for (size_t g = 0; g < act.size(); ++g) gidx[(size_t)act[g]] = (int32_t)g;
   if (gidx[0] < 0) return bail(fail(WDD_E_ARG, "v = 0 is not active (empty aperture?)"));
@@ -571,6 +587,8 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   p->opart_cap = std::max(1, colfft_tiles(*p));
   ALLOC(p->d_opart, (size_t)p->opart_cap * act.size() * sizeof(float2));
   ALLOC(p->d_gidx, (size_t)p->S * sizeof(int32_t));
+  ALLOC(p->d_iota, (size_t)Sy * sizeof(int32_t));
+  ALLOC(p->d_ones, (size_t)Sy * p->mask_words * sizeof(uint32_t));
   ALLOC(p->d_spec, (size_t)p->S * sizeof(float2));
   ALLOC(p->d_img_tmp, (size_t)p->S * sizeof(float2));
   ALLOC(p->d_meta, 2 * p->meta_slot_bytes);
@@ -590,9 +608,10 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
             up(p->d_col_vx, p->col_vx.data(), p->col_vx.size() * sizeof(int32_t)) &&
             up(p->d_W, W.data(), W.size() * sizeof(float2)) && up(p->d_act_vy, p->act_vy.data(), act.size() * 4) &&
             up(p->d_col_off, p->col_off.data(), p->col_off.size() * 4) && up(p->d_vpos, vpos.data(), act.size() * 4) &&
-            up(p->d_gidx, gidx.data(), gidx.size() * 4) &&
+            up(p->d_gidx, gidx.data(), gidx.size() * 4) && up(p->d_iota, iota.data(), iota.size() * 4) &&
             up(p->d_flush_tiles, p->flush_tiles.data(), p->flush_tiles.size() * sizeof(int2));
-  ok = ok && cudaMemset(p->d_G, 0, W.size() * sizeof(float2)) == cudaSuccess &&
+  ok = ok && cudaMemset(p->d_ones, 0xFF, (size_t)Sy * p->mask_words * sizeof(uint32_t)) == cudaSuccess &&
+       cudaMemset(p->d_G, 0, W.size() * sizeof(float2)) == cudaSuccess &&
        cudaMemset(p->d_Call, 0, (size_t)p->S * K * sizeof(float)) == cudaSuccess &&
        cudaMemset(p->d_spec, 0, (size_t)p->S * sizeof(float2)) == cudaSuccess;
   if (!ok) return bail(fail(WDD_E_CUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError())));
