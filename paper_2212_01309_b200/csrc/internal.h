@@ -32,7 +32,8 @@ struct Plan {
   std::vector<int2> flush_tiles;      // (column j, first row i0) of 32-row tiles
   std::vector<uint64_t> seen;         // S bits
   std::vector<uint8_t> row_dirty;     // Sy: row has coefficients in d_Call not yet flushed into G
-  std::vector<uint32_t> pending;      // Sy x mask_words bits: position ingested, not yet flushed
+  std::vector<uint32_t> pending;      // Sy x mask_words bits: position ingested, not yet row-transformed
+  std::vector<uint8_t> row_staged;    // Sy: R holds this row's DFT, not yet folded into G
   int mask_words = 1;                 // ceil(Sx / 32)
   int64_t frames_ingested = 0;
 
