@@ -82,9 +82,17 @@ __device__ __forceinline__ unsigned long long gtime() {
 #ifndef WDD_NS
 #define WDD_NS 8
 #endif
-constexpr int kProjThreads = 480;   // MMA1, MMA2, TMA, 2 x 4 converter warps, 4 epilogue warps
+#ifndef WDD_LEAN
+#define WDD_LEAN 1
+#endif
+// WDD_LEAN: two CTAs per SM (one converter group, shallower rings, <= 113 KB smem, <= 256 TMEM
+// columns) so that one CTA's pipeline fill / drain overlaps the other's streaming.
+constexpr bool kLean = WDD_LEAN != 0;
+constexpr int kNGroups = kLean ? 1 : 2;                       // converter groups
+constexpr int kProjThreads = 96 + kNGroups * 128 + 128;       // MMA1, MMA2, TMA, converters, epilogue
+constexpr int kEpi0 = 96 + kNGroups * 128;                    // first epilogue thread
 constexpr int kConv = 128;          // threads per converter group (2 groups: even / odd chunks)
-constexpr int kNA = 4;              // TMEM A-operand ring (u16 path)
+constexpr int kNA = kLean ? 2 : 4;  // TMEM A-operand ring (u16 path)
 constexpr uint32_t kLBO = 2064;     // no-swizzle K-major: bytes between K-adjacent core matrices of a
                                     // 128-row operand (16 row groups x 128 B + 16 B bank-rotation pad)
 
@@ -106,19 +114,24 @@ struct ProjCfg {
   static constexpr int kFPT = Q >= 128 ? 1 : 128 / Q;     // frames per stage-1 tile
   static constexpr int kTPF = Q >= 128 ? Q / 128 : 1;     // stage-1 tiles per frame (= stage-2 K chunks)
   static constexpr int kK2 = Q >= 128 ? 128 : Q;          // stage-2 K chunk (detector rows)
-  static constexpr int kG2 = Q >= 128 ? 128 / L : ((128 / L) / kFPT) * kFPT;  // max frames per group
-  static constexpr int kA2 = (kK2 / 8) * (int)kLBO;       // one A2 plane (K-major, no swizzle)
+  // stage-2 MMA M: 64 rows (frame, a) when a group of whole stage-1 tiles fits, else 128.  The
+  // M = 64 accumulator occupies lanes 0-15 of each TMEM lane quadrant (row m -> lane m%16 + 32(m/16)).
+  static constexpr int kM2 = (64 / L) >= kFPT ? 64 : 128;
+  static constexpr int kG2 = Q >= 128 ? kM2 / L : ((kM2 / L) / kFPT) * kFPT;  // max frames per group
+  static constexpr uint32_t kLBO2 = (kM2 / 8) * 128 + 16; // A2: bytes between K-adjacent core matrices
+  static constexpr int kA2 = (kK2 / 8) * (int)kLBO2;      // one A2 plane (K-major, no swizzle)
   static constexpr int kAcc1 = kN;                        // per acc1 slot (both count planes accumulate here)
-  static constexpr int kNAcc = 4;                         // acc1 ring
+  static constexpr int kNAcc = kLean ? 2 : 4;             // acc1 ring
   static constexpr int kACols = kKC / 2;                  // TMEM columns of one A1 chunk (fp16 pairs)
   static constexpr int tA = 0;                            // TMEM column map
   static constexpr int tP1 = tA + kNA * kACols;          // one plane-1 buffer per converter group
-  static constexpr int tAcc1 = tP1 + 2 * kACols;
+  static constexpr int tAcc1 = tP1 + kNGroups * kACols;
   static constexpr int tAcc2 = tAcc1 + kNAcc * kAcc1;
   static constexpr int kTmemCols = pow2_cols(tAcc2 + kN);
   static_assert(tAcc2 + kN <= 512, "TMEM");
   static constexpr int kFixed = (U16 ? 0 : 2 * kSlot) + align_up(2 * kA2, 1024) + align_up(kB, 1024) + 512;
-  static constexpr int kNSfit = ((232448 - kFixed) / kSlot) & ~1;
+  static constexpr int kNSraw = (((kLean ? 113 * 1024 : 232448) - kFixed) / kSlot) & ~1;
+  static constexpr int kNSfit = kNSraw < 2 ? 2 : kNSraw;   // (lean: configs that do not fit run 1 CTA/SM)
   static constexpr int kNS = kNSfit < WDD_NS ? kNSfit : WDD_NS;  // raw ring (even: group = job parity)
   static constexpr int off_ring = 0;
   static constexpr int off_P1 = off_ring + kNS * kSlot;   // f32 path only
@@ -180,7 +193,7 @@ __device__ __forceinline__ void tile_coords(int64_t g, int tt, int g2, int64_t n
 }
 
 template <int Q, int L, bool U16>
-__global__ void __launch_bounds__(kProjThreads, 1)
+__global__ void __launch_bounds__(kProjThreads, kLean ? 2 : 1)
     project_kernel(ProjArgs a, const __grid_constant__ CUtensorMap tmap) {
   using Cfg = ProjCfg<Q, L, U16>;
   constexpr int K = L * L;
@@ -264,7 +277,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
           tc_fence_after();
           const uint32_t acc = tbase + Cfg::tAcc1 + s1 * Cfg::kAcc1;
           for (int c = 0; c < Cfg::kCPT; ++c, ++job) {
-            const uint32_t grp = job & 1u;
+            const uint32_t grp = kNGroups == 2 ? (job & 1u) : 0u;
             mbar_wait(U16 ? &a_full[slot] : &raw_full[slot], sphase);
             TRACE(5, slot);
             tc_fence_after();
@@ -295,7 +308,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
   } else if (warp == 1) {
     // ================= stage-2 MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16(128, Cfg::kN);
+      constexpr uint32_t idesc = idesc_f16(Cfg::kM2, Cfg::kN);
       const uint32_t a20 = smem_u32(sA2), b0 = smem_u32(sB);
       const uint32_t acc2 = tbase + Cfg::tAcc2;
       mbar_wait(b_full, 0);
@@ -309,7 +322,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
           for (int plane = 0; plane < 2; ++plane) {
 #pragma unroll
             for (int kk = 0; kk < Cfg::kK2 / 16; ++kk) {
-              const uint64_t ad = smem_desc_noswz(a20 + plane * Cfg::kA2 + 2 * kk * kLBO, kLBO, 128);
+              const uint64_t ad = smem_desc_noswz(a20 + plane * Cfg::kA2 + 2 * kk * Cfg::kLBO2, Cfg::kLBO2, 128);
               const uint64_t bd = smem_desc_noswz(b0 + (h * (Cfg::kK2 / 8) + 2 * kk) * Cfg::kLBO_B, Cfg::kLBO_B, 128);
               mma_f16_ss(acc2, ad, bd, idesc, (h > 0 || plane > 0 || kk > 0) ? 1u : 0u);
             }
@@ -343,7 +356,7 @@ __global__ void __launch_bounds__(kProjThreads, 1)
         }
       }
     }
-  } else if (warp < 11) {
+  } else if (warp < 3 + 4 * kNGroups) {
     // ================= converters: group cg handles the jobs (chunks) with job % 2 == cg
     const int cg = (warp - 3) >> 2;
     const int ct = tid - 96 - cg * kConv;
@@ -360,11 +373,11 @@ __global__ void __launch_bounds__(kProjThreads, 1)
         int valid;
         tile_coords<Q, L, U16>(g, tt, g2, n, row0, valid);
         for (int c = 0; c < Cfg::kCPT; ++c, ++job) {
-          if ((job & 1u) != (uint32_t)cg) continue;
+          if (kNGroups == 2 && (job & 1u) != (uint32_t)cg) continue;
           const uint32_t slot = job % Cfg::kNS, sphase = (job / Cfg::kNS) & 1u;
           const uint32_t aslot = job % kNA, aphase = (job / kNA) & 1u;
           bool resid = false;
-          uint32_t* wf = wflag + cg * 8 + ((job >> 1) & 1) * 4;
+          uint32_t* wf = wflag + cg * 8 + ((job / kNGroups) & 1) * 4;
           if constexpr (U16) {
             constexpr int kW = Cfg::kACols;               // 32-bit words of this row in the chunk
             const uint8_t* src = ring + slot * Cfg::kSlot;
@@ -491,17 +504,19 @@ __global__ void __launch_bounds__(kProjThreads, 1)
     }
   } else {
     // ================= epilogue (128 threads; TMEM lane quadrant = warp % 4)
-    const int et = tid - 352;
+    const int et = tid - kEpi0;
     const int quad = warp & 3;
     const int row = quad * 32 + lane;                    // TMEM lane == tile row == A2 m index
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const uint32_t acc2 = tbase + Cfg::tAcc2 + lane_addr;
     uint32_t tile = 0, s2_issued = 0;
     int64_t pending = -1;   // frame0 of a group whose stage-2 result has not been stored yet
+    // accumulator row held by this thread's lane (M = 64: lanes 0-15 of each quadrant)
+    const int m2 = Cfg::kM2 == 128 ? row : (lane < 16 ? quad * 16 + lane : 1 << 20);
     auto stage2_epilogue = [&](int64_t frame0) {
       float d[Cfg::kN];
       tmem_ld_cols<Cfg::kN>(acc2, d);
-      const int f = row / L, aa = row % L;
+      const int f = m2 / L, aa = m2 % L;
       const int64_t fg = frame0 + f;
       if (f < g2 && fg < n) {
         float* dst = a.C + (a.idx ? (int64_t)__ldg(a.idx + fg) : fg) * K + aa * L;
@@ -533,12 +548,12 @@ __global__ void __launch_bounds__(kProjThreads, 1)
           tc_fence_after();
           if (pending >= 0) { stage2_epilogue(pending); pending = -1; }
         }
-        // A2 element (m = f*L + a, k), K-major no swizzle: (k/8)*kLBO + (m/8)*128 + (m%8)*16 + (k%8)*2
+        // A2 element (m = f*L + a, k), K-major no swizzle: (k/8)*kLBO2 + (m/8)*128 + (m%8)*16 + (k%8)*2
         int f, k;
         if constexpr (Q >= 128) { f = tt % g2; k = row; }
         else { f = tt * Cfg::kFPT + row / Q; k = row % Q; }
         {
-          uint8_t* base = sA2 + (k >> 3) * kLBO + (k & 7) * 2;
+          uint8_t* base = sA2 + (k >> 3) * Cfg::kLBO2 + (k & 7) * 2;
 #pragma unroll
           for (int q = 0; q < L; ++q) {
             const int m = f * L + q;
@@ -608,12 +623,13 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
     const int64_t per_cta = (groups + p.sm_count - 1) / p.sm_count * c;
     if (per_cta <= best) { best = per_cta; g2 = c; }
   }
-  // Frames per CTA: about 1 MiB of frame data per CTA, so that a small batch occupies only part
+  // Frames per CTA: about 1 MiB (lean: 512 KiB) of frame data per CTA, so that a small batch occupies only part
   // of the GPU and consecutive (PDL-chained) batches stream concurrently on the other SMs instead
   // of each batch paying its own pipeline fill and drain on every SM.  WDD_PROJ_MIN_FRAMES
   // overrides (0 = spread every batch over all SMs).
   static const int env_frames = [] { const char* e = std::getenv("WDD_PROJ_MIN_FRAMES"); return e ? std::atoi(e) : -1; }();
-  const int min_frames = env_frames >= 0 ? env_frames : std::max(4, (1 << 20) / (Q * Q * (U16 ? 2 : 4)));
+  const int min_frames = env_frames >= 0 ? env_frames
+                                         : std::max(4, (kLean ? (1 << 19) : (1 << 20)) / (Q * Q * (U16 ? 2 : 4)));
   if (min_frames > 0) g2 = Cfg::kG2;
   const int64_t groups = (n + g2 - 1) / g2;
   int grid = (int)std::min<int64_t>(groups, (int64_t)p.sm_count);
@@ -884,7 +900,7 @@ static int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
 // output.
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                              Args&&... args) {
+                              bool pdl, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -894,7 +910,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 // tuning override "a,b" from the environment (unset: (-1, 0))
@@ -1018,7 +1034,10 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
         init = true;
       }
       dim3 grid(p.K / (2 << logP), n_rows);
-      return launch_pdl(rowfft_kernel<LOGN>, grid, dim3(nt), smem, st, (const float*)p.d_Call, rows, masks,
+      // (with two projection CTAs per SM a PDL-launched row FFT would park its CTAs next to the
+      // last projection CTAs and slow them down: launch it after the projection completes)
+      static const int rowfft_pdl = [] { const char* e = std::getenv("WDD_ROWFFT_PDL"); return e ? std::atoi(e) : (kLean ? 0 : 1); }();
+      return launch_pdl(rowfft_kernel<LOGN>, grid, dim3(nt), smem, st, rowfft_pdl != 0, (const float*)p.d_Call, rows, masks,
                         p.mask_words, (const float2*)p.d_twx, (const int32_t*)p.d_col_vx, p.d_R, logP, p.Sy, p.K,
                         p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)));
     });
@@ -1130,7 +1149,7 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
       }
       dim3 grid(p.K >> logKT, p.n_vx);
       static const int2 knob = env_pair("WDD_COLFFT");
-      return launch_pdl(colfft_kernel<LOGN>, grid, dim3(knob.y > 0 ? knob.y : 256), smem, st, p.d_R, rows, n_rows,
+      return launch_pdl(colfft_kernel<LOGN>, grid, dim3(knob.y > 0 ? knob.y : 256), smem, st, true, p.d_R, rows, n_rows,
                         (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G,
                         (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.K,
                         (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0);
@@ -1313,7 +1332,7 @@ cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* 
     cudaError_t e = with_log(lx, [&](auto LN) {
       constexpr int L = decltype(LN)::value;
       const size_t smem = ((size_t)p.Sx << lr) * 8 + (size_t)p.Sx * 8 + 16;
-      return launch_pdl(img_rows_kernel<L>, dim3(p.Sy >> lr), dim3(256), smem, st, op, tiles, (int64_t)p.n_act,
+      return launch_pdl(img_rows_kernel<L>, dim3(p.Sy >> lr), dim3(256), smem, st, true, op, tiles, (int64_t)p.n_act,
                         (const int32_t*)p.d_gidx, (const float2*)p.d_twx, p.d_img_tmp, lr);
     });
     if (e != cudaSuccess) return e;
@@ -1321,7 +1340,7 @@ cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* 
     return with_log(ly, [&](auto LN) {
       constexpr int L = decltype(LN)::value;
       const size_t smem = ((size_t)p.Sy << lc) * 8 + (size_t)p.Sy * 8 + 16;
-return launch_pdl(img_cols_kernel<L>, dim3(p.Sx >> lc), dim3(256), smem, st, (const float2*)p.d_img_tmp,
+return launch_pdl(img_cols_kernel<L>, dim3(p.Sx >> lc), dim3(256), smem, st, true, (const float2*)p.d_img_tmp,
                         (const float2*)p.d_twy, out, p.Sx, lc, (float)(1.0 / std::sqrt((double)S)), op, tiles,
                         (int64_t)p.n_act, (int64_t)p.g_dc, p.normalize);
     });
