@@ -31,6 +31,8 @@
 #include "internal.h"
 #include "tc.cuh"
 #include "fft.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace wdd {
 
@@ -1318,6 +1320,102 @@ __global__ void __launch_bounds__(256) img_cols_kernel(const float2* __restrict_
   }
 }
 
+// a8 in one launch for images up to 256 x 256: a cluster of CS CTAs, CTA r owns RB = Sy/CS rows
+// for the row pass and CB = Sx/CS columns for the column pass; the transposition between the two
+// passes goes through distributed shared memory (no global round trip, one launch).
+template <int LX, int LY, int CS>
+__global__ void __launch_bounds__(256) img_fused_kernel(const float2* __restrict__ op, int tiles, int64_t n_act,
+                                                        const int32_t* __restrict__ gidx,
+                                                        const float2* __restrict__ twx, const float2* __restrict__ twy,
+                                                        float2* __restrict__ out, float scale, int64_t g_dc,
+                                                        int normalize) {
+  constexpr int SX = 1 << LX, SY = 1 << LY, RB = SY / CS, CB = SX / CS;
+  constexpr int LRB = LY - (CS == 16 ? 4 : CS == 8 ? 3 : CS == 4 ? 2 : CS == 2 ? 1 : 0);
+  constexpr int LCB = LX - (CS == 16 ? 4 : CS == 8 ? 3 : CS == 4 ? 2 : CS == 2 ? 1 : 0);
+  extern __shared__ __align__(16) float2 fsm[];
+  float2* xr = fsm;                         // [SX][RB]  row pass (frequency vx at slot fslot<LX>)
+  float2* xc = xr + SX * RB;                // [SY][CB]  column pass
+  float2* stx = xc + SY * CB;               // [SX]
+  float2* sty = stx + SX;                   // [SY]
+  cg::cluster_group cluster = cg::this_cluster();
+  const int r = (int)cluster.block_rank();
+  pdl_trigger();
+  for (int i = threadIdx.x; i < SX; i += blockDim.x) stx[i] = __ldg(twx + i);
+  for (int i = threadIdx.x; i < SY; i += blockDim.x) sty[i] = __ldg(twy + i);
+  pdl_wait();   // partial readouts of the preceding flush / readout kernel
+  const int vy0 = r * RB;
+  for (int e = threadIdx.x; e < SX * RB; e += blockDim.x) {
+    const int c = e >> LX, vx = e & (SX - 1);
+    const int g = __ldg(gidx + (int64_t)(vy0 + c) * SX + vx);
+    const float2 v = g >= 0 ? sum_tiles(op, tiles, n_act, g) : make_float2(0.f, 0.f);
+    xr[(vx << LRB) + c] = make_float2(v.x, -v.y);    // conj(o): O = DFT2(conj o) / sqrt(S)
+  }
+  __syncthreads();
+  fft::fft_seq<LX>(xr, stx, LRB);
+  cluster.sync();                           // every CTA's row pass is complete
+  const int x0 = r * CB;
+  for (int e = threadIdx.x; e < SY * CB; e += blockDim.x) {
+    const int vy = e >> LCB, cc = e & (CB - 1);
+    const float2* src = cluster.map_shared_rank(xr, vy / RB);
+    xc[e] = src[(fft::fslot<LX>(x0 + cc) << LRB) + (vy % RB)];
+  }
+  cluster.sync();                           // remote reads done before any CTA exits
+  fft::fft_seq<LY>(xc, sty, LCB);
+  float2 f = make_float2(scale, 0.f);
+  if (normalize) {
+    const float2 w = inv_principal_sqrt(sum_tiles(op, tiles, n_act, g_dc));
+    f = make_float2(w.x * scale, w.y * scale);
+  }
+  for (int e = threadIdx.x; e < SY * CB; e += blockDim.x) {
+    const int y = e >> LCB, cc = e & (CB - 1);
+    out[(int64_t)y * SX + x0 + cc] = cmul(xc[(fft::fslot<LY>(y) << LCB) + cc], f);
+  }
+}
+
+template <int LX, int LY>
+static cudaError_t launch_img_fused(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st) {
+  constexpr int CS = (LX >= 4 && LY >= 4) ? 16 : 1 << (LX < LY ? LX : LY);
+  constexpr int SX = 1 << LX, SY = 1 << LY;
+  constexpr size_t smem = (size_t)(SX * (SY / CS) + SY * (SX / CS) + SX + SY) * 8;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(img_fused_kernel<LX, LY, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e == cudaSuccess && CS > 8)
+      e = cudaFuncSetAttribute(img_fused_kernel<LX, LY, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, img_fused_kernel<LX, LY, CS>, op, tiles, (int64_t)p.n_act,
+                            (const int32_t*)p.d_gidx, (const float2*)p.d_twx, (const float2*)p.d_twy, out,
+                            (float)(1.0 / std::sqrt((double)p.S)), (int64_t)p.g_dc, p.normalize);
+}
+
+static cudaError_t launch_img_fused_dispatch(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st) {
+  return with_log(ilog2(p.Sx), [&](auto LNX) {
+    constexpr int LX = decltype(LNX)::value;
+    return with_log(ilog2(p.Sy), [&](auto LNY) -> cudaError_t {
+      constexpr int LY = decltype(LNY)::value;
+      if constexpr (LX <= 8 && LY <= 8) return launch_img_fused<LX, LY>(p, op, tiles, out, st);
+      else return cudaErrorInvalidValue;
+    });
+  });
+}
+
 bool finalize_uses_fft(const Plan& p) {
   return is_pow2(p.Sx) && is_pow2(p.Sy) && p.Sx >= 2 && p.Sy >= 2 && p.Sx <= (1 << kFftMaxLog) &&
          p.Sy <= (1 << kFftMaxLog);
@@ -1325,6 +1423,8 @@ bool finalize_uses_fft(const Plan& p) {
 
 cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st) {
   const int64_t S = p.S;
+  static const int no_fused = [] { const char* e = std::getenv("WDD_IMG_UNFUSED"); return e ? std::atoi(e) : 0; }();
+  if (finalize_uses_fft(p) && p.Sx <= 256 && p.Sy <= 256 && !no_fused) return launch_img_fused_dispatch(p, op, tiles, out, st);
   if (finalize_uses_fft(p)) {
     // rows: 2^lr rows per CTA (<= 32 KB of shared memory, at least 16 CTAs when the image allows)
     const int lx = ilog2(p.Sx), ly = ilog2(p.Sy);
