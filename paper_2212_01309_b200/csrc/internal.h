@@ -121,5 +121,6 @@ cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* 
 // host helper: pack the fp16 B operand image of the projection kernel
 void pack_basis_fp16(const Plan& p, std::vector<uint16_t>& out, double& scale);
 size_t project_smem_bytes(int Q, int L);
+bool project_is_lean(const Plan& p);   // projection runs two CTAs per SM for this plan
 
 }  // namespace wdd

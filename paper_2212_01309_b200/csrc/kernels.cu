@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <climits>
 #include <type_traits>
 #include <cmath>
@@ -89,20 +90,22 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 // WDD_LEAN: two CTAs per SM (one converter group, shallower rings, <= 113 KB smem, <= 256 TMEM
 // columns) so that one CTA's pipeline fill / drain overlaps the other's streaming.
-constexpr bool kLean = WDD_LEAN != 0;
-constexpr int kNGroups = kLean ? 1 : 2;                       // converter groups
-constexpr int kProjThreads = 96 + kNGroups * 128 + 128;       // MMA1, MMA2, TMA, converters, epilogue
-constexpr int kEpi0 = 96 + kNGroups * 128;                    // first epilogue thread
+constexpr bool kLeanAllowed = WDD_LEAN != 0;   // per configuration: lean only where it fits
 constexpr int kConv = 128;          // threads per converter group (2 groups: even / odd chunks)
-constexpr int kNA = kLean ? 2 : 4;  // TMEM A-operand ring (u16 path)
 constexpr uint32_t kLBO = 2064;     // no-swizzle K-major: bytes between K-adjacent core matrices of a
                                     // 128-row operand (16 row groups x 128 B + 16 B bank-rotation pad)
 
 __host__ __device__ constexpr int pow2_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
-template <int Q, int L, bool U16>
-struct ProjCfg {
+template <int Q, int L, bool U16, bool LEAN>
+struct ProjCfgT {
+  static constexpr bool kLean = LEAN;
+  static constexpr int kNGroups = LEAN ? 1 : 2;                     // converter groups
+  static constexpr int kThreads = 96 + kNGroups * 128 + 128;        // MMA1, MMA2, TMA, converters, epilogue
+  static constexpr int kMinBlocks = LEAN ? 2 : 1;
+  static constexpr int kEpi0 = 96 + kNGroups * 128;                 // first epilogue thread
+  static constexpr int kNA = LEAN ? 2 : 4;                          // TMEM A-operand ring (u16 path)
   static constexpr int kKC = Q >= 64 ? 64 : Q;            // K elements (pixels) per A1 chunk
   static constexpr int kCPT = Q / kKC;                    // chunks per stage-1 tile
   static constexpr int kSpan = kKC * 2;                   // bytes per row of a raw u16 chunk (swizzle span)
@@ -120,10 +123,12 @@ struct ProjCfg {
   // M = 64 accumulator occupies lanes 0-15 of each TMEM lane quadrant (row m -> lane m%16 + 32(m/16)).
   static constexpr int kM2 = (64 / L) >= kFPT ? 64 : 128;
   static constexpr int kG2 = Q >= 128 ? kM2 / L : ((kM2 / L) / kFPT) * kFPT;  // max frames per group
-  static constexpr uint32_t kLBO2 = (kM2 / 8) * 128 + 16; // A2: bytes between K-adjacent core matrices
-  static constexpr int kA2 = (kK2 / 8) * (int)kLBO2;      // one A2 plane (K-major, no swizzle)
+  // A2 is MN-major (no swizzle): core matrix = 8 consecutive m (16 bytes) x 8 k, k-blocks at
+  // 128 bytes, m-blocks at kSBO2, so the epilogue stores 8 values of a frame row as one 16-byte word
+  static constexpr uint32_t kSBO2 = (kK2 / 8) * 128;
+  static constexpr int kA2 = (kM2 / 8) * (int)kSBO2;       // one A2 plane
   static constexpr int kAcc1 = kN;                        // per acc1 slot (both count planes accumulate here)
-  static constexpr int kNAcc = kLean ? 2 : 4;             // acc1 ring
+  static constexpr int kNAcc = LEAN ? 2 : 4;              // acc1 ring
   static constexpr int kACols = kKC / 2;                  // TMEM columns of one A1 chunk (fp16 pairs)
   static constexpr int tA = 0;                            // TMEM column map
   static constexpr int tP1 = tA + kNA * kACols;          // one plane-1 buffer per converter group
@@ -132,7 +137,7 @@ struct ProjCfg {
   static constexpr int kTmemCols = pow2_cols(tAcc2 + kN);
   static_assert(tAcc2 + kN <= 512, "TMEM");
   static constexpr int kFixed = (U16 ? 0 : 2 * kSlot) + align_up(2 * kA2, 1024) + align_up(kB, 1024) + 512;
-  static constexpr int kNSraw = (((kLean ? 113 * 1024 : 232448) - kFixed) / kSlot) & ~1;
+  static constexpr int kNSraw = (((LEAN ? 113 * 1024 : 232448) - kFixed) / kSlot) & ~1;
   static constexpr int kNSfit = kNSraw < 2 ? 2 : kNSraw;   // (lean: configs that do not fit run 1 CTA/SM)
   static constexpr int kNS = kNSfit < WDD_NS ? kNSfit : WDD_NS;  // raw ring (even: group = job parity)
   static constexpr int off_ring = 0;
@@ -143,10 +148,22 @@ struct ProjCfg {
   static constexpr int kBars = 2 * kNS + 2 * kNA + 2 * kNAcc + 5;
   static constexpr int off_misc = off_bar + 8 * kBars;    // meta[kNS+kNA], wflag[2 groups][2][4], tmem slot
   static constexpr int smem = off_misc + 4 * (kNS + kNA) + 64 + 16;
+  static constexpr int kTmemUsed = tAcc2 + kN;
   static_assert(kNS % 2 == 0 && kNA % 2 == 0, "even rings: converter group = job parity");
   static_assert(kG2 >= 1, "group");
   static_assert(smem <= 232448, "shared memory");
 };
+// Lean (two CTAs per SM) where both CTAs fit in shared memory and TMEM, else the full variant.
+template <int Q, int L, bool U16>
+struct ProjCfgSel {
+  using LeanCfg = ProjCfgT<Q, L, U16, true>;
+  static constexpr bool lean = kLeanAllowed && LeanCfg::smem <= 113 * 1024 && LeanCfg::kTmemUsed <= 256 &&
+                               LeanCfg::kNSraw >= 4;
+  using type = typename std::conditional<lean, LeanCfg, ProjCfgT<Q, L, U16, false>>::type;
+};
+template <int Q, int L, bool U16>
+using ProjCfg = typename ProjCfgSel<Q, L, U16>::type;
+
 
 __device__ __forceinline__ uint32_t magic_half2(uint32_t v10) {
   // v10 holds two 10-bit integers (bits 0-9 and 16-25).  (0x6400 | x) is fp16 1024 + x,
@@ -195,7 +212,7 @@ __device__ __forceinline__ void tile_coords(int64_t g, int tt, int g2, int64_t n
 }
 
 template <int Q, int L, bool U16>
-__global__ void __launch_bounds__(kProjThreads, kLean ? 2 : 1)
+__global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U16>::kMinBlocks)
     project_kernel(ProjArgs a, const __grid_constant__ CUtensorMap tmap) {
   using Cfg = ProjCfg<Q, L, U16>;
   constexpr int K = L * L;
@@ -208,16 +225,16 @@ __global__ void __launch_bounds__(kProjThreads, kLean ? 2 : 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::off_bar);
   uint64_t* raw_full = bars;                   // [kNS] slot filled (TMA tx / f32 converter)
   uint64_t* raw_empty = bars + Cfg::kNS;       // [kNS] slot free   (u16 converter / f32 MMA commit)
-  uint64_t* a_full = bars + 2 * Cfg::kNS;      // [kNA] TMEM A chunk written (u16)
-  uint64_t* a_empty = a_full + kNA;            // [kNA] TMEM A chunk consumed (u16)
-  uint64_t* p1_empty = a_empty + kNA;          // [2] per converter group
+  uint64_t* a_full = bars + 2 * Cfg::kNS;      // [Cfg::kNA] TMEM A chunk written (u16)
+  uint64_t* a_empty = a_full + Cfg::kNA;            // [Cfg::kNA] TMEM A chunk consumed (u16)
+  uint64_t* p1_empty = a_empty + Cfg::kNA;          // [2] per converter group
   uint64_t* acc1_full = p1_empty + 2;          // [kNAcc]
   uint64_t* acc1_empty = acc1_full + Cfg::kNAcc;
   uint64_t* a2_full = acc1_empty + Cfg::kNAcc;
   uint64_t* s2_done = a2_full + 1;
   uint64_t* b_full = s2_done + 1;               // basis operand image landed (bulk copy)
-  uint32_t* meta = reinterpret_cast<uint32_t*>(smem + Cfg::off_misc);   // [kNS + kNA]
-  uint32_t* wflag = meta + Cfg::kNS + kNA;                               // [2][2][4]
+  uint32_t* meta = reinterpret_cast<uint32_t*>(smem + Cfg::off_misc);   // [kNS + Cfg::kNA]
+  uint32_t* wflag = meta + Cfg::kNS + Cfg::kNA;                               // [2][2][4]
   uint32_t* tslot = wflag + 16;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -239,7 +256,7 @@ __global__ void __launch_bounds__(kProjThreads, kLean ? 2 : 1)
     // u16: each of the 4 converter warps releases its 32 rows of a raw slot as soon as it has them
     // in registers (f32: the stage-1 MMA commit releases the slot)
     for (int i = 0; i < Cfg::kNS; ++i) { mbar_init(&raw_full[i], 1); mbar_init(&raw_empty[i], U16 ? 4 : 1); }
-    for (int i = 0; i < kNA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
+    for (int i = 0; i < Cfg::kNA; ++i) { mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 1); }
     mbar_init(&p1_empty[0], 1);
     mbar_init(&p1_empty[1], 1);
     for (int i = 0; i < Cfg::kNAcc; ++i) { mbar_init(&acc1_full[i], 1); mbar_init(&acc1_empty[i], 4); }
@@ -279,7 +296,7 @@ __global__ void __launch_bounds__(kProjThreads, kLean ? 2 : 1)
           tc_fence_after();
           const uint32_t acc = tbase + Cfg::tAcc1 + s1 * Cfg::kAcc1;
           for (int c = 0; c < Cfg::kCPT; ++c, ++job) {
-            const uint32_t grp = kNGroups == 2 ? (job & 1u) : 0u;
+            const uint32_t grp = Cfg::kNGroups == 2 ? (job & 1u) : 0u;
             mbar_wait(U16 ? &a_full[slot] : &raw_full[slot], sphase);
             TRACE(5, slot);
             tc_fence_after();
@@ -301,7 +318,7 @@ __global__ void __launch_bounds__(kProjThreads, kLean ? 2 : 1)
               mma_commit(&p1_empty[grp]);
             }
             mma_commit(U16 ? &a_empty[slot] : &raw_empty[slot]);
-            if (++slot == (U16 ? kNA : Cfg::kNS)) { slot = 0; sphase ^= 1u; }
+            if (++slot == (U16 ? Cfg::kNA : Cfg::kNS)) { slot = 0; sphase ^= 1u; }
           }
           mma_commit(&acc1_full[s1]);
         }
@@ -310,7 +327,7 @@ __global__ void __launch_bounds__(kProjThreads, kLean ? 2 : 1)
   } else if (warp == 1) {
     // ================= stage-2 MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16(Cfg::kM2, Cfg::kN);
+      constexpr uint32_t idesc = idesc_f16(Cfg::kM2, Cfg::kN, 0, /*a_major=MN*/ 1, 0);
       const uint32_t a20 = smem_u32(sA2), b0 = smem_u32(sB);
       const uint32_t acc2 = tbase + Cfg::tAcc2;
       mbar_wait(b_full, 0);
@@ -324,7 +341,7 @@ __global__ void __launch_bounds__(kProjThreads, kLean ? 2 : 1)
           for (int plane = 0; plane < 2; ++plane) {
 #pragma unroll
             for (int kk = 0; kk < Cfg::kK2 / 16; ++kk) {
-              const uint64_t ad = smem_desc_noswz(a20 + plane * Cfg::kA2 + 2 * kk * Cfg::kLBO2, Cfg::kLBO2, 128);
+              const uint64_t ad = smem_desc_noswz(a20 + plane * Cfg::kA2 + kk * 256, 128, Cfg::kSBO2);
               const uint64_t bd = smem_desc_noswz(b0 + (h * (Cfg::kK2 / 8) + 2 * kk) * Cfg::kLBO_B, Cfg::kLBO_B, 128);
               mma_f16_ss(acc2, ad, bd, idesc, (h > 0 || plane > 0 || kk > 0) ? 1u : 0u);
             }
@@ -358,7 +375,7 @@ __global__ void __launch_bounds__(kProjThreads, kLean ? 2 : 1)
         }
       }
     }
-  } else if (warp < 3 + 4 * kNGroups) {
+  } else if (warp < 3 + 4 * Cfg::kNGroups) {
     // ================= converters: group cg handles the jobs (chunks) with job % 2 == cg
     const int cg = (warp - 3) >> 2;
     const int ct = tid - 96 - cg * kConv;
@@ -375,11 +392,11 @@ __global__ void __launch_bounds__(kProjThreads, kLean ? 2 : 1)
         int valid;
         tile_coords<Q, L, U16>(g, tt, g2, n, row0, valid);
         for (int c = 0; c < Cfg::kCPT; ++c, ++job) {
-          if (kNGroups == 2 && (job & 1u) != (uint32_t)cg) continue;
+          if (Cfg::kNGroups == 2 && (job & 1u) != (uint32_t)cg) continue;
           const uint32_t slot = job % Cfg::kNS, sphase = (job / Cfg::kNS) & 1u;
-          const uint32_t aslot = job % kNA, aphase = (job / kNA) & 1u;
+          const uint32_t aslot = job % Cfg::kNA, aphase = (job / Cfg::kNA) & 1u;
           bool resid = false;
-          uint32_t* wf = wflag + cg * 8 + ((job / kNGroups) & 1) * 4;
+          uint32_t* wf = wflag + cg * 8 + ((job / Cfg::kNGroups) & 1) * 4;
           if constexpr (U16) {
             constexpr int kW = Cfg::kACols;               // 32-bit words of this row in the chunk
             const uint8_t* src = ring + slot * Cfg::kSlot;
@@ -506,7 +523,7 @@ __global__ void __launch_bounds__(kProjThreads, kLean ? 2 : 1)
     }
   } else {
     // ================= epilogue (128 threads; TMEM lane quadrant = warp % 4)
-    const int et = tid - kEpi0;
+    const int et = tid - Cfg::kEpi0;
     const int quad = warp & 3;
     const int row = quad * 32 + lane;                    // TMEM lane == tile row == A2 m index
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
@@ -550,20 +567,26 @@ __global__ void __launch_bounds__(kProjThreads, kLean ? 2 : 1)
           tc_fence_after();
           if (pending >= 0) { stage2_epilogue(pending); pending = -1; }
         }
-        // A2 element (m = f*L + a, k), K-major no swizzle: (k/8)*kLBO2 + (m/8)*128 + (m%8)*16 + (k%8)*2
+        // A2 element (m = f*L + a, k), MN-major: (m/8)*kSBO2 + (k/8)*128 + (k%8)*16 + (m%8)*2
         int f, k;
         if constexpr (Q >= 128) { f = tt % g2; k = row; }
         else { f = tt * Cfg::kFPT + row / Q; k = row % Q; }
         {
-          uint8_t* base = sA2 + (k >> 3) * Cfg::kLBO2 + (k & 7) * 2;
+          uint8_t* base = sA2 + (k >> 3) * 128 + (k & 7) * 16 + ((f * L) >> 3) * Cfg::kSBO2;
 #pragma unroll
-          for (int q = 0; q < L; ++q) {
-            const int m = f * L + q;
-            const __half hi = __float2half_rn(t[q]);
-            const __half lo = __float2half_rn(t[q] - __half2float(hi));
-            uint8_t* p = base + (m >> 3) * 128 + (m & 7) * 16;
-            *reinterpret_cast<__half*>(p) = hi;
-            *reinterpret_cast<__half*>(p + Cfg::kA2) = lo;
+          for (int q0 = 0; q0 < L; q0 += 8) {
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const __half h0 = __float2half_rn(t[q0 + 2 * e]), h1 = __float2half_rn(t[q0 + 2 * e + 1]);
+              const __half l0 = __float2half_rn(t[q0 + 2 * e] - __half2float(h0));
+              const __half l1 = __float2half_rn(t[q0 + 2 * e + 1] - __half2float(h1));
+              hw[e] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+              lw[e] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+            }
+            uint8_t* p = base + (q0 >> 3) * Cfg::kSBO2;
+            *reinterpret_cast<uint4*>(p) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(p + Cfg::kA2) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
           }
         }
         if (et == 0) TRACE(10, tile);
@@ -631,10 +654,10 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
   // overrides (0 = spread every batch over all SMs).
   static const int env_frames = [] { const char* e = std::getenv("WDD_PROJ_MIN_FRAMES"); return e ? std::atoi(e) : -1; }();
   const int min_frames = env_frames >= 0 ? env_frames
-                                         : std::max(4, (kLean ? (1 << 19) : (1 << 20)) / (Q * Q * (U16 ? 2 : 4)));
+                                         : std::max(4, (Cfg::kLean ? (1 << 19) : (1 << 20)) / (Q * Q * (U16 ? 2 : 4)));
   if (min_frames > 0) g2 = Cfg::kG2;
   const int64_t groups = (n + g2 - 1) / g2;
-  int grid = (int)std::min<int64_t>(groups, (int64_t)p.sm_count);
+  int grid = (int)std::min<int64_t>(groups, (int64_t)p.sm_count * Cfg::kMinBlocks);
   if (min_frames > 0) grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, (n + min_frames - 1) / min_frames));
   CUtensorMap tmap;
   std::memset(&tmap, 0, sizeof tmap);
@@ -656,7 +679,7 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
              no_wait ? 0 : 1};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kProjThreads);
+  cfg.blockDim = dim3(Cfg::kThreads);
   cfg.dynamicSmemBytes = Cfg::smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -700,6 +723,17 @@ extern "C" int wdd_trace_ctas(unsigned long long* host /* 8192 x 5 */) {
   return (int)(n < 8192 ? n : 8192);
 }
 #endif
+
+bool project_is_lean(const Plan& p) {
+#define WDD_LEAN_CASE(QQ, LL) \
+  if (p.Q == QQ && p.L == LL) return p.dtype == 0 ? ProjCfg<QQ, LL, true>::kLean : ProjCfg<QQ, LL, false>::kLean;
+  WDD_LEAN_CASE(32, 8) WDD_LEAN_CASE(32, 16) WDD_LEAN_CASE(32, 32)
+  WDD_LEAN_CASE(64, 8) WDD_LEAN_CASE(64, 16) WDD_LEAN_CASE(64, 32)
+  WDD_LEAN_CASE(128, 8) WDD_LEAN_CASE(128, 16) WDD_LEAN_CASE(128, 24) WDD_LEAN_CASE(128, 32)
+  WDD_LEAN_CASE(256, 8) WDD_LEAN_CASE(256, 16) WDD_LEAN_CASE(256, 24) WDD_LEAN_CASE(256, 32)
+#undef WDD_LEAN_CASE
+  return false;
+}
 
 size_t project_smem_bytes(int Q, int L) {
 #define WDD_SMEM_CASE(QQ, LL) if (Q == QQ && L == LL) return ProjCfg<QQ, LL, true>::smem;
@@ -1038,8 +1072,9 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
       dim3 grid(p.K / (2 << logP), n_rows);
       // (with two projection CTAs per SM a PDL-launched row FFT would park its CTAs next to the
       // last projection CTAs and slow them down: launch it after the projection completes)
-      static const int rowfft_pdl = [] { const char* e = std::getenv("WDD_ROWFFT_PDL"); return e ? std::atoi(e) : (kLean ? 0 : 1); }();
-      return launch_pdl(rowfft_kernel<LOGN>, grid, dim3(nt), smem, st, rowfft_pdl != 0, (const float*)p.d_Call, rows, masks,
+      static const int env_pdl = [] { const char* e = std::getenv("WDD_ROWFFT_PDL"); return e ? std::atoi(e) : -1; }();
+      const bool rowfft_pdl = env_pdl >= 0 ? env_pdl != 0 : !project_is_lean(p);
+      return launch_pdl(rowfft_kernel<LOGN>, grid, dim3(nt), smem, st, rowfft_pdl, (const float*)p.d_Call, rows, masks,
                         p.mask_words, (const float2*)p.d_twx, (const int32_t*)p.d_col_vx, p.d_R, logP, p.Sy, p.K,
                         p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)));
     });

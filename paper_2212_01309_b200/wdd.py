@@ -44,7 +44,7 @@ class _Info(ctypes.Structure):
                 ("wavelength_A", ctypes.c_double), ("step_A", ctypes.c_double), ("eps", ctypes.c_double),
                 ("bytes_G", ctypes.c_int64), ("bytes_bank", ctypes.c_int64), ("bytes_R", ctypes.c_int64),
                 ("bytes_C", ctypes.c_int64), ("frames_ingested", ctypes.c_int64), ("nranks", ctypes.c_int32),
-                ("rank", ctypes.c_int32)]
+                ("rank", ctypes.c_int32), ("proj_ctas_per_sm", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
 
 _lib = None
