@@ -128,27 +128,29 @@ struct ProjCfgT {
   static constexpr uint32_t kSBO2 = (kK2 / 8) * 128;
   static constexpr int kA2 = (kM2 / 8) * (int)kSBO2;       // one A2 plane
   static constexpr int kAcc1 = kN;                        // per acc1 slot (both count planes accumulate here)
-  static constexpr int kNAcc = LEAN ? 2 : 4;              // acc1 ring
+  static constexpr int kNB2 = LEAN ? 1 : 2;               // stage-2 A2 images / accumulators in flight
+  // acc1 ring: 4 deep unless TMEM (A ring + plane-1 buffers + acc1 + acc2 images) would exceed 512 columns
+  static constexpr int kNAcc = (LEAN || (kNA + kNGroups) * (Q >= 64 ? 32 : Q / 2) + (4 + kNB2) * 2 * L > 512) ? 2 : 4;
   static constexpr int kACols = kKC / 2;                  // TMEM columns of one A1 chunk (fp16 pairs)
   static constexpr int tA = 0;                            // TMEM column map
   static constexpr int tP1 = tA + kNA * kACols;          // one plane-1 buffer per converter group
   static constexpr int tAcc1 = tP1 + kNGroups * kACols;
   static constexpr int tAcc2 = tAcc1 + kNAcc * kAcc1;
-  static constexpr int kTmemCols = pow2_cols(tAcc2 + kN);
-  static_assert(tAcc2 + kN <= 512, "TMEM");
-  static constexpr int kFixed = (U16 ? 0 : 2 * kSlot) + align_up(2 * kA2, 1024) + align_up(kB, 1024) + 512;
+  static constexpr int kTmemCols = pow2_cols(tAcc2 + kNB2 * kN);
+  static_assert(tAcc2 + kNB2 * kN <= 512, "TMEM");
+  static constexpr int kFixed = (U16 ? 0 : 2 * kSlot) + align_up(kNB2 * 2 * kA2, 1024) + align_up(kB, 1024) + 512;
   static constexpr int kNSraw = (((LEAN ? 113 * 1024 : 232448) - kFixed) / kSlot) & ~1;
   static constexpr int kNSfit = kNSraw < 2 ? 2 : kNSraw;   // (lean: configs that do not fit run 1 CTA/SM)
   static constexpr int kNS = kNSfit < WDD_NS ? kNSfit : WDD_NS;  // raw ring (even: group = job parity)
   static constexpr int off_ring = 0;
   static constexpr int off_P1 = off_ring + kNS * kSlot;   // f32 path only
   static constexpr int off_A2 = off_P1 + (U16 ? 0 : 2 * kSlot);
-  static constexpr int off_B = off_A2 + align_up(2 * kA2, 1024);
+  static constexpr int off_B = off_A2 + align_up(kNB2 * 2 * kA2, 1024);
   static constexpr int off_bar = off_B + align_up(kB, 1024);
-  static constexpr int kBars = 2 * kNS + 2 * kNA + 2 * kNAcc + 5;
+  static constexpr int kBars = 2 * kNS + 2 * kNA + 2 * kNAcc + 3 * kNB2 + 3;
   static constexpr int off_misc = off_bar + 8 * kBars;    // meta[kNS+kNA], wflag[2 groups][2][4], tmem slot
   static constexpr int smem = off_misc + 4 * (kNS + kNA) + 64 + 16;
-  static constexpr int kTmemUsed = tAcc2 + kN;
+  static constexpr int kTmemUsed = tAcc2 + kNB2 * kN;
   static_assert(kNS % 2 == 0 && kNA % 2 == 0, "even rings: converter group = job parity");
   static_assert(kG2 >= 1, "group");
   static_assert(smem <= 232448, "shared memory");
@@ -230,9 +232,10 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
   uint64_t* p1_empty = a_empty + Cfg::kNA;          // [2] per converter group
   uint64_t* acc1_full = p1_empty + 2;          // [kNAcc]
   uint64_t* acc1_empty = acc1_full + Cfg::kNAcc;
-  uint64_t* a2_full = acc1_empty + Cfg::kNAcc;
-  uint64_t* s2_done = a2_full + 1;
-  uint64_t* b_full = s2_done + 1;               // basis operand image landed (bulk copy)
+  uint64_t* a2_full = acc1_empty + Cfg::kNAcc;  // [kNB2] A2 image written
+  uint64_t* s2_done = a2_full + Cfg::kNB2;      // [kNB2] stage-2 MMAs reading A2 image done
+  uint64_t* acc2_empty = s2_done + Cfg::kNB2;   // [kNB2] stage-2 accumulator read by the epilogue
+  uint64_t* b_full = acc2_empty + Cfg::kNB2;    // basis operand image landed (bulk copy)
   uint32_t* meta = reinterpret_cast<uint32_t*>(smem + Cfg::off_misc);   // [kNS + Cfg::kNA]
   uint32_t* wflag = meta + Cfg::kNS + Cfg::kNA;                               // [2][2][4]
   uint32_t* tslot = wflag + 16;
@@ -260,8 +263,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
     mbar_init(&p1_empty[0], 1);
     mbar_init(&p1_empty[1], 1);
     for (int i = 0; i < Cfg::kNAcc; ++i) { mbar_init(&acc1_full[i], 1); mbar_init(&acc1_empty[i], 4); }
-    mbar_init(a2_full, 1);
-    mbar_init(s2_done, 1);
+    for (int i = 0; i < Cfg::kNB2; ++i) { mbar_init(&a2_full[i], 1); mbar_init(&s2_done[i], 1); mbar_init(&acc2_empty[i], 4); }
     mbar_init(b_full, 1);
     fence_mbar_init();
     mbar_arrive_expect_tx(b_full, Cfg::kB);
@@ -329,24 +331,28 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_f16(Cfg::kM2, Cfg::kN, 0, /*a_major=MN*/ 1, 0);
       const uint32_t a20 = smem_u32(sA2), b0 = smem_u32(sB);
-      const uint32_t acc2 = tbase + Cfg::tAcc2;
       mbar_wait(b_full, 0);
-      uint32_t phase = 0;
+      uint32_t c2 = 0;
       for (int64_t gi = 0; gi < my_groups; ++gi) {
-        for (int h = 0; h < Cfg::kTPF; ++h, phase ^= 1u) {
-          mbar_wait(a2_full, phase);
+        const uint32_t gb = (uint32_t)(gi % Cfg::kNB2);
+        const uint32_t acc2 = tbase + Cfg::tAcc2 + gb * Cfg::kN;
+        for (int h = 0; h < Cfg::kTPF; ++h, ++c2) {
+          const uint32_t ab = c2 % Cfg::kNB2;
+          mbar_wait(&a2_full[ab], (c2 / Cfg::kNB2) & 1u);
+          if (h == 0 && gi >= Cfg::kNB2) mbar_wait(&acc2_empty[gb], (uint32_t)((gi / Cfg::kNB2) - 1) & 1u);
           TRACE(12, h);
           tc_fence_after();
+          const uint32_t a2 = a20 + ab * 2 * Cfg::kA2;
 #pragma unroll 1
           for (int plane = 0; plane < 2; ++plane) {
 #pragma unroll
             for (int kk = 0; kk < Cfg::kK2 / 16; ++kk) {
-              const uint64_t ad = smem_desc_noswz(a20 + plane * Cfg::kA2 + kk * 256, 128, Cfg::kSBO2);
+              const uint64_t ad = smem_desc_noswz(a2 + plane * Cfg::kA2 + kk * 256, 128, Cfg::kSBO2);
               const uint64_t bd = smem_desc_noswz(b0 + (h * (Cfg::kK2 / 8) + 2 * kk) * Cfg::kLBO_B, Cfg::kLBO_B, 128);
               mma_f16_ss(acc2, ad, bd, idesc, (h > 0 || plane > 0 || kk > 0) ? 1u : 0u);
             }
           }
-          mma_commit(s2_done);
+          mma_commit(&s2_done[ab]);
         }
       }
     }
@@ -527,14 +533,21 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
     const int quad = warp & 3;
     const int row = quad * 32 + lane;                    // TMEM lane == tile row == A2 m index
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    const uint32_t acc2 = tbase + Cfg::tAcc2 + lane_addr;
-    uint32_t tile = 0, s2_issued = 0;
-    int64_t pending = -1;   // frame0 of a group whose stage-2 result has not been stored yet
+    uint32_t tile = 0, c2 = 0;
+    // groups whose stage-2 result has not been stored yet (at most kNB2 + 1): (frame0, gi, last chunk)
+    int64_t pend_f0[Cfg::kNB2 + 1] = {};
+    int64_t pend_gi[Cfg::kNB2 + 1] = {};
+    uint32_t pend_c[Cfg::kNB2 + 1] = {};
+    int npend = 0;
     // accumulator row held by this thread's lane (M = 64: lanes 0-15 of each quadrant)
     const int m2 = Cfg::kM2 == 128 ? row : (lane < 16 ? quad * 16 + lane : 1 << 20);
-    auto stage2_epilogue = [&](int64_t frame0) {
+    auto stage2_epilogue = [&](int64_t frame0, int64_t gi) {
+      const uint32_t gb = (uint32_t)(gi % Cfg::kNB2);
       float d[Cfg::kN];
-      tmem_ld_cols<Cfg::kN>(acc2, d);
+      tmem_ld_cols<Cfg::kN>(tbase + Cfg::tAcc2 + gb * Cfg::kN + lane_addr, d);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc2_empty[gb]);
       const int f = m2 / L, aa = m2 % L;
       const int64_t fg = frame0 + f;
       if (f < g2 && fg < n) {
@@ -545,6 +558,14 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
                                  (d[b + 2] + d[L + b + 2]) * a.sc2, (d[b + 3] + d[L + b + 3]) * a.sc2);
           *reinterpret_cast<float4*>(dst + b) = v;
         }
+      }
+    };
+    // store every pending group whose last stage-2 chunk is <= cdone (all those MMAs have completed)
+    auto flush_pending = [&](uint32_t cdone) {
+      while (npend > 0 && pend_c[0] <= cdone) {
+        stage2_epilogue(pend_f0[0], pend_gi[0]);
+        for (int i = 1; i < npend; ++i) { pend_f0[i - 1] = pend_f0[i]; pend_gi[i - 1] = pend_gi[i]; pend_c[i - 1] = pend_c[i]; }
+        --npend;
       }
     };
     for (int64_t gi = 0; gi < my_groups; ++gi) {
@@ -562,17 +583,18 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc1_empty[s1]);
-        if (tt % tph == 0 && s2_issued > 0) {   // A2 is free once the previous stage-2 chunk is done
-          mbar_wait(s2_done, (s2_issued - 1) & 1u);
+        const uint32_t ab = c2 % Cfg::kNB2;
+        if (tt % tph == 0 && c2 >= (uint32_t)Cfg::kNB2) {   // A2 image ab is free once chunk c2 - kNB2 is done
+          mbar_wait(&s2_done[ab], ((c2 / Cfg::kNB2) - 1) & 1u);
           tc_fence_after();
-          if (pending >= 0) { stage2_epilogue(pending); pending = -1; }
+          flush_pending(c2 - Cfg::kNB2);
         }
         // A2 element (m = f*L + a, k), MN-major: (m/8)*kSBO2 + (k/8)*128 + (k%8)*16 + (m%8)*2
         int f, k;
         if constexpr (Q >= 128) { f = tt % g2; k = row; }
         else { f = tt * Cfg::kFPT + row / Q; k = row % Q; }
         {
-          uint8_t* base = sA2 + (k >> 3) * 128 + (k & 7) * 16 + ((f * L) >> 3) * Cfg::kSBO2;
+          uint8_t* base = sA2 + ab * 2 * Cfg::kA2 + (k >> 3) * 128 + (k & 7) * 16 + ((f * L) >> 3) * Cfg::kSBO2;
 #pragma unroll
           for (int q0 = 0; q0 < L; q0 += 8) {
             uint32_t hw[4], lw[4];
@@ -593,16 +615,21 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
         if (tt % tph == tph - 1) {   // stage-2 K chunk complete
           fence_proxy_async_smem();
           named_sync(2, 128);
-          if (et == 0) { mbar_arrive(a2_full); TRACE(11, tile); }
-          ++s2_issued;
+          if (et == 0) { mbar_arrive(&a2_full[ab]); TRACE(11, tile); }
+          ++c2;
         }
       }
-      pending = g * g2;
+      pend_f0[npend] = g * g2;
+      pend_gi[npend] = gi;
+      pend_c[npend] = c2 - 1;
+      ++npend;
     }
-    if (s2_issued > 0) {
-      mbar_wait(s2_done, (s2_issued - 1) & 1u);
+    // drain: wait for the last chunk of each pending group in order
+    while (npend > 0) {
+      const uint32_t cl = pend_c[0];
+      mbar_wait(&s2_done[cl % Cfg::kNB2], (cl / Cfg::kNB2) & 1u);
       tc_fence_after();
-      if (pending >= 0) stage2_epilogue(pending);
+      flush_pending(cl);
     }
   }
   tc_fence_before();
