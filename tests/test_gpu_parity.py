@@ -284,7 +284,7 @@ def test_non_power_of_two_scan(wdd, torch_cuda, Sy, Sx):
     assert rel(out.cpu().numpy(), ref["O"]) < TOL
 
 
-@pytest.mark.parametrize("rows_per_readout", [1, 2, 5, 8])
+@pytest.mark.parametrize("rows_per_readout", [1, 2, 5, 8, 16])
 def test_live_readout_cadence(wdd, torch_cuda, rows_per_readout):
     # frames arrive in scan order; a readout every r rows flushes r staged rows into G (few rows:
     # DFT-matrix rank update; more: FFT along y with the missing rows as zeros).  Every readout
@@ -306,3 +306,24 @@ def test_live_readout_cadence(wdd, torch_cuda, rows_per_readout):
             assert rel(out.cpu().numpy(), ref["O"]) < TOL, b
     G, act = plan.get_accumulator()
     assert rel(G.cpu().numpy(), _oracle_all(cfg, fr, idx)["G"][act]) < TOL
+
+
+def test_medium_live_cadence_pruned_flush(wdd, torch_cuda):
+    # 128-row scan read out every 32 rows: each flush is an aligned block of 2^5 rows, which takes
+    # the pruned y transform (4 FFTs of 32 points instead of one of 128)
+    torch = torch_cuda
+    cfg = CONFIGS["medium"]
+    idx = np.arange(cfg.S)
+    fr = _frames(cfg, idx)
+    fr_dev = _to_dev(torch, fr)
+    plan = wdd.Plan.from_config(cfg)
+    step = 32 * cfg.Sx
+    for a in range(0, cfg.S, step):
+        for b in range(a, a + step, cfg.batch):
+            plan.ingest(fr_dev[b:b + cfg.batch], idx[b:b + cfg.batch])
+        out = plan.readout()
+    torch.cuda.synchronize()
+    ref = _oracle_all(cfg, fr, idx)
+    assert rel(out.cpu().numpy(), ref["O"]) < TOL
+    G, act = plan.get_accumulator()
+    assert rel(G.cpu().numpy(), ref["G"][act]) < TOL
