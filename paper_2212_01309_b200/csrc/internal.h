@@ -112,6 +112,8 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
 // per-k-tile partial Wiener readout d_opart[colfft_tiles][n_act].
 cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st);
 bool flush_uses_fft(const Plan& p, int n_rows);
+int flush_kind(const Plan& p, int n_rows);    // 2 tensor-core GEMM, 1 FFT, 0 DFT matrix
+int flush_tiles(const Plan& p, int n_rows);   // partial-readout tiles a flush writes (0: none)
 int colfft_tiles(const Plan& p);
 bool finalize_uses_fft(const Plan& p);
 // o[g] = sum_k G[g][k] W[g][k] (one warp per active v)

@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cuda_bf16.h>
 #include <vector>
 
 #include "internal.h"
@@ -1180,6 +1181,236 @@ __global__ void __launch_bounds__(256) flush_kernel(const float2* __restrict__ R
   }
 }
 
+// =====================================================================================
+// a5 + a6 on the tensor cores: the phase-weighted rank update as the batched complex GEMM of the
+// north star,  G[(j, vy)][k] (+)= sum_r F[vy][r] R[j][row_r][k],  F[vy][r] = W_Sy^{vy row_r}/sqrt(Sy)
+// (the DFT matrix of eq:outer_prod / P:411-414 restricted to the active vy of column j and the
+// staged rows), with the tile's share of the Wiener readout sum_k G K_v fused into the epilogue.
+// CTA = (column j, tile of 128 active vy, tile of NT coefficients); the K dimension runs over the
+// staged rows, 32 rows (64 real K: re / im parts) per chunk, double-buffered in shared memory.
+// Complex -> real: D_re = [Fr | -Fi] x [Rr ; Ri], D_im = [Fi | Fr] x [Rr ; Ri] (two fp32 TMEM
+// accumulators, M = 128 vy rows, N = NT).  Precision: both operands split into bf16 hi + lo,
+// three passes (hi.hi + hi.lo + lo.hi), fp32 accumulation (~1e-5 relative per term).
+// =====================================================================================
+constexpr int kCgM = 128;                                  // active vy per tile (MMA M)
+constexpr uint32_t kCgLBOA = (kCgM / 8) * 128;             // A (K-major): bytes between K-adjacent core matrices
+
+__device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+// x = hi + lo with hi = bf16(x), lo = bf16(x - hi), packed for two values
+__device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  const float2 hf = __bfloat1622float2(h);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = bf16x2_bits(a - hf.x, b - hf.y);
+}
+
+// CTA = (column j, tile of 128 active vy, k-chunk): the A operand (the F tile of all staged rows,
+// <= kCgRows rows) is built once; the CTA then walks its k-chunk in NT-coefficient tiles with the
+// B tile of the next tile built (R -> bf16 hi / lo) while the MMAs of the current one run, and the
+// epilogue of a tile overlapping the MMAs of the next (two TMEM accumulator pairs).  Each thread
+// owns one vy row and half the tile's coefficients, so the Wiener-readout dot product accumulates
+// in registers across the whole k-chunk.
+constexpr int kCgRows = 64;                                 // staged rows the GEMM form takes
+constexpr int kCgKmax = 2 * kCgRows;                        // real K (re / im parts)
+constexpr int kCgAfull = kCgM * kCgKmax * 2;                // one A plane over all staged rows (32 KB)
+constexpr int kCgNT = 64;                                   // coefficients per tile
+constexpr int kCgBt = kCgNT * kCgKmax * 2;                  // one B plane of a tile (16 KB)
+constexpr uint32_t kCgSBOBf = (kCgKmax / 8) * 128;          // B (MN-major): N-adjacent core matrices
+constexpr int kCgSmem = 4 * kCgAfull + 2 * 2 * kCgBt;       // A [acc][plane] + B [buf][plane] = 192 KB
+
+__global__ void __launch_bounds__(256, 1) colgemm_kernel(const float2* __restrict__ R, const int32_t* __restrict__ rows,
+                                                         int n_rows, const float2* __restrict__ tw, int Sy,
+                                                         float inv_sqrt_sy, const int32_t* __restrict__ col_off,
+                                                         const int32_t* __restrict__ act_vy, float2* __restrict__ G,
+                                                         const float2* __restrict__ W, float2* __restrict__ opart,
+                                                         int64_t n_act, int K, int ktiles, int overwrite) {
+  extern __shared__ __align__(1024) uint8_t cg_smem[];
+  __shared__ int svy[kCgM];
+  __shared__ int srow[kCgRows];
+  __shared__ uint64_t mma_done[2];
+  __shared__ uint32_t tslot;
+  __shared__ float2 sdot[kCgM];
+  uint8_t* sA = cg_smem;                                     // [acc re/im][plane hi/lo]
+  uint8_t* sB = cg_smem + 4 * kCgAfull;                      // [buf][plane]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int j = blockIdx.z, vt = blockIdx.y, kc = blockIdx.x;
+  pdl_trigger();
+  const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
+  const int i0 = vt * kCgM;
+  if (i0 >= mj) return;                                      // (grid covers the longest column)
+  const int kr = (n_rows + 7) & ~7;                          // rows used, padded to a core matrix
+  const int kreal = 2 * kr;                                  // real K
+  if (tid < kCgM) svy[tid] = i0 + tid < mj ? __ldg(act_vy + g0 + i0 + tid) : -1;
+  if (tid == 0) {
+    mbar_init(&mma_done[0], 1);
+    mbar_init(&mma_done[1], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<4 * kCgNT>(&tslot);
+  pdl_wait();                                                // R of the row DFT, G of earlier flushes
+  if (tid < kr) srow[tid] = tid < n_rows ? rows[tid] : -1;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  const bool sy_pow2 = (Sy & (Sy - 1)) == 0;
+  // A (K-major, M = 128): element (m, k) at (k/8)*LBO + (m/8)*128 + (m%8)*16 + (k%8)*2, k = d*kr + r;
+  // thread -> (vy row m, group of 8 staged rows): 8 twiddles -> 16-byte stores
+  for (int w = tid; w < kCgM * (kr / 8); w += 256) {
+    const int m = w % kCgM, rg = w / kCgM;
+    const int vy = svy[m];
+    float fr[8], fi[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int row = srow[rg * 8 + e];
+      float2 f = make_float2(0.f, 0.f);
+      if (vy >= 0 && row >= 0) f = __ldg(tw + (sy_pow2 ? ((vy * row) & (Sy - 1)) : (int)(((int64_t)vy * row) % Sy)));
+      fr[e] = f.x * inv_sqrt_sy;
+      fi[e] = f.y * inv_sqrt_sy;
+    }
+    const uint32_t off_re = (uint32_t)rg * kCgLBOA + (m >> 3) * 128 + (m & 7) * 16;
+    const uint32_t off_im = off_re + (uint32_t)(kr / 8) * kCgLBOA;
+    uint32_t h[4], l[4], hn[4], ln[4], hp[4], lp[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      split_bf16x2(fr[2 * e], fr[2 * e + 1], h[e], l[e]);
+      split_bf16x2(-fi[2 * e], -fi[2 * e + 1], hn[e], ln[e]);
+      split_bf16x2(fi[2 * e], fi[2 * e + 1], hp[e], lp[e]);
+    }
+    *reinterpret_cast<uint4*>(sA + 0 * kCgAfull + off_re) = make_uint4(h[0], h[1], h[2], h[3]);     // re: [Fr | -Fi]
+    *reinterpret_cast<uint4*>(sA + 1 * kCgAfull + off_re) = make_uint4(l[0], l[1], l[2], l[3]);
+    *reinterpret_cast<uint4*>(sA + 0 * kCgAfull + off_im) = make_uint4(hn[0], hn[1], hn[2], hn[3]);
+    *reinterpret_cast<uint4*>(sA + 1 * kCgAfull + off_im) = make_uint4(ln[0], ln[1], ln[2], ln[3]);
+    *reinterpret_cast<uint4*>(sA + 2 * kCgAfull + off_re) = make_uint4(hp[0], hp[1], hp[2], hp[3]); // im: [Fi | Fr]
+    *reinterpret_cast<uint4*>(sA + 3 * kCgAfull + off_re) = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+    *reinterpret_cast<uint4*>(sA + 2 * kCgAfull + off_im) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(sA + 3 * kCgAfull + off_im) = make_uint4(l[0], l[1], l[2], l[3]);
+  }
+  const int kbase = kc * ktiles * kCgNT;
+  const float2* Rj = R + (int64_t)j * Sy * K;
+  // B (MN-major, N = NT): element (n, k) at (n/8)*SBO + (k/8)*128 + (k%8)*16 + (n%8)*2, k = d*kr + r
+  auto build_b = [&](int t, int buf) {
+    uint8_t* sb = sB + buf * 2 * kCgBt;
+    const int k0 = kbase + t * kCgNT;
+    for (int w = tid; w < kr * (kCgNT / 8); w += 256) {
+      const int r = w % kr, nb = w / kr;
+      const int row = srow[r];
+      float4 v[4];
+      if (row >= 0) {
+        const float4* src = reinterpret_cast<const float4*>(Rj + (int64_t)row * K + k0 + nb * 8);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = __ldg(src + e);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      uint32_t rh[4], rl[4], ih[4], il[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        split_bf16x2(v[e].x, v[e].z, rh[e], rl[e]);
+        split_bf16x2(v[e].y, v[e].w, ih[e], il[e]);
+      }
+      const uint32_t off = nb * kCgSBOBf + (r >> 3) * 128 + (r & 7) * 16;
+      const uint32_t offi = off + (uint32_t)(kr / 8) * 128;
+      *reinterpret_cast<uint4*>(sb + off) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
+      *reinterpret_cast<uint4*>(sb + kCgBt + off) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
+      *reinterpret_cast<uint4*>(sb + offi) = make_uint4(ih[0], ih[1], ih[2], ih[3]);
+      *reinterpret_cast<uint4*>(sb + kCgBt + offi) = make_uint4(il[0], il[1], il[2], il[3]);
+    }
+  };
+  constexpr uint32_t idesc = idesc_f16(kCgM, kCgNT, /*bf16*/ 1, /*a K-major*/ 0, /*b MN-major*/ 1);
+  auto issue = [&](int t) {   // thread 0: MMAs of tile t into TMEM pair t & 1
+    tc_fence_after();
+    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB + (t & 1) * 2 * kCgBt);
+    const uint32_t d0 = tbase + (t & 1) * 2 * kCgNT;
+    bool first = true;
+#pragma unroll 1
+    for (int pass = 0; pass < 3; ++pass) {                   // hi.hi, hi.lo, lo.hi
+      const int pa = pass == 2 ? 1 : 0, pb = pass == 1 ? 1 : 0;
+#pragma unroll 1
+      for (int kk = 0; kk < kreal / 16; ++kk) {
+#pragma unroll
+        for (int acc = 0; acc < 2; ++acc) {
+          const uint64_t ad = smem_desc_noswz(a0 + (acc * 2 + pa) * kCgAfull + kk * 2 * kCgLBOA, kCgLBOA, 128);
+          const uint64_t bd = smem_desc_noswz(b0 + pb * kCgBt + kk * 256, 128, kCgSBOBf);
+          mma_f16_ss(d0 + acc * kCgNT, ad, bd, idesc, first ? 0u : 1u);
+        }
+        first = false;
+      }
+    }
+    mma_commit(&mma_done[t & 1]);
+  };
+  build_b(0, 0);
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (tid == 0) issue(0);
+  const int quad = warp & 3, half = warp >> 2;
+  const int m = quad * 32 + lane;
+  const bool valid = svy[m] >= 0;
+  const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+  const int64_t grow = (int64_t)(g0 + i0 + m) * K;
+  float2 dot = make_float2(0.f, 0.f);
+  for (int t = 0; t < ktiles; ++t) {
+    if (t + 1 < ktiles) {
+      if (t >= 1) mbar_wait(&mma_done[(t + 1) & 1], ((t - 1) >> 1) & 1u);   // B buffer of tile t - 1 free
+      build_b(t + 1, (t + 1) & 1);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncthreads();                                       // (also: epilogue t - 1 done with TMEM pair)
+      if (tid == 0) issue(t + 1);
+    }
+    mbar_wait(&mma_done[t & 1], (t >> 1) & 1u);
+    tc_fence_after();
+    // epilogue of tile t: G (+)= D, dot += G K over this thread's row and half of the coefficients
+    const uint32_t d0 = tbase + lane_addr + (t & 1) * 2 * kCgNT + half * (kCgNT / 2);
+    float dr[kCgNT / 2], di[kCgNT / 2];
+    tmem_ld_cols<kCgNT / 2>(d0, dr);
+    tmem_ld_cols<kCgNT / 2>(d0 + kCgNT, di);
+    if (valid) {
+      const int k0 = kbase + t * kCgNT + half * (kCgNT / 2);
+      float4* Gr = reinterpret_cast<float4*>(G + grow + k0);
+      const float4* Wr = reinterpret_cast<const float4*>(W + grow + k0);
+      float4 o[kCgNT / 4], w[kCgNT / 4];
+#pragma unroll
+      for (int q = 0; q < kCgNT / 4; ++q) {
+        o[q] = overwrite ? make_float4(0.f, 0.f, 0.f, 0.f) : Gr[q];
+        w[q] = __ldg(Wr + q);
+      }
+#pragma unroll
+      for (int q = 0; q < kCgNT / 4; ++q) {
+        const float4 gn = make_float4(o[q].x + dr[2 * q], o[q].y + di[2 * q], o[q].z + dr[2 * q + 1], o[q].w + di[2 * q + 1]);
+        Gr[q] = gn;
+        dot.x = fmaf(gn.x, w[q].x, fmaf(-gn.y, w[q].y, fmaf(gn.z, w[q].z, fmaf(-gn.w, w[q].w, dot.x))));
+        dot.y = fmaf(gn.x, w[q].y, fmaf(gn.y, w[q].x, fmaf(gn.z, w[q].w, fmaf(gn.w, w[q].z, dot.y))));
+      }
+    }
+    tc_fence_before();
+  }
+  if (half == 1) sdot[m] = dot;
+  __syncthreads();
+  if (half == 0 && valid) {
+    const float2 d1 = sdot[m];
+    opart[(int64_t)kc * n_act + g0 + i0 + m] = make_float2(dot.x + d1.x, dot.y + d1.y);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<4 * kCgNT>(tbase);
+}
+
+// k-chunks of the GEMM flush: enough CTAs to fill two waves of the GPU
+static int colgemm_chunks(const Plan& p) {
+  int max_mj = 0;
+  for (int j = 0; j < p.n_vx; ++j) max_mj = std::max(max_mj, p.col_off[j + 1] - p.col_off[j]);
+  const int ctas = p.n_vx * ((max_mj + kCgM - 1) / kCgM);
+  const int tiles = p.K / kCgNT;
+  int ch = std::max(1, std::min(tiles, (2 * p.sm_count + ctas - 1) / ctas));
+  while (tiles % ch) ++ch;
+  return ch;
+}
+
 static int colfft_logkt(const Plan& p) {
   static const int2 knob = env_pair("WDD_COLFFT");   // (log2 k per CTA, threads) override
   int logKT = ilog2(std::max(2, std::min(32, kFftSmem / (8 * p.Sy))));
@@ -1196,9 +1427,45 @@ bool flush_uses_fft(const Plan& p, int n_rows) {
   return is_pow2(p.Sy) && p.Sy >= 2 && p.Sy <= (1 << kFftMaxLog) && n_rows >= std::max(4, ilog2(p.Sy));
 }
 
+// Which form of the rank update a flush of n_rows staged rows uses: 2 = tensor-core DFT GEMM,
+// 1 = FFT along y, 0 = SIMT DFT matrix.  WDD_FLUSH=gemm|fft|dft overrides.
+int flush_kind(const Plan& p, int n_rows) {
+  static const int env = [] {
+    const char* e = std::getenv("WDD_FLUSH");
+    if (!e) return -1;
+    return std::strcmp(e, "gemm") == 0 ? 2 : std::strcmp(e, "fft") == 0 ? 1 : std::strcmp(e, "dft") == 0 ? 0 : -1;
+  }();
+  const bool gemm_ok = n_rows <= kCgRows && p.K % kCgNT == 0;
+  if (env == 2) return gemm_ok ? 2 : (flush_uses_fft(p, n_rows) ? 1 : 0);
+  if (env == 1) return flush_uses_fft(p, n_rows) ? 1 : (gemm_ok ? 2 : 0);
+  if (env == 0) return 0;
+  return flush_uses_fft(p, n_rows) ? 1 : (gemm_ok ? 2 : 0);
+}
+
+int flush_tiles(const Plan& p, int n_rows) {
+  const int k = flush_kind(p, n_rows);
+  return k == 2 ? colgemm_chunks(p) : k == 1 ? colfft_tiles(p) : 0;
+}
+
 cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st) {
   if (n_rows <= 0) return cudaSuccess;
-  if (flush_uses_fft(p, n_rows)) {
+  if (flush_kind(p, n_rows) == 2) {
+    int max_mj = 0;
+    for (int j = 0; j < p.n_vx; ++j) max_mj = std::max(max_mj, p.col_off[j + 1] - p.col_off[j]);
+    static bool init = false;
+    if (!init) {
+      cudaError_t e = cudaFuncSetAttribute(colgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCgSmem);
+      if (e != cudaSuccess) return e;
+      init = true;
+    }
+    const int ch = colgemm_chunks(p);
+    dim3 grid(ch, (max_mj + kCgM - 1) / kCgM, p.n_vx);
+    return launch_pdl(colgemm_kernel, grid, dim3(256), (size_t)kCgSmem, st, true, (const float2*)p.d_R, rows, n_rows,
+                      (const float2*)p.d_twy, p.Sy, (float)(1.0 / std::sqrt((double)p.Sy)),
+                      (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G, (const float2*)p.d_W,
+                      p.d_opart, (int64_t)p.n_act, p.K, (p.K / kCgNT) / ch, overwrite ? 1 : 0);
+  }
+  if (flush_kind(p, n_rows) == 1) {
     const int logSy = ilog2(p.Sy);
     const int logKT = colfft_logkt(p);
     const size_t smem = ((size_t)p.Sy << logKT) * 8 + (size_t)p.Sy * 8 + 16;

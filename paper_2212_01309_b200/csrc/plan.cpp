@@ -416,7 +416,7 @@ wdd_status flush(Plan& p) {
   }
   for (int32_t sy : rows) p.row_staged[sy] = 0;
   p.G_zero = false;
-  p.opart_tiles = flush_uses_fft(p, n_rows) ? colfft_tiles(p) : 0;
+  p.opart_tiles = flush_tiles(p, n_rows);
   return WDD_OK;
 }
 
@@ -610,7 +610,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ALLOC(p->d_vpos, act.size() * 4);
   ALLOC(p->d_flush_tiles, p->flush_tiles.size() * sizeof(int2));
   ALLOC(p->d_o, act.size() * sizeof(float2));
-  p->opart_cap = std::max(1, colfft_tiles(*p));
+  p->opart_cap = std::max(1, std::max(colfft_tiles(*p), flush_tiles(*p, 1 << 20)));
   ALLOC(p->d_opart, (size_t)p->opart_cap * act.size() * sizeof(float2));
   ALLOC(p->d_gidx, (size_t)p->S * sizeof(int32_t));
   ALLOC(p->d_iota, (size_t)Sy * sizeof(int32_t));
