@@ -681,8 +681,12 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
   // of each batch paying its own pipeline fill and drain on every SM.  WDD_PROJ_MIN_FRAMES
   // overrides (0 = spread every batch over all SMs).
   static const int env_frames = [] { const char* e = std::getenv("WDD_PROJ_MIN_FRAMES"); return e ? std::atoi(e) : -1; }();
-  const int min_frames = env_frames >= 0 ? env_frames
-                                         : std::max(4, (Cfg::kLean ? (1 << 19) : (1 << 20)) / (Q * Q * (U16 ? 2 : 4)));
+  int min_frames = env_frames >= 0 ? env_frames
+                                   : std::max(4, (Cfg::kLean ? (1 << 19) : (1 << 20)) / (Q * Q * (U16 ? 2 : 4)));
+  // the first batch after a reset finds the GPU idle: spread it over every CTA slot so the chained
+  // launches of the following batches find a full machine instead of ramping up one grid at a time
+  static const int wide_first = [] { const char* e = std::getenv("WDD_PROJ_WIDE_FIRST"); return e ? std::atoi(e) : 1; }();
+  if (wide_first && p.frames_ingested == 0 && env_frames < 0) min_frames = 1;
   if (min_frames > 0) g2 = Cfg::kG2;
   const int64_t groups = (n + g2 - 1) / g2;
   int grid = (int)std::min<int64_t>(groups, (int64_t)p.sm_count * Cfg::kMinBlocks);
