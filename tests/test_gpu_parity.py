@@ -148,6 +148,7 @@ def test_full_scan_parity(wdd, torch_cuda, name):
     out2 = plan.readout()
     torch.cuda.synchronize()
     assert np.array_equal(out2.cpu().numpy(), Oimg)
+    plan.sync()   # raises if a device-side wait timed out
 
 
 def test_live_equals_offline_random_partitions(wdd, torch_cuda):
