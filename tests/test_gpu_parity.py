@@ -328,3 +328,29 @@ def test_medium_live_cadence_pruned_flush(wdd, torch_cuda):
     assert rel(out.cpu().numpy(), ref["O"]) < TOL
     G, act = plan.get_accumulator()
     assert rel(G.cpu().numpy(), ref["G"][act]) < TOL
+
+
+def test_back_to_back_acquisitions_same_plan(wdd, torch_cuda):
+    # reset -> full scan -> readout, three times on one plan without host synchronisation in
+    # between: the launches of one acquisition must not overtake the flush / readout of the last
+    torch = torch_cuda
+    cfg = CONFIGS["tiny"]
+    idx = np.arange(cfg.S)
+    fr = _frames(cfg, idx)
+    fr_dev = _to_dev(torch, fr)
+    plan = wdd.Plan.from_config(cfg)
+    s = torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        plan.reset()
+        for a in range(0, cfg.S, 128):
+            plan.ingest(fr_dev[a:a + 128], idx[a:a + 128], s)
+        out = torch.empty((cfg.Sy, cfg.Sx), dtype=torch.complex64, device="cuda")
+        with torch.cuda.stream(s):
+            plan.readout(out)
+        outs.append(out)
+    torch.cuda.synchronize()
+    ref = _oracle_all(cfg, fr, idx)["O"]
+    for o in outs:
+        assert rel(o.cpu().numpy(), ref) < TOL
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
