@@ -890,21 +890,28 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 3 : 2) colfft_kernel(const fl
                                                      const int32_t* __restrict__ col_off,
                                                      const int32_t* __restrict__ act_vy, float2* __restrict__ G,
                                                      const float2* __restrict__ W, float2* __restrict__ opart,
-                                                     int64_t n_act, int logKT, int K, float scale, int overwrite) {
+                                                     int64_t n_act, int logKT, int K, float scale, int overwrite,
+                                                     int tpc) {
   constexpr int Sy = 1 << LOGN;
   extern __shared__ __align__(16) float2 fsm[];
   const int KT = 1 << logKT;
   __shared__ int srow[Sy];                // staged rows
   __shared__ int svy[Sy];                 // slot of each active vy of column j
+  __shared__ float2 sdot[Sy];             // per-row readout partial over this CTA's k-tiles
   float2* x = fsm;                       // [Sy][KT]
   float2* stw = fsm + (Sy << logKT);     // [Sy] twiddles
-  const int j = blockIdx.y, k0 = blockIdx.x * KT;
+  const int j = blockIdx.y;
   pdl_trigger();
   const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
   for (int i = threadIdx.x; i < Sy; i += blockDim.x) stw[i] = __ldg(tw + i);
   for (int i = threadIdx.x; i < n_rows; i += blockDim.x) srow[i] = __ldg(rows + i);
-  for (int i = threadIdx.x; i < mj; i += blockDim.x) svy[i] = fft::fslot<LOGN>(__ldg(act_vy + g0 + i));
+  for (int i = threadIdx.x; i < mj; i += blockDim.x) {
+    svy[i] = fft::fslot<LOGN>(__ldg(act_vy + g0 + i));
+    sdot[i] = make_float2(0.f, 0.f);
+  }
   pdl_wait();   // R (row DFT) and G of the preceding kernels
+  for (int t = 0; t < tpc; ++t) {
+  const int k0 = (blockIdx.x * tpc + t) * KT;
   if (n_rows < Sy)
     for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x) x[e] = make_float2(0.f, 0.f);
   __syncthreads();
@@ -960,9 +967,12 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 3 : 2) colfft_kernel(const fl
         d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
         d.y += __shfl_xor_sync(0xffffffffu, d.y, off);
       }
-      if (pp == 0 && i < mj) opart[(int64_t)blockIdx.x * n_act + g0 + i] = d;
+      if (pp == 0 && i < mj) { sdot[i].x += d.x; sdot[i].y += d.y; }
     }
   }
+  __syncthreads();   // x reused by the next k-tile; sdot settled
+  }
+  for (int i = threadIdx.x; i < mj; i += blockDim.x) opart[(int64_t)blockIdx.x * n_act + g0 + i] = sdot[i];
 }
 
 static int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
@@ -1427,7 +1437,18 @@ static int colfft_logkt(const Plan& p) {
   return logKT;
 }
 
-int colfft_tiles(const Plan& p) { return p.K >> colfft_logkt(p); }
+// k-tiles per y-FFT CTA (<= 4, measured best at Medium and Live) keeping >= 2 waves of CTAs
+static int colfft_tpc(const Plan& p) {
+  const int tiles = p.K >> colfft_logkt(p);
+  int tpc = 1;
+  while (tpc < 4 && tpc * 2 <= tiles && tiles % (tpc * 2) == 0 && (int64_t)(tiles / (tpc * 2)) * p.n_vx >= 2 * p.sm_count)
+    tpc *= 2;
+  static const int env = [] { const char* e = std::getenv("WDD_COLFFT_TPC"); return e ? std::atoi(e) : 0; }();
+  if (env > 0 && tiles % env == 0) tpc = env;
+  return tpc;
+}
+
+int colfft_tiles(const Plan& p) { return (p.K >> colfft_logkt(p)) / colfft_tpc(p); }
 
 bool flush_uses_fft(const Plan& p, int n_rows) {
   // FFT along y costs ~5 Sy log2(Sy) flops per (column, k) whatever the number of staged rows r;
@@ -1486,12 +1507,13 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
         if (e != cudaSuccess) return e;
         init = true;
       }
-      dim3 grid(p.K >> logKT, p.n_vx);
+      const int tpc = colfft_tpc(p);
+      dim3 grid((p.K >> logKT) / tpc, p.n_vx);
       static const int2 knob = env_pair("WDD_COLFFT");
       return launch_pdl(colfft_kernel<LOGN>, grid, dim3(knob.y > 0 ? knob.y : 256), smem, st, true, p.d_R, rows, n_rows,
                         (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G,
                         (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.K,
-                        (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0);
+                        (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0, tpc);
     });
   }
   dim3 grid((unsigned)p.flush_tiles.size(), (p.K + 63) / 64);
