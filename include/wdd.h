@@ -65,7 +65,14 @@ typedef struct {
   int32_t normalize;     /* 0 = literal Algorithm 2 output, 1 = divide by sqrt(o_0)*/
   int32_t device;        /* CUDA device ordinal; the plan's buffers live there                */
   int32_t combine;       /* multi-rank readout: 0 = allreduce o (default), 1 = allreduce G    */
-  int32_t reserved[4];   /* must be zero                                                      */
+  int32_t accumulator;   /* 0 = G(q,k) materialised and updated at every flush (north star);
+                            1 = spectrum only: each flush adds its increment of the
+                            Wiener readout o_v = sum_k G[v,k] K_v[k] (linear in G) to a running o
+                            and never reads or writes G; wdd_get_accumulator forms G on demand
+                            from the coefficient store (one full row DFT + rank update).  Needs a
+                            power-of-two Sy in [2, 1024]; multi-rank readout always sums o
+                            (combine is ignored).                                               */
+  int32_t reserved[3];   /* must be zero                                                      */
 } wdd_plan_opts;
 
 /* Plan creation (host, blocking): derives dq, R, sigma; computes in float64 the basis Psi,

@@ -64,6 +64,11 @@ struct Plan {
   int opart_cap = 1;                  // rows of d_opart
   int opart_tiles = 0;                // valid partial-readout rows for the current G (0: stale)
   bool G_zero = true;                 // G is logically zero (reset); its memory may be stale
+  // spectrum-only accumulator (opts.accumulator = 1): each flush adds its increment
+  // of o = sum_k G K_v to d_oacc; R keeps every row's DFT so G = F_y R is formed on demand
+  bool o_only = false;
+  float2* d_oacc = nullptr;           // n_act
+  std::vector<uint32_t> ingested;     // spectrum-only plans: Sy x mask_words positions ingested since the reset
   float2* d_spec = nullptr;           // Sy*Sx
   float2* d_img_tmp = nullptr;        // Sy*Sx scratch of the image transform (row pass)
   void* d_meta = nullptr;             // per-chunk row tables
@@ -110,7 +115,11 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
 // rank update (a5) of the listed staged rows of R into G; FFT along y or DFT matrix
 // (overwrite: G is logically zero, write instead of accumulate).  The FFT form also writes the
 // per-k-tile partial Wiener readout d_opart[colfft_tiles][n_act].
-cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st);
+// o_only: spectrum-only plans -- no G update, the partial readouts are of this flush's increment
+cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st,
+                         bool o_only = false);
+// o_acc += sum of `tiles` partial readouts (spectrum-only plans)
+cudaError_t launch_oacc(const Plan& p, int tiles, cudaStream_t st);
 bool flush_uses_fft(const Plan& p, int n_rows);
 int flush_kind(const Plan& p, int n_rows);    // 2 tensor-core GEMM, 1 FFT, 0 DFT matrix
 int flush_tiles(const Plan& p, int n_rows);   // partial-readout tiles a flush writes (0: none)

@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 3 : 2) colfft_kernel(const fl
                                                      const int32_t* __restrict__ act_vy, float2* __restrict__ G,
                                                      const float2* __restrict__ W, float2* __restrict__ opart,
                                                      int64_t n_act, int logKT, int K, float scale, int overwrite,
-                                                     int tpc) {
+                                                     int tpc, int o_only) {
   constexpr int Sy = 1 << LOGN;
   extern __shared__ __align__(16) float2 fsm[];
   const int KT = 1 << logKT;
@@ -948,7 +948,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 3 : 2) colfft_kernel(const fl
       const int i = ib + u * rpp + rs;
       const int64_t gi = (int64_t)(g0 + i) * K2 + (k0 >> 1) + pp;
       w[u] = i < mj ? __ldg(W4 + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
-      o[u] = (i < mj && !overwrite) ? G4[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+      o[u] = (i < mj && !overwrite && !o_only) ? G4[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -959,7 +959,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 3 : 2) colfft_kernel(const fl
         const float4 z = *reinterpret_cast<const float4*>(x + (svy[i] << logKT) + 2 * pp);
         const float4 gn = make_float4(fmaf(z.x, scale, o[u].x), fmaf(z.y, scale, o[u].y), fmaf(z.z, scale, o[u].z),
                                       fmaf(z.w, scale, o[u].w));
-        G4[(int64_t)(g0 + i) * K2 + (k0 >> 1) + pp] = gn;
+        if (!o_only) G4[(int64_t)(g0 + i) * K2 + (k0 >> 1) + pp] = gn;
         d.x = fmaf(gn.x, w[u].x, fmaf(-gn.y, w[u].y, fmaf(gn.z, w[u].z, -gn.w * w[u].w)));
         d.y = fmaf(gn.x, w[u].y, fmaf(gn.y, w[u].x, fmaf(gn.z, w[u].w, gn.w * w[u].z)));
       }
@@ -1244,7 +1244,7 @@ __global__ void __launch_bounds__(256, 1) colgemm_kernel(const float2* __restric
                                                          float inv_sqrt_sy, const int32_t* __restrict__ col_off,
                                                          const int32_t* __restrict__ act_vy, float2* __restrict__ G,
                                                          const float2* __restrict__ W, float2* __restrict__ opart,
-                                                         int64_t n_act, int K, int ktiles, int overwrite) {
+                                                         int64_t n_act, int K, int ktiles, int overwrite, int o_only) {
   extern __shared__ __align__(1024) uint8_t cg_smem[];
   __shared__ int svy[kCgM];
   __shared__ int srow[kCgRows];
@@ -1394,13 +1394,13 @@ __global__ void __launch_bounds__(256, 1) colgemm_kernel(const float2* __restric
       float4 o[kCgNT / 4], w[kCgNT / 4];
 #pragma unroll
       for (int q = 0; q < kCgNT / 4; ++q) {
-        o[q] = overwrite ? make_float4(0.f, 0.f, 0.f, 0.f) : Gr[q];
+        o[q] = (overwrite || o_only) ? make_float4(0.f, 0.f, 0.f, 0.f) : Gr[q];
         w[q] = __ldg(Wr + q);
       }
 #pragma unroll
       for (int q = 0; q < kCgNT / 4; ++q) {
         const float4 gn = make_float4(o[q].x + dr[2 * q], o[q].y + di[2 * q], o[q].z + dr[2 * q + 1], o[q].w + di[2 * q + 1]);
-        Gr[q] = gn;
+        if (!o_only) Gr[q] = gn;
         dot.x = fmaf(gn.x, w[q].x, fmaf(-gn.y, w[q].y, fmaf(gn.z, w[q].z, fmaf(-gn.w, w[q].w, dot.x))));
         dot.y = fmaf(gn.x, w[q].y, fmaf(gn.y, w[q].x, fmaf(gn.z, w[q].w, fmaf(gn.w, w[q].z, dot.y))));
       }
@@ -1465,10 +1465,15 @@ int flush_kind(const Plan& p, int n_rows) {
     return std::strcmp(e, "gemm") == 0 ? 2 : std::strcmp(e, "fft") == 0 ? 1 : std::strcmp(e, "dft") == 0 ? 0 : -1;
   }();
   const bool gemm_ok = n_rows <= kCgRows && p.K % kCgNT == 0;
-  if (env == 2) return gemm_ok ? 2 : (flush_uses_fft(p, n_rows) ? 1 : 0);
-  if (env == 1) return flush_uses_fft(p, n_rows) ? 1 : (gemm_ok ? 2 : 0);
-  if (env == 0) return 0;
-  return flush_uses_fft(p, n_rows) ? 1 : (gemm_ok ? 2 : 0);
+  int k;
+  if (env == 2) k = gemm_ok ? 2 : (flush_uses_fft(p, n_rows) ? 1 : 0);
+  else if (env == 1) k = flush_uses_fft(p, n_rows) ? 1 : (gemm_ok ? 2 : 0);
+  else if (env == 0) k = 0;
+  else k = flush_uses_fft(p, n_rows) ? 1 : (gemm_ok ? 2 : 0);
+  // spectrum-only plans need the fused partial readout, which the SIMT DFT flush lacks (their Sy
+  // is a power of two <= 2^kFftMaxLog, checked at plan creation, so the FFT always applies)
+  if (k == 0 && p.o_only) k = gemm_ok ? 2 : 1;
+  return k;
 }
 
 int flush_tiles(const Plan& p, int n_rows) {
@@ -1476,7 +1481,7 @@ int flush_tiles(const Plan& p, int n_rows) {
   return k == 2 ? colgemm_chunks(p) : k == 1 ? colfft_tiles(p) : 0;
 }
 
-cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st) {
+cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st, bool o_only) {
   if (n_rows <= 0) return cudaSuccess;
   if (flush_kind(p, n_rows) == 2) {
     int max_mj = 0;
@@ -1492,7 +1497,7 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
     return launch_pdl(colgemm_kernel, grid, dim3(256), (size_t)kCgSmem, st, true, (const float2*)p.d_R, rows, n_rows,
                       (const float2*)p.d_twy, p.Sy, (float)(1.0 / std::sqrt((double)p.Sy)),
                       (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G, (const float2*)p.d_W,
-                      p.d_opart, (int64_t)p.n_act, p.K, (p.K / kCgNT) / ch, overwrite ? 1 : 0);
+                      p.d_opart, (int64_t)p.n_act, p.K, (p.K / kCgNT) / ch, overwrite ? 1 : 0, o_only ? 1 : 0);
   }
   if (flush_kind(p, n_rows) == 1) {
     const int logSy = ilog2(p.Sy);
@@ -1513,9 +1518,10 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
       return launch_pdl(colfft_kernel<LOGN>, grid, dim3(knob.y > 0 ? knob.y : 256), smem, st, true, p.d_R, rows, n_rows,
                         (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G,
                         (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.K,
-                        (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0, tpc);
+                        (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0, tpc, o_only ? 1 : 0);
     });
   }
+  if (o_only) return cudaErrorNotSupported;   // unreachable: flush_kind never picks the DFT for these
   dim3 grid((unsigned)p.flush_tiles.size(), (p.K + 63) / 64);
   flush_kernel<<<grid, 256, 0, st>>>(p.d_R, p.d_Fy, rows, n_rows, p.d_flush_tiles, p.d_col_off, p.d_act_vy,
                                      p.d_G, p.Sy, p.K, overwrite ? 1 : 0);
@@ -1571,6 +1577,20 @@ __device__ __forceinline__ float2 sum_tiles(const float2* __restrict__ op, int t
     }
   }
   return acc;
+}
+
+// Spectrum-only accumulator: o[g] += sum over the flush's partial readouts (fixed order).
+__global__ void oacc_kernel(const float2* __restrict__ op, int tiles, int64_t n_act, float2* __restrict__ o) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_act) return;
+  const float2 d = sum_tiles(op, tiles, n_act, g);
+  const float2 v = o[g];
+  o[g] = make_float2(v.x + d.x, v.y + d.y);
+}
+
+cudaError_t launch_oacc(const Plan& p, int tiles, cudaStream_t st) {
+  oacc_kernel<<<(unsigned)((p.n_act + 255) / 256), 256, 0, st>>>(p.d_opart, tiles, p.n_act, p.d_oacc);
+  return cudaGetLastError();
 }
 
 __global__ void scatter_kernel(const float2* __restrict__ op, int tiles, const int32_t* __restrict__ vpos,

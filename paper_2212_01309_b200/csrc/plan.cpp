@@ -340,6 +340,7 @@ wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, in
     const int sy = idx[i] / p.Sx, sx = idx[i] % p.Sx;
     p.row_dirty[sy] = 1;
     p.pending[(size_t)sy * p.mask_words + (sx >> 5)] |= 1u << (sx & 31);
+    if (p.o_only) p.ingested[(size_t)sy * p.mask_words + (sx >> 5)] |= 1u << (sx & 31);
   }
   return WDD_OK;
 }
@@ -412,16 +413,54 @@ wdd_status flush(Plan& p) {
   }
   {
     Prof pr(p, kSlotFlush, p.stream);
-    CUDA_TRY(launch_flush(p, dr, n_rows, p.G_zero, p.stream));
+    CUDA_TRY(launch_flush(p, dr, n_rows, p.G_zero, p.stream, p.o_only));
   }
   for (int32_t sy : rows) p.row_staged[sy] = 0;
+  if (p.o_only) {                     // o += this flush's increment; G is not touched
+    Prof pr(p, kSlotReadout, p.stream);
+    CUDA_TRY(launch_oacc(p, flush_tiles(p, n_rows), p.stream));
+    return WDD_OK;
+  }
   p.G_zero = false;
   p.opart_tiles = flush_tiles(p, n_rows);
   return WDD_OK;
 }
 
+// Spectrum-only plans keep no G: form it on request from the coefficient store, which holds every
+// position ingested since the reset (never cleared, each position ingested at most once) -- row
+// DFT of every ingested position into R (scratch here: flush() has emptied it), then one rank
+// update into G with overwrite.
+wdd_status form_G(Plan& p) {
+  std::vector<int32_t> rows;
+  for (int sy = 0; sy < p.Sy; ++sy)
+    for (int w = 0; w < p.mask_words; ++w)
+      if (p.ingested[(size_t)sy * p.mask_words + w]) {
+        rows.push_back(sy);
+        break;
+      }
+  if (rows.empty()) {
+    CUDA_TRY(cudaMemsetAsync(p.d_G, 0, (size_t)p.n_act * p.K * sizeof(float2), p.stream));
+    return WDD_OK;
+  }
+  const int n_rows = (int)rows.size();
+  std::vector<int32_t> blob(rows);
+  const size_t mask_off = ((size_t)n_rows + 3) / 4 * 4;
+  blob.resize(mask_off + (size_t)n_rows * p.mask_words, 0);
+  for (int r = 0; r < n_rows; ++r)
+    for (int w = 0; w < p.mask_words; ++w)
+      blob[mask_off + (size_t)r * p.mask_words + w] = (int32_t)p.ingested[(size_t)rows[r] * p.mask_words + w];
+  void* d = nullptr;
+  wdd_status s = upload_meta(p, blob.data(), blob.size() * sizeof(int32_t), &d);
+  if (s != WDD_OK) return s;
+  const int32_t* dr = static_cast<const int32_t*>(d);
+  CUDA_TRY(launch_rowdft(p, dr, reinterpret_cast<const uint32_t*>(dr + mask_off), n_rows, p.stream));
+  CUDA_TRY(launch_flush(p, dr, n_rows, /*overwrite*/ true, p.stream, false));
+  return WDD_OK;
+}
+
 // Make the memory of G hold its logical value (after a reset nothing has been written yet).
 wdd_status materialize_G(Plan& p) {
+  if (p.o_only) return form_G(p);
   if (p.G_zero) {
     CUDA_TRY(cudaMemsetAsync(p.d_G, 0, (size_t)p.n_act * p.K * sizeof(float2), p.stream));
     p.G_zero = false;
@@ -436,7 +475,7 @@ void free_plan(Plan* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   cudaDeviceSynchronize();
   if (p->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(p->nccl));
-  void* bufs[] = {p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
+  void* bufs[] = {p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
                   p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec, p->d_img_tmp,
                   p->d_meta, p->d_stage[0], p->d_stage[1]};
   for (void* b : bufs)
@@ -487,12 +526,16 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
     return fail(WDD_E_ARG, "step, wavelength and semi-angle must be > 0");
   if (o.dtype != 0 && o.dtype != 1) return fail(WDD_E_ARG, "dtype must be 0 (u16) or 1 (f32)");
   if (o.combine != 0 && o.combine != 1) return fail(WDD_E_ARG, "combine must be 0 or 1");
+  if (o.accumulator != 0 && o.accumulator != 1) return fail(WDD_E_ARG, "accumulator must be 0 (G) or 1 (spectrum)");
+  if (o.accumulator == 1 && (Sy < 2 || Sy > 1024 || (Sy & (Sy - 1)) != 0))
+    return fail(WDD_E_ARG, "the spectrum-only accumulator needs a power-of-two Sy in [2, 1024] (got %d)", Sy);
 
   Plan* p = new Plan();
   p->Sy = Sy; p->Sx = Sx; p->Q = Q; p->L = L; p->K = K; p->S = (int64_t)Sy * Sx;
   p->dtype = o.dtype; p->normalize = o.normalize ? 1 : 0; p->device = o.device; p->combine = o.combine;
   p->step = step_A; p->lambda = probe->wavelength_A; p->alpha = probe->semiangle_rad; p->defocus = probe->defocus_A;
   p->eps = wiener_eps;
+  p->o_only = o.accumulator == 1;
   p->dq = o.det_px_rad > 0 ? o.det_px_rad / p->lambda : 1.0 / (Q * step_A);  // R17
   p->qa = p->alpha / p->lambda;                                               // R7
   p->R = p->qa / p->dq;
@@ -588,6 +631,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   p->seen.assign((size_t)(p->S + 63) / 64, 0);
   p->row_dirty.assign(Sy, 0);
   p->row_staged.assign(Sy, 0);
+  p->ingested.assign(p->o_only ? (size_t)Sy * p->mask_words : 0, 0u);
   p->pending.assign((size_t)Sy * p->mask_words, 0);
 
 #define ALLOC(ptr, bytes)                                                                           \
@@ -613,6 +657,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   p->opart_cap = std::max(1, std::max(colfft_tiles(*p), flush_tiles(*p, 1 << 20)));
   ALLOC(p->d_opart, (size_t)p->opart_cap * act.size() * sizeof(float2));
   ALLOC(p->d_gidx, (size_t)p->S * sizeof(int32_t));
+  ALLOC(p->d_oacc, act.size() * sizeof(float2));
   ALLOC(p->d_iota, (size_t)Sy * sizeof(int32_t));
   ALLOC(p->d_ones, (size_t)Sy * p->mask_words * sizeof(uint32_t));
   ALLOC(p->d_spec, (size_t)p->S * sizeof(float2));
@@ -636,7 +681,8 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
             up(p->d_col_off, p->col_off.data(), p->col_off.size() * 4) && up(p->d_vpos, vpos.data(), act.size() * 4) &&
             up(p->d_gidx, gidx.data(), gidx.size() * 4) && up(p->d_iota, iota.data(), iota.size() * 4) &&
             up(p->d_flush_tiles, p->flush_tiles.data(), p->flush_tiles.size() * sizeof(int2));
-  ok = ok && cudaMemset(p->d_ones, 0xFF, (size_t)Sy * p->mask_words * sizeof(uint32_t)) == cudaSuccess &&
+  ok = ok && cudaMemset(p->d_oacc, 0, act.size() * sizeof(float2)) == cudaSuccess &&
+       cudaMemset(p->d_ones, 0xFF, (size_t)Sy * p->mask_words * sizeof(uint32_t)) == cudaSuccess &&
        cudaMemset(p->d_G, 0, W.size() * sizeof(float2)) == cudaSuccess &&
        cudaMemset(p->d_Call, 0, (size_t)p->S * K * sizeof(float)) == cudaSuccess &&
        cudaMemset(p->d_spec, 0, (size_t)p->S * sizeof(float2)) == cudaSuccess;
@@ -720,7 +766,16 @@ wdd_status wdd_readout(wdd_plan_t plan, void* complex_out_dev) {
   if (s != WDD_OK) return s;
   const float2* op = p.d_opart;
   int tiles = p.opart_tiles;
-  if (p.nranks > 1) {
+  if (p.o_only) {
+    op = p.d_oacc;
+    tiles = 1;
+    if (p.nranks > 1) {   // sum the ranks' running spectra (a copy: the running sum stays per rank)
+      CUDA_TRY(cudaMemcpyAsync(p.d_o, p.d_oacc, (size_t)p.n_act * sizeof(float2), cudaMemcpyDeviceToDevice, p.stream));
+      NCCL_TRY(ncclAllReduce(p.d_o, p.d_o, (size_t)p.n_act * 2, ncclFloat, ncclSum, reinterpret_cast<ncclComm_t>(p.nccl),
+                             p.stream));
+      op = p.d_o;
+    }
+  } else if (p.nranks > 1) {
     // multi-rank: every rank reduces its partial accumulator the same way, then NCCL sums
     if ((s = materialize_G(p)) != WDD_OK) return s;
     const float2* G = p.d_G;
@@ -789,6 +844,8 @@ wdd_status wdd_reset(wdd_plan_t plan) {
   Plan& p = *P(plan);
   CUDA_TRY(cudaSetDevice(p.device));
   p.G_zero = true;          // the next flush writes G instead of accumulating (no clearing pass)
+  if (p.o_only) CUDA_TRY(cudaMemsetAsync(p.d_oacc, 0, (size_t)p.n_act * sizeof(float2), p.stream));
+  std::fill(p.ingested.begin(), p.ingested.end(), 0u);
   p.opart_tiles = 0;
   // coefficients of frames ingested but never flushed are simply forgotten: only pending
   // positions are ever read from the coefficient store

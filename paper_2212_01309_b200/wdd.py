@@ -33,7 +33,7 @@ class _Probe(ctypes.Structure):
 class _Opts(ctypes.Structure):
     _fields_ = [("det_px_rad", ctypes.c_double), ("sigma_px", ctypes.c_double),
                 ("dtype", ctypes.c_int32), ("normalize", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("combine", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+                ("combine", ctypes.c_int32), ("accumulator", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class _Info(ctypes.Structure):
@@ -132,7 +132,7 @@ class Plan:
     def __init__(self, scan_shape, step_A: float, det_shape, K: int, wavelength_A: float,
                  semiangle_rad: float, defocus_A: float = 0.0, wiener_eps: float = 1e-3, *,
                  dtype: str = "u16", normalize: bool = False, device: int = 0, sigma_px: float = 0.0,
-                 det_px_rad: float = 0.0, combine: int = 0):
+                 det_px_rad: float = 0.0, combine: int = 0, accumulator: str = "G"):
         lib = load_library()
         scan = (ctypes.c_int32 * 2)(*[int(v) for v in scan_shape])
         det = (ctypes.c_int32 * 2)(*[int(v) for v in det_shape])
@@ -144,6 +144,7 @@ class Plan:
         opts.normalize = int(bool(normalize))
         opts.device = int(device)
         opts.combine = int(combine)
+        opts.accumulator = {"G": 0, "spectrum": 1}[accumulator]
         h = ctypes.c_void_p()
         _check(lib.wdd_plan_create(scan, float(step_A), det, int(K), ctypes.byref(probe), float(wiener_eps),
                                    ctypes.byref(opts), ctypes.byref(h)))

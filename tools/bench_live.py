@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--pool-frames", type=int, default=8192)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--accumulator", default="G", choices=["G", "spectrum"])
     args = ap.parse_args()
     import torch
     import paper_2212_01309_b200 as wdd
@@ -39,13 +40,16 @@ def main():
     pool = torch.cat([dense_frames_torch(pix[a:a + 4096], cnt[a:a + 4096], cfg.Q, "cuda")
                       for a in range(0, pool_n, 4096)])
     frame_bytes = cfg.Q * cfg.Q * 2
-    plan = wdd.Plan.from_config(cfg)
+    plan = wdd.Plan.from_config(cfg, accumulator=args.accumulator)
     info = plan.info()
     st = torch.cuda.Stream()
     torch.cuda.set_stream(st)
     out = torch.empty((cfg.Sy, cfg.Sx), dtype=torch.complex64, device="cuda")
     rows_per_readout = cfg.readout_rows or cfg.Sy
     n_batches = (cfg.S + batch - 1) // batch
+
+    import time
+    host_us = []
 
     def scan(record):
         plan.reset()
@@ -60,7 +64,10 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            plan.ingest(frames, np.arange(a0, a1, dtype=np.int32), st)
+            idx_b = np.arange(a0, a1, dtype=np.int32)
+            h0 = time.perf_counter()
+            plan.ingest(frames, idx_b, st)
+            host_us.append((time.perf_counter() - h0) * 1e6)
             e1.record(st)
             lat.append((e0, e1))
             rows = a1 // cfg.Sx
@@ -88,16 +95,19 @@ def main():
     n_readouts = len(res[0][2])
     # algorithmic bytes of a whole scan: frames + C write/read + R write/read + per flush the G
     # read-modify-write (write only on the first flush) and the bank read of the fused readout
+    # (spectrum-only accumulator: no G traffic, only the bank read per flush)
+    g_passes = (3 * n_readouts - 1) if args.accumulator == "G" else n_readouts
     b_scan = cfg.S * (frame_bytes + 8 * cfg.K + 16 * info["n_vx"] * cfg.K / cfg.Sx) + \
-        info["n_act"] * cfg.K * 8 * (3 * n_readouts - 1)
+        info["n_act"] * cfg.K * 8 * g_passes
     line = {
-        "config": cfg.name, "scan": [cfg.Sy, cfg.Sx], "detector": [cfg.Q, cfg.Q], "K": cfg.K, "batch": batch,
+        "config": cfg.name, "accumulator": args.accumulator, "scan": [cfg.Sy, cfg.Sx], "detector": [cfg.Q, cfg.Q], "K": cfg.K, "batch": batch,
         "readouts_per_scan": n_readouts, "scan_ms": total_ms, "frames_per_s": fps,
         "step_roofline_frames_per_s": peaks["hbm_gbs"] * 1e9 / (b_scan / cfg.S),
         "frac": fps / (peaks["hbm_gbs"] * 1e9 / (b_scan / cfg.S)),
         "ingest_latency_us": {"p50": float(np.percentile(lat, 50)), "p99": float(np.percentile(lat, 99)),
                               "max": float(lat.max()), "n": int(len(lat))},
         "readout_latency_us": {"p50": float(np.percentile(rdl, 50)), "max": float(rdl.max()), "n": int(len(rdl))},
+        "host_us_per_ingest_call": {"p50": float(np.percentile(host_us, 50)), "max": float(np.max(host_us))},
         "pool_frames": pool_n, "pool_bytes": pool_n * frame_bytes,
         "timing": "CUDA events on the ingest stream, eager calls, median of %d scans" % args.reps,
     }
