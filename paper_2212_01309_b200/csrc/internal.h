@@ -133,5 +133,12 @@ cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* 
 void pack_basis_fp16(const Plan& p, std::vector<uint16_t>& out, double& scale);
 size_t project_smem_bytes(int Q, int L);
 bool project_is_lean(const Plan& p);   // projection runs two CTAs per SM for this plan
+// plan-time Wiener bank (Algorithm 1) on the GPU in float64 (bank.cu): q_host = detector grid
+// (Q), apx_host = aperture pixel interval of each detector row (x > y: empty), [ax_lo,
+// ax_lo + n_axc) the aperture's column range; writes n_act x K complex64 (or complex128 if f64)
+// in accumulator order to W_dev; needs the plan's column tables on the device; synchronous
+cudaError_t build_bank(const Plan& p, const double* q_host, const int2* apx_host, int ax_lo, int n_axc, void* W_dev,
+                       bool f64);
+constexpr double kPi = 3.14159265358979323846;
 
 }  // namespace wdd

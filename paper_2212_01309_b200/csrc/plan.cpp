@@ -52,7 +52,6 @@ wdd_status fail(wdd_status s, const char* fmt, ...) {
     if (r_ != ncclSuccess) return fail(WDD_E_NCCL, "%s: %s", #expr, ncclGetErrorString(r_)); \
   } while (0)
 
-constexpr double kPi = 3.14159265358979323846;
 
 // ------------------------------------------------------------------ plan math (float64)
 // Normalised Hermite functions by the three-term recurrence (R3).
@@ -141,60 +140,29 @@ void active_set(const Plan& p, const std::vector<double>& q, const ApertureRows&
     if (on[i]) act.push_back(cand[i].first * p.Sx + cand[i].second);
 }
 
-// Wiener bank K_v = conj(H(Y_v)) / (|H(Y_v)|^2 + eps) (Algorithm 1), Y_v evaluated
-// on the lens of the two apertures only (Y_v is 0 elsewhere).  Output in accumulator order.
-template <typename OutT>
-void wiener_bank(const Plan& p, const std::vector<double>& q, const ApertureRows& ap, OutT* W) {
-  const int L = p.L, K = p.K;
-  const double qa2 = p.qa * p.qa, c0 = -kPi * p.lambda * p.defocus;
-  const unsigned nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
-  std::atomic<int64_t> next(0);
-  auto work = [&]() {
-    std::vector<std::complex<double>> H((size_t)K), T((size_t)L);
-    for (;;) {
-      const int64_t g0 = next.fetch_add(16);
-      if (g0 >= p.n_act) break;
-      for (int64_t g = g0; g < std::min<int64_t>(p.n_act, g0 + 16); ++g) {
-        const int v = p.active_v[g];
-        const int vy = v / p.Sx, vx = v % p.Sx;
-        const double sy = (double)signed_freq(vy, p.Sy) / ((double)p.Sy * p.step);
-        const double sx = (double)signed_freq(vx, p.Sx) / ((double)p.Sx * p.step);
-        std::fill(H.begin(), H.end(), 0.0);
-        for (int my = 0; my < p.Q; ++my) {
-          const double a = q[my] + sy;
-          bool any = false;
-          std::fill(T.begin(), T.end(), 0.0);
-          for (int e = ap.row_begin[my]; e < ap.row_begin[my + 1]; ++e) {
-            const int mx = ap.mx[e];
-            const double b = q[mx] + sx;
-            const double s2 = a * a + b * b;
-            if (!(s2 <= qa2)) continue;
-            any = true;
-            const double u2 = q[my] * q[my] + q[mx] * q[mx];
-            // p_hat(q) * conj(p_hat(q + q_hat)), p_hat = exp(-i pi lambda df |q|^2) inside
-            const std::complex<double> y = std::complex<double>(std::cos(c0 * u2), std::sin(c0 * u2)) *
-                                           std::complex<double>(std::cos(c0 * s2), -std::sin(c0 * s2));
-            const double* px = &p.basis[(size_t)mx * L];
-            for (int aa = 0; aa < L; ++aa) T[aa] += px[aa] * y;
-          }
-          if (!any) continue;
-          const double* py = &p.basis[(size_t)my * L];
-          for (int aa = 0; aa < L; ++aa)
-            for (int bb = 0; bb < L; ++bb) H[(size_t)aa * L + bb] += py[bb] * T[aa];
-        }
-        for (int k = 0; k < K; ++k) {
-          const std::complex<double> w = std::conj(H[k]) / (std::norm(H[k]) + p.eps);
-          W[g * K + k] = OutT{(decltype(OutT{}.x))w.real(), (decltype(OutT{}.x))w.imag()};
-        }
-      }
-    }
-  };
-  std::vector<std::thread> th;
-  for (unsigned t = 0; t < nt; ++t) th.emplace_back(work);
-  for (auto& t : th) t.join();
+// Aperture pixel interval of every detector row (the disc's rows are contiguous) and the
+// aperture's column range, the tables the GPU bank build (bank.cu) works from.
+struct ApertureIntervals {
+  std::vector<int2> rows;
+  int ax_lo = 0, n_axc = 0;
+};
+
+bool aperture_intervals(const Plan& p, const ApertureRows& ap, ApertureIntervals& out) {
+  out.rows.assign(p.Q, make_int2(1, 0));
+  int lo = p.Q, hi = -1;
+  for (int my = 0; my < p.Q; ++my) {
+    const int b = ap.row_begin[my], e = ap.row_begin[my + 1];
+    if (b == e) continue;
+    if (ap.mx[e - 1] - ap.mx[b] != e - 1 - b) return false;
+    out.rows[my] = make_int2(ap.mx[b], ap.mx[e - 1]);
+    lo = std::min(lo, ap.mx[b]);
+    hi = std::max(hi, ap.mx[e - 1]);
+  }
+  out.ax_lo = hi >= lo ? lo : 0;
+  out.n_axc = hi >= lo ? hi - lo + 1 : 0;
+  return true;
 }
 
-struct d2 { double x, y; };
 
 void twiddles(int n_out, const int32_t* freqs, int S, std::vector<float2>& F) {
   // F[j][s] = exp(-2 pi i ((f_j * s) mod S) / S) / sqrt(S)  (integer angle reduction)
@@ -596,9 +564,10 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   fft_twiddles(Sx, twx);
   fft_twiddles(Sy, twy);
 
-  // bank
-  std::vector<float2> W((size_t)p->n_act * K);
-  wiener_bank<float2>(*p, q, ap, W.data());
+  // bank: built on the device once the column tables are there (below)
+  ApertureIntervals apiv;
+  if (!aperture_intervals(*p, ap, apiv)) return bail(fail(WDD_E_ARG, "aperture rows are not pixel intervals"));
+  const size_t nW = (size_t)p->n_act * K;
 
   // device buffers
   std::vector<uint16_t> bpack;
@@ -644,9 +613,9 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ALLOC(p->d_twx, twx.size() * sizeof(float2));
   ALLOC(p->d_twy, twy.size() * sizeof(float2));
   ALLOC(p->d_col_vx, p->col_vx.size() * sizeof(int32_t));
-  ALLOC(p->d_W, W.size() * sizeof(float2));
-  ALLOC(p->d_G, W.size() * sizeof(float2));
-  if (p->combine == 1) ALLOC(p->d_Gsum, W.size() * sizeof(float2));
+  ALLOC(p->d_W, nW * sizeof(float2));
+  ALLOC(p->d_G, nW * sizeof(float2));
+  if (p->combine == 1) ALLOC(p->d_Gsum, nW * sizeof(float2));
   ALLOC(p->d_R, (size_t)p->n_vx * Sy * K * sizeof(float2));
   ALLOC(p->d_Call, (size_t)p->S * K * sizeof(float));
   ALLOC(p->d_act_vy, act.size() * 4);
@@ -677,16 +646,20 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
             up(p->d_Fx, Fx.data(), Fx.size() * sizeof(float2)) && up(p->d_Fy, Fy.data(), Fy.size() * sizeof(float2)) &&
             up(p->d_twx, twx.data(), twx.size() * sizeof(float2)) && up(p->d_twy, twy.data(), twy.size() * sizeof(float2)) &&
             up(p->d_col_vx, p->col_vx.data(), p->col_vx.size() * sizeof(int32_t)) &&
-            up(p->d_W, W.data(), W.size() * sizeof(float2)) && up(p->d_act_vy, p->act_vy.data(), act.size() * 4) &&
+            up(p->d_act_vy, p->act_vy.data(), act.size() * 4) &&
             up(p->d_col_off, p->col_off.data(), p->col_off.size() * 4) && up(p->d_vpos, vpos.data(), act.size() * 4) &&
             up(p->d_gidx, gidx.data(), gidx.size() * 4) && up(p->d_iota, iota.data(), iota.size() * 4) &&
             up(p->d_flush_tiles, p->flush_tiles.data(), p->flush_tiles.size() * sizeof(int2));
   ok = ok && cudaMemset(p->d_oacc, 0, act.size() * sizeof(float2)) == cudaSuccess &&
        cudaMemset(p->d_ones, 0xFF, (size_t)Sy * p->mask_words * sizeof(uint32_t)) == cudaSuccess &&
-       cudaMemset(p->d_G, 0, W.size() * sizeof(float2)) == cudaSuccess &&
+       cudaMemset(p->d_G, 0, nW * sizeof(float2)) == cudaSuccess &&
        cudaMemset(p->d_Call, 0, (size_t)p->S * K * sizeof(float)) == cudaSuccess &&
        cudaMemset(p->d_spec, 0, (size_t)p->S * sizeof(float2)) == cudaSuccess;
   if (!ok) return bail(fail(WDD_E_CUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError())));
+  {
+    const cudaError_t e = build_bank(*p, q.data(), apiv.rows.data(), apiv.ax_lo, apiv.n_axc, p->d_W, false);
+    if (e != cudaSuccess) return bail(fail(WDD_E_CUDA, "bank build: %s", cudaGetErrorString(e)));
+  }
   if (cufftPlan2d(&p->fft, Sy, Sx, CUFFT_C2C) != CUFFT_SUCCESS) return bail(fail(WDD_E_CUDA, "cufftPlan2d failed"));
   p->fft_ok = true;
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(WDD_E_CUDA, "plan upload sync failed"));
@@ -906,11 +879,19 @@ wdd_status wdd_get_tables(wdd_plan_t plan, double* basis, double* bank, int32_t*
   const Plan& p = *P(plan);
   if (basis) std::memcpy(basis, p.basis.data(), p.basis.size() * sizeof(double));
   if (active_v) std::memcpy(active_v, p.active_v.data(), p.active_v.size() * 4);
-  if (bank) {
+  if (bank) {   // the same device build as the plan's bank, in complex128
     std::vector<double> q(p.Q);
     for (int m = 0; m < p.Q; ++m) q[m] = (double)(m - p.Q / 2) * p.dq;
-    ApertureRows ap = aperture(p, q);
-    wiener_bank<d2>(p, q, ap, reinterpret_cast<d2*>(bank));
+    ApertureIntervals apiv;
+    if (!aperture_intervals(p, aperture(p, q), apiv)) return fail(WDD_E_ARG, "aperture rows are not pixel intervals");
+    CUDA_TRY(cudaSetDevice(p.device));
+    void* d = nullptr;
+    const size_t bytes = (size_t)p.n_act * p.K * 2 * sizeof(double);
+    CUDA_TRY(cudaMalloc(&d, bytes));
+    cudaError_t e = build_bank(p, q.data(), apiv.rows.data(), apiv.ax_lo, apiv.n_axc, d, true);
+    if (e == cudaSuccess) e = cudaMemcpy(bank, d, bytes, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(WDD_E_CUDA, "bank build: %s", cudaGetErrorString(e));
   }
   return WDD_OK;
 }

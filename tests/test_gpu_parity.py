@@ -61,8 +61,9 @@ def test_plan_tables(wdd, torch_cuda, name):
     assert info["n_vx"] == len(np.unique(oact % cfg.Sx))
 
 
-@pytest.mark.parametrize("name", ["tiny", "medium"])
+@pytest.mark.parametrize("name", ["tiny", "medium", "large"])
 def test_bank_matches_oracle(wdd, torch_cuda, name):
+    # the plan's bank is built on the GPU in float64 (bank.cu); tables() runs the same kernel
     cfg = CONFIGS[name]
     plan = wdd.Plan.from_config(cfg)
     g = O.geometry(cfg)
