@@ -1596,7 +1596,9 @@ cudaError_t launch_oacc(const Plan& p, int tiles, cudaStream_t st) {
 __global__ void scatter_kernel(const float2* __restrict__ op, int tiles, const int32_t* __restrict__ vpos,
                                int64_t n_act, float2* __restrict__ spec) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < n_act) spec[vpos[g]] = sum_tiles(op, tiles, n_act, g);
+  pdl_trigger();
+  pdl_wait();   // partial readouts of the preceding flush / readout kernel
+  if (g < n_act) spec[__ldg(vpos + g)] = sum_tiles(op, tiles, n_act, g);
 }
 
 // =====================================================================================
@@ -1632,8 +1634,7 @@ __global__ void conj_scale_kernel(float2* __restrict__ out, int64_t S, double in
 // as two passes of the shared-memory FFT: rows (A[vy][x] = sum_vx conj o[vy][vx] W_Sx^{vx x})
 // into a scratch image, then columns with the unitary scale and the optional 1/sqrt(o_0).
 template <int LOGN>
-__global__ void __launch_bounds__(256) img_rows_kernel(const float2* __restrict__ op, int tiles, int64_t n_act,
-                                                       const int32_t* __restrict__ gidx, const float2* __restrict__ tw,
+__global__ void __launch_bounds__(256) img_rows_kernel(const float2* __restrict__ spec, const float2* __restrict__ tw,
                                                        float2* __restrict__ A, int logc) {
   constexpr int N = 1 << LOGN;
   extern __shared__ __align__(16) float2 fsm[];
@@ -1642,11 +1643,10 @@ __global__ void __launch_bounds__(256) img_rows_kernel(const float2* __restrict_
   const int vy0 = blockIdx.x << logc;
   pdl_trigger();
   for (int i = threadIdx.x; i < N; i += blockDim.x) stw[i] = __ldg(tw + i);
-  pdl_wait();   // partial readouts of the preceding flush / readout kernel
+  pdl_wait();   // the spectrum of the preceding scatter kernel
   for (int e = threadIdx.x; e < (N << logc); e += blockDim.x) {
     const int c = e >> LOGN, vx = e & (N - 1);
-    const int g = __ldg(gidx + (int64_t)(vy0 + c) * N + vx);
-    const float2 v = g >= 0 ? sum_tiles(op, tiles, n_act, g) : make_float2(0.f, 0.f);
+    const float2 v = __ldg(spec + (int64_t)(vy0 + c) * N + vx);
     x[(vx << logc) + c] = make_float2(v.x, -v.y);
   }
   __syncthreads();
@@ -1671,8 +1671,7 @@ __device__ __forceinline__ float2 inv_principal_sqrt(float2 o0) {
 template <int LOGN>
 __global__ void __launch_bounds__(256) img_cols_kernel(const float2* __restrict__ A, const float2* __restrict__ tw,
                                                        float2* __restrict__ out, int Sx, int logc, float scale,
-                                                       const float2* __restrict__ op, int tiles, int64_t n_act,
-                                                       int64_t g_dc, int normalize) {
+                                                       const float2* __restrict__ spec, int normalize) {
   constexpr int N = 1 << LOGN;     // Sy
   extern __shared__ __align__(16) float2 fsm[];
   const int cnt = 1 << logc;
@@ -1690,7 +1689,7 @@ __global__ void __launch_bounds__(256) img_cols_kernel(const float2* __restrict_
   fft::fft_seq<LOGN>(x, stw, logc);
   float2 f = make_float2(scale, 0.f);
   if (normalize) {
-    const float2 w = inv_principal_sqrt(sum_tiles(op, tiles, n_act, g_dc));
+    const float2 w = inv_principal_sqrt(__ldg(spec));   // o_0 (v = 0 is image position 0)
     f = make_float2(w.x * scale, w.y * scale);
   }
   for (int e = threadIdx.x; e < (N << logc); e += blockDim.x) {
@@ -1703,11 +1702,9 @@ __global__ void __launch_bounds__(256) img_cols_kernel(const float2* __restrict_
 // for the row pass and CB = Sx/CS columns for the column pass; the transposition between the two
 // passes goes through distributed shared memory (no global round trip, one launch).
 template <int LX, int LY, int CS>
-__global__ void __launch_bounds__(256) img_fused_kernel(const float2* __restrict__ op, int tiles, int64_t n_act,
-                                                        const int32_t* __restrict__ gidx,
+__global__ void __launch_bounds__(256) img_fused_kernel(const float2* __restrict__ spec,
                                                         const float2* __restrict__ twx, const float2* __restrict__ twy,
-                                                        float2* __restrict__ out, float scale, int64_t g_dc,
-                                                        int normalize) {
+                                                        float2* __restrict__ out, float scale, int normalize) {
   constexpr int SX = 1 << LX, SY = 1 << LY, RB = SY / CS, CB = SX / CS;
   constexpr int LRB = LY - (CS == 16 ? 4 : CS == 8 ? 3 : CS == 4 ? 2 : CS == 2 ? 1 : 0);
   constexpr int LCB = LX - (CS == 16 ? 4 : CS == 8 ? 3 : CS == 4 ? 2 : CS == 2 ? 1 : 0);
@@ -1721,12 +1718,11 @@ __global__ void __launch_bounds__(256) img_fused_kernel(const float2* __restrict
   pdl_trigger();
   for (int i = threadIdx.x; i < SX; i += blockDim.x) stx[i] = __ldg(twx + i);
   for (int i = threadIdx.x; i < SY; i += blockDim.x) sty[i] = __ldg(twy + i);
-  pdl_wait();   // partial readouts of the preceding flush / readout kernel
+  pdl_wait();   // the spectrum of the preceding scatter kernel
   const int vy0 = r * RB;
   for (int e = threadIdx.x; e < SX * RB; e += blockDim.x) {
     const int c = e >> LX, vx = e & (SX - 1);
-    const int g = __ldg(gidx + (int64_t)(vy0 + c) * SX + vx);
-    const float2 v = g >= 0 ? sum_tiles(op, tiles, n_act, g) : make_float2(0.f, 0.f);
+    const float2 v = __ldg(spec + (int64_t)(vy0 + c) * SX + vx);
     xr[(vx << LRB) + c] = make_float2(v.x, -v.y);    // conj(o): O = DFT2(conj o) / sqrt(S)
   }
   __syncthreads();
@@ -1742,7 +1738,7 @@ __global__ void __launch_bounds__(256) img_fused_kernel(const float2* __restrict
   fft::fft_seq<LY>(xc, sty, LCB);
   float2 f = make_float2(scale, 0.f);
   if (normalize) {
-    const float2 w = inv_principal_sqrt(sum_tiles(op, tiles, n_act, g_dc));
+    const float2 w = inv_principal_sqrt(__ldg(spec));
     f = make_float2(w.x * scale, w.y * scale);
   }
   for (int e = threadIdx.x; e < SY * CB; e += blockDim.x) {
@@ -1752,7 +1748,7 @@ __global__ void __launch_bounds__(256) img_fused_kernel(const float2* __restrict
 }
 
 template <int LX, int LY>
-static cudaError_t launch_img_fused(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st) {
+static cudaError_t launch_img_fused(const Plan& p, float2* out, cudaStream_t st) {
   constexpr int CS = (LX >= 4 && LY >= 4) ? 16 : 1 << (LX < LY ? LX : LY);
   constexpr int SX = 1 << LX, SY = 1 << LY;
   constexpr size_t smem = (size_t)(SX * (SY / CS) + SY * (SX / CS) + SX + SY) * 8;
@@ -1779,17 +1775,16 @@ static cudaError_t launch_img_fused(const Plan& p, const float2* op, int tiles, 
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, img_fused_kernel<LX, LY, CS>, op, tiles, (int64_t)p.n_act,
-                            (const int32_t*)p.d_gidx, (const float2*)p.d_twx, (const float2*)p.d_twy, out,
-                            (float)(1.0 / std::sqrt((double)p.S)), (int64_t)p.g_dc, p.normalize);
+  return cudaLaunchKernelEx(&cfg, img_fused_kernel<LX, LY, CS>, (const float2*)p.d_spec, (const float2*)p.d_twx,
+                            (const float2*)p.d_twy, out, (float)(1.0 / std::sqrt((double)p.S)), p.normalize);
 }
 
-static cudaError_t launch_img_fused_dispatch(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st) {
+static cudaError_t launch_img_fused_dispatch(const Plan& p, float2* out, cudaStream_t st) {
   return with_log(ilog2(p.Sx), [&](auto LNX) {
     constexpr int LX = decltype(LNX)::value;
     return with_log(ilog2(p.Sy), [&](auto LNY) -> cudaError_t {
       constexpr int LY = decltype(LNY)::value;
-      if constexpr (LX <= 8 && LY <= 8) return launch_img_fused<LX, LY>(p, op, tiles, out, st);
+      if constexpr (LX <= 8 && LY <= 8) return launch_img_fused<LX, LY>(p, out, st);
       else return cudaErrorInvalidValue;
     });
   });
@@ -1800,31 +1795,48 @@ bool finalize_uses_fft(const Plan& p) {
          p.Sy <= (1 << kFftMaxLog);
 }
 
+// The partial readouts are first summed (fixed order) and scattered to image order (one coalesced
+// pass over the tiles; inactive positions of d_spec stay zero from plan creation), then the 2-D
+// transform reads whole spectrum rows.  Images up to 128 x 128 take the one-launch cluster
+// kernel; larger power-of-two images the row and column passes (>= 128 CTAs each); other sizes
+// (or WDD_IMG=cufft) cuFFT.
 cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st) {
   const int64_t S = p.S;
-  static const int no_fused = [] { const char* e = std::getenv("WDD_IMG_UNFUSED"); return e ? std::atoi(e) : 0; }();
-  if (finalize_uses_fft(p) && p.Sx <= 256 && p.Sy <= 256 && !no_fused) return launch_img_fused_dispatch(p, op, tiles, out, st);
-  if (finalize_uses_fft(p)) {
-    // rows: 2^lr rows per CTA (<= 32 KB of shared memory, at least 16 CTAs when the image allows)
+  static const int img_mode = [] {
+    const char* e = std::getenv("WDD_IMG");
+    return !e ? 0 : std::strcmp(e, "cufft") == 0 ? 1 : std::strcmp(e, "unfused") == 0 ? 2 : std::strcmp(e, "fused") == 0 ? 3 : 0;
+  }();
+  {
+    cudaError_t e = launch_pdl(scatter_kernel, dim3((unsigned)((p.n_act + 255) / 256)), dim3(256), 0, st, true, op,
+                               tiles, (const int32_t*)p.d_vpos, (int64_t)p.n_act, p.d_spec);
+    if (e != cudaSuccess) return e;
+  }
+  const bool own = finalize_uses_fft(p) && img_mode != 1;
+  const int fused_max = img_mode == 3 ? 256 : img_mode == 2 ? 0 : 128;
+  if (own && p.Sx <= fused_max && p.Sy <= fused_max) return launch_img_fused_dispatch(p, out, st);
+  if (own) {
     const int lx = ilog2(p.Sx), ly = ilog2(p.Sy);
-    int lr = std::max(0, std::min(ilog2(std::max(1, 4096 / p.Sx)), ly - 4));
+    // 2^lr rows per CTA: enough sequences for the threads of the FFT passes, >= 128 CTAs if possible
+    const int lr = std::max(0, std::min(ilog2(std::max(1, 4096 / p.Sx)), ly - 7));
     cudaError_t e = with_log(lx, [&](auto LN) {
       constexpr int L = decltype(LN)::value;
       const size_t smem = ((size_t)p.Sx << lr) * 8 + (size_t)p.Sx * 8 + 16;
-      return launch_pdl(img_rows_kernel<L>, dim3(p.Sy >> lr), dim3(256), smem, st, true, op, tiles, (int64_t)p.n_act,
-                        (const int32_t*)p.d_gidx, (const float2*)p.d_twx, p.d_img_tmp, lr);
+      // threads: the larger FFT pass has N1 << lr independent register DFTs
+      const int nt = std::max(32, std::min(256, fft::Split<L>::N1 << lr));
+      return launch_pdl(img_rows_kernel<L>, dim3(p.Sy >> lr), dim3(nt), smem, st, true, (const float2*)p.d_spec,
+                        (const float2*)p.d_twx, p.d_img_tmp, lr);
     });
     if (e != cudaSuccess) return e;
-    int lc = std::max(0, std::min(ilog2(std::max(1, 4096 / p.Sy)), lx - 4));
+    const int lc = std::max(0, std::min(ilog2(std::max(1, 4096 / p.Sy)), lx - 7));
     return with_log(ly, [&](auto LN) {
       constexpr int L = decltype(LN)::value;
       const size_t smem = ((size_t)p.Sy << lc) * 8 + (size_t)p.Sy * 8 + 16;
-return launch_pdl(img_cols_kernel<L>, dim3(p.Sx >> lc), dim3(256), smem, st, true, (const float2*)p.d_img_tmp,
-                        (const float2*)p.d_twy, out, p.Sx, lc, (float)(1.0 / std::sqrt((double)S)), op, tiles,
-                        (int64_t)p.n_act, (int64_t)p.g_dc, p.normalize);
+      const int nt = std::max(32, std::min(256, fft::Split<L>::N1 << lc));
+      return launch_pdl(img_cols_kernel<L>, dim3(p.Sx >> lc), dim3(nt), smem, st, true, (const float2*)p.d_img_tmp,
+                        (const float2*)p.d_twy, out, p.Sx, lc, (float)(1.0 / std::sqrt((double)S)),
+                        (const float2*)p.d_spec, p.normalize);
     });
   }
-  scatter_kernel<<<(unsigned)((p.n_act + 255) / 256), 256, 0, st>>>(op, tiles, p.d_vpos, p.n_act, p.d_spec);
   if (cufftSetStream(p.fft, st) != CUFFT_SUCCESS) return cudaErrorUnknown;
   if (cufftExecC2C(p.fft, reinterpret_cast<cufftComplex*>(p.d_spec), reinterpret_cast<cufftComplex*>(out),
                    CUFFT_INVERSE) != CUFFT_SUCCESS)

@@ -180,13 +180,32 @@ class Plan:
         self.close()
 
     # ---- hot path
+    def _check_frames(self, frames, n: int, device: bool):
+        """Shape / dtype / contiguity of a frame batch against the plan (the C ABI takes a bare
+        pointer and trusts n)."""
+        shape = tuple(frames.shape)
+        if shape != (n, self.Q, self.Q):
+            raise ValueError(f"frames shape {shape} != ({n}, {self.Q}, {self.Q}) for {n} scan indices")
+        want = "uint16" if self.dtype == "u16" else "float32"
+        if want not in str(frames.dtype):
+            raise ValueError(f"frames dtype {frames.dtype}, plan expects {want}")
+        if hasattr(frames, "is_contiguous"):
+            if not frames.is_contiguous():
+                raise ValueError("frames must be contiguous")
+            if device != frames.is_cuda:
+                raise ValueError("frames must be on the " + ("device" if device else "host"))
+        elif isinstance(frames, np.ndarray) and not frames.flags["C_CONTIGUOUS"]:
+            raise ValueError("frames must be contiguous")
+
     def ingest(self, frames, scan_idx, stream=None):
         idx = _idx(scan_idx)
+        self._check_frames(frames, len(idx), True)
         _check(self._lib.wdd_ingest(self._h, _ptr(frames), idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                     len(idx), _stream(stream)))
 
     def ingest_host(self, frames, scan_idx, stream=None):
         idx = _idx(scan_idx)
+        self._check_frames(frames, len(idx), False)
         _check(self._lib.wdd_ingest_host(self._h, _ptr(frames), idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                          len(idx), _stream(stream)))
 
