@@ -70,6 +70,11 @@ struct Plan {
   float2* d_oacc = nullptr;           // n_act
   std::vector<uint32_t> ingested;     // spectrum-only plans: Sy x mask_words positions ingested since the reset
   float2* d_spec = nullptr;           // Sy*Sx
+  // pipelined GEMM flush (rgemm_kernel): (column j, first vy) of 128-row tiles, G / W tensor maps
+  std::vector<int2> rg_items;
+  int2* d_rg_items = nullptr;
+  alignas(64) unsigned char rg_tmap[6 * 128] = {};   // RgMaps (kernels.cu): W, G, R tensor maps
+  bool rg_ready = false;
   float2* d_img_tmp = nullptr;        // Sy*Sx scratch of the image transform (row pass)
   void* d_meta = nullptr;             // per-chunk row tables
   void* h_meta = nullptr;             // pinned host mirror of d_meta (2 slots)
@@ -116,13 +121,16 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
 // (overwrite: G is logically zero, write instead of accumulate).  The FFT form also writes the
 // per-k-tile partial Wiener readout d_opart[colfft_tiles][n_act].
 // o_only: spectrum-only plans -- no G update, the partial readouts are of this flush's increment
+// kind: flush_kind() result to use (-1: choose); row0 >= 0: the rows are row0 .. row0 + n_rows - 1
 cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st,
-                         bool o_only = false);
+                         bool o_only = false, int kind = -1, int row0 = -1);
 // o_acc += sum of `tiles` partial readouts (spectrum-only plans)
 cudaError_t launch_oacc(const Plan& p, int tiles, cudaStream_t st);
 bool flush_uses_fft(const Plan& p, int n_rows);
-int flush_kind(const Plan& p, int n_rows);    // 2 tensor-core GEMM, 1 FFT, 0 DFT matrix
-int flush_tiles(const Plan& p, int n_rows);   // partial-readout tiles a flush writes (0: none)
+int flush_kind(const Plan& p, int n_rows, bool allow_rg = true);   // 3 pipelined GEMM, 2 GEMM, 1 FFT, 0 DFT matrix
+int flush_tiles(const Plan& p, int n_rows, int kind = -1);   // partial-readout tiles a flush writes (0: none)
+bool rgemm_possible(const Plan& p, int n_rows);
+cudaError_t rgemm_prepare(Plan& p);   // tensor maps + item table of the pipelined GEMM flush
 int colfft_tiles(const Plan& p);
 bool finalize_uses_fft(const Plan& p);
 // o[g] = sum_k G[g][k] W[g][k] (one warp per active v)

@@ -818,6 +818,19 @@ using fft::cmul;
 constexpr int kU = 8;   // loads in flight per thread in the FFT kernels' staging loops
 constexpr int kFftMaxLog = 10;   // FFT path for scan axes up to 1024 (DFT-matrix kernels beyond)
 
+__device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+// x = hi + lo with hi = bf16(x), lo = bf16(x - hi), packed for two values
+__device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  const float2 hf = __bfloat1622float2(h);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = bf16x2_bits(a - hf.x, b - hf.y);
+}
+
+
 // a4 by FFT.  CTA = (k-tile of 2P coefficients, one pending scan row).  Two real coefficient
 // sequences k, k+1 share one complex FFT (z = C_k + i C_{k+1}); X_k[v] = (Z[v] + conj Z[-v]) / 2,
 // X_{k+1}[v] = (Z[v] - conj Z[-v]) / 2i.  Non-pending positions enter as zeros.
@@ -1213,18 +1226,6 @@ __global__ void __launch_bounds__(256) flush_kernel(const float2* __restrict__ R
 constexpr int kCgM = 128;                                  // active vy per tile (MMA M)
 constexpr uint32_t kCgLBOA = (kCgM / 8) * 128;             // A (K-major): bytes between K-adjacent core matrices
 
-__device__ __forceinline__ uint32_t bf16x2_bits(float a, float b) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<const uint32_t*>(&h);
-}
-// x = hi + lo with hi = bf16(x), lo = bf16(x - hi), packed for two values
-__device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  const float2 hf = __bfloat1622float2(h);
-  hi = *reinterpret_cast<const uint32_t*>(&h);
-  lo = bf16x2_bits(a - hf.x, b - hf.y);
-}
-
 // CTA = (column j, tile of 128 active vy, k-chunk): the A operand (the F tile of all staged rows,
 // <= kCgRows rows) is built once; the CTA then walks its k-chunk in NT-coefficient tiles with the
 // B tile of the next tile built (R -> bf16 hi / lo) while the MMAs of the current one run, and the
@@ -1418,6 +1419,423 @@ __global__ void __launch_bounds__(256, 1) colgemm_kernel(const float2* __restric
   if (warp == 0) tmem_dealloc<4 * kCgNT>(tbase);
 }
 
+// =====================================================================================
+// a5 + a6 on the tensor cores, memory-pipelined (flushes of <= 64 rows: the Live cadence).
+//   G[(j, vy)][k] (+)= sum_r F[vy][r] R[j][sy_r][k],  F[vy][r] = W_Sy^{vy sy_r} / sqrt(Sy)
+// (eq:outer_prod, restricted to the active vy of column j and the flush's rows r),
+// with the Wiener readout sum_k G K_v accumulated per vy row in the epilogue.
+// Persistent CTAs walk work items (column j, 128 active vy, k-chunk) in 32-coefficient MMA tiles.
+// Two shared-memory rings with different lifetimes:
+//   B ring (NB x 16 KB)   the R tile (flush rows x 32 complex, fp32, TMA SWIZZLE_128B boxes; one
+//                         bulk copy per row when the rows are not contiguous), converted in place to
+//                         bf16 hi / lo planes of B = [Rr | Ri] (N = 64, MN-major, K = flush row);
+//                         freed by the MMA commit;
+//   W/G ring (NW x 32 KB) per 16-coefficient half tile one SWIZZLE_128B box of W and one of G
+//                         (G only when read: not on the first flush after a reset, not for
+//                         spectrum-only plans; 16-row boxes for the tail tile of a column); freed
+//                         by the epilogue.
+// Roles:  warp 0 producer (TMA); warps 2-3 converters; warp 1 MMA issuer: D1 = Fr B, D2 = Fi B as
+// bf16 three-pass products (hi.hi + hi.lo + lo.hi, fp32 accumulation), A = F from TMEM (built once
+// per item), M = 128, N = 64, K = 16 per instruction; warps 4-7 and 8-11 two epilogue groups taking
+// alternate MMA tiles, thread = one vy row (TMEM lane): D_re = Fr Rr - Fi Ri, D_im = Fr Ri + Fi Rr,
+// G (+)= D stored, dot += G K_v; the dot of the whole k-chunk lands in opart[chunk][g].
+// =====================================================================================
+constexpr int kRgNT = 32;                                    // coefficients per MMA tile
+constexpr int kRgN = 2 * kRgNT;                              // MMA N: [Rr | Ri]
+constexpr int kRgRows = 64;                                  // flush rows the GEMM form takes (MMA K)
+constexpr int kRgPlaneB = (kRgN / 8) * (kRgRows / 8) * 128;  // 8 KB: element (n, r) at
+                                                             // (n/8)*1024 + (r/8)*128 + (r%8)*16 + (n%8)*2
+constexpr int kRgStB = 2 * kRgPlaneB;                        // 16 KB = the fp32 R tile (two 128-B halves x 64 rows)
+constexpr int kRgHalfR = kRgRows * 128;                      // 8 KB: one 16-coefficient half of the R tile
+constexpr int kRgM = 128;
+constexpr int kRgNB = 3;                                     // B ring depth (MMA tiles)
+constexpr int kRgBoxGW = kRgM * 128;                         // 16 KB: 128 rows x 16 complex
+constexpr int kRgStWG = 2 * kRgBoxGW;                        // 32 KB: W box + G box of one half tile
+constexpr int kRgNW = 5;                                     // W/G ring depth (half tiles)
+constexpr int kRgNAcc = 2;                                   // TMEM accumulator ring depth
+constexpr int kRgOffWG = kRgNB * kRgStB;
+constexpr int kRgBarOff = kRgOffWG + kRgNW * kRgStWG;
+constexpr int kRgNBars = 3 * kRgNB + 2 * kRgNW + 2 * kRgNAcc + 1;
+constexpr int kRgSmem = kRgBarOff + 8 * kRgNBars + 16 + 4 * kRgRows + 2 * kRgM * 8;
+constexpr int kRgThreads = 384;   // producer, MMA, 2 converter warps, 2 x 4 epilogue warps
+constexpr int kRgFCols = kRgRows / 2;                        // TMEM columns of one F plane (bf16 pairs)
+constexpr int kRgTmemF = 0;                                  // planes: Fr hi, Fr lo, Fi hi, Fi lo
+constexpr int kRgTmemAcc = 4 * kRgFCols;                     // 128: [acc][D1 | D2], 2 x 64 columns each
+constexpr int kRgTmemCols = 512;
+static_assert(kRgSmem <= 232448, "rgemm shared memory");
+static_assert(kRgTmemAcc + kRgNAcc * 2 * kRgN <= kRgTmemCols, "rgemm TMEM");
+
+struct RgArgs {
+  const float2* R;           // R[j][sy][k]
+  const int32_t* rows;       // flush row r -> scan row
+  int n_rows;
+  const float2* tw;          // Sy FFT twiddles
+  int Sy;
+  float inv_sqrt_sy;
+  const int32_t* col_off;
+  const int32_t* act_vy;
+  const int2* items;         // (column j, first vy i0)
+  int n_items;               // item tiles (j, i0); work items = n_items * n_kc
+  int n_kc;                  // k-chunks per item tile
+  float2* G;
+  float2* opart;
+  int64_t n_act;
+  int K;
+  int read_g, write_g;
+  int row0;                  // >= 0: the flush rows are row0 .. row0 + n_rows - 1 (TMA boxes of R)
+};
+
+// Tensor maps (TMA), all with 16-complex (128-byte) inner boxes and SWIZZLE_128B: W and G with
+// 16- and 128-row boxes (one 128-row box per full tile reads ~1.6x faster than eight 16-row
+// boxes: tools/tma_stride_probe.cu), R with 16- and 64-row boxes.
+struct RgMaps {
+  CUtensorMap w16, g16, w128, g128, r16, r64;
+};
+
+__global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __grid_constant__ RgMaps tm) {
+  extern __shared__ __align__(1024) uint8_t rg_smem[];
+  TRACE_DECL
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rg_smem + kRgBarOff);
+  uint64_t* r_full = bars;                    // [NB] R tile landed (TMA tx)
+  uint64_t* b_full = r_full + kRgNB;          // [NB] B planes written (2 converter warps)
+  uint64_t* b_empty = b_full + kRgNB;         // [NB] MMA commit
+  uint64_t* wg_full = b_empty + kRgNB;        // [NW] W / G half tile landed (TMA tx)
+  uint64_t* wg_empty = wg_full + kRgNW;       // [NW] the epilogue group's store issuer (after the TMA store read it)
+  uint64_t* acc_full = wg_empty + kRgNW;      // [NAcc]
+  uint64_t* acc_empty = acc_full + kRgNAcc;   // [NAcc] 4 epilogue warps
+  uint64_t* f_full = acc_empty + kRgNAcc;     // F of the current item in TMEM
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(f_full + 1);
+  int* srow = reinterpret_cast<int*>(tslot + 4);
+  float2* sdot = reinterpret_cast<float2*>(srow + kRgRows);   // [2][128] group-1 partial dots
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int KT = a.K / kRgNT, kt_per = KT / a.n_kc;          // MMA tiles per work item
+  const int kr = (a.n_rows + 15) & ~15;
+  const int64_t n_work = (int64_t)a.n_items * a.n_kc;
+  if (tid == 0) {
+    for (int i = 0; i < kRgNB; ++i) { mbar_init(&r_full[i], 1); mbar_init(&b_full[i], 2); mbar_init(&b_empty[i], 1); }
+    for (int i = 0; i < kRgNW; ++i) { mbar_init(&wg_full[i], 1); mbar_init(&wg_empty[i], 1); }
+    for (int i = 0; i < kRgNAcc; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
+    mbar_init(f_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<kRgTmemCols>(tslot);
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm.w16); prefetch_tmap(&tm.g16); prefetch_tmap(&tm.w128);
+    prefetch_tmap(&tm.g128); prefetch_tmap(&tm.r16); prefetch_tmap(&tm.r64);
+  }
+  pdl_trigger();
+  pdl_wait();   // R of the row FFT, G / opart of earlier kernels
+  if (tid < kRgRows) srow[tid] = tid < a.n_rows ? __ldg(a.rows + tid) : 0;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    // ---------------- producer: per MMA tile c the R tile (B ring), then its two W / G half tiles
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();             // W and G: each byte read once per flush
+      const int kr16 = (a.n_rows + 15) >> 4;
+      const uint32_t rbytes = 2 * (a.row0 >= 0 ? kr16 * 16 : a.n_rows) * 128;
+      uint32_t c = 0;
+      for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const int2 it = a.items[w / a.n_kc];
+        const int kc = (int)(w % a.n_kc);
+        const int g0 = __ldg(a.col_off + it.x), grow = g0 + it.y;
+        // W / G rows of this item only: the tail tile of a column must not pull in the next
+        // column's rows (16-row boxes there)
+        const int nb16 = (min(kRgM, __ldg(a.col_off + it.x + 1) - grow) + 15) >> 4;
+        const uint32_t wgbytes = nb16 * 16 * 128 * (a.read_g ? 2 : 1);
+        const float2* Rj = a.R + (int64_t)it.x * a.Sy * a.K;
+        for (int t = 0; t < kt_per; ++t, ++c) {
+          const int kt = kc * kt_per + t;
+          // R tile
+          {
+            const int sb = c % kRgNB;
+            mbar_wait(&b_empty[sb], ((c / kRgNB) & 1u) ^ 1u);
+            TRACE(0, c);
+            uint8_t* st = rg_smem + sb * kRgStB;
+            mbar_arrive_expect_tx(&r_full[sb], rbytes);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int x = (kt * 2 + h) * 32;               // float column of the half
+              if (a.row0 >= 0) {
+                if (kr16 == 4) {
+                  tma_load_2d(st + h * kRgHalfR, &tm.r64, x, it.x * a.Sy + a.row0, &r_full[sb]);
+                } else {
+                  for (int b = 0; b < kr16; ++b)
+                    tma_load_2d(st + h * kRgHalfR + b * 16 * 128, &tm.r16, x, it.x * a.Sy + a.row0 + 16 * b, &r_full[sb]);
+                }
+              } else {
+                for (int r = 0; r < a.n_rows; ++r)
+                  bulk_load(st + h * kRgHalfR + r * 128, Rj + (int64_t)srow[r] * a.K + kt * kRgNT + h * 16, 128,
+                            &r_full[sb]);
+              }
+            }
+          }
+          // W / G half tiles
+#pragma unroll 1
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t cw = 2 * c + h;
+            const int sw = cw % kRgNW;
+            mbar_wait(&wg_empty[sw], ((cw / kRgNW) & 1u) ^ 1u);
+            uint8_t* st = rg_smem + kRgOffWG + sw * kRgStWG;
+            const int x = (kt * 2 + h) * 32;
+            mbar_arrive_expect_tx(&wg_full[sw], wgbytes);
+            if (nb16 == kRgM / 16) {
+              tma_load_2d_hint(st, &tm.w128, x, grow, &wg_full[sw], pol);
+              if (a.read_g) tma_load_2d_hint(st + kRgBoxGW, &tm.g128, x, grow, &wg_full[sw], pol);
+            } else {
+              for (int b = 0; b < nb16; ++b) {
+                tma_load_2d_hint(st + b * 16 * 128, &tm.w16, x, grow + 16 * b, &wg_full[sw], pol);
+                if (a.read_g) tma_load_2d_hint(st + kRgBoxGW + b * 16 * 128, &tm.g16, x, grow + 16 * b, &wg_full[sw], pol);
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 2 || warp == 3) {
+    // ---------------- converters: item (flush row r, 8-coefficient group q8): 64 bytes of R in,
+    // 16 bytes per plane out, in place (every item is read before any is written)
+    const int ct = tid - 64;
+    const int swz_mask = a.row0 >= 0 ? 7 : 0;              // TMA rows arrive SWIZZLE_128B
+    uint32_t c = 0;
+    for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
+      for (int t = 0; t < kt_per; ++t, ++c) {
+        const int sb = c % kRgNB;
+        mbar_wait(&r_full[sb], (c / kRgNB) & 1u);
+        if (ct == 0) TRACE(1, c);
+        uint8_t* st = rg_smem + sb * kRgStB;
+        float4 v[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int item = ct + 64 * i, r = item >> 2, q8 = item & 3;
+          const int h = q8 >> 1;                             // 16-coefficient half
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int chunk = ((q8 & 1) * 4 + u) ^ (r & swz_mask);
+            v[i][u] = r < a.n_rows ? *reinterpret_cast<const float4*>(st + h * kRgHalfR + r * 128 + chunk * 16)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+        named_sync(2, 64);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int item = ct + 64 * i, r = item >> 2, q8 = item & 3;
+          if (r < kr) {
+            uint32_t rh[4], rl[4], ih[4], il[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {                  // complex 2u, 2u + 1 of the group
+              split_bf16x2(v[i][u].x, v[i][u].z, rh[u], rl[u]);
+              split_bf16x2(v[i][u].y, v[i][u].w, ih[u], il[u]);
+            }
+            uint8_t* d = st + (r >> 3) * 128 + (r & 7) * 16;
+            *reinterpret_cast<uint4*>(d + q8 * 1024) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
+            *reinterpret_cast<uint4*>(d + (4 + q8) * 1024) = make_uint4(ih[0], ih[1], ih[2], ih[3]);
+            *reinterpret_cast<uint4*>(d + kRgPlaneB + q8 * 1024) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
+            *reinterpret_cast<uint4*>(d + kRgPlaneB + (4 + q8) * 1024) = make_uint4(il[0], il[1], il[2], il[3]);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&b_full[sb]);
+        if (ct == 0) TRACE(2, c);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16(kRgM, kRgN, /*bf16*/ 1, /*A K-major*/ 0, /*B MN-major*/ 1);
+      const int nkk = kr / 16;
+      uint32_t c = 0, item = 0;
+      for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item) {
+        mbar_wait(f_full, item & 1u);                        // F of this item in TMEM
+        for (int t = 0; t < kt_per; ++t, ++c) {
+          const int sb = c % kRgNB, ac = c % kRgNAcc;
+          mbar_wait(&b_full[sb], (c / kRgNB) & 1u);
+          mbar_wait(&acc_empty[ac], ((c / kRgNAcc) & 1u) ^ 1u);
+          TRACE(3, c);
+          tc_fence_after();
+          // descriptors: one base per stage, offsets added to the address field (addr >> 4)
+          const uint64_t bdesc = smem_desc_noswz(smem_u32(rg_smem + sb * kRgStB), 128, 1024);
+          const uint32_t d1 = tbase + kRgTmemAcc + ac * 2 * kRgN, d2 = d1 + kRgN;
+#pragma unroll
+          for (int pass = 0; pass < 3; ++pass) {             // hi.hi, hi.lo, lo.hi
+            const int fa = pass == 2 ? 1 : 0, pb = pass == 1 ? 1 : 0;
+            const uint32_t fr = tbase + kRgTmemF + (0 + fa) * kRgFCols;
+            const uint32_t fi = tbase + kRgTmemF + (2 + fa) * kRgFCols;
+#pragma unroll
+            for (int kk = 0; kk < kRgRows / 16; ++kk) {
+              if (kk < nkk) {
+                const uint64_t bd = bdesc + (uint64_t)((pb * kRgPlaneB + kk * 256) >> 4);
+                const uint32_t acc = (pass > 0 || kk > 0) ? 1u : 0u;
+                mma_f16_ts(d1, fr + kk * 8, bd, idesc, acc);
+                mma_f16_ts(d2, fi + kk * 8, bd, idesc, acc);
+              }
+            }
+          }
+          mma_commit(&b_empty[sb]);                          // B planes consumed
+          mma_commit(&acc_full[ac]);
+          TRACE(4, c);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: two groups of 4 warps take alternate MMA tiles; thread = vy row m
+    // of the item (TMEM lane).  Group 0 also builds F.
+    const int grp = (warp - 4) >> 2;
+    const int quad = warp & 3, m = quad * 32 + lane;
+    const uint64_t st_pol = policy_evict_first();           // G is re-read only at the next flush
+    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+    const bool sy_pow2 = (a.Sy & (a.Sy - 1)) == 0;
+    uint32_t c = 0, item = 0;
+    for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item) {
+      const int2 it = a.items[w / a.n_kc];
+      const int kc = (int)(w % a.n_kc);
+      const int g0 = __ldg(a.col_off + it.x), mj = __ldg(a.col_off + it.x + 1) - g0;
+      const bool valid = it.y + m < mj;
+      const int64_t g = (int64_t)g0 + it.y + m;
+      const int nvalid = min(kRgM, mj - it.y);                // rows of this item
+      const int full16 = nvalid >> 4;                          // 16-row boxes stored by TMA
+      if (grp == 0) {
+        // F row of this vy over the flush rows, bf16 hi / lo of Fr and Fi, 32 rows at a time,
+        // once every MMA of the previous item is complete (its last accumulator is full)
+        if (c > 0) {
+          const uint32_t cl = c - 1;
+          mbar_wait(&acc_full[cl % kRgNAcc], (cl / kRgNAcc) & 1u);
+        }
+        const int vy = valid ? __ldg(a.act_vy + g) : 0;
+#pragma unroll 1
+        for (int r0 = 0; r0 < kr; r0 += 32) {
+          uint32_t h[16], l[16], ih[16], il[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            float fr2[2], fi2[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int r = r0 + 2 * u + e;
+              float2 f = make_float2(0.f, 0.f);
+              if (valid && r < a.n_rows) {
+                const int sy = srow[r];
+                f = __ldg(a.tw + (sy_pow2 ? ((vy * sy) & (a.Sy - 1)) : (int)(((int64_t)vy * sy) % a.Sy)));
+              }
+              fr2[e] = f.x * a.inv_sqrt_sy;
+              fi2[e] = f.y * a.inv_sqrt_sy;
+            }
+            split_bf16x2(fr2[0], fr2[1], h[u], l[u]);
+            split_bf16x2(fi2[0], fi2[1], ih[u], il[u]);
+          }
+          const uint32_t col = tbase + lane_addr + kRgTmemF + r0 / 2;
+          tmem_st16(col + 0 * kRgFCols, h);
+          tmem_st16(col + 1 * kRgFCols, l);
+          tmem_st16(col + 2 * kRgFCols, ih);
+          tmem_st16(col + 3 * kRgFCols, il);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        named_sync(1, 128);
+        if (tid == 128) mbar_arrive(f_full);
+      }
+      float2 dot = make_float2(0.f, 0.f);
+      for (int t = 0; t < kt_per; ++t, ++c) {
+        if ((int)(c & 1u) != grp) continue;
+        const int ac = c % kRgNAcc;
+        mbar_wait(&acc_full[ac], (c / kRgNAcc) & 1u);
+        if (m == 0 && grp == 0) TRACE(5, c);
+        tc_fence_after();
+        const uint32_t d1 = tbase + lane_addr + kRgTmemAcc + ac * 2 * kRgN, d2 = d1 + kRgN;
+        const int k0 = (kc * kt_per + t) * kRgNT;
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t cw = 2 * c + hh;
+          const int sw = cw % kRgNW;
+          // D1 = [Fr Rr | Fr Ri], D2 = [Fi Rr | Fi Ri]: this half's 4 x 16 columns, one wait
+          uint32_t dd[64];
+          tmem_ld8_raw(d1 + 16 * hh, dd);
+          tmem_ld8_raw(d1 + 16 * hh + 8, dd + 8);
+          tmem_ld8_raw(d1 + kRgNT + 16 * hh, dd + 16);
+          tmem_ld8_raw(d1 + kRgNT + 16 * hh + 8, dd + 24);
+          tmem_ld8_raw(d2 + 16 * hh, dd + 32);
+          tmem_ld8_raw(d2 + 16 * hh + 8, dd + 40);
+          tmem_ld8_raw(d2 + kRgNT + 16 * hh, dd + 48);
+          tmem_ld8_raw(d2 + kRgNT + 16 * hh + 8, dd + 56);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 64; ++q) asm volatile("" : "+r"(dd[q]));
+          if (hh == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ac]);
+          }
+          const float* ar = reinterpret_cast<const float*>(dd);        // Fr Rr
+          const float* ai = ar + 16;                                    // Fr Ri
+          const float* br = ar + 32;                                    // Fi Rr
+          const float* bi = ar + 48;                                    // Fi Ri
+          mbar_wait(&wg_full[sw], (cw / kRgNW) & 1u);
+          uint8_t* sbox = rg_smem + kRgOffWG + sw * kRgStWG;
+          if (valid) {
+            const uint8_t* sw8 = sbox + m * 128;
+            uint8_t* sg8 = sbox + kRgBoxGW + m * 128;
+            float4 wv[8], ov[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {                    // 16-byte chunk q = coefficients 2q, 2q + 1
+              const int off = (q ^ (m & 7)) * 16;            // SWIZZLE_128B
+              wv[q] = *reinterpret_cast<const float4*>(sw8 + off);
+              ov[q] = a.read_g ? *reinterpret_cast<const float4*>(sg8 + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            // rows in whole 16-row boxes go back through smem and a TMA store (full 128-byte
+            // lines); the rows of a partial last box are stored directly
+            const bool direct = m >= full16 * 16;
+            float4* Gr = reinterpret_cast<float4*>(a.G + g * a.K + k0 + 16 * hh);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int n0 = 2 * q, n1 = 2 * q + 1;
+              const float4 gv = make_float4(ov[q].x + (ar[n0] - bi[n0]), ov[q].y + (ai[n0] + br[n0]),
+                                            ov[q].z + (ar[n1] - bi[n1]), ov[q].w + (ai[n1] + br[n1]));
+              if (a.write_g) {
+                if (direct) Gr[q] = gv;
+                else *reinterpret_cast<float4*>(sg8 + (q ^ (m & 7)) * 16) = gv;
+              }
+              dot.x = fmaf(gv.x, wv[q].x, fmaf(-gv.y, wv[q].y, fmaf(gv.z, wv[q].z, fmaf(-gv.w, wv[q].w, dot.x))));
+              dot.y = fmaf(gv.x, wv[q].y, fmaf(gv.y, wv[q].x, fmaf(gv.z, wv[q].w, fmaf(gv.w, wv[q].z, dot.y))));
+            }
+          }
+          if (a.write_g) fence_proxy_async_smem();           // smem G writes -> TMA store
+          named_sync(4 + grp, 128);                          // the group is done with this W / G stage
+          if ((tid & 127) == 0) {
+            if (a.write_g && full16 > 0) {
+              const int x = ((kc * kt_per + t) * 2 + hh) * 32;
+              if (full16 == kRgM / 16) {
+                tma_store_2d_hint(&tm.g128, x, g0 + it.y, sbox + kRgBoxGW, st_pol);
+              } else {
+                for (int b = 0; b < full16; ++b)
+                  tma_store_2d_hint(&tm.g16, x, g0 + it.y + 16 * b, sbox + kRgBoxGW + b * 16 * 128, st_pol);
+              }
+              bulk_commit();
+              bulk_wait_read0();                             // smem read by the store: stage reusable
+            }
+            mbar_arrive(&wg_empty[sw]);
+          }
+        }
+        if (m == 0 && grp == 0) TRACE(6, c);
+      }
+      // combine the two groups' partial dots (fixed order: group 0 + group 1)
+      float2* sd = sdot + (item & 1u) * kRgM;
+      if (grp == 1) sd[m] = dot;
+      named_sync(3, 256);
+      if (grp == 0 && valid) {
+        const float2 d1v = sd[m];
+        a.opart[(int64_t)kc * a.n_act + g] = make_float2(dot.x + d1v.x, dot.y + d1v.y);
+      }
+    }
+    if ((tid & 127) == 0) bulk_wait0();                     // the G stores have completed
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<kRgTmemCols>(tbase);
+}
+
 // k-chunks of the GEMM flush: enough CTAs to fill two waves of the GPU
 static int colgemm_chunks(const Plan& p) {
   int max_mj = 0;
@@ -1450,23 +1868,93 @@ static int colfft_tpc(const Plan& p) {
 
 int colfft_tiles(const Plan& p) { return (p.K >> colfft_logkt(p)) / colfft_tpc(p); }
 
+// k-chunks of the pipelined GEMM flush: enough work items for ~4 per CTA
+static int rgemm_nkc(const Plan& p) {
+  const int KT = p.K / kRgNT;
+  int nkc = 1;
+  while (nkc * 2 <= KT && KT % (nkc * 2) == 0 && (int64_t)p.rg_items.size() * nkc < 4 * p.sm_count) nkc *= 2;
+  return nkc;
+}
+
+bool rgemm_possible(const Plan& p, int n_rows) {
+  return p.rg_ready && n_rows >= 1 && n_rows <= kRgRows && p.K % kRgNT == 0 && is_pow2(p.Sx) && p.Sx >= 2 &&
+         p.Sx <= (1 << kFftMaxLog);
+}
+
+// Tensor maps of G and W for the pipelined GEMM flush (2-D fp32 [n_act][2K], 32-float x 128-row
+// boxes, SWIZZLE_128B); built once per plan.
+cudaError_t rgemm_prepare(Plan& p) {
+  p.rg_ready = false;
+  p.rg_items.clear();
+  for (int j = 0; j < p.n_vx; ++j)
+    for (int i0 = 0; i0 < p.col_off[j + 1] - p.col_off[j]; i0 += kRgM) p.rg_items.push_back(make_int2(j, i0));
+  auto enc = get_encode();
+  if (!enc || p.K % kRgNT) return cudaSuccess;   // (the FFT / DFT flushes remain)
+  static_assert(sizeof(RgMaps) <= sizeof(p.rg_tmap), "tensor map storage");
+  RgMaps* maps = reinterpret_cast<RgMaps*>(p.rg_tmap);
+  auto make = [&](CUtensorMap* tm, void* base, uint64_t rows, uint32_t box_rows) {
+    const cuuint64_t dims[2] = {(cuuint64_t)2 * p.K, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)p.K * sizeof(float2)};
+    const cuuint32_t box[2] = {32u, box_rows};   // 16 complex (128 B) x box_rows
+    const cuuint32_t estr[2] = {1u, 1u};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+  };
+  if (!make(&maps->w16, p.d_W, p.n_act, 16) || !make(&maps->g16, p.d_G, p.n_act, 16) ||
+      !make(&maps->w128, p.d_W, p.n_act, kRgM) || !make(&maps->g128, p.d_G, p.n_act, kRgM) ||
+      !make(&maps->r16, p.d_R, (uint64_t)p.n_vx * p.Sy, 16) || !make(&maps->r64, p.d_R, (uint64_t)p.n_vx * p.Sy, 64))
+    return cudaSuccess;
+  if (cudaMalloc(&p.d_rg_items, p.rg_items.size() * sizeof(int2)) != cudaSuccess) return cudaErrorMemoryAllocation;
+  cudaError_t e = cudaMemcpy(p.d_rg_items, p.rg_items.data(), p.rg_items.size() * sizeof(int2), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(rgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRgSmem);
+  if (e != cudaSuccess) return e;
+  p.rg_ready = true;
+  return cudaSuccess;
+}
+
+static cudaError_t launch_rgemm(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, bool o_only,
+                                cudaStream_t st, int row0) {
+  const int nkc = rgemm_nkc(p);
+  RgArgs a{(const float2*)p.d_R, rows, n_rows, (const float2*)p.d_twy, p.Sy,
+           (float)(1.0 / std::sqrt((double)p.Sy)), (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy,
+           (const int2*)p.d_rg_items, (int)p.rg_items.size(), nkc, p.d_G, p.d_opart, (int64_t)p.n_act, p.K,
+           (!overwrite && !o_only) ? 1 : 0, o_only ? 0 : 1, row0};
+  const int64_t work = (int64_t)p.rg_items.size() * nkc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::min<int64_t>(work, p.sm_count));
+  cfg.blockDim = dim3(kRgThreads);
+  cfg.dynamicSmemBytes = kRgSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, rgemm_kernel, a, *reinterpret_cast<const RgMaps*>(p.rg_tmap));
+}
+
 bool flush_uses_fft(const Plan& p, int n_rows) {
   // FFT along y costs ~5 Sy log2(Sy) flops per (column, k) whatever the number of staged rows r;
   // the DFT-matrix update ~8 r m_j with m_j (active vy of the column) a fraction of Sy.
   return is_pow2(p.Sy) && p.Sy >= 2 && p.Sy <= (1 << kFftMaxLog) && n_rows >= std::max(4, ilog2(p.Sy));
 }
 
-// Which form of the rank update a flush of n_rows staged rows uses: 2 = tensor-core DFT GEMM,
-// 1 = FFT along y, 0 = SIMT DFT matrix.  WDD_FLUSH=gemm|fft|dft overrides.
-int flush_kind(const Plan& p, int n_rows) {
+// Which form of the rank update a flush of n_rows staged rows uses: 3 = pipelined tensor-core
+// GEMM (rgemm_kernel; R in its tile layout), 2 = tensor-core DFT GEMM, 1 = FFT along y, 0 = SIMT
+// DFT matrix.  WDD_FLUSH=rgemm|gemm|fft|dft overrides; allow_rg = false excludes 3 (R in fp32).
+int flush_kind(const Plan& p, int n_rows, bool allow_rg) {
   static const int env = [] {
     const char* e = std::getenv("WDD_FLUSH");
     if (!e) return -1;
-    return std::strcmp(e, "gemm") == 0 ? 2 : std::strcmp(e, "fft") == 0 ? 1 : std::strcmp(e, "dft") == 0 ? 0 : -1;
+    return std::strcmp(e, "rgemm") == 0 ? 3 : std::strcmp(e, "gemm") == 0 ? 2 : std::strcmp(e, "fft") == 0 ? 1
+         : std::strcmp(e, "dft") == 0 ? 0 : -1;
   }();
+  if (allow_rg && rgemm_possible(p, n_rows) && (env == -1 || env == 3)) return 3;
   const bool gemm_ok = n_rows <= kCgRows && p.K % kCgNT == 0;
   int k;
-  if (env == 2) k = gemm_ok ? 2 : (flush_uses_fft(p, n_rows) ? 1 : 0);
+  if (env == 2 || env == 3) k = gemm_ok ? 2 : (flush_uses_fft(p, n_rows) ? 1 : 0);
   else if (env == 1) k = flush_uses_fft(p, n_rows) ? 1 : (gemm_ok ? 2 : 0);
   else if (env == 0) k = 0;
   else k = flush_uses_fft(p, n_rows) ? 1 : (gemm_ok ? 2 : 0);
@@ -1476,14 +1964,17 @@ int flush_kind(const Plan& p, int n_rows) {
   return k;
 }
 
-int flush_tiles(const Plan& p, int n_rows) {
-  const int k = flush_kind(p, n_rows);
-  return k == 2 ? colgemm_chunks(p) : k == 1 ? colfft_tiles(p) : 0;
+int flush_tiles(const Plan& p, int n_rows, int kind) {
+  const int k = kind >= 0 ? kind : flush_kind(p, n_rows);
+  return k == 3 ? rgemm_nkc(p) : k == 2 ? colgemm_chunks(p) : k == 1 ? colfft_tiles(p) : 0;
 }
 
-cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st, bool o_only) {
+cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st, bool o_only,
+                         int kind, int row0) {
   if (n_rows <= 0) return cudaSuccess;
-  if (flush_kind(p, n_rows) == 2) {
+  if (kind < 0) kind = flush_kind(p, n_rows);
+  if (kind == 3) return launch_rgemm(p, rows, n_rows, overwrite, o_only, st, row0);
+  if (kind == 2) {
     int max_mj = 0;
     for (int j = 0; j < p.n_vx; ++j) max_mj = std::max(max_mj, p.col_off[j + 1] - p.col_off[j]);
     static bool init = false;
@@ -1499,7 +1990,7 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
                       (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G, (const float2*)p.d_W,
                       p.d_opart, (int64_t)p.n_act, p.K, (p.K / kCgNT) / ch, overwrite ? 1 : 0, o_only ? 1 : 0);
   }
-  if (flush_kind(p, n_rows) == 1) {
+  if (kind == 1) {
     const int logSy = ilog2(p.Sy);
     const int logKT = colfft_logkt(p);
     const size_t smem = ((size_t)p.Sy << logKT) * 8 + (size_t)p.Sy * 8 + 16;

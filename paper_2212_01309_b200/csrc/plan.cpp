@@ -371,8 +371,10 @@ wdd_status flush(Plan& p) {
     if (p.row_staged[sy]) rows.push_back(sy);
   const int n_rows = (int)rows.size();
   if (n_rows == 0) return WDD_OK;
+  const int kind = flush_kind(p, n_rows);
   const int32_t* dr = nullptr;
-  if (rows.back() - rows.front() == n_rows - 1) {
+  const bool contig = rows.back() - rows.front() == n_rows - 1;
+  if (contig) {
     dr = p.d_iota + rows.front();
   } else {
     void* d = nullptr;
@@ -381,16 +383,16 @@ wdd_status flush(Plan& p) {
   }
   {
     Prof pr(p, kSlotFlush, p.stream);
-    CUDA_TRY(launch_flush(p, dr, n_rows, p.G_zero, p.stream, p.o_only));
+    CUDA_TRY(launch_flush(p, dr, n_rows, p.G_zero, p.stream, p.o_only, kind, contig ? rows.front() : -1));
   }
   for (int32_t sy : rows) p.row_staged[sy] = 0;
   if (p.o_only) {                     // o += this flush's increment; G is not touched
     Prof pr(p, kSlotReadout, p.stream);
-    CUDA_TRY(launch_oacc(p, flush_tiles(p, n_rows), p.stream));
+    CUDA_TRY(launch_oacc(p, flush_tiles(p, n_rows, kind), p.stream));
     return WDD_OK;
   }
   p.G_zero = false;
-  p.opart_tiles = flush_tiles(p, n_rows);
+  p.opart_tiles = flush_tiles(p, n_rows, kind);
   return WDD_OK;
 }
 
@@ -443,7 +445,7 @@ void free_plan(Plan* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   cudaDeviceSynchronize();
   if (p->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(p->nccl));
-  void* bufs[] = {p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
+  void* bufs[] = {p->d_rg_items, p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
                   p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec, p->d_img_tmp,
                   p->d_meta, p->d_stage[0], p->d_stage[1]};
   for (void* b : bufs)
@@ -623,7 +625,8 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ALLOC(p->d_vpos, act.size() * 4);
   ALLOC(p->d_flush_tiles, p->flush_tiles.size() * sizeof(int2));
   ALLOC(p->d_o, act.size() * sizeof(float2));
-  p->opart_cap = std::max(1, std::max(colfft_tiles(*p), flush_tiles(*p, 1 << 20)));
+  if (rgemm_prepare(*p) != cudaSuccess) return bail(fail(WDD_E_CUDA, "GEMM flush setup failed"));
+  p->opart_cap = std::max({1, colfft_tiles(*p), flush_tiles(*p, 1 << 20), p->rg_ready ? flush_tiles(*p, 64, 3) : 1});
   ALLOC(p->d_opart, (size_t)p->opart_cap * act.size() * sizeof(float2));
   ALLOC(p->d_gidx, (size_t)p->S * sizeof(int32_t));
   ALLOC(p->d_oacc, act.size() * sizeof(float2));

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--pool", type=int, default=4096)
     ap.add_argument("--accumulator", default="G")
+    ap.add_argument("--readout-rows", type=int, default=0, help="also read out every N rows")
     args = ap.parse_args()
     import torch
     import paper_2212_01309_b200 as wdd
@@ -44,6 +45,8 @@ def main():
             p0 = a % pool_n
             fr = pool[p0:p0 + (b - a)] if p0 + (b - a) <= pool_n else pool[:b - a]
             plan.ingest(fr, np.arange(a, b, dtype=np.int32), st)
+            if args.readout_rows and (b // cfg.Sx) % args.readout_rows == 0 and b < n and b % cfg.Sx == 0:
+                plan.readout(out)
         plan.readout(out)
         torch.cuda.synchronize()
     print("ok", cfg.name, n, "frames")
