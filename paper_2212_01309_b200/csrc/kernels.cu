@@ -139,7 +139,11 @@ struct ProjCfgT {
   static constexpr int tAcc2 = tAcc1 + kNAcc * kAcc1;
   static constexpr int kTmemCols = pow2_cols(tAcc2 + kNB2 * kN);
   static_assert(tAcc2 + kNB2 * kN <= 512, "TMEM");
-  static constexpr int kFixed = (U16 ? 0 : 2 * kSlot) + align_up(kNB2 * 2 * kA2, 1024) + align_up(kB, 1024) + 512;
+  // stage-2 C rows go out through a per-warp shared-memory transpose (512-byte coalesced stores
+  // instead of 16-byte pieces of 16 rows) where it fits: Q = 128, L = 32 (C is 1/8 of the bytes)
+  static constexpr bool kCStage = !LEAN && Q == 128 && L == 32 && kM2 == 64;
+  static constexpr int kCStageB = kCStage ? 4 * 16 * L * 4 : 0;
+  static constexpr int kFixed = (U16 ? 0 : 2 * kSlot) + align_up(kNB2 * 2 * kA2, 1024) + align_up(kB, 1024) + kCStageB + 512;
   static constexpr int kNSraw = (((LEAN ? 113 * 1024 : 232448) - kFixed) / kSlot) & ~1;
   static constexpr int kNSfit = kNSraw < 2 ? 2 : kNSraw;   // (lean: configs that do not fit run 1 CTA/SM)
   static constexpr int kNS = kNSfit < WDD_NS ? kNSfit : WDD_NS;  // raw ring (even: group = job parity)
@@ -147,7 +151,8 @@ struct ProjCfgT {
   static constexpr int off_P1 = off_ring + kNS * kSlot;   // f32 path only
   static constexpr int off_A2 = off_P1 + (U16 ? 0 : 2 * kSlot);
   static constexpr int off_B = off_A2 + align_up(kNB2 * 2 * kA2, 1024);
-  static constexpr int off_bar = off_B + align_up(kB, 1024);
+  static constexpr int off_C = off_B + align_up(kB, 1024);
+  static constexpr int off_bar = off_C + kCStageB;
   static constexpr int kBars = 2 * kNS + 2 * kNA + 2 * kNAcc + 3 * kNB2 + 3;
   static constexpr int off_misc = off_bar + 8 * kBars;    // meta[kNS+kNA], wflag[2 groups][2][4], tmem slot
   static constexpr int smem = off_misc + 4 * (kNS + kNA) + 64 + 16;
@@ -551,6 +556,33 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
       if (lane == 0) mbar_arrive(&acc2_empty[gb]);
       const int f = m2 / L, aa = m2 % L;
       const int64_t fg = frame0 + f;
+      if constexpr (Cfg::kCStage) {
+        // lanes 0-15 of this warp hold rows aa0 .. aa0 + 15 of one frame (a contiguous 16 L floats
+        // of C): rows into the warp's staging (16-byte chunks XOR-swizzled by row), then the warp
+        // stores them as 512-byte contiguous pieces
+        float* stg = reinterpret_cast<float*>(smem + Cfg::off_C) + quad * 16 * L;
+        if (lane < 16) {
+#pragma unroll
+          for (int b = 0; b < L; b += 4)
+            *reinterpret_cast<float4*>(stg + lane * L + (((b >> 2) ^ (lane & 7)) << 2)) =
+                make_float4((d[b] + d[L + b]) * a.sc2, (d[b + 1] + d[L + b + 1]) * a.sc2,
+                            (d[b + 2] + d[L + b + 2]) * a.sc2, (d[b + 3] + d[L + b + 3]) * a.sc2);
+        }
+        __syncwarp();
+        const int fw = (quad * 16) / L;                      // the warp's frame (warp-uniform)
+        const int64_t fgw = frame0 + fw;
+        if (fw < g2 && fgw < n) {
+          float* dst = a.C + (a.idx ? (int64_t)__ldg(a.idx + fgw) : fgw) * K + ((quad * 16) % L) * L;
+#pragma unroll
+          for (int i = 0; i < (16 * L) / 128; ++i) {
+            const int e = i * 128 + lane * 4;                // float index in the warp's 16 rows
+            const int r = e / L, cq = (e % L) >> 2;
+            *reinterpret_cast<float4*>(dst + e) = *reinterpret_cast<const float4*>(stg + r * L + ((cq ^ (r & 7)) << 2));
+          }
+        }
+        __syncwarp();
+        return;
+      }
       if (f < g2 && fg < n) {
         float* dst = a.C + (a.idx ? (int64_t)__ldg(a.idx + fg) : fg) * K + aa * L;
 #pragma unroll

@@ -1,0 +1,4 @@
+#!/bin/bash
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+for mf in 0 1 4 6 12; do for c in live box; do WDD_PROJ_MIN_FRAMES=$mf timeout 300 python tools/bench_live.py --config $c --reps 2 > /tmp/o.txt 2>&1; tail -1 /tmp/o.txt | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('mf=$mf $c', round(d['frames_per_s']/1e6,2), 'frac', round(d['frac'],3), 'ingest p50', round(d['ingest_latency_us']['p50'],1), 'readout', round(d['readout_latency_us']['p50'],1))" || tail -3 /tmp/o.txt; done; done
