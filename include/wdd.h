@@ -147,7 +147,7 @@ typedef struct {
   int64_t bytes_G, bytes_bank, bytes_R, bytes_C;
   int64_t frames_ingested;
   int32_t nranks, rank;
-  int32_t proj_ctas_per_sm;   /* projection kernel variant: 2 = lean (two CTAs per SM), 1 = full */
+  int32_t proj_ctas_per_sm;   /* resident projection CTAs per SM (occupancy query; 2 = lean variant) */
   int32_t reserved0;
 } wdd_plan_info;
 wdd_status wdd_get_info(wdd_plan_t plan, wdd_plan_info* info);

@@ -141,6 +141,7 @@ cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* 
 void pack_basis_fp16(const Plan& p, std::vector<uint16_t>& out, double& scale);
 size_t project_smem_bytes(int Q, int L);
 bool project_is_lean(const Plan& p);   // projection runs two CTAs per SM for this plan
+int project_occupancy(const Plan& p);  // resident projection CTAs per SM (runtime occupancy query)
 // plan-time Wiener bank (Algorithm 1) on the GPU in float64 (bank.cu): q_host = detector grid
 // (Q), apx_host = aperture pixel interval of each detector row (x > y: empty), [ax_lo,
 // ax_lo + n_axc) the aperture's column range; writes n_act x K complex64 (or complex128 if f64)

@@ -23,6 +23,7 @@
 #include <climits>
 #include <type_traits>
 #include <cmath>
+#include <ctime>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -93,6 +94,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // columns) so that one CTA's pipeline fill / drain overlaps the other's streaming.
 constexpr bool kLeanAllowed = WDD_LEAN != 0;   // per configuration: lean only where it fits
 constexpr int kConv = 128;          // threads per converter group (2 groups: even / odd chunks)
+constexpr int kLeanSmem = 110 * 1024;   // shared-memory budget of a lean (two CTAs per SM) projection CTA
 constexpr uint32_t kLBO = 2064;     // no-swizzle K-major: bytes between K-adjacent core matrices of a
                                     // 128-row operand (16 row groups x 128 B + 16 B bank-rotation pad)
 
@@ -131,7 +133,9 @@ struct ProjCfgT {
   static constexpr int kAcc1 = kN;                        // per acc1 slot (both count planes accumulate here)
   static constexpr int kNB2 = LEAN ? 1 : 2;               // stage-2 A2 images / accumulators in flight
   // acc1 ring: 4 deep unless TMEM (A ring + plane-1 buffers + acc1 + acc2 images) would exceed 512 columns
-  static constexpr int kNAcc = (LEAN || (kNA + kNGroups) * (Q >= 64 ? 32 : Q / 2) + (4 + kNB2) * 2 * L > 512) ? 2 : 4;
+  // (lean: 2, or 1 where two would not leave both CTAs of an SM their 256 TMEM columns)
+  static constexpr int kNAcc = LEAN ? ((kNA + kNGroups) * (Q >= 64 ? 32 : Q / 2) + (2 + kNB2) * 2 * L > 256 ? 1 : 2)
+                                    : ((kNA + kNGroups) * (Q >= 64 ? 32 : Q / 2) + (4 + kNB2) * 2 * L > 512 ? 2 : 4);
   static constexpr int kACols = kKC / 2;                  // TMEM columns of one A1 chunk (fp16 pairs)
   static constexpr int tA = 0;                            // TMEM column map
   static constexpr int tP1 = tA + kNA * kACols;          // one plane-1 buffer per converter group
@@ -144,7 +148,9 @@ struct ProjCfgT {
   static constexpr bool kCStage = !LEAN && Q == 128 && L == 32 && kM2 == 64;
   static constexpr int kCStageB = kCStage ? 4 * 16 * L * 4 : 0;
   static constexpr int kFixed = (U16 ? 0 : 2 * kSlot) + align_up(kNB2 * 2 * kA2, 1024) + align_up(kB, 1024) + kCStageB + 512;
-  static constexpr int kNSraw = (((LEAN ? 113 * 1024 : 232448) - kFixed) / kSlot) & ~1;
+  // (lean: two CTAs and their per-CTA reservation must share the SM's 228 KB -- 110 KB each leaves
+  // room; measured: 112.3 KB CTAs did not co-reside.  Two converter groups need an even ring.)
+  static constexpr int kNSraw = (((LEAN ? kLeanSmem : 232448) - kFixed) / kSlot) & (kNGroups == 2 ? ~1 : ~0);
   static constexpr int kNSfit = kNSraw < 2 ? 2 : kNSraw;   // (lean: configs that do not fit run 1 CTA/SM)
   static constexpr int kNS = kNSfit < WDD_NS ? kNSfit : WDD_NS;  // raw ring (even: group = job parity)
   static constexpr int off_ring = 0;
@@ -157,7 +163,7 @@ struct ProjCfgT {
   static constexpr int off_misc = off_bar + 8 * kBars;    // meta[kNS+kNA], wflag[2 groups][2][4], tmem slot
   static constexpr int smem = off_misc + 4 * (kNS + kNA) + 64 + 16;
   static constexpr int kTmemUsed = tAcc2 + kNB2 * kN;
-  static_assert(kNS % 2 == 0 && kNA % 2 == 0, "even rings: converter group = job parity");
+  static_assert((kNGroups == 1 || kNS % 2 == 0) && kNA % 2 == 0, "even rings: converter group = job parity");
   static_assert(kG2 >= 1, "group");
   static_assert(smem <= 232448, "shared memory");
 };
@@ -165,8 +171,8 @@ struct ProjCfgT {
 template <int Q, int L, bool U16>
 struct ProjCfgSel {
   using LeanCfg = ProjCfgT<Q, L, U16, true>;
-  static constexpr bool lean = kLeanAllowed && LeanCfg::smem <= 113 * 1024 && LeanCfg::kTmemUsed <= 256 &&
-                               LeanCfg::kNSraw >= 4;
+  static constexpr bool lean = kLeanAllowed && LeanCfg::smem <= kLeanSmem && LeanCfg::kTmemUsed <= 256 &&
+                               LeanCfg::kNSraw >= 3;
   using type = typename std::conditional<lean, LeanCfg, ProjCfgT<Q, L, U16, false>>::type;
 };
 template <int Q, int L, bool U16>
@@ -781,6 +787,7 @@ extern "C" int wdd_trace_dump(unsigned long long* host, int max_n) {
   cudaMemcpyToSymbol(g_trace, zeros, sizeof zeros);
   return n;
 }
+
 extern "C" int wdd_trace_ctas(unsigned long long* host /* 8192 x 5 */) {
   cudaDeviceSynchronize();
   unsigned n = 0;
@@ -801,6 +808,29 @@ bool project_is_lean(const Plan& p) {
   WDD_LEAN_CASE(256, 8) WDD_LEAN_CASE(256, 16) WDD_LEAN_CASE(256, 24) WDD_LEAN_CASE(256, 32)
 #undef WDD_LEAN_CASE
   return false;
+}
+
+// resident projection CTAs per SM as the runtime computes it (registers, smem, threads)
+int project_occupancy(const Plan& p) {
+  int n = 0;
+#define WDD_OCC_CASE(QQ, LL)                                                                         \
+  if (p.Q == QQ && p.L == LL) {                                                                      \
+    if (p.dtype == 0) {                                                                              \
+      using C = ProjCfg<QQ, LL, true>;                                                               \
+      cudaFuncSetAttribute(project_kernel<QQ, LL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem); \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, project_kernel<QQ, LL, true>, C::kThreads, C::smem); \
+    } else {                                                                                         \
+      using C = ProjCfg<QQ, LL, false>;                                                              \
+      cudaFuncSetAttribute(project_kernel<QQ, LL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem); \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, project_kernel<QQ, LL, false>, C::kThreads, C::smem); \
+    }                                                                                                \
+  }
+  WDD_OCC_CASE(32, 8) WDD_OCC_CASE(32, 16) WDD_OCC_CASE(32, 32)
+  WDD_OCC_CASE(64, 8) WDD_OCC_CASE(64, 16) WDD_OCC_CASE(64, 32)
+  WDD_OCC_CASE(128, 8) WDD_OCC_CASE(128, 16) WDD_OCC_CASE(128, 24) WDD_OCC_CASE(128, 32)
+  WDD_OCC_CASE(256, 8) WDD_OCC_CASE(256, 16) WDD_OCC_CASE(256, 24) WDD_OCC_CASE(256, 32)
+#undef WDD_OCC_CASE
+  return n;
 }
 
 size_t project_smem_bytes(int Q, int L) {
@@ -1462,7 +1492,8 @@ __global__ void __launch_bounds__(256, 1) colgemm_kernel(const float2* __restric
 //                         bulk copy per row when the rows are not contiguous), converted in place to
 //                         bf16 hi / lo planes of B = [Rr | Ri] (N = 64, MN-major, K = flush row);
 //                         freed by the MMA commit;
-//   W/G ring (NW x 32 KB) per 16-coefficient half tile one SWIZZLE_128B box of W and one of G
+//   W/G ring (2 x 3 x 32 KB, three stages owned by each epilogue group)
+//                         per 16-coefficient half tile one SWIZZLE_128B box of W and one of G
 //                         (G only when read: not on the first flush after a reset, not for
 //                         spectrum-only plans; 16-row boxes for the tail tile of a column); freed
 //                         by the epilogue.
@@ -1480,10 +1511,17 @@ constexpr int kRgPlaneB = (kRgN / 8) * (kRgRows / 8) * 128;  // 8 KB: element (n
 constexpr int kRgStB = 2 * kRgPlaneB;                        // 16 KB = the fp32 R tile (two 128-B halves x 64 rows)
 constexpr int kRgHalfR = kRgRows * 128;                      // 8 KB: one 16-coefficient half of the R tile
 constexpr int kRgM = 128;
-constexpr int kRgNB = 3;                                     // B ring depth (MMA tiles)
+constexpr int kRgNB = 2;                                     // B ring depth (MMA tiles)
 constexpr int kRgBoxGW = kRgM * 128;                         // 16 KB: 128 rows x 16 complex
 constexpr int kRgStWG = 2 * kRgBoxGW;                        // 32 KB: W box + G box of one half tile
-constexpr int kRgNW = 5;                                     // W/G ring depth (half tiles)
+#ifndef WDD_RG_NWG
+#define WDD_RG_NWG 3
+#endif
+// W/G stages per epilogue group.  Each group owns its stages: the two groups run out of lockstep,
+// and a barrier shared by both would let the group that is ahead pass a parity wait on a phase two
+// behind (observed as rare hangs and faults with 5 shared stages)
+constexpr int kRgNWG = WDD_RG_NWG;
+constexpr int kRgNW = 2 * kRgNWG;                            // W/G ring depth (half tiles)
 constexpr int kRgNAcc = 2;                                   // TMEM accumulator ring depth
 constexpr int kRgOffWG = kRgNB * kRgStB;
 constexpr int kRgBarOff = kRgOffWG + kRgNW * kRgStWG;
@@ -1496,6 +1534,15 @@ constexpr int kRgTmemAcc = 4 * kRgFCols;                     // 128: [acc][D1 | 
 constexpr int kRgTmemCols = 512;
 static_assert(kRgSmem <= 232448, "rgemm shared memory");
 static_assert(kRgTmemAcc + kRgNAcc * 2 * kRgN <= kRgTmemCols, "rgemm TMEM");
+
+#ifdef WDD_RG_DEBUG
+// hang hunting: per CTA and role the tile counter and the barrier being waited for (readable by
+// the host on a side stream while the kernel runs: wdd_rg_debug)
+__device__ unsigned g_rgdbg[148 * 8];
+#define RGDBG(role, c, code) do { *(volatile unsigned*)&g_rgdbg[blockIdx.x * 8 + (role)] = ((c) << 8) | (code); } while (0)
+#else
+#define RGDBG(role, c, code)
+#endif
 
 struct RgArgs {
   const float2* R;           // R[j][sy][k]
@@ -1584,6 +1631,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
           // R tile
           {
             const int sb = c % kRgNB;
+            RGDBG(0, c, 1);
             mbar_wait(&b_empty[sb], ((c / kRgNB) & 1u) ^ 1u);
             TRACE(0, c);
             uint8_t* st = rg_smem + sb * kRgStB;
@@ -1608,9 +1656,10 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
           // W / G half tiles
 #pragma unroll 1
           for (int h = 0; h < 2; ++h) {
-            const uint32_t cw = 2 * c + h;
-            const int sw = cw % kRgNW;
-            mbar_wait(&wg_empty[sw], ((cw / kRgNW) & 1u) ^ 1u);
+            const uint32_t u = (c >> 1) * 2 + h;              // half tile index within the group (c & 1)
+            const int sw = (int)(c & 1u) * kRgNWG + (int)(u % kRgNWG);
+            RGDBG(0, c, 2 + h);
+            mbar_wait(&wg_empty[sw], ((u / kRgNWG) & 1u) ^ 1u);
             uint8_t* st = rg_smem + kRgOffWG + sw * kRgStWG;
             const int x = (kt * 2 + h) * 32;
             mbar_arrive_expect_tx(&wg_full[sw], wgbytes);
@@ -1636,7 +1685,9 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
     for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x) {
       for (int t = 0; t < kt_per; ++t, ++c) {
         const int sb = c % kRgNB;
+        if (ct == 0) RGDBG(1, c, 1);
         mbar_wait(&r_full[sb], (c / kRgNB) & 1u);
+        if (ct == 0) RGDBG(1, c, 2);
         if (ct == 0) TRACE(1, c);
         uint8_t* st = rg_smem + sb * kRgStB;
         float4 v[4][4];
@@ -1682,11 +1733,15 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
       const int nkk = kr / 16;
       uint32_t c = 0, item = 0;
       for (int64_t w = blockIdx.x; w < n_work; w += gridDim.x, ++item) {
+        RGDBG(2, c, 1);
         mbar_wait(f_full, item & 1u);                        // F of this item in TMEM
         for (int t = 0; t < kt_per; ++t, ++c) {
           const int sb = c % kRgNB, ac = c % kRgNAcc;
+          RGDBG(2, c, 2);
           mbar_wait(&b_full[sb], (c / kRgNB) & 1u);
+          RGDBG(2, c, 3);
           mbar_wait(&acc_empty[ac], ((c / kRgNAcc) & 1u) ^ 1u);
+          RGDBG(2, c, 4);
           TRACE(3, c);
           tc_fence_after();
           // descriptors: one base per stage, offsets added to the address field (addr >> 4)
@@ -1735,6 +1790,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
         // once every MMA of the previous item is complete (its last accumulator is full)
         if (c > 0) {
           const uint32_t cl = c - 1;
+          if (m == 0) RGDBG(3, c, 1);
           mbar_wait(&acc_full[cl % kRgNAcc], (cl / kRgNAcc) & 1u);
         }
         const int vy = valid ? __ldg(a.act_vy + g) : 0;
@@ -1773,15 +1829,17 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
       for (int t = 0; t < kt_per; ++t, ++c) {
         if ((int)(c & 1u) != grp) continue;
         const int ac = c % kRgNAcc;
+        if (m == 0) RGDBG(3 + grp, c, 2);
         mbar_wait(&acc_full[ac], (c / kRgNAcc) & 1u);
+        if (m == 0) RGDBG(3 + grp, c, 3);
         if (m == 0 && grp == 0) TRACE(5, c);
         tc_fence_after();
         const uint32_t d1 = tbase + lane_addr + kRgTmemAcc + ac * 2 * kRgN, d2 = d1 + kRgN;
         const int k0 = (kc * kt_per + t) * kRgNT;
 #pragma unroll 1
         for (int hh = 0; hh < 2; ++hh) {
-          const uint32_t cw = 2 * c + hh;
-          const int sw = cw % kRgNW;
+          const uint32_t u = (c >> 1) * 2 + hh;               // half tile index within this group
+          const int sw = grp * kRgNWG + (int)(u % kRgNWG);
           // D1 = [Fr Rr | Fr Ri], D2 = [Fi Rr | Fi Ri]: this half's 4 x 16 columns, one wait
           uint32_t dd[64];
           tmem_ld8_raw(d1 + 16 * hh, dd);
@@ -1804,7 +1862,9 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
           const float* ai = ar + 16;                                    // Fr Ri
           const float* br = ar + 32;                                    // Fi Rr
           const float* bi = ar + 48;                                    // Fi Ri
-          mbar_wait(&wg_full[sw], (cw / kRgNW) & 1u);
+          if (m == 0) RGDBG(3 + grp, c, 4 + hh);
+          mbar_wait(&wg_full[sw], (u / kRgNWG) & 1u);
+          if (m == 0) RGDBG(3 + grp, c, 6 + hh);
           uint8_t* sbox = rg_smem + kRgOffWG + sw * kRgStWG;
           if (valid) {
             const uint8_t* sw8 = sbox + m * 128;
@@ -1855,7 +1915,9 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
       // combine the two groups' partial dots (fixed order: group 0 + group 1)
       float2* sd = sdot + (item & 1u) * kRgM;
       if (grp == 1) sd[m] = dot;
+      if (m == 0) RGDBG(3 + grp, c, 9);
       named_sync(3, 256);
+      if (m == 0) RGDBG(3 + grp, c, 10);
       if (grp == 0 && valid) {
         const float2 d1v = sd[m];
         a.opart[(int64_t)kc * a.n_act + g] = make_float2(dot.x + d1v.x, dot.y + d1v.y);
@@ -2369,4 +2431,21 @@ cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* 
   return cudaGetLastError();
 }
 
+#ifdef WDD_RG_DEBUG
+}  // namespace wdd
+extern "C" int wdd_rg_debug(unsigned* host /* 148 x 8 */) {
+  cudaStream_t s;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return -1;
+  void* d = nullptr;
+  cudaGetSymbolAddress(&d, wdd::g_rgdbg);
+  cudaMemcpyAsync(host, d, sizeof(unsigned) * 148 * 8, cudaMemcpyDeviceToHost, s);
+  for (int i = 0; i < 2000; ++i) {
+    if (cudaStreamQuery(s) == cudaSuccess) return 0;
+    struct timespec ts = {0, 1000000};
+    nanosleep(&ts, nullptr);
+  }
+  return -2;
+}
+namespace wdd {
+#endif
 }  // namespace wdd

@@ -872,7 +872,7 @@ wdd_status wdd_get_info(wdd_plan_t plan, wdd_plan_info* info) {
   i.sigma_px = p.sigma; i.wavelength_A = p.lambda; i.step_A = p.step; i.eps = p.eps;
   i.bytes_G = p.n_act * p.K * 8; i.bytes_bank = i.bytes_G; i.bytes_R = (int64_t)p.n_vx * p.Sy * p.K * 8;
   i.bytes_C = p.chunk_cap * p.K * 4; i.frames_ingested = p.frames_ingested; i.nranks = p.nranks; i.rank = p.rank;
-  i.proj_ctas_per_sm = project_is_lean(p) ? 2 : 1;
+  i.proj_ctas_per_sm = project_occupancy(p);
   *info = i;
   return WDD_OK;
 }

@@ -31,7 +31,8 @@ def main():
         k = lib.wdd_trace_dump(buf, 65536)
     ev = sorted((v >> 16, (v >> 8) & 0xff, v & 0xff) for v in buf[:k] if v)
     t0 = ev[0][0]
-    for t, c, j in ev[:200]:
+    w0 = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+    for t, c, j in ev[w0:w0 + 120]:
         print(f"{(t - t0) / 1000:9.3f} us  {NAMES.get(c, c):18s} {j}")
     for c in sorted(NAMES):
         ts = [t for t, cc, _ in ev if cc == c]
