@@ -110,3 +110,34 @@ def test_live_streaming_cadence(env):
 def test_box_full_scan_one_gpu(env):
     r = _run(env, "box", 16384, 0)
     print("box", _check(r))
+
+
+@pytest.mark.parametrize("accumulator", ["G", "spectrum"])
+def test_live_repeated_scans_deterministic(env, accumulator):
+    # The Live cadence runs the pipelined tensor-core flush (rgemm_kernel): a warp-specialised
+    # kernel with several barrier rings.  Three back-to-back scans on one plan, every readout of
+    # every scan compared bit for bit with the first scan's: a synchronisation error anywhere in
+    # the ring protocol shows up as a changed byte (or a hang / fault) long before it shows up in a
+    # relative-L2 comparison.
+    torch, wdd = env
+    cfg = CONFIGS["live"]
+    pool_n = 4096
+    pool = dense_frames_torch(*sparse_events(SEED, np.arange(pool_n), cfg.Q), cfg.Q, "cuda")
+    plan = wdd.Plan.from_config(cfg, accumulator=accumulator)
+    scans = []
+    for _ in range(3):
+        plan.reset()
+        outs = []
+        done = 0
+        for a in range(0, cfg.S, cfg.batch):
+            plan.ingest(pool[a % pool_n:a % pool_n + cfg.batch], np.arange(a, a + cfg.batch, dtype=np.int32))
+            rows = (a + cfg.batch) // cfg.Sx
+            if rows - done >= cfg.readout_rows:
+                done = rows
+                outs.append(plan.readout().clone())
+        torch.cuda.synchronize()
+        scans.append(torch.stack(outs).cpu().numpy())
+    assert scans[0].shape[0] == cfg.Sy // cfg.readout_rows
+    assert np.all(np.isfinite(scans[0]))
+    for s in scans[1:]:
+        assert np.array_equal(s, scans[0])
