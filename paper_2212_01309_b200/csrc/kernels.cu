@@ -145,7 +145,7 @@ struct ProjCfgT {
   static_assert(tAcc2 + kNB2 * kN <= 512, "TMEM");
   // stage-2 C rows go out through a per-warp shared-memory transpose (512-byte coalesced stores
   // instead of 16-byte pieces of 16 rows) where it fits: Q = 128, L = 32 (C is 1/8 of the bytes)
-  static constexpr bool kCStage = !LEAN && Q == 128 && L == 32 && kM2 == 64;
+  static constexpr bool kCStage = Q == 128 && L == 32 && kM2 == 64;
   static constexpr int kCStageB = kCStage ? 4 * 16 * L * 4 : 0;
   static constexpr int kFixed = (U16 ? 0 : 2 * kSlot) + align_up(kNB2 * 2 * kA2, 1024) + align_up(kB, 1024) + kCStageB + 512;
   // (lean: two CTAs and their per-CTA reservation must share the SM's 228 KB -- 110 KB each leaves
