@@ -771,8 +771,8 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
 
 cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* C, const int32_t* idx,
                            cudaStream_t st) {
-  WDD_PROJ_CASE(32, 8) WDD_PROJ_CASE(32, 16) WDD_PROJ_CASE(32, 32)
-  WDD_PROJ_CASE(64, 8) WDD_PROJ_CASE(64, 16) WDD_PROJ_CASE(64, 32)
+  WDD_PROJ_CASE(32, 8) WDD_PROJ_CASE(32, 16) WDD_PROJ_CASE(32, 24) WDD_PROJ_CASE(32, 32)
+  WDD_PROJ_CASE(64, 8) WDD_PROJ_CASE(64, 16) WDD_PROJ_CASE(64, 24) WDD_PROJ_CASE(64, 32)
   WDD_PROJ_CASE(128, 8) WDD_PROJ_CASE(128, 16) WDD_PROJ_CASE(128, 24) WDD_PROJ_CASE(128, 32)
   WDD_PROJ_CASE(256, 8) WDD_PROJ_CASE(256, 16) WDD_PROJ_CASE(256, 24) WDD_PROJ_CASE(256, 32)
   return cudaErrorInvalidValue;
@@ -802,8 +802,8 @@ extern "C" int wdd_trace_ctas(unsigned long long* host /* 8192 x 5 */) {
 bool project_is_lean(const Plan& p) {
 #define WDD_LEAN_CASE(QQ, LL) \
   if (p.Q == QQ && p.L == LL) return p.dtype == 0 ? ProjCfg<QQ, LL, true>::kLean : ProjCfg<QQ, LL, false>::kLean;
-  WDD_LEAN_CASE(32, 8) WDD_LEAN_CASE(32, 16) WDD_LEAN_CASE(32, 32)
-  WDD_LEAN_CASE(64, 8) WDD_LEAN_CASE(64, 16) WDD_LEAN_CASE(64, 32)
+  WDD_LEAN_CASE(32, 8) WDD_LEAN_CASE(32, 16) WDD_LEAN_CASE(32, 24) WDD_LEAN_CASE(32, 32)
+  WDD_LEAN_CASE(64, 8) WDD_LEAN_CASE(64, 16) WDD_LEAN_CASE(64, 24) WDD_LEAN_CASE(64, 32)
   WDD_LEAN_CASE(128, 8) WDD_LEAN_CASE(128, 16) WDD_LEAN_CASE(128, 24) WDD_LEAN_CASE(128, 32)
   WDD_LEAN_CASE(256, 8) WDD_LEAN_CASE(256, 16) WDD_LEAN_CASE(256, 24) WDD_LEAN_CASE(256, 32)
 #undef WDD_LEAN_CASE
@@ -825,8 +825,8 @@ int project_occupancy(const Plan& p) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, project_kernel<QQ, LL, false>, C::kThreads, C::smem); \
     }                                                                                                \
   }
-  WDD_OCC_CASE(32, 8) WDD_OCC_CASE(32, 16) WDD_OCC_CASE(32, 32)
-  WDD_OCC_CASE(64, 8) WDD_OCC_CASE(64, 16) WDD_OCC_CASE(64, 32)
+  WDD_OCC_CASE(32, 8) WDD_OCC_CASE(32, 16) WDD_OCC_CASE(32, 24) WDD_OCC_CASE(32, 32)
+  WDD_OCC_CASE(64, 8) WDD_OCC_CASE(64, 16) WDD_OCC_CASE(64, 24) WDD_OCC_CASE(64, 32)
   WDD_OCC_CASE(128, 8) WDD_OCC_CASE(128, 16) WDD_OCC_CASE(128, 24) WDD_OCC_CASE(128, 32)
   WDD_OCC_CASE(256, 8) WDD_OCC_CASE(256, 16) WDD_OCC_CASE(256, 24) WDD_OCC_CASE(256, 32)
 #undef WDD_OCC_CASE
@@ -835,8 +835,8 @@ int project_occupancy(const Plan& p) {
 
 size_t project_smem_bytes(int Q, int L) {
 #define WDD_SMEM_CASE(QQ, LL) if (Q == QQ && L == LL) return ProjCfg<QQ, LL, true>::smem;
-  WDD_SMEM_CASE(32, 8) WDD_SMEM_CASE(32, 16) WDD_SMEM_CASE(32, 32)
-  WDD_SMEM_CASE(64, 8) WDD_SMEM_CASE(64, 16) WDD_SMEM_CASE(64, 32)
+  WDD_SMEM_CASE(32, 8) WDD_SMEM_CASE(32, 16) WDD_SMEM_CASE(32, 24) WDD_SMEM_CASE(32, 32)
+  WDD_SMEM_CASE(64, 8) WDD_SMEM_CASE(64, 16) WDD_SMEM_CASE(64, 24) WDD_SMEM_CASE(64, 32)
   WDD_SMEM_CASE(128, 8) WDD_SMEM_CASE(128, 16) WDD_SMEM_CASE(128, 24) WDD_SMEM_CASE(128, 32)
   WDD_SMEM_CASE(256, 8) WDD_SMEM_CASE(256, 16) WDD_SMEM_CASE(256, 24) WDD_SMEM_CASE(256, 32)
 #undef WDD_SMEM_CASE

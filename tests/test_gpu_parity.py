@@ -91,7 +91,7 @@ def test_projection_parity(wdd, torch_cuda, name, n):
     assert r < 1e-5 and mx < 1e-5, (r, mx)
 
 
-@pytest.mark.parametrize("Q,L", [(32, 8), (64, 16), (128, 16), (128, 32), (256, 32), (256, 24)])
+@pytest.mark.parametrize("Q,L", [(32, 8), (64, 16), (64, 24), (128, 16), (128, 32), (256, 32), (256, 24)])
 def test_projection_high_counts_and_float(wdd, torch_cuda, Q, L):
     # counts >= 1024 exercise the second (high-bit) plane; float frames the fp16 residual plane.
     base = CONFIGS["medium"].with_(Q=Q, L=L, Sy=16, Sx=16)
