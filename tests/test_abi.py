@@ -47,3 +47,11 @@ def test_error_path_without_gpu():
     with pytest.raises(w.WddError) as e:
         w.Plan((32, 32), 0.2, (32, 32), 64, 0.0197, 0.02, wiener_eps=0.0)
     assert e.value.name == "WDD_E_ARG"
+
+
+def test_gpu_simulator_builds_and_exports():
+    # the GPU forward simulator (test-input generator, synth/gpu.py) cross-compiles here
+    import ctypes
+    from synth import gpu as sim
+    lib = ctypes.CDLL(sim.build())
+    assert hasattr(lib, "sim_frames")
