@@ -152,6 +152,17 @@ typedef struct {
 } wdd_plan_info;
 wdd_status wdd_get_info(wdd_plan_t plan, wdd_plan_info* info);
 
+/* Conventional (full) WDD of a whole scan with the plan's geometry, probe and eps -- the paper's
+ * comparison method (eq:deconv_mat P:90-95 and eq:extract P:97-106), no
+ * dimensionality reduction: the unitary scan DFT of the 4-D data, per scan frequency v the
+ * inverse detector DFT chi_v and the probe's W_P^v = F^-1(Y_v), the Wiener quotient
+ * chi_v conj(W_P) / (|W_P|^2 + eps) summed over r (R12), and O = conj(F^-1_unitary(x)) (R13;
+ * / sqrt(x_0) if the plan normalises).  frames_dev: DEVICE, S = Sy*Sx frames of Q x Q in the
+ * plan's dtype, in scan order (s = sy*Sx + sx); complex_out_dev: DEVICE, Sy*Sx complex64.
+ * Stream-ordered on `stream`; allocates S*Q*Q*8 bytes of device scratch for the call
+ * (WDD_E_NOMEM if that fails); Q must be even.  Independent of the plan's ingest state. */
+wdd_status wdd_full_wdd(wdd_plan_t plan, const void* frames_dev, void* complex_out_dev, void* stream);
+
 /* Plan tables as the library computed them (host outputs, any may be NULL):
  *   basis  Q x L float64 (Psi[m][n]);  bank  n_act x K complex128 (accumulator order, before
  *   rounding to complex64);  active_v  n_act int32 (accumulator order). */

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("WDD_LIB_OUT") or os.path.join(HERE, "_lib", "libwdd.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "bank.cu", "plan.cpp")]
+SOURCES = [os.path.join(CSRC, f) for f in ("kernels.cu", "bank.cu", "fullwdd.cu", "plan.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("internal.h", "tc.cuh", "fft.cuh")] + [os.path.join(ROOT, "include", "wdd.h")]
 
 NVCC_FLAGS = [

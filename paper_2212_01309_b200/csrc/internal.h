@@ -149,5 +149,8 @@ int project_occupancy(const Plan& p);  // resident projection CTAs per SM (runti
 cudaError_t build_bank(const Plan& p, const double* q_host, const int2* apx_host, int ax_lo, int n_axc, void* W_dev,
                        bool f64);
 constexpr double kPi = 3.14159265358979323846;
+// conventional (full) WDD of a whole scan (fullwdd.cu): frames_dev S x Q x Q in
+// scan order, out_dev Sy x Sx complex64; stream-ordered on p.stream; err receives a message
+wdd_status full_wdd(Plan& p, const void* frames_dev, void* out_dev, char* err, size_t errn);
 
 }  // namespace wdd

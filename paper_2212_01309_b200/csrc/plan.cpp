@@ -899,6 +899,19 @@ wdd_status wdd_get_tables(wdd_plan_t plan, double* basis, double* bank, int32_t*
   return WDD_OK;
 }
 
+wdd_status wdd_full_wdd(wdd_plan_t plan, const void* frames_dev, void* complex_out_dev, void* stream) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (!frames_dev || !complex_out_dev) return fail(WDD_E_ARG, "NULL buffer");
+  if (p.capturing) return fail(WDD_E_STATE, "wdd_full_wdd cannot be captured");
+  CUDA_TRY(cudaSetDevice(p.device));
+  use_stream(p, reinterpret_cast<cudaStream_t>(stream));
+  char msg[256] = {0};
+  const wdd_status s = full_wdd(p, frames_dev, complex_out_dev, msg, sizeof msg);
+  if (s != WDD_OK) return fail(s, "%s", msg);
+  return WDD_OK;
+}
+
 wdd_status wdd_project(wdd_plan_t plan, const void* frames_dev, int64_t n, void* C_out_dev, void* stream) {
   if (check_plan(plan)) return WDD_E_ARG;
   Plan& p = *P(plan);

@@ -67,6 +67,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "wdd_readout_host": [P, V],
             "wdd_destroy": [P],
             "wdd_get_accumulator": [P, V, ctypes.POINTER(I32), ctypes.POINTER(I64)],
+            "wdd_full_wdd": [P, V, V, V],
             "wdd_reset": [P],
             "wdd_nccl_get_unique_id": [ctypes.c_char_p],
             "wdd_set_comm": [P, I32, I32, ctypes.c_char_p],
@@ -257,6 +258,15 @@ class Plan:
         _check(self._lib.wdd_get_tables(self._h, basis.ctypes.data, None if W is None else W.ctypes.data,
                                         act.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
         return basis, W, act
+
+    def full_wdd(self, frames, out=None, stream=None):
+        """Conventional (full) WDD of a whole scan (frames: (S, Q, Q) device tensor in scan order)."""
+        import torch
+        self._check_frames(frames, self.Sy * self.Sx, True)
+        if out is None:
+            out = torch.empty((self.Sy, self.Sx), dtype=torch.complex64, device=frames.device)
+        _check(self._lib.wdd_full_wdd(self._h, _ptr(frames), _ptr(out), _stream(stream)))
+        return out
 
     def project(self, frames, out=None, stream=None):
         import torch
