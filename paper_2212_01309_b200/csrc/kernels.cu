@@ -130,18 +130,25 @@ struct ProjCfgT {
   // 128 bytes, m-blocks at kSBO2, so the epilogue stores 8 values of a frame row as one 16-byte word
   static constexpr uint32_t kSBO2 = (kK2 / 8) * 128;
   static constexpr int kA2 = (kM2 / 8) * (int)kSBO2;       // one A2 plane
-  static constexpr int kAcc1 = kN;                        // per acc1 slot (both count planes accumulate here)
+  // Lean variant with L >= 24: the Psi_hi and Psi_lo products accumulate into the same fp32
+  // accumulator (two MMAs with N = L: the sum the epilogue would otherwise form, done by the
+  // tensor core), which halves the accumulators' TMEM and the epilogue's loads (Large: 141 -> 123
+  // us per 16k frames).  Elsewhere one MMA with N = 2L and the sum in the epilogue measured faster
+  // (the extra MMAs cost the full Q = 256 kernel ~10%); M = 128 would also need N >= 16 for L = 8.
+  static constexpr bool kSplitAcc = LEAN && L >= 24;
+  static constexpr int kNacc = kSplitAcc ? L : kN;        // accumulator columns (both stages)
+  static constexpr int kAcc1 = kNacc;                     // per acc1 slot (both count planes accumulate here)
   static constexpr int kNB2 = LEAN ? 1 : 2;               // stage-2 A2 images / accumulators in flight
   // acc1 ring: 4 deep unless TMEM (A ring + plane-1 buffers + acc1 + acc2 images) would exceed 512 columns
   // (lean: 2, or 1 where two would not leave both CTAs of an SM their 256 TMEM columns)
-  static constexpr int kNAcc = LEAN ? ((kNA + kNGroups) * (Q >= 64 ? 32 : Q / 2) + (2 + kNB2) * 2 * L > 256 ? 1 : 2)
-                                    : ((kNA + kNGroups) * (Q >= 64 ? 32 : Q / 2) + (4 + kNB2) * 2 * L > 512 ? 2 : 4);
+  static constexpr int kNAcc = LEAN ? ((kNA + kNGroups) * (Q >= 64 ? 32 : Q / 2) + (2 + kNB2) * kNacc > 256 ? 1 : 2)
+                                    : ((kNA + kNGroups) * (Q >= 64 ? 32 : Q / 2) + (4 + kNB2) * kNacc > 512 ? 2 : 4);
   static constexpr int kACols = kKC / 2;                  // TMEM columns of one A1 chunk (fp16 pairs)
   static constexpr int tA = 0;                            // TMEM column map
   static constexpr int tP1 = tA + kNA * kACols;          // one plane-1 buffer per converter group
   static constexpr int tAcc1 = tP1 + kNGroups * kACols;
   static constexpr int tAcc2 = tAcc1 + kNAcc * kAcc1;
-  static constexpr int kTmemCols = pow2_cols(tAcc2 + kNB2 * kN);
+  static constexpr int kTmemCols = pow2_cols(tAcc2 + kNB2 * kNacc);
   static_assert(tAcc2 + kNB2 * kN <= 512, "TMEM");
   // stage-2 C rows go out through a per-warp shared-memory transpose (512-byte coalesced stores
   // instead of 16-byte pieces of 16 rows) where it fits: Q = 128, L = 32 (C is 1/8 of the bytes)
@@ -162,7 +169,7 @@ struct ProjCfgT {
   static constexpr int kBars = 2 * kNS + 2 * kNA + 2 * kNAcc + 3 * kNB2 + 3;
   static constexpr int off_misc = off_bar + 8 * kBars;    // meta[kNS+kNA], wflag[2 groups][2][4], tmem slot
   static constexpr int smem = off_misc + 4 * (kNS + kNA) + 64 + 16;
-  static constexpr int kTmemUsed = tAcc2 + kNB2 * kN;
+  static constexpr int kTmemUsed = tAcc2 + kNB2 * kNacc;
   static_assert((kNGroups == 1 || kNS % 2 == 0) && kNA % 2 == 0, "even rings: converter group = job parity");
   static_assert(kG2 >= 1, "group");
   static_assert(smem <= 232448, "shared memory");
@@ -298,7 +305,8 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
   if (warp == 0) {
     // ================= stage-1 MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16(128, Cfg::kN);
+      constexpr uint32_t idesc = idesc_f16(128, Cfg::kNacc);
+      constexpr uint64_t kLoOff = (uint64_t)((L / 8) * 128) >> 4;   // Psi_lo rows of the B image (descriptor units)
       const uint32_t ring0 = smem_u32(ring), p10 = smem_u32(sP1), b0 = smem_u32(sB);
       mbar_wait(b_full, 0);
       uint32_t slot = 0, sphase = 0, tile = 0, job = 0;
@@ -321,6 +329,11 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
               const uint32_t accum = (c > 0 || kk > 0) ? 1u : 0u;
               if constexpr (U16) mma_f16_ts(acc, tbase + Cfg::tA + slot * Cfg::kACols + kk * 8, bd, idesc, accum);
               else mma_f16_ss(acc, smem_desc_noswz(ring0 + slot * Cfg::kSlot + 2 * kk * kLBO, kLBO, 128), bd, idesc, accum);
+              if constexpr (Cfg::kSplitAcc) {
+                if constexpr (U16) mma_f16_ts(acc, tbase + Cfg::tA + slot * Cfg::kACols + kk * 8, bd + kLoOff, idesc, 1u);
+                else mma_f16_ss(acc, smem_desc_noswz(ring0 + slot * Cfg::kSlot + 2 * kk * kLBO, kLBO, 128), bd + kLoOff,
+                                idesc, 1u);
+              }
             }
             if (has_p1) {
 #pragma unroll
@@ -328,6 +341,11 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
                 const uint64_t bd = smem_desc_noswz(b0 + (c * (Cfg::kKC / 8) + 2 * kk) * Cfg::kLBO_B, Cfg::kLBO_B, 128);
                 if constexpr (U16) mma_f16_ts(acc, tbase + Cfg::tP1 + grp * Cfg::kACols + kk * 8, bd, idesc, 1u);
                 else mma_f16_ss(acc, smem_desc_noswz(p10 + grp * Cfg::kSlot + 2 * kk * kLBO, kLBO, 128), bd, idesc, 1u);
+                if constexpr (Cfg::kSplitAcc) {
+                  if constexpr (U16) mma_f16_ts(acc, tbase + Cfg::tP1 + grp * Cfg::kACols + kk * 8, bd + kLoOff, idesc, 1u);
+                  else mma_f16_ss(acc, smem_desc_noswz(p10 + grp * Cfg::kSlot + 2 * kk * kLBO, kLBO, 128), bd + kLoOff,
+                                  idesc, 1u);
+                }
               }
               mma_commit(&p1_empty[grp]);
             }
@@ -341,13 +359,14 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
   } else if (warp == 1) {
     // ================= stage-2 MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_f16(Cfg::kM2, Cfg::kN, 0, /*a_major=MN*/ 1, 0);
+      constexpr uint32_t idesc = idesc_f16(Cfg::kM2, Cfg::kNacc, 0, /*a_major=MN*/ 1, 0);
+      constexpr uint64_t kLoOff = (uint64_t)((L / 8) * 128) >> 4;
       const uint32_t a20 = smem_u32(sA2), b0 = smem_u32(sB);
       mbar_wait(b_full, 0);
       uint32_t c2 = 0;
       for (int64_t gi = 0; gi < my_groups; ++gi) {
         const uint32_t gb = (uint32_t)(gi % Cfg::kNB2);
-        const uint32_t acc2 = tbase + Cfg::tAcc2 + gb * Cfg::kN;
+        const uint32_t acc2 = tbase + Cfg::tAcc2 + gb * Cfg::kNacc;
         for (int h = 0; h < Cfg::kTPF; ++h, ++c2) {
           const uint32_t ab = c2 % Cfg::kNB2;
           mbar_wait(&a2_full[ab], (c2 / Cfg::kNB2) & 1u);
@@ -362,6 +381,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
               const uint64_t ad = smem_desc_noswz(a2 + plane * Cfg::kA2 + kk * 256, 128, Cfg::kSBO2);
               const uint64_t bd = smem_desc_noswz(b0 + (h * (Cfg::kK2 / 8) + 2 * kk) * Cfg::kLBO_B, Cfg::kLBO_B, 128);
               mma_f16_ss(acc2, ad, bd, idesc, (h > 0 || plane > 0 || kk > 0) ? 1u : 0u);
+              if constexpr (Cfg::kSplitAcc) mma_f16_ss(acc2, ad, bd + kLoOff, idesc, 1u);
             }
           }
           mma_commit(&s2_done[ab]);
@@ -555,8 +575,10 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
     const int m2 = Cfg::kM2 == 128 ? row : (lane < 16 ? quad * 16 + lane : 1 << 20);
     auto stage2_epilogue = [&](int64_t frame0, int64_t gi) {
       const uint32_t gb = (uint32_t)(gi % Cfg::kNB2);
-      float d[Cfg::kN];
-      tmem_ld_cols<Cfg::kN>(tbase + Cfg::tAcc2 + gb * Cfg::kN + lane_addr, d);
+      float d[Cfg::kNacc];
+      tmem_ld_cols<Cfg::kNacc>(tbase + Cfg::tAcc2 + gb * Cfg::kNacc + lane_addr, d);
+      // value of accumulator column b (the hi + lo sum: formed by the MMAs, or here for L = 8)
+      auto dv = [&](int b) { if constexpr (Cfg::kSplitAcc) return d[b]; else return d[b] + d[(L + b) % Cfg::kNacc]; };
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc2_empty[gb]);
@@ -571,8 +593,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
 #pragma unroll
           for (int b = 0; b < L; b += 4)
             *reinterpret_cast<float4*>(stg + lane * L + (((b >> 2) ^ (lane & 7)) << 2)) =
-                make_float4((d[b] + d[L + b]) * a.sc2, (d[b + 1] + d[L + b + 1]) * a.sc2,
-                            (d[b + 2] + d[L + b + 2]) * a.sc2, (d[b + 3] + d[L + b + 3]) * a.sc2);
+                make_float4(dv(b) * a.sc2, dv(b + 1) * a.sc2, dv(b + 2) * a.sc2, dv(b + 3) * a.sc2);
         }
         __syncwarp();
         const int fw = (quad * 16) / L;                      // the warp's frame (warp-uniform)
@@ -593,8 +614,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
         float* dst = a.C + (a.idx ? (int64_t)__ldg(a.idx + fg) : fg) * K + aa * L;
 #pragma unroll
         for (int b = 0; b < L; b += 4) {
-          float4 v = make_float4((d[b] + d[L + b]) * a.sc2, (d[b + 1] + d[L + b + 1]) * a.sc2,
-                                 (d[b + 2] + d[L + b + 2]) * a.sc2, (d[b + 3] + d[L + b + 3]) * a.sc2);
+          float4 v = make_float4(dv(b) * a.sc2, dv(b + 1) * a.sc2, dv(b + 2) * a.sc2, dv(b + 3) * a.sc2);
           *reinterpret_cast<float4*>(dst + b) = v;
         }
       }
@@ -614,11 +634,14 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
         mbar_wait(&acc1_full[s1], (tile / Cfg::kNAcc) & 1u);
         if (et == 0) TRACE(8, tile);
         tc_fence_after();
-        float acc[Cfg::kN];
+        float acc[Cfg::kNacc];
         float t[L];
-        tmem_ld_cols<Cfg::kN>(tbase + Cfg::tAcc1 + s1 * Cfg::kAcc1 + lane_addr, acc);
+        tmem_ld_cols<Cfg::kNacc>(tbase + Cfg::tAcc1 + s1 * Cfg::kAcc1 + lane_addr, acc);
 #pragma unroll
-        for (int q = 0; q < L; ++q) t[q] = (acc[q] + acc[L + q]) * a.sc1;
+        for (int q = 0; q < L; ++q) {
+          if constexpr (Cfg::kSplitAcc) t[q] = acc[q] * a.sc1;
+          else t[q] = (acc[q] + acc[(L + q) % Cfg::kNacc]) * a.sc1;
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc1_empty[s1]);
