@@ -355,3 +355,33 @@ def test_back_to_back_acquisitions_same_plan(wdd, torch_cuda):
     for o in outs:
         assert rel(o.cpu().numpy(), ref) < TOL
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
+@pytest.mark.parametrize("accumulator", ["G", "spectrum"])
+def test_multi_plan_row_shards_sum_to_single_plan(wdd, torch_cuda, accumulator):
+    # SURVEY §4 item 5, "multi-GPU without a cluster": three plans on one device ingest disjoint
+    # row shards (bench.py's sharding); the sum of their accumulators and of their spectra -- what
+    # the NCCL combine of wdd_readout adds up -- equals one plan that ingested everything
+    # (linearity of Algorithm 2).
+    torch = torch_cuda
+    cfg = CONFIGS["medium"].with_(Sy=32, Sx=32)
+    idx = np.arange(cfg.S)
+    fr_dev = _to_dev(torch, _frames(cfg, idx))
+    whole = wdd.Plan.from_config(cfg, accumulator=accumulator)
+    _ingest_batches(torch, whole, fr_dev, idx, 100)
+    G1, act = whole.get_accumulator()
+    img1 = whole.readout()
+    Gs, spec = 0, 0
+    for rows in np.array_split(np.arange(cfg.Sy), 3):
+        sh = (rows[:, None] * cfg.Sx + np.arange(cfg.Sx)[None, :]).reshape(-1)
+        p = wdd.Plan.from_config(cfg, accumulator=accumulator)
+        _ingest_batches(torch, p, fr_dev[sh[0]:sh[-1] + 1], sh, 77)      # (a shard is a run of rows)
+        G, a2 = p.get_accumulator()
+        assert np.array_equal(a2, act)
+        Gs = Gs + G.cpu().numpy().astype(np.complex128)
+        im = p.readout().cpu().numpy().astype(np.complex128)
+        spec = spec + np.fft.fft2(np.conj(im), norm="ortho")
+    torch.cuda.synchronize()
+    assert rel(Gs, G1.cpu().numpy()) < 1e-5
+    spec1 = np.fft.fft2(np.conj(img1.cpu().numpy().astype(np.complex128)), norm="ortho")
+    assert rel(spec, spec1) < 1e-5
