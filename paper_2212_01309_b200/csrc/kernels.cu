@@ -1700,8 +1700,8 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
       }
     }
   } else if (warp == 2 || warp == 3) {
-    // ---------------- converters: item (flush row r, 8-coefficient group q8): 64 bytes of R in,
-    // 16 bytes per plane out, in place (every item is read before any is written)
+    // ---------------- converters: thread = flush row r, groups q8 = 0..3 of 8 coefficients: 64 bytes
+    // of R in, 16 bytes per plane out per group, in place (every row is read before any is written)
     const int ct = tid - 64;
     const int swz_mask = a.row0 >= 0 ? 7 : 0;              // TMA rows arrive SWIZZLE_128B
     uint32_t c = 0;
@@ -1716,7 +1716,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
         float4 v[4][4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int item = ct + 64 * i, r = item >> 2, q8 = item & 3;
+          const int r = ct, q8 = i;                        // a warp phase = 8 rows, one group: no bank conflicts
           const int h = q8 >> 1;                             // 16-coefficient half
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -1728,7 +1728,7 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
         named_sync(2, 64);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int item = ct + 64 * i, r = item >> 2, q8 = item & 3;
+          const int r = ct, q8 = i;                        // a warp phase = 8 rows, one group: no bank conflicts
           if (r < kr) {
             uint32_t rh[4], rl[4], ih[4], il[4];
 #pragma unroll
