@@ -1988,6 +1988,8 @@ int colfft_tiles(const Plan& p) { return (p.K >> colfft_logkt(p)) / colfft_tpc(p
 // k-chunks of the pipelined GEMM flush: enough work items for ~4 per CTA
 static int rgemm_nkc(const Plan& p) {
   const int KT = p.K / kRgNT;
+  static const int env = [] { const char* e = std::getenv("WDD_RG_NKC"); return e ? std::atoi(e) : 0; }();
+  if (env > 0 && KT % env == 0) return env;
   int nkc = 1;
   while (nkc * 2 <= KT && KT % (nkc * 2) == 0 && (int64_t)p.rg_items.size() * nkc < 4 * p.sm_count) nkc *= 2;
   return nkc;
