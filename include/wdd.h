@@ -159,8 +159,9 @@ wdd_status wdd_get_info(wdd_plan_t plan, wdd_plan_info* info);
  * chi_v conj(W_P) / (|W_P|^2 + eps) summed over r (R12), and O = conj(F^-1_unitary(x)) (R13;
  * / sqrt(x_0) if the plan normalises).  frames_dev: DEVICE, S = Sy*Sx frames of Q x Q in the
  * plan's dtype, in scan order (s = sy*Sx + sx); complex_out_dev: DEVICE, Sy*Sx complex64.
- * Stream-ordered on `stream`; allocates S*Q*Q*8 bytes of device scratch for the call
- * (WDD_E_NOMEM if that fails); Q must be even.  Independent of the plan's ingest state. */
+ * Stream-ordered on `stream`; the first call allocates 2*S*Q*Q*8 bytes of device scratch and the
+ * cuFFT plans, kept by the plan until wdd_destroy (WDD_E_NOMEM if the scratch is not available);
+ * Q must be even.  Independent of the plan's ingest state. */
 wdd_status wdd_full_wdd(wdd_plan_t plan, const void* frames_dev, void* complex_out_dev, void* stream);
 
 /* Plan tables as the library computed them (host outputs, any may be NULL):

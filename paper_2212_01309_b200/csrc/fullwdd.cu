@@ -9,7 +9,8 @@
 // |W_P|^2, so only the pre-modulation (-1)^(my+mx) is applied (folded into the frame load for
 // chi).  The transforms are cuFFT (this workload is not the reduced method's path); the frame
 // load, Y_v, the Wiener combine + sum and the image step are kernels here.  Memory: S x Q^2
-// complex64 for Gf (Medium 2.1 GB, Large 8.6 GB) plus a batch of Y_v.
+// complex64 twice (Gf in pixel-major and scan-frequency-major order: Medium 4.3 GB, Large 17 GB)
+// plus a batch of Y_v.
 #include <cuda_runtime.h>
 #include <cufft.h>
 
@@ -25,13 +26,41 @@
 namespace wdd {
 namespace {
 
+// frames [s][m] -> (-1)^(my+mx) I as complex64, transposed to [m][s] (pixel-major: the scan DFT of
+// each detector pixel is then a contiguous batch), through 32 x 32 shared-memory tiles
 template <typename T>
-__global__ void fw_load_kernel(const T* __restrict__ frames, int64_t S, int Q, float2* __restrict__ A) {
-  const int64_t n = S * Q * Q;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int m = (int)(e % (Q * Q));
-    const int sgn = (((m / Q) + (m % Q)) & 1) ? -1 : 1;
-    A[e] = make_float2((float)frames[e] * (float)sgn, 0.f);
+__global__ void fw_load_kernel(const T* __restrict__ frames, int64_t S, int QQ, int Q, float2* __restrict__ A) {
+  __shared__ float tile[32][33];
+  const int64_t s0 = (int64_t)blockIdx.y * 32;
+  const int m0 = blockIdx.x * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t s = s0 + dy;
+    const int m = m0 + threadIdx.x;
+    tile[dy][threadIdx.x] = (s < S && m < QQ) ? (float)frames[s * QQ + m] : 0.f;
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int m = m0 + dy;
+    const int64_t s = s0 + threadIdx.x;
+    if (m < QQ && s < S) {
+      const float sg = (((m / Q) + (m % Q)) & 1) ? -1.f : 1.f;
+      A[(int64_t)m * S + s] = make_float2(tile[threadIdx.x][dy] * sg, 0.f);
+    }
+  }
+}
+
+// complex64 [rows][cols] -> [cols][rows], 32 x 32 tiles
+__global__ void fw_transpose_kernel(const float2* __restrict__ in, int64_t rows, int64_t cols, float2* __restrict__ out) {
+  __shared__ float2 tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t r = r0 + dy, c = c0 + threadIdx.x;
+    tile[dy][threadIdx.x] = (r < rows && c < cols) ? in[r * cols + c] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int64_t c = c0 + dy, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) out[c * rows + r] = tile[threadIdx.x][dy];
   }
 }
 
@@ -114,90 +143,114 @@ __global__ void fw_image_kernel(float2* __restrict__ out, int64_t S, float scale
 
 }  // namespace
 
+// Workspace cached in the plan across calls (the cuFFT plans and the 2 x S x Q^2 scratch cost
+// milliseconds to create).
+struct FullWddWork {
+  float2 *A = nullptr, *B = nullptr, *Y = nullptr, *spec = nullptr;
+  int32_t* dv = nullptr;
+  cufftHandle scan = 0, det = 0, yplan = 0, img = 0;
+  bool ok = false;
+};
+
+void full_wdd_release(Plan& p) {
+  FullWddWork* w = p.fw;
+  if (!w) return;
+  if (w->scan) cufftDestroy(w->scan);
+  if (w->det) cufftDestroy(w->det);
+  if (w->yplan) cufftDestroy(w->yplan);
+  if (w->img) cufftDestroy(w->img);
+  cudaFree(w->A);
+  cudaFree(w->B);
+  cudaFree(w->Y);
+  cudaFree(w->spec);
+  cudaFree(w->dv);
+  delete w;
+  p.fw = nullptr;
+}
+
+static constexpr int kFwYBatch = 512;                   // scan frequencies per Y_v batch
+
+static wdd_status fw_prepare(Plan& p, char* err, size_t errn) {
+  if (p.fw && p.fw->ok) return WDD_OK;
+  full_wdd_release(p);
+  FullWddWork* w = new FullWddWork();
+  p.fw = w;
+  const int Q = p.Q;
+  const int64_t S = p.S, QQ = (int64_t)Q * Q;
+  if (cudaMalloc(&w->A, (size_t)S * QQ * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc(&w->B, (size_t)S * QQ * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc(&w->Y, (size_t)kFwYBatch * QQ * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc(&w->spec, (size_t)S * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc(&w->dv, p.active_v.size() * sizeof(int32_t)) != cudaSuccess) {
+    std::snprintf(err, errn, "full WDD: %.1f GB of device scratch not available", 2.0 * S * QQ * 8 / 1e9);
+    full_wdd_release(p);
+    return WDD_E_NOMEM;
+  }
+  int sdims[2] = {p.Sy, p.Sx}, ddims[2] = {Q, Q};
+  if (cudaMemcpy(w->dv, p.active_v.data(), p.active_v.size() * sizeof(int32_t), cudaMemcpyHostToDevice) !=
+          cudaSuccess ||
+      cufftPlanMany(&w->scan, 2, sdims, nullptr, 1, (int)S, nullptr, 1, (int)S, CUFFT_C2C, (int)QQ) != CUFFT_SUCCESS ||
+      cufftPlanMany(&w->det, 2, ddims, nullptr, 1, (int)QQ, nullptr, 1, (int)QQ, CUFFT_C2C, (int)S) != CUFFT_SUCCESS ||
+      cufftPlanMany(&w->yplan, 2, ddims, nullptr, 1, (int)QQ, nullptr, 1, (int)QQ, CUFFT_C2C, kFwYBatch) !=
+          CUFFT_SUCCESS ||
+      cufftPlan2d(&w->img, p.Sy, p.Sx, CUFFT_C2C) != CUFFT_SUCCESS) {
+    std::snprintf(err, errn, "full WDD: cuFFT plan creation failed");
+    full_wdd_release(p);
+    return WDD_E_CUDA;
+  }
+  w->ok = true;
+  return WDD_OK;
+}
+
 wdd_status full_wdd(Plan& p, const void* frames_dev, void* out_dev, char* err, size_t errn) {
   auto fail = [&](const char* what) {
     std::snprintf(err, errn, "full WDD: %s", what);
     return WDD_E_CUDA;
   };
   if ((p.Q & 1) || p.S > INT32_MAX) { std::snprintf(err, errn, "full WDD needs even Q"); return WDD_E_ARG; }
+  const wdd_status pr = fw_prepare(p, err, errn);
+  if (pr != WDD_OK) return pr;
+  FullWddWork* w = p.fw;
   const int Q = p.Q;
   const int64_t S = p.S, QQ = (int64_t)Q * Q;
   cudaStream_t st = p.stream;
-  float2* A = nullptr;
-  float2* Y = nullptr;
-  float2* spec = nullptr;
-  int32_t* dv = nullptr;
-  cufftHandle scan_plan = 0, det_plan = 0, img_plan = 0;
-  const int nb = 512;                                   // scan frequencies per Y_v batch
-  wdd_status rc = WDD_OK;
-  do {
-    if (cudaMallocAsync(&A, (size_t)S * QQ * sizeof(float2), st) != cudaSuccess) { rc = WDD_E_NOMEM; break; }
-    if (cudaMallocAsync(&Y, (size_t)nb * QQ * sizeof(float2), st) != cudaSuccess) { rc = WDD_E_NOMEM; break; }
-    if (cudaMallocAsync(&spec, (size_t)S * sizeof(float2), st) != cudaSuccess ||
-        cudaMallocAsync(&dv, p.active_v.size() * sizeof(int32_t), st) != cudaSuccess) { rc = WDD_E_NOMEM; break; }
-    if (cudaMemcpyAsync(dv, p.active_v.data(), p.active_v.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st) !=
-            cudaSuccess ||
-        cudaMemsetAsync(spec, 0, (size_t)S * sizeof(float2), st) != cudaSuccess) { rc = fail("upload"); break; }
-    // (a) frames -> (-1)^m I, scan DFT per detector pixel (stride Q^2 between scan positions)
-    const int blocks = (int)std::min<int64_t>((S * QQ + 255) / 256, 148 * 32);
-    if (p.dtype == 0) fw_load_kernel<uint16_t><<<blocks, 256, 0, st>>>(static_cast<const uint16_t*>(frames_dev), S, Q, A);
-    else fw_load_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(frames_dev), S, Q, A);
-    int sdims[2] = {p.Sy, p.Sx};
-    if (cufftPlanMany(&scan_plan, 2, sdims, sdims, (int)QQ, 1, sdims, (int)QQ, 1, CUFFT_C2C, (int)QQ) != CUFFT_SUCCESS ||
-        cufftSetStream(scan_plan, st) != CUFFT_SUCCESS ||
-        cufftExecC2C(scan_plan, reinterpret_cast<cufftComplex*>(A), reinterpret_cast<cufftComplex*>(A),
-                     CUFFT_FORWARD) != CUFFT_SUCCESS) { rc = fail("scan FFT"); break; }
-    // (b) chi_v for every v: inverse detector DFT of each scan-frequency row (the 1/sqrt(S) of
-    // the unitary scan DFT is folded into the combine scale)
-    int ddims[2] = {Q, Q};
-    const int64_t vb = 4096;
-    if (cufftPlanMany(&det_plan, 2, ddims, nullptr, 1, (int)QQ, nullptr, 1, (int)QQ, CUFFT_C2C, (int)vb) !=
-            CUFFT_SUCCESS || cufftSetStream(det_plan, st) != CUFFT_SUCCESS) { rc = fail("detector plan"); break; }
-    for (int64_t v0 = 0; v0 < S && rc == WDD_OK; v0 += vb) {
-      cufftHandle ph = det_plan, tmp = 0;
-      if (S - v0 < vb) {
-        if (cufftPlanMany(&tmp, 2, ddims, nullptr, 1, (int)QQ, nullptr, 1, (int)QQ, CUFFT_C2C, (int)(S - v0)) !=
-                CUFFT_SUCCESS || cufftSetStream(tmp, st) != CUFFT_SUCCESS) { rc = fail("detector plan"); break; }
-        ph = tmp;
-      }
-      if (cufftExecC2C(ph, reinterpret_cast<cufftComplex*>(A + v0 * QQ), reinterpret_cast<cufftComplex*>(A + v0 * QQ),
-                       CUFFT_INVERSE) != CUFFT_SUCCESS) rc = fail("detector FFT");
-      if (tmp) cufftDestroy(tmp);
-    }
-    if (rc != WDD_OK) break;
-    // (c) W_P for the active v in batches, Wiener combine and sum
-    cufftHandle yplan = 0;
-    if (cufftPlanMany(&yplan, 2, ddims, nullptr, 1, (int)QQ, nullptr, 1, (int)QQ, CUFFT_C2C, nb) != CUFFT_SUCCESS ||
-        cufftSetStream(yplan, st) != CUFFT_SUCCESS) { rc = fail("probe plan"); break; }
-    const double cph = kPi * p.lambda * p.defocus;
-    const double chi_s = 1.0 / ((double)Q * std::sqrt((double)S)), wp_s = 1.0 / Q;   // unitary scales
-    for (int64_t a = 0; a < p.n_act && rc == WDD_OK; a += nb) {
-      const int m = (int)std::min<int64_t>(nb, p.n_act - a);
-      fw_y_kernel<<<dim3((unsigned)((QQ + 255) / 256), nb), 256, 0, st>>>(dv + a, m, Q, p.dq, p.qa * p.qa, cph, p.Sy,
-                                                                         p.Sx, p.step, Y);
-      if (cufftExecC2C(yplan, reinterpret_cast<cufftComplex*>(Y), reinterpret_cast<cufftComplex*>(Y), CUFFT_INVERSE) !=
-          CUFFT_SUCCESS) { rc = fail("probe FFT"); break; }
-      fw_combine_kernel<<<m, 256, 0, st>>>(A, Y, dv + a, Q, chi_s, wp_s, p.eps, spec);
-    }
-    cufftDestroy(yplan);
-    if (rc != WDD_OK) break;
-    // (d) O = conj(F^-1_unitary(x)) [/ sqrt(x_0)]
-    if (cufftPlan2d(&img_plan, p.Sy, p.Sx, CUFFT_C2C) != CUFFT_SUCCESS || cufftSetStream(img_plan, st) != CUFFT_SUCCESS ||
-        cufftExecC2C(img_plan, reinterpret_cast<cufftComplex*>(spec), static_cast<cufftComplex*>(out_dev),
-                     CUFFT_INVERSE) != CUFFT_SUCCESS) { rc = fail("image FFT"); break; }
-    fw_image_kernel<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(static_cast<float2*>(out_dev), S,
-                                                                  (float)(1.0 / std::sqrt((double)S)), spec,
-                                                                  p.normalize);
-    if (cudaGetLastError() != cudaSuccess) rc = fail("kernel launch");
-  } while (false);
-  if (scan_plan) cufftDestroy(scan_plan);
-  if (det_plan) cufftDestroy(det_plan);
-  if (img_plan) cufftDestroy(img_plan);
-  cudaFreeAsync(A, st);
-  cudaFreeAsync(Y, st);
-  cudaFreeAsync(spec, st);
-  cudaFreeAsync(dv, st);
-  return rc;
+  if (cufftSetStream(w->scan, st) != CUFFT_SUCCESS || cufftSetStream(w->det, st) != CUFFT_SUCCESS ||
+      cufftSetStream(w->yplan, st) != CUFFT_SUCCESS || cufftSetStream(w->img, st) != CUFFT_SUCCESS)
+    return fail("cuFFT stream");
+  if (cudaMemsetAsync(w->spec, 0, (size_t)S * sizeof(float2), st) != cudaSuccess) return fail("memset");
+  // (a) frames -> (-1)^m I transposed to pixel-major B[m][s]; scan DFT of every pixel (contiguous
+  // batches); transpose back to A[v][m] for the detector transforms
+  const dim3 tb(32, 8);
+  const dim3 tg1((unsigned)((QQ + 31) / 32), (unsigned)((S + 31) / 32));
+  if (p.dtype == 0) fw_load_kernel<uint16_t><<<tg1, tb, 0, st>>>(static_cast<const uint16_t*>(frames_dev), S, (int)QQ, Q, w->B);
+  else fw_load_kernel<float><<<tg1, tb, 0, st>>>(static_cast<const float*>(frames_dev), S, (int)QQ, Q, w->B);
+  if (cufftExecC2C(w->scan, reinterpret_cast<cufftComplex*>(w->B), reinterpret_cast<cufftComplex*>(w->B),
+                   CUFFT_FORWARD) != CUFFT_SUCCESS) return fail("scan FFT");
+  const dim3 tg2((unsigned)((S + 31) / 32), (unsigned)((QQ + 31) / 32));
+  fw_transpose_kernel<<<tg2, tb, 0, st>>>(w->B, QQ, S, w->A);
+  // (b) chi_v for every v: inverse detector DFT of each scan-frequency row (the 1/sqrt(S) of the
+  // unitary scan DFT is folded into the combine scale)
+  if (cufftExecC2C(w->det, reinterpret_cast<cufftComplex*>(w->A), reinterpret_cast<cufftComplex*>(w->A),
+                   CUFFT_INVERSE) != CUFFT_SUCCESS) return fail("detector FFT");
+  // (c) W_P for the active v in batches, Wiener combine and sum
+  const double cph = kPi * p.lambda * p.defocus;
+  const double chi_s = 1.0 / ((double)Q * std::sqrt((double)S)), wp_s = 1.0 / Q;   // unitary scales
+  for (int64_t a = 0; a < p.n_act; a += kFwYBatch) {
+    const int m = (int)std::min<int64_t>(kFwYBatch, p.n_act - a);
+    fw_y_kernel<<<dim3((unsigned)((QQ + 255) / 256), kFwYBatch), 256, 0, st>>>(w->dv + a, m, Q, p.dq, p.qa * p.qa, cph,
+                                                                              p.Sy, p.Sx, p.step, w->Y);
+    if (cufftExecC2C(w->yplan, reinterpret_cast<cufftComplex*>(w->Y), reinterpret_cast<cufftComplex*>(w->Y),
+                     CUFFT_INVERSE) != CUFFT_SUCCESS) return fail("probe FFT");
+    fw_combine_kernel<<<m, 256, 0, st>>>(w->A, w->Y, w->dv + a, Q, chi_s, wp_s, p.eps, w->spec);
+  }
+  // (d) O = conj(F^-1_unitary(x)) [/ sqrt(x_0)]
+  if (cufftExecC2C(w->img, reinterpret_cast<cufftComplex*>(w->spec), static_cast<cufftComplex*>(out_dev),
+                   CUFFT_INVERSE) != CUFFT_SUCCESS) return fail("image FFT");
+  fw_image_kernel<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(static_cast<float2*>(out_dev), S,
+                                                                (float)(1.0 / std::sqrt((double)S)), w->spec,
+                                                                p.normalize);
+  if (cudaGetLastError() != cudaSuccess) return fail("kernel launch");
+  return WDD_OK;
 }
 
 }  // namespace wdd

@@ -11,6 +11,8 @@
 
 namespace wdd {
 
+struct FullWddWork;   // fullwdd.cu: scratch + cuFFT plans of wdd_full_wdd, kept across calls
+
 enum ProfSlot { kSlotProject = 0, kSlotRowDft = 1, kSlotFlush = 2, kSlotReadout = 3, kSlotFinalize = 4, kNumSlots = 5 };
 
 struct Plan {
@@ -75,6 +77,7 @@ struct Plan {
   int2* d_rg_items = nullptr;
   alignas(64) unsigned char rg_tmap[6 * 128] = {};   // RgMaps (kernels.cu): W, G, R tensor maps
   bool rg_ready = false;
+  FullWddWork* fw = nullptr;          // conventional-WDD workspace (first wdd_full_wdd call)
   float2* d_img_tmp = nullptr;        // Sy*Sx scratch of the image transform (row pass)
   void* d_meta = nullptr;             // per-chunk row tables
   void* h_meta = nullptr;             // pinned host mirror of d_meta (2 slots)
@@ -152,5 +155,6 @@ constexpr double kPi = 3.14159265358979323846;
 // conventional (full) WDD of a whole scan (fullwdd.cu): frames_dev S x Q x Q in
 // scan order, out_dev Sy x Sx complex64; stream-ordered on p.stream; err receives a message
 wdd_status full_wdd(Plan& p, const void* frames_dev, void* out_dev, char* err, size_t errn);
+void full_wdd_release(Plan& p);
 
 }  // namespace wdd

@@ -445,6 +445,7 @@ void free_plan(Plan* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   cudaDeviceSynchronize();
   if (p->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(p->nccl));
+  full_wdd_release(*p);
   void* bufs[] = {p->d_rg_items, p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
                   p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec, p->d_img_tmp,
                   p->d_meta, p->d_stage[0], p->d_stage[1]};
