@@ -919,8 +919,20 @@ __device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uin
 // a4 by FFT.  CTA = (k-tile of 2P coefficients, one pending scan row).  Two real coefficient
 // sequences k, k+1 share one complex FFT (z = C_k + i C_{k+1}); X_k[v] = (Z[v] + conj Z[-v]) / 2,
 // X_{k+1}[v] = (Z[v] - conj Z[-v]) / 2i.  Non-pending positions enter as zeros.
+#ifndef WDD_RF_MINB_SMALL
+#define WDD_RF_MINB_SMALL 3
+#endif
+#ifndef WDD_RF_MINB_LARGE
+#define WDD_RF_MINB_LARGE 2
+#endif
+#ifndef WDD_CF_MINB_SMALL
+#define WDD_CF_MINB_SMALL 3
+#endif
+#ifndef WDD_CF_MINB_LARGE
+#define WDD_CF_MINB_LARGE 2
+#endif
 template <int LOGN>
-__global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) rowfft_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MINB_LARGE) rowfft_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
                                                      const uint32_t* __restrict__ masks, int mask_words,
                                                      const float2* __restrict__ tw, const int32_t* __restrict__ col_vx,
                                                      float2* __restrict__ R, int logP, int Sy, int K, int n_vx,
@@ -946,9 +958,12 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) rowfft_kernel(const fl
   // two coefficient pairs (16 bytes) per load; requires P >= 2
   const float4* Crow = reinterpret_cast<const float4*>(C + (int64_t)sy * Sx * K + k0);
   const int lq = logP - 1, total = Sx << lq;            // 16-byte pieces
-  // loads in flight per thread: 4 where four CTAs share an SM (64 registers), 8 otherwise
-  // (measured: Large row FFT 306 -> 251 us with 4; no change at Sx = 512)
-  constexpr int kURow = LOGN <= 8 ? 4 : 8;
+  // loads in flight per thread: fewer for the short rows (register budget of 3 CTAs per SM;
+  // measured: Large row FFT 306 -> 251 us with 4 at 4 CTAs / SM; no change at Sx = 512)
+#ifndef WDD_KU_ROW_SMALL
+#define WDD_KU_ROW_SMALL 4
+#endif
+  constexpr int kURow = LOGN <= 8 ? WDD_KU_ROW_SMALL : 8;
   for (int base = 0; base < total; base += kURow * (int)blockDim.x) {
     float4 v[kURow];
 #pragma unroll
@@ -986,7 +1001,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? 4 : 2) rowfft_kernel(const fl
 // Wiener readout  opart[t][g] = sum_{k in tile t} G[g][k] K_g[k], so a readout never
 // re-reads G.  The partial sums are combined over tiles in a fixed order by the image transform.
 template <int LOGN>
-__global__ void __launch_bounds__(256, LOGN <= 8 ? 3 : 2) colfft_kernel(const float2* __restrict__ R, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MINB_LARGE) colfft_kernel(const float2* __restrict__ R, const int32_t* __restrict__ rows,
                                                      int n_rows, const float2* __restrict__ tw,
                                                      const int32_t* __restrict__ col_off,
                                                      const int32_t* __restrict__ act_vy, float2* __restrict__ G,
