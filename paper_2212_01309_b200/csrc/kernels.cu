@@ -1120,7 +1120,10 @@ static int2 env_pair(const char* name) {
 }
 
 static bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
-constexpr int kFftSmem = 64 * 1024;   // FFT working set per CTA (the twiddle table is added)
+#ifndef WDD_FFT_SMEM
+#define WDD_FFT_SMEM (64 * 1024)
+#endif
+constexpr int kFftSmem = WDD_FFT_SMEM;   // FFT working set per CTA (the twiddle table is added)
 
 template <typename F>
 static cudaError_t with_log(int logn, F&& f) {
