@@ -2331,9 +2331,12 @@ __global__ void __launch_bounds__(256) img_cols_kernel(const float2* __restrict_
 
 // a8 in one launch for images up to 256 x 256: a cluster of CS CTAs, CTA r owns RB = Sy/CS rows
 // for the row pass and CB = Sx/CS columns for the column pass; the transposition between the two
-// passes goes through distributed shared memory (no global round trip, one launch).
+// passes goes through distributed shared memory (no global round trip, one launch).  The spectrum
+// rows are gathered straight from the partial readouts (o_v = their fixed-order tile sum, zero for
+// inactive v through gidx), so no scatter pass runs before it.
 template <int LX, int LY, int CS>
-__global__ void __launch_bounds__(256) img_fused_kernel(const float2* __restrict__ spec,
+__global__ void __launch_bounds__(256) img_fused_kernel(const float2* __restrict__ op, int tiles, int64_t n_act,
+                                                        const int32_t* __restrict__ gidx, int g_dc,
                                                         const float2* __restrict__ twx, const float2* __restrict__ twy,
                                                         float2* __restrict__ out, float scale, int normalize) {
   constexpr int SX = 1 << LX, SY = 1 << LY, RB = SY / CS, CB = SX / CS;
@@ -2349,11 +2352,12 @@ __global__ void __launch_bounds__(256) img_fused_kernel(const float2* __restrict
   pdl_trigger();
   for (int i = threadIdx.x; i < SX; i += blockDim.x) stx[i] = __ldg(twx + i);
   for (int i = threadIdx.x; i < SY; i += blockDim.x) sty[i] = __ldg(twy + i);
-  pdl_wait();   // the spectrum of the preceding scatter kernel
+  pdl_wait();   // the partial readouts of the preceding flush / readout kernel
   const int vy0 = r * RB;
   for (int e = threadIdx.x; e < SX * RB; e += blockDim.x) {
     const int c = e >> LX, vx = e & (SX - 1);
-    const float2 v = __ldg(spec + (int64_t)(vy0 + c) * SX + vx);
+    const int g = __ldg(gidx + (int64_t)(vy0 + c) * SX + vx);
+    const float2 v = g >= 0 ? sum_tiles(op, tiles, n_act, g) : make_float2(0.f, 0.f);
     xr[(vx << LRB) + c] = make_float2(v.x, -v.y);    // conj(o): O = DFT2(conj o) / sqrt(S)
   }
   __syncthreads();
@@ -2369,7 +2373,7 @@ __global__ void __launch_bounds__(256) img_fused_kernel(const float2* __restrict
   fft::fft_seq<LY>(xc, sty, LCB);
   float2 f = make_float2(scale, 0.f);
   if (normalize) {
-    const float2 w = inv_principal_sqrt(__ldg(spec));
+    const float2 w = inv_principal_sqrt(sum_tiles(op, tiles, n_act, g_dc));
     f = make_float2(w.x * scale, w.y * scale);
   }
   for (int e = threadIdx.x; e < SY * CB; e += blockDim.x) {
@@ -2379,7 +2383,7 @@ __global__ void __launch_bounds__(256) img_fused_kernel(const float2* __restrict
 }
 
 template <int LX, int LY>
-static cudaError_t launch_img_fused(const Plan& p, float2* out, cudaStream_t st) {
+static cudaError_t launch_img_fused(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st) {
   constexpr int CS = (LX >= 4 && LY >= 4) ? 16 : 1 << (LX < LY ? LX : LY);
   constexpr int SX = 1 << LX, SY = 1 << LY;
   constexpr size_t smem = (size_t)(SX * (SY / CS) + SY * (SX / CS) + SX + SY) * 8;
@@ -2406,16 +2410,18 @@ static cudaError_t launch_img_fused(const Plan& p, float2* out, cudaStream_t st)
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, img_fused_kernel<LX, LY, CS>, (const float2*)p.d_spec, (const float2*)p.d_twx,
+  return cudaLaunchKernelEx(&cfg, img_fused_kernel<LX, LY, CS>, op, tiles, (int64_t)p.n_act,
+                            (const int32_t*)p.d_gidx, (int)p.g_dc, (const float2*)p.d_twx,
                             (const float2*)p.d_twy, out, (float)(1.0 / std::sqrt((double)p.S)), p.normalize);
 }
 
-static cudaError_t launch_img_fused_dispatch(const Plan& p, float2* out, cudaStream_t st) {
+static cudaError_t launch_img_fused_dispatch(const Plan& p, const float2* op, int tiles, float2* out,
+                                             cudaStream_t st) {
   return with_log(ilog2(p.Sx), [&](auto LNX) {
     constexpr int LX = decltype(LNX)::value;
     return with_log(ilog2(p.Sy), [&](auto LNY) -> cudaError_t {
       constexpr int LY = decltype(LNY)::value;
-      if constexpr (LX <= 8 && LY <= 8) return launch_img_fused<LX, LY>(p, out, st);
+      if constexpr (LX <= 8 && LY <= 8) return launch_img_fused<LX, LY>(p, op, tiles, out, st);
       else return cudaErrorInvalidValue;
     });
   });
@@ -2426,25 +2432,25 @@ bool finalize_uses_fft(const Plan& p) {
          p.Sy <= (1 << kFftMaxLog);
 }
 
-// The partial readouts are first summed (fixed order) and scattered to image order (one coalesced
-// pass over the tiles; inactive positions of d_spec stay zero from plan creation), then the 2-D
-// transform reads whole spectrum rows.  Images up to 128 x 128 take the one-launch cluster
-// kernel; larger power-of-two images the row and column passes (>= 128 CTAs each); other sizes
-// (or WDD_IMG=cufft) cuFFT.
+// Images up to 128 x 128 take the one-launch cluster kernel, which gathers o from the partial
+// readouts itself.  Otherwise the partial readouts are first summed (fixed order) and scattered
+// to image order (one coalesced pass over the tiles; inactive positions of d_spec stay zero from
+// plan creation), then larger power-of-two images take the row and column passes (>= 128 CTAs
+// each) and other sizes (or WDD_IMG=cufft) cuFFT.
 cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st) {
   const int64_t S = p.S;
   static const int img_mode = [] {
     const char* e = std::getenv("WDD_IMG");
     return !e ? 0 : std::strcmp(e, "cufft") == 0 ? 1 : std::strcmp(e, "unfused") == 0 ? 2 : std::strcmp(e, "fused") == 0 ? 3 : 0;
   }();
+  const bool own = finalize_uses_fft(p) && img_mode != 1;
+  const int fused_max = img_mode == 3 ? 256 : img_mode == 2 ? 0 : 128;
+  if (own && p.Sx <= fused_max && p.Sy <= fused_max) return launch_img_fused_dispatch(p, op, tiles, out, st);
   {
     cudaError_t e = launch_pdl(scatter_kernel, dim3((unsigned)((p.n_act + 255) / 256)), dim3(256), 0, st, true, op,
                                tiles, (const int32_t*)p.d_vpos, (int64_t)p.n_act, p.d_spec);
     if (e != cudaSuccess) return e;
   }
-  const bool own = finalize_uses_fft(p) && img_mode != 1;
-  const int fused_max = img_mode == 3 ? 256 : img_mode == 2 ? 0 : 128;
-  if (own && p.Sx <= fused_max && p.Sy <= fused_max) return launch_img_fused_dispatch(p, out, st);
   if (own) {
     const int lx = ilog2(p.Sx), ly = ilog2(p.Sy);
     // 2^lr rows per CTA: enough sequences for the threads of the FFT passes, >= 128 CTAs if possible
