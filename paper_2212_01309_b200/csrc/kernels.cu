@@ -716,6 +716,24 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+// 2-D fp32 tensor map (no swizzle) of a row-major [rows][inner] array with the given row pitch,
+// for the shared-memory FFTs' tile loads; false if it cannot be encoded (callers then load with
+// plain vector loads).  WDD_FFT_TMA=0 disables it.
+static bool fft_tmap(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t rows, uint64_t pitch_bytes,
+                     uint32_t bx, uint32_t by) {
+  static const bool off = [] { const char* e = std::getenv("WDD_FFT_TMA"); return e && std::atoi(e) == 0; }();
+  std::memset(tm, 0, sizeof(*tm));
+  auto enc = get_encode();
+  if (off || !enc || bx * 4 % 16 || bx > 256 || by > 256 || pitch_bytes % 16 || (uintptr_t)base % 16) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)pitch_bytes};
+  const cuuint32_t box[2] = {bx, by};
+  const cuuint32_t estr[2] = {1u, 1u};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int Q, int L, bool U16>
 static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n, float* C, const int32_t* idx,
                                     cudaStream_t st) {
@@ -936,11 +954,13 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
                                                      const uint32_t* __restrict__ masks, int mask_words,
                                                      const float2* __restrict__ tw, const int32_t* __restrict__ col_vx,
                                                      float2* __restrict__ R, int logP, int Sy, int K, int n_vx,
-                                                     float scale) {
+                                                     float scale, const __grid_constant__ CUtensorMap tmC, int use_tma) {
   constexpr int Sx = 1 << LOGN;
+  constexpr int kBY = Sx < 256 ? Sx : 256;   // rows per TMA box
   extern __shared__ __align__(16) float2 fsm[];
   __shared__ uint32_t smask[(Sx + 31) / 32];
   __shared__ int2 sslot[Sx];             // (slot of v, slot of -v) per active column j
+  __shared__ __align__(8) uint64_t lbar;
   const int P = 1 << logP;
   float2* x = fsm;                       // [Sx][P]
   float2* stw = fsm + (Sx << logP);      // [Sx] twiddles
@@ -951,8 +971,27 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
     const int v = __ldg(col_vx + j);
     sslot[j] = make_int2(fft::fslot<LOGN>(v), fft::fslot<LOGN>((Sx - v) & (Sx - 1)));
   }
+  if (use_tma && threadIdx.x == 0) {
+    mbar_init(&lbar, 1);
+    fence_mbar_init();
+  }
   pdl_wait();   // C of the projection kernels (and the uploaded row list / masks)
   const int sy = rows[r];
+  if (use_tma) {
+    // the CTA's whole Sx x 2P slice of C in flight at once (one or two TMA boxes, pitch 2P floats =
+    // the FFT's [Sx][P] layout); positions outside the pending mask are zeroed afterwards
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(&lbar, (uint32_t)(Sx * P * 8));
+      for (int b = 0; b < Sx / kBY; ++b) tma_load_2d(x + ((b * kBY) << logP), &tmC, k0, sy * Sx + b * kBY, &lbar);
+    }
+    if (threadIdx.x < mask_words) smask[threadIdx.x] = masks[(int64_t)r * mask_words + threadIdx.x];
+    __syncthreads();
+    mbar_wait(&lbar, 0);
+    for (int sx = threadIdx.x; sx < Sx; sx += blockDim.x)
+      if (!((smask[sx >> 5] >> (sx & 31)) & 1u))
+        for (int pp = 0; pp < P; ++pp) x[(sx << logP) + pp] = make_float2(0.f, 0.f);
+    __syncthreads();
+  } else {
   if (threadIdx.x < mask_words) smask[threadIdx.x] = masks[(int64_t)r * mask_words + threadIdx.x];
   __syncthreads();
   // two coefficient pairs (16 bytes) per load; requires P >= 2
@@ -983,6 +1022,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
     }
   }
   __syncthreads();
+  }
   fft::fft_seq<LOGN>(x, stw, logP);
   const float hs = 0.5f * scale;
   for (int e = threadIdx.x; e < (n_vx << logP); e += blockDim.x) {
@@ -1007,11 +1047,15 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
                                                      const int32_t* __restrict__ act_vy, float2* __restrict__ G,
                                                      const float2* __restrict__ W, float2* __restrict__ opart,
                                                      int64_t n_act, int logKT, int K, float scale, int overwrite,
-                                                     int tpc, int o_only) {
+                                                     int tpc, int o_only, const __grid_constant__ CUtensorMap tmR,
+                                                     int use_tma) {
   constexpr int Sy = 1 << LOGN;
+  constexpr int kBY = Sy < 256 ? Sy : 256;   // rows per TMA box
   extern __shared__ __align__(16) float2 fsm[];
   const int KT = 1 << logKT;
   __shared__ int srow[Sy];                // staged rows
+  __shared__ uint8_t sstaged[Sy];         // row staged (TMA path: the others are zeroed)
+  __shared__ __align__(8) uint64_t lbar;
   __shared__ int svy[Sy];                 // slot of each active vy of column j
   __shared__ float2 sdot[Sy];             // per-row readout partial over this CTA's k-tiles
   float2* x = fsm;                       // [Sy][KT]
@@ -1020,20 +1064,46 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   pdl_trigger();
   const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
   for (int i = threadIdx.x; i < Sy; i += blockDim.x) stw[i] = __ldg(tw + i);
-  for (int i = threadIdx.x; i < n_rows; i += blockDim.x) srow[i] = __ldg(rows + i);
   for (int i = threadIdx.x; i < mj; i += blockDim.x) {
     svy[i] = fft::fslot<LOGN>(__ldg(act_vy + g0 + i));
     sdot[i] = make_float2(0.f, 0.f);
   }
-  pdl_wait();   // R (row DFT) and G of the preceding kernels
+  if (use_tma) {
+    for (int i = threadIdx.x; i < Sy; i += blockDim.x) sstaged[i] = n_rows < Sy ? 0 : 1;
+    if (threadIdx.x == 0) {
+      mbar_init(&lbar, 1);
+      fence_mbar_init();
+    }
+  }
+  pdl_wait();   // R (row DFT) and G of the preceding kernels (and the uploaded row list)
+  for (int i = threadIdx.x; i < n_rows; i += blockDim.x) srow[i] = __ldg(rows + i);
+  if (use_tma && n_rows < Sy) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_rows; i += blockDim.x) sstaged[srow[i]] = 1;
+  }
   for (int t = 0; t < tpc; ++t) {
   const int k0 = (blockIdx.x * tpc + t) * KT;
+  const int hKT = KT >> 1, lh = logKT - 1;             // 16-byte pieces per row
+  if (use_tma) {
+    // the Sy x KT tile of R[j] in flight at once (pitch KT complex = the FFT's [Sy][KT] layout);
+    // rows not staged are zeroed afterwards
+    __syncthreads();                                   // x free (previous tile), sstaged set
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();                        // generic writes of x before the async refill
+      mbar_arrive_expect_tx(&lbar, (uint32_t)(Sy * KT * 8));
+      for (int b = 0; b < Sy / kBY; ++b)
+        tma_load_2d(x + ((b * kBY) << logKT), &tmR, 2 * k0, j * Sy + b * kBY, &lbar);
+    }
+    mbar_wait(&lbar, (uint32_t)(t & 1));
+    if (n_rows < Sy)
+      for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x)
+        if (!sstaged[e >> logKT]) x[e] = make_float2(0.f, 0.f);
+  } else {
   if (n_rows < Sy)
     for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x) x[e] = make_float2(0.f, 0.f);
   __syncthreads();
   // staged rows of R[j] (k0 .. k0+KT), two coefficients (16 bytes) per load, kU loads in flight
   const float4* Rj = reinterpret_cast<const float4*>(R + (int64_t)j * Sy * K + k0);
-  const int hKT = KT >> 1, lh = logKT - 1;             // 16-byte pieces per row
   const int total = n_rows << lh;
   for (int base = 0; base < total; base += kU * (int)blockDim.x) {
     float4 v[kU];
@@ -1048,6 +1118,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
 #pragma unroll
     for (int u = 0; u < kU; ++u)
       if (dst[u] >= 0) *reinterpret_cast<float4*>(x + dst[u]) = v[u];
+  }
   }
   __syncthreads();
   fft::fft_seq<LOGN>(x, stw, logKT);
@@ -1239,9 +1310,12 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
       // last projection CTAs and slow them down: launch it after the projection completes)
       static const int env_pdl = [] { const char* e = std::getenv("WDD_ROWFFT_PDL"); return e ? std::atoi(e) : -1; }();
       const bool rowfft_pdl = env_pdl >= 0 ? env_pdl != 0 : !project_is_lean(p);
+      CUtensorMap tmC;
+      const bool tma = fft_tmap(&tmC, p.d_Call, (uint64_t)p.K, (uint64_t)p.S, (uint64_t)p.K * 4, 2u << logP,
+                                (uint32_t)std::min(p.Sx, 256));
       return launch_pdl(rowfft_kernel<LOGN>, grid, dim3(nt), smem, st, rowfft_pdl, (const float*)p.d_Call, rows, masks,
                         p.mask_words, (const float2*)p.d_twx, (const int32_t*)p.d_col_vx, p.d_R, logP, p.Sy, p.K,
-                        p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)));
+                        p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, tma ? 1 : 0);
     });
   }
   static bool init = false;
@@ -2146,10 +2220,14 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
       const int tpc = colfft_tpc(p);
       dim3 grid((p.K >> logKT) / tpc, p.n_vx);
       static const int2 knob = env_pair("WDD_COLFFT");
+      CUtensorMap tmR;
+      const bool tma = fft_tmap(&tmR, p.d_R, (uint64_t)p.K * 2, (uint64_t)p.n_vx * p.Sy, (uint64_t)p.K * 8,
+                                2u << logKT, (uint32_t)std::min(p.Sy, 256));
       return launch_pdl(colfft_kernel<LOGN>, grid, dim3(knob.y > 0 ? knob.y : 256), smem, st, true, p.d_R, rows, n_rows,
                         (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G,
                         (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.K,
-                        (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0, tpc, o_only ? 1 : 0);
+                        (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0, tpc, o_only ? 1 : 0, tmR,
+                        tma ? 1 : 0);
     });
   }
   if (o_only) return cudaErrorNotSupported;   // unreachable: flush_kind never picks the DFT for these
