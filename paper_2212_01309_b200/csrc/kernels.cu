@@ -2067,11 +2067,12 @@ static int colfft_logkt(const Plan& p) {
   return logKT;
 }
 
-// k-tiles per y-FFT CTA (<= 4, measured best at Medium and Live) keeping >= 2 waves of CTAs
+// k-tiles per y-FFT CTA (<= 2: with the TMA tile loads, 4 was 1.5% slower at Large and equal at
+// Live) keeping >= 2 waves of CTAs
 static int colfft_tpc(const Plan& p) {
   const int tiles = p.K >> colfft_logkt(p);
   int tpc = 1;
-  while (tpc < 4 && tpc * 2 <= tiles && tiles % (tpc * 2) == 0 && (int64_t)(tiles / (tpc * 2)) * p.n_vx >= 2 * p.sm_count)
+  while (tpc < 2 && tpc * 2 <= tiles && tiles % (tpc * 2) == 0 && (int64_t)(tiles / (tpc * 2)) * p.n_vx >= 2 * p.sm_count)
     tpc *= 2;
   static const int env = [] { const char* e = std::getenv("WDD_COLFFT_TPC"); return e ? std::atoi(e) : 0; }();
   if (env > 0 && tiles % env == 0) tpc = env;
