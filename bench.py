@@ -144,6 +144,24 @@ def oracle_baseline(cfg, n_frames: int, repeats: int = 1):
     return n_frames / t, cores, t
 
 
+def host_info():
+    """CPU model and the BLAS thread count the oracle ran with (SURVEY §8(d) CPU timing)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = max((d.get("num_threads", 0) for d in threadpool_info() if d.get("user_api") == "blas"),
+                   default=None)
+    except Exception:
+        pass
+    return {"cpu_model": model, "blas_threads": blas}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -166,7 +184,8 @@ def run_reference(args):
                    "sample_frames": n, "global_batch": n},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"first {n} scan positions of {cfg.name}: projection + FFT accumulation "
-                                   f"+ Wiener readout + IDFT, float64 NumPy, median of {args.steps}"},
+                                   f"+ Wiener readout + IDFT, float64 NumPy, median of {args.steps}",
+                         **host_info()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
@@ -346,10 +365,14 @@ def main():
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            v, cores, t = oracle_baseline(cfg, args.ref_frames)
+            # the whole acquisition (Medium: 16 384 frames, ~2 s per pass), median of 5 passes:
+            # about 10 s of CPU work
+            n_cpu = min(cfg.S, max(args.ref_frames, 16384))
+            v, cores, t = oracle_baseline(cfg, n_cpu, repeats=5)
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                   "sample": f"first {args.ref_frames} scan positions of {cfg.name}: projection + FFT "
-                             f"accumulation + Wiener readout + IDFT, float64 NumPy ({t:.1f} s)"}
+                   "sample": f"first {n_cpu} scan positions of {cfg.name} (the whole scan for Medium): "
+                             f"projection + FFT accumulation + Wiener readout + IDFT, float64 NumPy, "
+                             f"median of 5 passes ({t:.1f} s each)", **host_info()}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
