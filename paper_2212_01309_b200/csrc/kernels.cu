@@ -1049,6 +1049,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
                                                      int64_t n_act, int logKT, int K, float scale, int overwrite,
                                                      int tpc, int o_only, const __grid_constant__ CUtensorMap tmR,
                                                      int use_tma) {
+  // use_tma: bit 0 = R tiles by TMA, bit 3 = L2 prefetch of the output stage's W / G rows
   constexpr int Sy = 1 << LOGN;
   constexpr int kBY = Sy < 256 ? Sy : 256;   // rows per TMA box
   extern __shared__ __align__(16) float2 fsm[];
@@ -1068,7 +1069,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     svy[i] = fft::fslot<LOGN>(__ldg(act_vy + g0 + i));
     sdot[i] = make_float2(0.f, 0.f);
   }
-  if (use_tma) {
+  if (use_tma & 1) {
     for (int i = threadIdx.x; i < Sy; i += blockDim.x) sstaged[i] = n_rows < Sy ? 0 : 1;
     if (threadIdx.x == 0) {
       mbar_init(&lbar, 1);
@@ -1077,14 +1078,14 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   }
   pdl_wait();   // R (row DFT) and G of the preceding kernels (and the uploaded row list)
   for (int i = threadIdx.x; i < n_rows; i += blockDim.x) srow[i] = __ldg(rows + i);
-  if (use_tma && n_rows < Sy) {
+  if ((use_tma & 1) && n_rows < Sy) {
     __syncthreads();
     for (int i = threadIdx.x; i < n_rows; i += blockDim.x) sstaged[srow[i]] = 1;
   }
   for (int t = 0; t < tpc; ++t) {
   const int k0 = (blockIdx.x * tpc + t) * KT;
   const int hKT = KT >> 1, lh = logKT - 1;             // 16-byte pieces per row
-  if (use_tma) {
+  if (use_tma & 1) {
     // the Sy x KT tile of R[j] in flight at once (pitch KT complex = the FFT's [Sy][KT] layout);
     // rows not staged are zeroed afterwards
     __syncthreads();                                   // x free (previous tile), sstaged set
@@ -1119,6 +1120,18 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     for (int u = 0; u < kU; ++u)
       if (dst[u] >= 0) *reinterpret_cast<float4*>(x + dst[u]) = v[u];
   }
+  }
+  if (use_tma & 8) {
+    // the output stage's W (and G) rows of this k-tile into L2 while the transform runs: its
+    // dependent load rounds then wait on L2, not DRAM
+    const int lpr = KT >= 16 ? KT >> 4 : 1;            // 128-byte lines per row segment
+    const bool pg = !overwrite && !o_only;
+    for (int e = threadIdx.x; e < mj * lpr; e += blockDim.x) {
+      const int i = e / lpr, l = e - i * lpr;
+      const int64_t off = (int64_t)(g0 + i) * K + k0 + 16 * l;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(W + off));
+      if (pg) asm volatile("prefetch.global.L2 [%0];" ::"l"(G + off));
+    }
   }
   __syncthreads();
   fft::fft_seq<LOGN>(x, stw, logKT);
@@ -2223,6 +2236,9 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
       const int tpc = colfft_tpc(p);
       dim3 grid((p.K >> logKT) / tpc, p.n_vx);
       static const int2 knob = env_pair("WDD_COLFFT");
+      // L2 prefetch of the output stage's rows: Large readout 339 -> 333 us, Box 3.77 -> 3.65 ms;
+      // none at Medium (-0.15%: fewer load rounds per tile), so only from Sy = 256
+      static const bool pf_on = [] { const char* e = std::getenv("WDD_COLFFT_PF"); return !(e && std::atoi(e) == 0); }();
       CUtensorMap tmR;
       const bool tma = fft_tmap(&tmR, p.d_R, (uint64_t)p.K * 2, (uint64_t)p.n_vx * p.Sy, (uint64_t)p.K * 8,
                                 2u << logKT, (uint32_t)std::min(p.Sy, 256));
@@ -2230,7 +2246,7 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
                         (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G,
                         (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.K,
                         (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0, tpc, o_only ? 1 : 0, tmR,
-                        tma ? 1 : 0);
+                        (tma ? 1 : 0) | (pf_on && p.Sy >= 256 ? 8 : 0));
     });
   }
   if (o_only) return cudaErrorNotSupported;   // unreachable: flush_kind never picks the DFT for these
