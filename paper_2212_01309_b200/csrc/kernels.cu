@@ -138,7 +138,10 @@ struct ProjCfgT {
   static constexpr bool kSplitAcc = LEAN && L >= 24;
   static constexpr int kNacc = kSplitAcc ? L : kN;        // accumulator columns (both stages)
   static constexpr int kAcc1 = kNacc;                     // per acc1 slot (both count planes accumulate here)
-  static constexpr int kNB2 = LEAN ? 1 : 2;               // stage-2 A2 images / accumulators in flight
+#ifndef WDD_LEAN_NB2
+#define WDD_LEAN_NB2 1
+#endif
+  static constexpr int kNB2 = LEAN ? WDD_LEAN_NB2 : 2;    // stage-2 A2 images / accumulators in flight
   // acc1 ring: 4 deep unless TMEM (A ring + plane-1 buffers + acc1 + acc2 images) would exceed 512 columns
   // (lean: 2, or 1 where two would not leave both CTAs of an SM their 256 TMEM columns)
   static constexpr int kNAcc = LEAN ? ((kNA + kNGroups) * (Q >= 64 ? 32 : Q / 2) + (2 + kNB2) * kNacc > 256 ? 1 : 2)
