@@ -1,0 +1,74 @@
+"""GPU checks of the alternative code paths behind the library's environment knobs (DESIGN.md
+"Tuning knobs"; each knob is read once per process, so every variant runs in its own process).
+
+* Pure data-movement alternatives must give bit-identical images: the FFT kernels' TMA tile loads
+  against per-thread vector loads (WDD_FFT_TMA=0) and the y-FFT's L2 prefetch (WDD_COLFFT_PF=0).
+  Both read the same bytes into the same shared-memory layout and run the same arithmetic.
+* Alternative arithmetic (image transform by cuFFT or two passes, the DFT-matrix and tensor-core
+  rank-update flushes) must agree to float32 rounding of a different summation order: relative
+  L2 <= 1e-5 against the default path (the oracle tolerance is 1e-4, P:815 readout).
+
+Input: Large geometry (Sy = Sx = 256, so the y-FFT prefetch is active), 65 536 seeded sparse
+counting-detector frames (synth/sparse.py, the benchmarks' frame pool).  The comparison is GPU
+against GPU; the oracle parity of the default path is in test_gpu_fullsize.py."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2212_01309_b200 as wdd
+from synth import CONFIGS
+from synth.sparse import dense_frames_torch, sparse_events
+cfg = CONFIGS["large"]
+plan = wdd.Plan.from_config(cfg)
+b = 16384
+for a in range(0, cfg.S, b):
+    idx = np.arange(a, a + b)
+    fr = dense_frames_torch(*sparse_events(5, idx, cfg.Q), cfg.Q, "cuda")
+    plan.ingest(fr, idx.astype(np.int32))
+out = plan.readout()
+torch.cuda.synchronize()
+np.save({path!r}, out.cpu().numpy())
+"""
+
+
+def _run(tmp_path, name, env_extra):
+    path = str(tmp_path / f"{name}.npy")
+    env = dict(os.environ)
+    for k in [k for k in env if k.startswith("WDD_")]:
+        if k != "WDD_LIB":
+            del env[k]
+    env.update(env_extra)
+    r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, path=path)], env=env, cwd=ROOT,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return np.load(path)
+
+
+@pytest.fixture(scope="module")
+def default_image(tmp_path_factory):
+    from paper_2212_01309_b200 import build
+    build.build()
+    return _run(tmp_path_factory.mktemp("knobs"), "default", {})
+
+
+@pytest.mark.parametrize("env", [{"WDD_FFT_TMA": "0"}, {"WDD_COLFFT_PF": "0"}])
+def test_data_movement_variants_bit_identical(default_image, tmp_path, env):
+    img = _run(tmp_path, "v", env)
+    assert np.array_equal(img, default_image), env
+
+
+@pytest.mark.parametrize("env", [{"WDD_IMG": "cufft"}, {"WDD_IMG": "unfused"}, {"WDD_FLUSH": "gemm"},
+                                 {"WDD_FLUSH": "dft"}])
+def test_arithmetic_variants_agree(default_image, tmp_path, env):
+    img = _run(tmp_path, "v", env)
+    err = np.linalg.norm(img - default_image) / np.linalg.norm(default_image)
+    assert err <= 1e-5, (env, err)
