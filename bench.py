@@ -216,6 +216,8 @@ def main():
     ap.add_argument("--config", default="medium")
     ap.add_argument("--batch", type=int, default=0, help="override the workload's batch (experiments only)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--acq-per-graph", type=int, default=4,
+                    help="acquisitions per captured graph (consecutive ones overlap readout and projection)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-frames", type=int, default=2048)
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -267,18 +269,36 @@ def main():
     launches_per_step = plan.launch_count(reset=True)
     torch.cuda.synchronize()
 
-    if args.no_graph:
-        step = step_eager
-    else:
-        plan.capture_begin(stream)
-        step_eager()
-        handle = plan.capture_end()
+    # A graph holds `acq_per_graph` consecutive acquisitions: inside it each acquisition's first
+    # projection overlaps the previous acquisition's readout (the plan alternates two coefficient
+    # stores across resets), as back-to-back scans do in a live session; graph launches themselves
+    # serialise.  `run(n)` performs exactly n steps (acquisitions).
+    A = max(1, args.acq_per_graph)
+    graphs = {}
 
-        def step():
-            plan.graph_launch(handle, stream)
+    def graph_for(n):
+        if n not in graphs:
+            plan.capture_begin(stream)
+            for _ in range(n):
+                step_eager()
+            graphs[n] = plan.capture_end()
+        return graphs[n]
 
-    for _ in range(max(3, args.warmup)):
-        step()
+    def run(n):
+        if args.no_graph:
+            for _ in range(n):
+                step_eager()
+            return
+        for _ in range(n // A):
+            plan.graph_launch(graph_for(A), stream)
+        if n % A:
+            plan.graph_launch(graph_for(n % A), stream)
+
+    if not args.no_graph:
+        graph_for(A)
+        if args.steps % A:
+            graph_for(args.steps % A)
+    run(max(3, args.warmup))
     torch.cuda.synchronize()
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -287,8 +307,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
-        for _ in range(args.steps):
-            step()
+        run(args.steps)
         ev1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -398,7 +417,7 @@ def main():
             "config": {"workload": cfg.name, "scan": [cfg.Sy, cfg.Sx], "detector": [cfg.Q, cfg.Q],
                        "K": cfg.K, "batch": batch, "global_batch": cfg.S, "parallelism": f"rows/{world}",
                        "l2": "inputs larger than L2 (537 MB of frames per step)",
-                       "graph": not args.no_graph},
+                       "graph": not args.no_graph, "acquisitions_per_graph": None if args.no_graph else A},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": _traffic(cfg.name), "kernel": "project_kernel",
                          "peak_source": peak_src, "bytes_per_launch": bytes_per_launch,

@@ -126,7 +126,10 @@ wdd_status wdd_destroy(wdd_plan_t plan);
 wdd_status wdd_get_accumulator(wdd_plan_t plan, void* G_out_dev, int32_t* active_v_host,
                                int64_t* n_act);
 
-/* Forget every ingested frame: G = 0, staging cleared, seen-bitmap cleared (stream-ordered). */
+/* Forget every ingested frame: G = 0, staging cleared, seen-bitmap cleared (stream-ordered).
+ * After ingests it also swaps the plan's two coefficient stores (2 x S x K float32, allocated at
+ * create; WDD_C_DOUBLE=0 allocates one), so the next acquisition's first projection may overlap
+ * the previous acquisition's readout, which still reads the old store.  No device work. */
 wdd_status wdd_reset(wdd_plan_t plan);
 
 /* Multi-rank combine over NCCL (NVLink / NVSwitch).  Rank 0 creates the id, the caller

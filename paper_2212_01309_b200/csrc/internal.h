@@ -53,6 +53,11 @@ struct Plan {
   float2* d_R = nullptr;              // n_vx * Sy * K   R[j][sy][k]
   float* d_Call = nullptr;            // S * K: coefficients of ingested frames at their scan
                                       // positions (only the pending ones are ever read)
+  float* d_Call_alt = nullptr;        // the other coefficient store: a reset after ingests swaps
+                                      // them, so the next acquisition's projection may overlap
+                                      // (PDL) the previous acquisition's readout, which still
+                                      // reads the old store
+  bool c_fresh = false;               // d_Call was swapped in by the last reset (not yet written)
   int32_t* d_act_vy = nullptr;
   int32_t* d_col_off = nullptr;
   int32_t* d_vpos = nullptr;          // n_act flattened v (scatter positions)

@@ -800,11 +800,12 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  // The first launch after a reset is an ordinary launch: it starts only once everything before it
-  // (the previous acquisition's flush and readout, which still read the coefficient store this
-  // launch overwrites) has completed.  Later launches of the acquisition write disjoint scan
-  // positions and overlap their predecessors programmatically.
-  cfg.numAttrs = p.frames_ingested == 0 ? 0 : 1;
+  // The first launch after a reset is an ordinary launch (it starts only once everything before it
+  // has completed: the previous acquisition's flush and readout may still read the coefficient
+  // store it overwrites) unless the reset swapped in the other store (c_fresh): then it too
+  // overlaps its predecessor, the previous readout, programmatically.  Later launches of the
+  // acquisition write disjoint scan positions and always overlap their predecessors.
+  cfg.numAttrs = (p.frames_ingested == 0 && !p.c_fresh) ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, a, tmap);
 }
 

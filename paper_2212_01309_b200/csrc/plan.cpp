@@ -212,6 +212,13 @@ struct Prof {
   }
 };
 
+// Two coefficient stores (WDD_C_DOUBLE=0: one; the first projection of every acquisition then waits
+// for the previous readout).
+bool double_c_store() {
+  static const bool on = [] { const char* e = std::getenv("WDD_C_DOUBLE"); return !(e && std::atoi(e) == 0); }();
+  return on;
+}
+
 wdd_status check_plan(wdd_plan_t plan) {
   if (!plan) return fail(WDD_E_ARG, "plan is NULL");
   return WDD_OK;
@@ -301,6 +308,7 @@ wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, in
     Prof pr(p, kSlotProject, st);
     CUDA_TRY(launch_project(p, frames_dev, nc, C, d_idx, st));
   }
+  p.c_fresh = false;
   // The row DFT of completed rows is deferred to the next flush (readout): launched per batch it
   // would sit between the PDL-chained projection launches and stall them (measured: 246 us vs
   // 162 us per Medium acquisition).
@@ -446,7 +454,7 @@ void free_plan(Plan* p) {
   cudaDeviceSynchronize();
   if (p->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(p->nccl));
   full_wdd_release(*p);
-  void* bufs[] = {p->d_rg_items, p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call,
+  void* bufs[] = {p->d_rg_items, p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call, p->d_Call_alt,
                   p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec, p->d_img_tmp,
                   p->d_meta, p->d_stage[0], p->d_stage[1]};
   for (void* b : bufs)
@@ -621,6 +629,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   if (p->combine == 1) ALLOC(p->d_Gsum, nW * sizeof(float2));
   ALLOC(p->d_R, (size_t)p->n_vx * Sy * K * sizeof(float2));
   ALLOC(p->d_Call, (size_t)p->S * K * sizeof(float));
+  if (double_c_store()) ALLOC(p->d_Call_alt, (size_t)p->S * K * sizeof(float));
   ALLOC(p->d_act_vy, act.size() * 4);
   ALLOC(p->d_col_off, p->col_off.size() * 4);
   ALLOC(p->d_vpos, act.size() * 4);
@@ -658,6 +667,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
        cudaMemset(p->d_ones, 0xFF, (size_t)Sy * p->mask_words * sizeof(uint32_t)) == cudaSuccess &&
        cudaMemset(p->d_G, 0, nW * sizeof(float2)) == cudaSuccess &&
        cudaMemset(p->d_Call, 0, (size_t)p->S * K * sizeof(float)) == cudaSuccess &&
+       (!p->d_Call_alt || cudaMemset(p->d_Call_alt, 0, (size_t)p->S * K * sizeof(float)) == cudaSuccess) &&
        cudaMemset(p->d_spec, 0, (size_t)p->S * sizeof(float2)) == cudaSuccess;
   if (!ok) return bail(fail(WDD_E_CUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError())));
   {
@@ -830,6 +840,12 @@ wdd_status wdd_reset(wdd_plan_t plan) {
   std::fill(p.row_dirty.begin(), p.row_dirty.end(), 0);
   std::fill(p.row_staged.begin(), p.row_staged.end(), 0);
   std::fill(p.pending.begin(), p.pending.end(), 0u);
+  if (p.d_Call_alt && p.frames_ingested > 0) {
+    // the previous acquisition's flush / readout may still read the current store: the next
+    // acquisition writes the other one, so its first projection need not wait for them
+    std::swap(p.d_Call, p.d_Call_alt);
+    p.c_fresh = true;
+  }
   p.frames_ingested = 0;
   return WDD_OK;
 }
