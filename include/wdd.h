@@ -129,7 +129,8 @@ wdd_status wdd_get_accumulator(wdd_plan_t plan, void* G_out_dev, int32_t* active
 /* Forget every ingested frame: G = 0, staging cleared, seen-bitmap cleared (stream-ordered).
  * After ingests it also swaps the plan's two coefficient stores (2 x S x K float32, allocated at
  * create; WDD_C_DOUBLE=0 allocates one), so the next acquisition's first projection may overlap
- * the previous acquisition's readout, which still reads the old store.  No device work. */
+ * the previous acquisition's readout, which still reads the old store.  Device work: none
+ * (spectrum-only plans: one memset of the running spectrum). */
 wdd_status wdd_reset(wdd_plan_t plan);
 
 /* Multi-rank combine over NCCL (NVLink / NVSwitch).  Rank 0 creates the id, the caller
