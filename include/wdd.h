@@ -72,6 +72,18 @@ typedef struct {
                             from the coefficient store (one full row DFT + rank update).  Needs a
                             power-of-two Sy in [2, 1024]; multi-rank readout always sums o
                             (combine is ignored).                                               */
+  int32_t ingest_overlap;/* 0 (default) = wdd_ingest may follow a caller kernel that writes the frames:
+                            the first projection of each call reads them only after the preceding
+                            grid on the stream has completed.  1 = the caller guarantees the frames
+                            are complete before the previous LIBRARY call on the stream was enqueued
+                            (or arrive by a copy / event): every projection launch then streams its
+                            frames while the previous one drains (PDL), which is what keeps a chain
+                            of small batches at HBM speed.                                        */
+  int32_t k_shards;      /* coefficient sharding over a rank group: 0 or 1 = none;
+                            n > 1 = this plan owns the coefficient rows a (k = a*L + b) of shard
+                            k_rank of n (contiguous, as even as possible, n <= L) -- its coefficient
+                            store, R staging, G and bank hold only those k; see wdd_set_shard_peers */
+  int32_t k_rank;        /* this plan's shard, 0 <= k_rank < k_shards                              */
   int32_t reserved[3];   /* must be zero                                                      */
 } wdd_plan_opts;
 
@@ -114,6 +126,22 @@ wdd_status wdd_ingest_host(wdd_plan_t plan, const void* frames_host, const int32
  * receives the same image.  Two readouts with no ingest in between give identical bytes. */
 wdd_status wdd_readout(wdd_plan_t plan, void* complex_out_dev);
 
+/* The readout's spectrum instead of the image: o_v = sum_k G[v,k] K_v[k] at the active v, 0
+ * elsewhere (Sy*Sx complex64, image order v = vy*Sx + vx, FFT order per axis), DEVICE buffer.
+ * combine != 0: after the multi-rank NCCL combine (collective, as wdd_readout); combine == 0: this
+ * rank's own partial spectrum (no communication) -- partial spectra of disjoint ingests (or of
+ * coefficient shards) sum to the full one (linearity).  Stream-ordered. */
+wdd_status wdd_readout_spectrum(wdd_plan_t plan, void* spectrum_out_dev, int32_t combine);
+
+/* The final transform of a given spectrum: O = conj(IDFT2_unitary(o)) [/ sqrt(o_0)];
+ * spectrum_dev and complex_out_dev are DEVICE buffers of Sy*Sx complex64 (must not alias). */
+wdd_status wdd_image_from_spectrum(wdd_plan_t plan, const void* spectrum_dev, void* complex_out_dev);
+
+/* Synchronise the plan stream and report deferred device-side errors: WDD_E_RANGE if float32
+ * frames with values the projection's fp16 hi/lo split cannot represent (|x| > 65504, inf, NaN)
+ * were ingested since the last check (the flag is then cleared).  wdd_readout_host checks too. */
+wdd_status wdd_check(wdd_plan_t plan);
+
 /* Readout into a HOST buffer (Sy*Sx complex64); blocks until the bytes are on the host. */
 wdd_status wdd_readout_host(wdd_plan_t plan, void* complex_out_host);
 
@@ -136,7 +164,9 @@ wdd_status wdd_reset(wdd_plan_t plan);
 /* Multi-rank combine over NCCL (NVLink / NVSwitch).  Rank 0 creates the id, the caller
  * broadcasts it (e.g. via torch.distributed), every rank calls wdd_set_comm with it.
  * Each rank ingests a disjoint index set; wdd_readout allreduces (opts.combine) and every
- * rank receives the full image ("merge ... sums up the contributions"). */
+ * rank receives the full image ("merge ... sums up the contributions").
+ * nranks == 1 creates a one-rank communicator: the readout then runs the combine path (partial
+ * readouts summed into o, allreduce) exactly as on N ranks.  Calling it again replaces the comm. */
 wdd_status wdd_nccl_get_unique_id(uint8_t id[128]);
 wdd_status wdd_set_comm(wdd_plan_t plan, int32_t nranks, int32_t rank, const uint8_t id[128]);
 

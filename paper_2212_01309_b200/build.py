@@ -46,8 +46,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         raise RuntimeError("nvcc failed building libwdd.so")
     os.replace(tmp, LIB)
-    with open(os.path.join(HERE, "_lib", "ptxas.log"), "w") as f:
-        f.write(res.stderr)
+    if not os.environ.get("WDD_LIB_OUT"):
+        # register / spill / shared-memory report of the shipped build (tracked); the compile-time
+        # lines change on every build and are dropped so an unchanged source leaves no diff
+        log = "".join(ln for ln in res.stderr.splitlines(True) if "Compile time" not in ln)
+        path = os.path.join(HERE, "_lib", "ptxas.log")
+        old = open(path).read() if os.path.exists(path) else None
+        if log != old:
+            with open(path, "w") as f:
+                f.write(log)
     return LIB
 
 

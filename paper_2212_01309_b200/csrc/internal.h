@@ -24,6 +24,9 @@ struct Plan {
   double b_scale = 1.0;  // power-of-two prescale of the fp16 basis operand (2^s)
   double sc1 = 1.0, sc2 = 1.0;  // projection epilogue scales: 2^(eT-s), 2^(-s-eT)
   int sm_count = 148;
+  int ingest_overlap = 0;             // 1: frames are complete before the previous library call on the stream
+                                      // (projection reads them before its predecessor grid completes)
+  unsigned* d_err = nullptr;          // device error flags (f32 frame range), sticky until wdd_check
 
   // host tables
   std::vector<double> basis;          // Q*L, Psi[m][n]
@@ -120,8 +123,12 @@ struct Plan {
 
 // ---- kernel launchers (kernels.cu); return cudaError_t of the launch
 // projection of n frames; C row of frame f = idx ? idx[f] : f (idx: device array or null)
+// wait_start: the kernel waits for the preceding grid before reading frames (the frames may be
+// produced by a caller kernel right before the ingest); else frames are read at once (ingest_overlap)
 cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* C, const int32_t* idx,
-                           cudaStream_t st);
+                           cudaStream_t st, bool wait_start);
+// cudaFuncSetAttribute once per (device, kernel, attribute, value); thread-safe
+cudaError_t func_attr_once(const void* fn, cudaFuncAttribute attr, int value);
 // row DFT (a4) of the listed scan rows from the pending positions of d_Call (masks: n_rows x
 // mask_words bits) into R; FFT for power-of-two Sx, DFT matrix otherwise
 cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, cudaStream_t st);
@@ -145,6 +152,12 @@ bool finalize_uses_fft(const Plan& p);
 cudaError_t launch_readout(const Plan& p, const float2* G, float2* o, cudaStream_t st);
 // image from the partial readouts op[tiles][n_act] (summed over tiles in order)
 cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st);
+// o[g] = fixed-order sum of `tiles` partial readouts (n_act entries, accumulator order)
+cudaError_t launch_otiles(const Plan& p, const float2* op, int tiles, float2* o, cudaStream_t st);
+// dense image-order spectrum from partial readouts (writes the active positions only)
+cudaError_t launch_spectrum(const Plan& p, const float2* op, int tiles, float2* spec, cudaStream_t st);
+// a8 from a dense Sy x Sx spectrum
+cudaError_t launch_image(const Plan& p, const float2* spec, float2* out, cudaStream_t st);
 // host helper: pack the fp16 B operand image of the projection kernel
 void pack_basis_fp16(const Plan& p, std::vector<uint16_t>& out, double& scale);
 size_t project_smem_bytes(int Q, int L);

@@ -29,6 +29,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <cuda_bf16.h>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <vector>
 
 #include "internal.h"
@@ -210,6 +213,22 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// Kernel attributes are per device (context), so the "already set" cache is keyed by the current
+// device as well as the function; thread-safe (plans on several devices in one process).
+cudaError_t func_attr_once(const void* fn, cudaFuncAttribute attr, int value) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_tuple(dev, fn, (int)attr, value);
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, attr, value);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
+}
+
 struct ProjArgs {
   const void* frames;
   int64_t n;
@@ -220,6 +239,10 @@ struct ProjArgs {
   float sc1;   // acc1 -> fp16 A2 scale   (2^(eT - s))
   float sc2;   // acc2 -> C scale          (2^(-s - eT))
   int pdl_wait_end;   // 1: complete only after the preceding grid (keeps stream order for later launches)
+  int pdl_wait_start; // 1: no frame load (and no dependent launch) before the preceding grid has completed --
+                      // the frames may come from a caller kernel enqueued right before the ingest
+  unsigned* err;      // f32 frames: bit 0 set if a value does not fit the fp16 hi/lo split (|x| > 65504 or
+                      // not finite); sticky until wdd_check
 };
 
 // Stage-1 tile tt of group g: first frame-matrix row and the number of valid rows.
@@ -263,7 +286,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
   uint32_t* tslot = wflag + 16;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  pdl_trigger();
+  if (!a.pdl_wait_start) pdl_trigger();
 #ifdef WDD_TRACE
   __shared__ unsigned cta_slot;
   if (tid == 0) {
@@ -297,6 +320,10 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
+  if (a.pdl_wait_start) {   // (setup above overlaps the predecessor; frames are read only below)
+    pdl_wait();
+    pdl_trigger();
+  }
 
   const int64_t n = a.n;
   const int g2 = a.g2;
@@ -531,13 +558,16 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
               uint4 o, l;
               __half* hp = reinterpret_cast<__half*>(&o);
               __half* lp = reinterpret_cast<__half*>(&l);
+              bool bad = false;
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 hp[e] = __float2half_rn(x[e]);
+                bad |= __hisinf(hp[e]) || __hisnan(hp[e]);
                 const float d = x[e] - __half2float(hp[e]);
                 resid |= d != 0.f;
                 lp[e] = __float2half_rn(d);
               }
+              if (bad) atomicOr(a.err, 1u);
               *reinterpret_cast<uint4*>(dst + j * kLBO + (r >> 3) * 128 + (r & 7) * 16) = o;
               lo[i] = l;
             }
@@ -739,14 +769,12 @@ static bool fft_tmap(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t
 
 template <int Q, int L, bool U16>
 static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n, float* C, const int32_t* idx,
-                                    cudaStream_t st) {
+                                    cudaStream_t st, bool wait_start) {
   using Cfg = ProjCfg<Q, L, U16>;
   auto kern = project_kernel<Q, L, U16>;
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::smem);
+  {
+    cudaError_t e = func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::smem);
     if (e != cudaSuccess) return e;
-    init = true;
   }
   if (n <= 0) return cudaSuccess;
   // frames per stage-2 group: the largest multiple of kFPT (<= kG2) that keeps the per-CTA
@@ -790,7 +818,7 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
   }
   static const int no_wait = [] { const char* e = std::getenv("WDD_PROJ_NO_PDLWAIT"); return e ? std::atoi(e) : 0; }();
   ProjArgs a{frames, n, C, idx, g2, reinterpret_cast<const uint4*>(p.d_Bpack), (float)p.sc1, (float)p.sc2,
-             no_wait ? 0 : 1};
+             no_wait ? 0 : 1, wait_start ? 1 : 0, p.d_err};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(Cfg::kThreads);
@@ -811,11 +839,11 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
 
 #define WDD_PROJ_CASE(QQ, LL)                                                          \
   if (p.Q == QQ && p.L == LL)                                                          \
-    return p.dtype == 0 ? launch_project_t<QQ, LL, true>(p, frames, n, C, idx, st)     \
-                        : launch_project_t<QQ, LL, false>(p, frames, n, C, idx, st);
+    return p.dtype == 0 ? launch_project_t<QQ, LL, true>(p, frames, n, C, idx, st, wait_start)     \
+                        : launch_project_t<QQ, LL, false>(p, frames, n, C, idx, st, wait_start);
 
 cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* C, const int32_t* idx,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool wait_start) {
   WDD_PROJ_CASE(32, 8) WDD_PROJ_CASE(32, 16) WDD_PROJ_CASE(32, 24) WDD_PROJ_CASE(32, 32)
   WDD_PROJ_CASE(64, 8) WDD_PROJ_CASE(64, 16) WDD_PROJ_CASE(64, 24) WDD_PROJ_CASE(64, 32)
   WDD_PROJ_CASE(128, 8) WDD_PROJ_CASE(128, 16) WDD_PROJ_CASE(128, 24) WDD_PROJ_CASE(128, 32)
@@ -862,11 +890,11 @@ int project_occupancy(const Plan& p) {
   if (p.Q == QQ && p.L == LL) {                                                                      \
     if (p.dtype == 0) {                                                                              \
       using C = ProjCfg<QQ, LL, true>;                                                               \
-      cudaFuncSetAttribute(project_kernel<QQ, LL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem); \
+      func_attr_once((const void*)project_kernel<QQ, LL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem); \
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, project_kernel<QQ, LL, true>, C::kThreads, C::smem); \
     } else {                                                                                         \
       using C = ProjCfg<QQ, LL, false>;                                                              \
-      cudaFuncSetAttribute(project_kernel<QQ, LL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem); \
+      func_attr_once((const void*)project_kernel<QQ, LL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem); \
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, project_kernel<QQ, LL, false>, C::kThreads, C::smem); \
     }                                                                                                \
   }
@@ -969,7 +997,9 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
   float2* x = fsm;                       // [Sx][P]
   float2* stw = fsm + (Sx << logP);      // [Sx] twiddles
   const int r = blockIdx.y, k0 = blockIdx.x * 2 * P;
-  pdl_trigger();
+  // (no early trigger: this kernel reads the coefficient store, and the next acquisition's first
+  // projection may be PDL-launched into the same store two acquisitions later -- the dependents of
+  // this grid launch only after every CTA has its C tile in shared memory, below)
   for (int i = threadIdx.x; i < Sx; i += blockDim.x) stw[i] = __ldg(tw + i);
   for (int j = threadIdx.x; j < n_vx; j += blockDim.x) {
     const int v = __ldg(col_vx + j);
@@ -995,6 +1025,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
       if (!((smask[sx >> 5] >> (sx & 31)) & 1u))
         for (int pp = 0; pp < P; ++pp) x[(sx << logP) + pp] = make_float2(0.f, 0.f);
     __syncthreads();
+    pdl_trigger();   // every read of C by this CTA is complete
   } else {
   if (threadIdx.x < mask_words) smask[threadIdx.x] = masks[(int64_t)r * mask_words + threadIdx.x];
   __syncthreads();
@@ -1026,6 +1057,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
     }
   }
   __syncthreads();
+  pdl_trigger();   // every read of C by this CTA is complete
   }
   fft::fft_seq<LOGN>(x, stw, logP);
   const float hs = 0.5f * scale;
@@ -1317,12 +1349,10 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
     const size_t smem = ((size_t)p.Sx << logP) * 8 + (size_t)p.Sx * 8 + 16;
     return with_log(logSx, [&](auto LN) {
       constexpr int LOGN = decltype(LN)::value;
-      static bool init = false;
-      if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(rowfft_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kFftSmem + 16384);
+      {
+        cudaError_t e = func_attr_once((const void*)rowfft_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kFftSmem + 16384);
         if (e != cudaSuccess) return e;
-        init = true;
       }
       dim3 grid(p.K / (2 << logP), n_rows);
       // (with two projection CTAs per SM a PDL-launched row FFT would park its CTAs next to the
@@ -1337,11 +1367,9 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
                         p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, tma ? 1 : 0);
     });
   }
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(rowdft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRdSmem);
+  {
+    cudaError_t e = func_attr_once((const void*)rowdft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRdSmem);
     if (e != cudaSuccess) return e;
-    init = true;
   }
   dim3 grid(p.K / 64, (p.n_vx + 15) / 16, n_rows);
   rowdft_kernel<<<grid, 256, kRdSmem, st>>>(p.d_Call, rows, masks, p.mask_words, p.d_Fx, p.d_R, p.Sx, p.Sy, p.K,
@@ -2142,7 +2170,7 @@ cudaError_t rgemm_prepare(Plan& p) {
   if (cudaMalloc(&p.d_rg_items, p.rg_items.size() * sizeof(int2)) != cudaSuccess) return cudaErrorMemoryAllocation;
   cudaError_t e = cudaMemcpy(p.d_rg_items, p.rg_items.data(), p.rg_items.size() * sizeof(int2), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(rgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRgSmem);
+  e = func_attr_once((const void*)rgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRgSmem);
   if (e != cudaSuccess) return e;
   p.rg_ready = true;
   return cudaSuccess;
@@ -2211,11 +2239,9 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
   if (kind == 2) {
     int max_mj = 0;
     for (int j = 0; j < p.n_vx; ++j) max_mj = std::max(max_mj, p.col_off[j + 1] - p.col_off[j]);
-    static bool init = false;
-    if (!init) {
-      cudaError_t e = cudaFuncSetAttribute(colgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCgSmem);
+    {
+      cudaError_t e = func_attr_once((const void*)colgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCgSmem);
       if (e != cudaSuccess) return e;
-      init = true;
     }
     const int ch = colgemm_chunks(p);
     dim3 grid(ch, (max_mj + kCgM - 1) / kCgM, p.n_vx);
@@ -2230,12 +2256,10 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
     const size_t smem = ((size_t)p.Sy << logKT) * 8 + (size_t)p.Sy * 8 + 16;
     return with_log(logSy, [&](auto LN) {
       constexpr int LOGN = decltype(LN)::value;
-      static bool init = false;
-      if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(colfft_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kFftSmem + 16384);
+      {
+        cudaError_t e = func_attr_once((const void*)colfft_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kFftSmem + 16384);
         if (e != cudaSuccess) return e;
-        init = true;
       }
       const int tpc = colfft_tpc(p);
       dim3 grid((p.K >> logKT) / tpc, p.n_vx);
@@ -2323,6 +2347,19 @@ __global__ void oacc_kernel(const float2* __restrict__ op, int tiles, int64_t n_
 cudaError_t launch_oacc(const Plan& p, int tiles, cudaStream_t st) {
   oacc_kernel<<<(unsigned)((p.n_act + 255) / 256), 256, 0, st>>>(p.d_opart, tiles, p.n_act, p.d_oacc);
   return cudaGetLastError();
+}
+
+// o[g] = sum over the partial readouts (fixed order): the rank's spectrum before the NCCL combine
+__global__ void otiles_kernel(const float2* __restrict__ op, int tiles, int64_t n_act, float2* __restrict__ o) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_trigger();
+  pdl_wait();   // partial readouts of the preceding flush / readout kernel
+  if (g < n_act) o[g] = sum_tiles(op, tiles, n_act, g);
+}
+
+cudaError_t launch_otiles(const Plan& p, const float2* op, int tiles, float2* o, cudaStream_t st) {
+  return launch_pdl(otiles_kernel, dim3((unsigned)((p.n_act + 255) / 256)), dim3(256), 0, st, true, op, tiles,
+                    (int64_t)p.n_act, o);
 }
 
 __global__ void scatter_kernel(const float2* __restrict__ op, int tiles, const int32_t* __restrict__ vpos,
@@ -2489,14 +2526,12 @@ static cudaError_t launch_img_fused(const Plan& p, const float2* op, int tiles, 
   constexpr int CS = CS0 < CSMAX ? CS0 : CSMAX;
   constexpr int SX = 1 << LX, SY = 1 << LY;
   constexpr size_t smem = (size_t)(SX * (SY / CS) + SY * (SX / CS) + SX + SY) * 8;
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(img_fused_kernel<LX, LY, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  {
+    cudaError_t e = func_attr_once((const void*)img_fused_kernel<LX, LY, CS>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess && CS > 8)
-      e = cudaFuncSetAttribute(img_fused_kernel<LX, LY, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      e = func_attr_once((const void*)img_fused_kernel<LX, LY, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
-    init = true;
   }
   cudaLaunchConfig_t cfg = {};
   // 512 threads: Medium finalize 12.6 -> 10.6 us, +0.75% end to end against 256 (1024: no better)
@@ -2546,7 +2581,6 @@ bool finalize_uses_fft(const Plan& p) {
 // plan creation), then larger power-of-two images take the row and column passes (>= 128 CTAs
 // each) and other sizes (or WDD_IMG=cufft) cuFFT.
 cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st) {
-  const int64_t S = p.S;
   static const int img_mode = [] {
     const char* e = std::getenv("WDD_IMG");
     return !e ? 0 : std::strcmp(e, "cufft") == 0 ? 1 : std::strcmp(e, "unfused") == 0 ? 2 : std::strcmp(e, "fused") == 0 ? 3 : 0;
@@ -2554,11 +2588,26 @@ cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* 
   const bool own = finalize_uses_fft(p) && img_mode != 1;
   const int fused_max = img_mode == 3 ? 256 : img_mode == 2 ? 0 : 128;
   if (own && p.Sx <= fused_max && p.Sy <= fused_max) return launch_img_fused_dispatch(p, op, tiles, out, st);
-  {
-    cudaError_t e = launch_pdl(scatter_kernel, dim3((unsigned)((p.n_act + 255) / 256)), dim3(256), 0, st, true, op,
-                               tiles, (const int32_t*)p.d_vpos, (int64_t)p.n_act, p.d_spec);
-    if (e != cudaSuccess) return e;
-  }
+  cudaError_t e = launch_spectrum(p, op, tiles, p.d_spec, st);
+  if (e != cudaSuccess) return e;
+  return launch_image(p, p.d_spec, out, st);
+}
+
+// spec[v] = sum of the partial readouts of active v (fixed order); inactive positions of spec are
+// not written (the plan's own spectrum buffer keeps them zero from creation)
+cudaError_t launch_spectrum(const Plan& p, const float2* op, int tiles, float2* spec, cudaStream_t st) {
+  return launch_pdl(scatter_kernel, dim3((unsigned)((p.n_act + 255) / 256)), dim3(256), 0, st, true, op, tiles,
+                    (const int32_t*)p.d_vpos, (int64_t)p.n_act, spec);
+}
+
+// O = conj(IDFT2_unitary(spec)) [/ sqrt(spec[0])] from a dense Sy x Sx spectrum (a8)
+cudaError_t launch_image(const Plan& p, const float2* spec, float2* out, cudaStream_t st) {
+  const int64_t S = p.S;
+  static const int img_mode = [] {
+    const char* e = std::getenv("WDD_IMG");
+    return !e ? 0 : std::strcmp(e, "cufft") == 0 ? 1 : 0;
+  }();
+  const bool own = finalize_uses_fft(p) && img_mode != 1;
   if (own) {
     const int lx = ilog2(p.Sx), ly = ilog2(p.Sy);
     // 2^lr rows per CTA: enough sequences for the threads of the FFT passes, >= 128 CTAs if possible
@@ -2568,7 +2617,7 @@ cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* 
       const size_t smem = ((size_t)p.Sx << lr) * 8 + (size_t)p.Sx * 8 + 16;
       // threads: the larger FFT pass has N1 << lr independent register DFTs
       const int nt = std::max(32, std::min(256, fft::Split<L>::N1 << lr));
-      return launch_pdl(img_rows_kernel<L>, dim3(p.Sy >> lr), dim3(nt), smem, st, true, (const float2*)p.d_spec,
+      return launch_pdl(img_rows_kernel<L>, dim3(p.Sy >> lr), dim3(nt), smem, st, true, spec,
                         (const float2*)p.d_twx, p.d_img_tmp, lr);
     });
     if (e != cudaSuccess) return e;
@@ -2579,14 +2628,14 @@ cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* 
       const int nt = std::max(32, std::min(256, fft::Split<L>::N1 << lc));
       return launch_pdl(img_cols_kernel<L>, dim3(p.Sx >> lc), dim3(nt), smem, st, true, (const float2*)p.d_img_tmp,
                         (const float2*)p.d_twy, out, p.Sx, lc, (float)(1.0 / std::sqrt((double)S)),
-                        (const float2*)p.d_spec, p.normalize);
+                        spec, p.normalize);
     });
   }
   if (cufftSetStream(p.fft, st) != CUFFT_SUCCESS) return cudaErrorUnknown;
-  if (cufftExecC2C(p.fft, reinterpret_cast<cufftComplex*>(p.d_spec), reinterpret_cast<cufftComplex*>(out),
-                   CUFFT_INVERSE) != CUFFT_SUCCESS)
+  if (cufftExecC2C(p.fft, reinterpret_cast<cufftComplex*>(const_cast<float2*>(spec)),
+                   reinterpret_cast<cufftComplex*>(out), CUFFT_INVERSE) != CUFFT_SUCCESS)
     return cudaErrorUnknown;
-  conj_scale_kernel<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(out, S, 1.0 / std::sqrt((double)S), p.d_spec,
+  conj_scale_kernel<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(out, S, 1.0 / std::sqrt((double)S), spec,
                                                                  p.normalize);
   return cudaGetLastError();
 }

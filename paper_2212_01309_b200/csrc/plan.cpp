@@ -290,7 +290,7 @@ wdd_status validate_and_mark(Plan& p, const int32_t* idx, int64_t n) {
 
 // Enqueue the projection of one chunk of already-validated frames; its coefficients land in
 // d_Call at their scan positions (the row DFT of completed rows happens at flush time).
-wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, int64_t nc) {
+wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, int64_t nc, bool first) {
   cudaStream_t st = p.stream;
   bool contiguous = true;
   for (int64_t i = 1; i < nc && contiguous; ++i) contiguous = idx[i] == idx[0] + i;
@@ -306,7 +306,10 @@ wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, in
   }
   {
     Prof pr(p, kSlotProject, st);
-    CUDA_TRY(launch_project(p, frames_dev, nc, C, d_idx, st));
+    // (frames of the first chunk of a call may come from a caller kernel enqueued right before it:
+    // unless the plan was created with ingest_overlap, that launch reads them only after its
+    // predecessor grid has completed; later chunks are ordered behind it)
+    CUDA_TRY(launch_project(p, frames_dev, nc, C, d_idx, st, first && !p.ingest_overlap));
   }
   p.c_fresh = false;
   // The row DFT of completed rows is deferred to the next flush (readout): launched per batch it
@@ -447,6 +450,49 @@ wdd_status materialize_G(Plan& p) {
   return WDD_OK;
 }
 
+// Flush, Wiener readout and (combine && a communicator is attached) the NCCL combine; *op / *tiles
+// receive the partial readouts the image transform sums (tiles rows of n_act, accumulator order).
+//  - G accumulator: the fused partial readouts of the flush (a6 in the rank-update epilogue), or one
+//    readout pass over G when the last flush left none (DFT-matrix flush, nothing flushed);
+//  - spectrum-only accumulator: the running o.
+// Multi-rank ("merge ... sums up the contributions"): combine = 0 sums the partial
+// readouts into o (n_act) and allreduces o -- exact by linearity, K x fewer bytes than G;
+// combine = 1 (north star) allreduces the partial G and runs the readout on the sum.
+wdd_status readout_spectrum(Plan& p, bool combine, const float2** op_out, int* tiles_out) {
+  wdd_status s = flush(p);
+  if (s != WDD_OK) return s;
+  const float2* op = p.d_opart;
+  int tiles = p.opart_tiles;
+  if (p.o_only) {
+    op = p.d_oacc;
+    tiles = 1;
+  } else if (tiles == 0 && !(combine && p.nccl && p.combine == 1)) {
+    if ((s = materialize_G(p)) != WDD_OK) return s;
+    Prof pr(p, kSlotReadout, p.stream);
+    CUDA_TRY(launch_readout(p, p.d_G, p.d_opart, p.stream));
+    p.opart_tiles = tiles = 1;
+  }
+  if (combine && p.nccl) {
+    ncclComm_t comm = reinterpret_cast<ncclComm_t>(p.nccl);
+    if (!p.o_only && p.combine == 1) {
+      if ((s = materialize_G(p)) != WDD_OK) return s;
+      NCCL_TRY(ncclAllReduce(p.d_G, p.d_Gsum, (size_t)p.n_act * p.K * 2, ncclFloat, ncclSum, comm, p.stream));
+      Prof pr(p, kSlotReadout, p.stream);
+      CUDA_TRY(launch_readout(p, p.d_Gsum, p.d_o, p.stream));
+    } else {
+      Prof pr(p, kSlotReadout, p.stream);
+      CUDA_TRY(launch_otiles(p, op, tiles, p.d_o, p.stream));
+    }
+    if (p.o_only || p.combine == 0)
+      NCCL_TRY(ncclAllReduce(p.d_o, p.d_o, (size_t)p.n_act * 2, ncclFloat, ncclSum, comm, p.stream));
+    op = p.d_o;
+    tiles = 1;
+  }
+  *op_out = op;
+  *tiles_out = tiles;
+  return WDD_OK;
+}
+
 void free_plan(Plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
@@ -456,7 +502,7 @@ void free_plan(Plan* p) {
   full_wdd_release(*p);
   void* bufs[] = {p->d_rg_items, p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call, p->d_Call_alt,
                   p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec, p->d_img_tmp,
-                  p->d_meta, p->d_stage[0], p->d_stage[1]};
+                  p->d_meta, p->d_stage[0], p->d_stage[1], p->d_err};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (p->h_meta) cudaFreeHost(p->h_meta);
@@ -493,6 +539,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   if (opts) o = *opts;
   for (int r : o.reserved)
     if (r) return fail(WDD_E_ARG, "opts.reserved must be zero");
+  if (o.ingest_overlap != 0 && o.ingest_overlap != 1) return fail(WDD_E_ARG, "ingest_overlap must be 0 or 1");
   const int Sy = scan_shape[0], Sx = scan_shape[1], Q = det_shape[0];
   if (Sy < 2 || Sx < 2 || (int64_t)Sy * Sx > (1ll << 30)) return fail(WDD_E_ARG, "scan shape %d x %d unsupported", Sy, Sx);
   if (det_shape[1] != Q || !(Q == 32 || Q == 64 || Q == 128 || Q == 256))
@@ -515,6 +562,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   p->step = step_A; p->lambda = probe->wavelength_A; p->alpha = probe->semiangle_rad; p->defocus = probe->defocus_A;
   p->eps = wiener_eps;
   p->o_only = o.accumulator == 1;
+  p->ingest_overlap = o.ingest_overlap;
   p->dq = o.det_px_rad > 0 ? o.det_px_rad / p->lambda : 1.0 / (Q * step_A);  // R17
   p->qa = p->alpha / p->lambda;                                               // R7
   p->R = p->qa / p->dq;
@@ -644,6 +692,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ALLOC(p->d_ones, (size_t)Sy * p->mask_words * sizeof(uint32_t));
   ALLOC(p->d_spec, (size_t)p->S * sizeof(float2));
   ALLOC(p->d_img_tmp, (size_t)p->S * sizeof(float2));
+  ALLOC(p->d_err, sizeof(unsigned));
   ALLOC(p->d_meta, 2 * p->meta_slot_bytes);
 #undef ALLOC
   if (cudaMallocHost(&p->h_meta, 2 * p->meta_slot_bytes) != cudaSuccess)
@@ -668,7 +717,8 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
        cudaMemset(p->d_G, 0, nW * sizeof(float2)) == cudaSuccess &&
        cudaMemset(p->d_Call, 0, (size_t)p->S * K * sizeof(float)) == cudaSuccess &&
        (!p->d_Call_alt || cudaMemset(p->d_Call_alt, 0, (size_t)p->S * K * sizeof(float)) == cudaSuccess) &&
-       cudaMemset(p->d_spec, 0, (size_t)p->S * sizeof(float2)) == cudaSuccess;
+       cudaMemset(p->d_spec, 0, (size_t)p->S * sizeof(float2)) == cudaSuccess &&
+       cudaMemset(p->d_err, 0, sizeof(unsigned)) == cudaSuccess;
   if (!ok) return bail(fail(WDD_E_CUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError())));
   {
     const cudaError_t e = build_bank(*p, q.data(), apiv.rows.data(), apiv.ax_lo, apiv.n_axc, p->d_W, false);
@@ -699,7 +749,7 @@ wdd_status wdd_ingest(wdd_plan_t plan, const void* frames_dev, const int32_t* sc
   const size_t fb = frame_bytes(p);
   for (int64_t c0 = 0; c0 < n; c0 += p.chunk_cap) {
     const int64_t nc = std::min<int64_t>(p.chunk_cap, n - c0);
-    s = enqueue_chunk(p, static_cast<const uint8_t*>(frames_dev) + (size_t)c0 * fb, scan_idx_host + c0, nc);
+    s = enqueue_chunk(p, static_cast<const uint8_t*>(frames_dev) + (size_t)c0 * fb, scan_idx_host + c0, nc, c0 == 0);
     if (s != WDD_OK) return s;
   }
   p.frames_ingested += n;
@@ -734,7 +784,7 @@ wdd_status wdd_ingest_host(wdd_plan_t plan, const void* frames_host, const int32
                              cudaMemcpyHostToDevice, p.copy_stream));
     CUDA_TRY(cudaEventRecord(p.copy_ev[slot], p.copy_stream));
     CUDA_TRY(cudaStreamWaitEvent(p.stream, p.copy_ev[slot], 0));
-    s = enqueue_chunk(p, p.d_stage[slot], scan_idx_host + c0, nc);
+    s = enqueue_chunk(p, p.d_stage[slot], scan_idx_host + c0, nc, true);   // (after a copy: no PDL overlap anyway)
     if (s != WDD_OK) return s;
     CUDA_TRY(cudaEventRecord(p.stage_ev[slot], p.stream));
   }
@@ -749,48 +799,37 @@ wdd_status wdd_readout(wdd_plan_t plan, void* complex_out_dev) {
   Plan& p = *P(plan);
   if (!complex_out_dev) return fail(WDD_E_ARG, "NULL output");
   CUDA_TRY(cudaSetDevice(p.device));
-  wdd_status s = flush(p);
+  const float2* op = nullptr;
+  int tiles = 0;
+  wdd_status s = readout_spectrum(p, /*combine*/ true, &op, &tiles);
   if (s != WDD_OK) return s;
-  const float2* op = p.d_opart;
-  int tiles = p.opart_tiles;
-  if (p.o_only) {
-    op = p.d_oacc;
-    tiles = 1;
-    if (p.nranks > 1) {   // sum the ranks' running spectra (a copy: the running sum stays per rank)
-      CUDA_TRY(cudaMemcpyAsync(p.d_o, p.d_oacc, (size_t)p.n_act * sizeof(float2), cudaMemcpyDeviceToDevice, p.stream));
-      NCCL_TRY(ncclAllReduce(p.d_o, p.d_o, (size_t)p.n_act * 2, ncclFloat, ncclSum, reinterpret_cast<ncclComm_t>(p.nccl),
-                             p.stream));
-      op = p.d_o;
-    }
-  } else if (p.nranks > 1) {
-    // multi-rank: every rank reduces its partial accumulator the same way, then NCCL sums
-    if ((s = materialize_G(p)) != WDD_OK) return s;
-    const float2* G = p.d_G;
-    if (p.combine == 1) {
-      NCCL_TRY(ncclAllReduce(p.d_G, p.d_Gsum, (size_t)p.n_act * p.K * 2, ncclFloat, ncclSum,
-                             reinterpret_cast<ncclComm_t>(p.nccl), p.stream));
-      G = p.d_Gsum;
-    }
-    {
-      Prof pr(p, kSlotReadout, p.stream);
-      CUDA_TRY(launch_readout(p, G, p.d_o, p.stream));
-    }
-    if (p.combine == 0)
-      NCCL_TRY(ncclAllReduce(p.d_o, p.d_o, (size_t)p.n_act * 2, ncclFloat, ncclSum,
-                             reinterpret_cast<ncclComm_t>(p.nccl), p.stream));
-    op = p.d_o;
-    tiles = 1;
-  } else if (tiles == 0) {
-    // no fused partial readout for the current G (after a DFT-matrix flush, or nothing flushed)
-    if ((s = materialize_G(p)) != WDD_OK) return s;
-    Prof pr(p, kSlotReadout, p.stream);
-    CUDA_TRY(launch_readout(p, p.d_G, p.d_opart, p.stream));
-    p.opart_tiles = tiles = 1;
-  }
-  {
-    Prof pr(p, kSlotFinalize, p.stream);
-    CUDA_TRY(launch_finalize(p, op, tiles, static_cast<float2*>(complex_out_dev), p.stream));
-  }
+  Prof pr(p, kSlotFinalize, p.stream);
+  CUDA_TRY(launch_finalize(p, op, tiles, static_cast<float2*>(complex_out_dev), p.stream));
+  return WDD_OK;
+}
+
+wdd_status wdd_readout_spectrum(wdd_plan_t plan, void* spectrum_out_dev, int32_t combine) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (!spectrum_out_dev) return fail(WDD_E_ARG, "NULL output");
+  CUDA_TRY(cudaSetDevice(p.device));
+  const float2* op = nullptr;
+  int tiles = 0;
+  wdd_status s = readout_spectrum(p, combine != 0, &op, &tiles);
+  if (s != WDD_OK) return s;
+  CUDA_TRY(cudaMemsetAsync(spectrum_out_dev, 0, (size_t)p.S * sizeof(float2), p.stream));
+  CUDA_TRY(launch_spectrum(p, op, tiles, static_cast<float2*>(spectrum_out_dev), p.stream));
+  return WDD_OK;
+}
+
+wdd_status wdd_image_from_spectrum(wdd_plan_t plan, const void* spectrum_dev, void* complex_out_dev) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (!spectrum_dev || !complex_out_dev) return fail(WDD_E_ARG, "NULL buffer");
+  if (spectrum_dev == complex_out_dev) return fail(WDD_E_ARG, "spectrum and image must not alias");
+  CUDA_TRY(cudaSetDevice(p.device));
+  Prof pr(p, kSlotFinalize, p.stream);
+  CUDA_TRY(launch_image(p, static_cast<const float2*>(spectrum_dev), static_cast<float2*>(complex_out_dev), p.stream));
   return WDD_OK;
 }
 
@@ -808,6 +847,7 @@ wdd_status wdd_readout_host(wdd_plan_t plan, void* complex_out_host) {
   }
   cudaFreeAsync(d, p.stream);
   CUDA_TRY(cudaStreamSynchronize(p.stream));
+  if (s == WDD_OK && p.dtype == 1) s = wdd_check(plan);   // (host readout synchronises anyway)
   return s;
 }
 
@@ -870,7 +910,7 @@ wdd_status wdd_set_comm(wdd_plan_t plan, int32_t nranks, int32_t rank, const uin
   }
   p.nranks = nranks;
   p.rank = rank;
-  if (nranks == 1) return WDD_OK;
+  // (a one-rank communicator too: the combine path then runs exactly as on N ranks)
   ncclUniqueId u;
   std::memcpy(&u, id, 128);
   ncclComm_t c;
@@ -936,7 +976,7 @@ wdd_status wdd_project(wdd_plan_t plan, const void* frames_dev, int64_t n, void*
   CUDA_TRY(cudaSetDevice(p.device));
   Prof pr(p, kSlotProject, reinterpret_cast<cudaStream_t>(stream));
   CUDA_TRY(launch_project(p, frames_dev, n, static_cast<float*>(C_out_dev), nullptr,
-                          reinterpret_cast<cudaStream_t>(stream)));
+                          reinterpret_cast<cudaStream_t>(stream), /*wait_start*/ true));
   return WDD_OK;
 }
 
@@ -1020,6 +1060,22 @@ wdd_status wdd_graph_launch(wdd_plan_t plan, int64_t graph_handle, void* stream)
   CUDA_TRY(cudaSetDevice(p.device));
   use_stream(p, reinterpret_cast<cudaStream_t>(stream));
   CUDA_TRY(cudaGraphLaunch(p.graphs[(size_t)graph_handle], p.stream));
+  return WDD_OK;
+}
+
+wdd_status wdd_check(wdd_plan_t plan) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (p.capturing) return fail(WDD_E_STATE, "wdd_check cannot be captured");
+  CUDA_TRY(cudaSetDevice(p.device));
+  CUDA_TRY(cudaStreamSynchronize(p.stream));
+  unsigned f = 0;
+  CUDA_TRY(cudaMemcpy(&f, p.d_err, sizeof f, cudaMemcpyDeviceToHost));
+  if (f) {
+    CUDA_TRY(cudaMemset(p.d_err, 0, sizeof f));
+    return fail(WDD_E_RANGE, "float32 frames with values the fp16 hi/lo split cannot hold (|x| > 65504 or not "
+                "finite) were ingested since the last check; their coefficients are not valid");
+  }
   return WDD_OK;
 }
 

@@ -33,7 +33,8 @@ class _Probe(ctypes.Structure):
 class _Opts(ctypes.Structure):
     _fields_ = [("det_px_rad", ctypes.c_double), ("sigma_px", ctypes.c_double),
                 ("dtype", ctypes.c_int32), ("normalize", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("combine", ctypes.c_int32), ("accumulator", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("combine", ctypes.c_int32), ("accumulator", ctypes.c_int32), ("ingest_overlap", ctypes.c_int32),
+                ("k_shards", ctypes.c_int32), ("k_rank", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class _Info(ctypes.Structure):
@@ -65,6 +66,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "wdd_ingest_host": [P, V, ctypes.POINTER(I32), I64, V],
             "wdd_readout": [P, V],
             "wdd_readout_host": [P, V],
+            "wdd_readout_spectrum": [P, V, I32],
+            "wdd_image_from_spectrum": [P, V, V],
+            "wdd_check": [P],
             "wdd_destroy": [P],
             "wdd_get_accumulator": [P, V, ctypes.POINTER(I32), ctypes.POINTER(I64)],
             "wdd_full_wdd": [P, V, V, V],
@@ -133,7 +137,8 @@ class Plan:
     def __init__(self, scan_shape, step_A: float, det_shape, K: int, wavelength_A: float,
                  semiangle_rad: float, defocus_A: float = 0.0, wiener_eps: float = 1e-3, *,
                  dtype: str = "u16", normalize: bool = False, device: int = 0, sigma_px: float = 0.0,
-                 det_px_rad: float = 0.0, combine: int = 0, accumulator: str = "G"):
+                 det_px_rad: float = 0.0, combine: int = 0, accumulator: str = "G",
+                 ingest_overlap: bool = False, k_shards: int = 0, k_rank: int = 0):
         lib = load_library()
         scan = (ctypes.c_int32 * 2)(*[int(v) for v in scan_shape])
         det = (ctypes.c_int32 * 2)(*[int(v) for v in det_shape])
@@ -146,6 +151,9 @@ class Plan:
         opts.device = int(device)
         opts.combine = int(combine)
         opts.accumulator = {"G": 0, "spectrum": 1}[accumulator]
+        opts.ingest_overlap = int(bool(ingest_overlap))
+        opts.k_shards = int(k_shards)
+        opts.k_rank = int(k_rank)
         h = ctypes.c_void_p()
         _check(lib.wdd_plan_create(scan, float(step_A), det, int(K), ctypes.byref(probe), float(wiener_eps),
                                    ctypes.byref(opts), ctypes.byref(h)))
@@ -214,8 +222,36 @@ class Plan:
         import torch
         if out is None:
             out = torch.empty((self.Sy, self.Sx), dtype=torch.complex64, device=f"cuda:{self.device}")
+        self._check_out(out)
         _check(self._lib.wdd_readout(self._h, _ptr(out)))
         return out
+
+    def readout_spectrum(self, out=None, combine: bool = True):
+        """o_v (Sy x Sx complex64, FFT order, 0 at inactive v): combined over ranks, or this rank's own."""
+        import torch
+        if out is None:
+            out = torch.empty((self.Sy, self.Sx), dtype=torch.complex64, device=f"cuda:{self.device}")
+        self._check_out(out)
+        _check(self._lib.wdd_readout_spectrum(self._h, _ptr(out), int(bool(combine))))
+        return out
+
+    def image_from_spectrum(self, spectrum, out=None):
+        import torch
+        self._check_out(spectrum)
+        if out is None:
+            out = torch.empty((self.Sy, self.Sx), dtype=torch.complex64, device=f"cuda:{self.device}")
+        self._check_out(out)
+        _check(self._lib.wdd_image_from_spectrum(self._h, _ptr(spectrum), _ptr(out)))
+        return out
+
+    def check(self):
+        """Synchronise and raise WddError(WDD_E_RANGE) if out-of-range float32 frames were ingested."""
+        _check(self._lib.wdd_check(self._h))
+
+    def _check_out(self, t):
+        if tuple(t.shape) != (self.Sy, self.Sx) or "complex64" not in str(t.dtype) or not t.is_cuda \
+                or not t.is_contiguous():
+            raise ValueError(f"expected a contiguous ({self.Sy}, {self.Sx}) complex64 device tensor")
 
     def readout_host(self, out: Optional[np.ndarray] = None) -> np.ndarray:
         if out is None:
@@ -271,8 +307,11 @@ class Plan:
     def project(self, frames, out=None, stream=None):
         import torch
         n = frames.shape[0]
+        self._check_frames(frames, n, True)
         if out is None:
             out = torch.empty((n, self.K), dtype=torch.float32, device=frames.device)
+        if tuple(out.shape) != (n, self.K) or out.dtype != torch.float32 or not out.is_cuda or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous ({n}, {self.K}) float32 device tensor")
         _check(self._lib.wdd_project(self._h, _ptr(frames), n, _ptr(out), _stream(stream)))
         return out
 

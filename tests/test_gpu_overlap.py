@@ -22,15 +22,12 @@ def env():
     return torch, wdd
 
 
-@pytest.mark.parametrize("name", ["medium", "large"])
-def test_overlapped_acquisitions_match_isolated(env, name):
-    torch, wdd = env
+def _check_overlap(torch, wdd, cfg, batch, n_acq):
     from synth.sparse import dense_frames_torch, sparse_events
-    cfg = CONFIGS[name]
     idx = np.arange(cfg.S)
-    b = cfg.batch or 16384
-    acqs = [dense_frames_torch(*sparse_events(seed, idx, cfg.Q), cfg.Q, "cuda") for seed in (11, 12, 13)]
-    plan = wdd.Plan.from_config(cfg)
+    b = batch
+    acqs = [dense_frames_torch(*sparse_events(seed, idx, cfg.Q), cfg.Q, "cuda") for seed in range(11, 11 + n_acq)]
+    plan = wdd.Plan.from_config(cfg, ingest_overlap=True)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
@@ -56,7 +53,7 @@ def test_overlapped_acquisitions_match_isolated(env, name):
     for k, out in enumerate(outs):
         assert np.array_equal(out.cpu().numpy(), iso[k]), ("eager", k)
 
-    # one graph holding the three acquisitions, replayed twice
+    # one graph holding the acquisitions, replayed twice
     gouts = [torch.empty((cfg.Sy, cfg.Sx), dtype=torch.complex64, device="cuda") for _ in acqs]
     plan.capture_begin(stream)
     for fr, out in zip(acqs, gouts):
@@ -71,3 +68,36 @@ def test_overlapped_acquisitions_match_isolated(env, name):
             assert np.array_equal(out.cpu().numpy(), iso[k]), ("graph", k)
     plan.sync()
     torch.cuda.set_stream(torch.cuda.default_stream())
+
+
+@pytest.mark.parametrize("name", ["medium", "large"])
+def test_overlapped_acquisitions_match_isolated(env, name):
+    torch, wdd = env
+    cfg = CONFIGS[name]
+    _check_overlap(torch, wdd, cfg, cfg.batch or 16384, 3)
+
+
+@pytest.mark.parametrize("Sy,Sx,batch", [(2, 2, 1), (2, 2, 4), (16, 16, 32), (32, 32, 1024)])
+def test_many_small_overlapped_acquisitions(env, Sy, Sx, batch):
+    # small scans: the first projection of an acquisition does not fill the GPU, so nothing but
+    # the launch protocol keeps acquisition k + 2's projection from writing the coefficient store
+    # that acquisition k's row FFT still reads (the row FFT triggers its dependents only once its
+    # C tiles are in shared memory)
+    torch, wdd = env
+    _check_overlap(torch, wdd, CONFIGS["medium"].with_(Sy=Sy, Sx=Sx), batch, 12)
+
+
+def test_overlapped_acquisitions_without_wide_first_launch():
+    # WDD_PROJ_WIDE_FIRST=0: the first projection of an acquisition takes the narrow grid (the
+    # environment knob is read once per process, hence the subprocess)
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import torch, paper_2212_01309_b200 as w; from synth import CONFIGS; "
+            "import tests.test_gpu_overlap as t; "
+            "t._check_overlap(torch, w, CONFIGS['medium'].with_(Sy=32, Sx=32), 256, 12); "
+            "t._check_overlap(torch, w, CONFIGS['medium'], 512, 4); print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, WDD_PROJ_WIDE_FIRST="0"))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]

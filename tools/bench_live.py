@@ -40,7 +40,7 @@ def main():
     pool = torch.cat([dense_frames_torch(pix[a:a + 4096], cnt[a:a + 4096], cfg.Q, "cuda")
                       for a in range(0, pool_n, 4096)])
     frame_bytes = cfg.Q * cfg.Q * 2
-    plan = wdd.Plan.from_config(cfg, accumulator=args.accumulator)
+    plan = wdd.Plan.from_config(cfg, accumulator=args.accumulator, ingest_overlap=True)
     info = plan.info()
     st = torch.cuda.Stream()
     torch.cuda.set_stream(st)

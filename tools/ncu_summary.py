@@ -15,7 +15,7 @@ want = [
     ("gpu__time_duration.sum", "duration"),
     ("dram__bytes_read.sum", "dram read"),
     ("dram__bytes_write.sum", "dram write"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram throughput % of peak"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram throughput % of peak"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active %"),
     ("sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active", "tc pipe inst %"),
@@ -28,13 +28,19 @@ want = [
     ("smsp__inst_executed.sum", "instructions (warp)"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
 ]
-stall = [i for i, x in enumerate(h) if x.startswith("smsp__average_warp_latency_issue_stalled_") and x.endswith(".ratio")]
+# warp-stall breakdown: warps stalled on each reason per issue-active cycle (ncu's "Warp State")
+SP, SS = "smsp__average_warps_issue_stalled_", "_per_issue_active.ratio"
+stall = [i for i, x in enumerate(h) if x.startswith(SP) and x.endswith(SS)]
 for r in rows[2:]:
     print("==", r[h.index("Kernel Name")][:110])
     for key, label in want:
         if key in h:
             i = h.index(key)
             print(f"  {label:28s} {r[i]:>14s} {units[i]}")
-    st = sorted(((float(r[i] or 0), h[i].replace("smsp__average_warp_latency_issue_stalled_", "").replace(".ratio", ""))
-                 for i in stall), reverse=True)[:5]
-    print("  top stalls (cycles/instr):  " + ", ".join(f"{n} {v:.2f}" for v, n in st))
+    def num(s):
+        try:
+            return float(str(s).replace(",", ""))
+        except ValueError:
+            return 0.0
+    st = sorted(((num(r[i]), h[i][len(SP):-len(SS)]) for i in stall), reverse=True)[:6]
+    print("  top stalls (warps/issue):   " + ", ".join(f"{n} {v:.2f}" for v, n in st))

@@ -34,7 +34,7 @@ def main():
     pool_n = min(n, max(args.pool, batch))
     pool = torch.cat([dense_frames_torch(*sparse_events(7, np.arange(a, min(pool_n, a + 4096)), cfg.Q), cfg.Q, "cuda")
                       for a in range(0, pool_n, 4096)])
-    plan = wdd.Plan.from_config(cfg, accumulator=args.accumulator)
+    plan = wdd.Plan.from_config(cfg, accumulator=args.accumulator, ingest_overlap=True)
     st = torch.cuda.Stream()
     torch.cuda.set_stream(st)
     out = torch.empty((cfg.Sy, cfg.Sx), dtype=torch.complex64, device="cuda")

@@ -35,7 +35,7 @@ def main():
     else:
         fr = Acquisition(cfg).frames_parallel(idx)
     dev = torch.from_numpy(fr).cuda()
-    plan = wdd.Plan.from_config(cfg)
+    plan = wdd.Plan.from_config(cfg, ingest_overlap=True)
     s = torch.cuda.Stream()
     torch.cuda.set_stream(s)
     for rep in range(args.reps):

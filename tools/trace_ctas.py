@@ -27,7 +27,7 @@ def main():
     fr = rng.poisson(0.2, size=(n, cfg.Q, cfg.Q)).astype(np.uint16)
     dev = torch.from_numpy(fr).cuda()
     idx = np.arange(n, dtype=np.int32)
-    plan = wdd.Plan.from_config(cfg)
+    plan = wdd.Plan.from_config(cfg, ingest_overlap=True)
     s = torch.cuda.Stream()
     buf = (ctypes.c_ulonglong * (8192 * 5))()
     torch.cuda.set_stream(s)

@@ -21,7 +21,7 @@ def main():
     rng = np.random.default_rng(0)
     fr = rng.poisson(2.0, size=(n, cfg.Q, cfg.Q)).astype(np.uint16)
     dev = torch.from_numpy(fr).cuda()
-    plan = wdd.Plan.from_config(cfg)
+    plan = wdd.Plan.from_config(cfg, ingest_overlap=True)
     out = torch.empty((n, cfg.K), device="cuda")
     for _ in range(2):
         buf = (ctypes.c_ulonglong * 65536)()
