@@ -60,7 +60,9 @@ struct Plan {
                                       // them, so the next acquisition's projection may overlap
                                       // (PDL) the previous acquisition's readout, which still
                                       // reads the old store
-  bool c_fresh = false;               // d_Call was swapped in by the last reset (not yet written)
+  bool c_fresh = false;               // d_Call was swapped in by the last reset (not yet written) and
+                                      // its first projection may be PDL-launched (see wdd_reset)
+  bool c_read_since_swap = false;     // a row transform (reader of d_Call) was launched since the last swap
   int32_t* d_act_vy = nullptr;
   int32_t* d_col_off = nullptr;
   int32_t* d_vpos = nullptr;          // n_act flattened v (scatter positions)

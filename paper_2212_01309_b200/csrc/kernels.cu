@@ -997,21 +997,24 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
   float2* x = fsm;                       // [Sx][P]
   float2* stw = fsm + (Sx << logP);      // [Sx] twiddles
   const int r = blockIdx.y, k0 = blockIdx.x * 2 * P;
-  // (no early trigger: this kernel reads the coefficient store, and the next acquisition's first
-  // projection may be PDL-launched into the same store two acquisitions later -- the dependents of
-  // this grid launch only after every CTA has its C tile in shared memory, below)
+  // use_tma bit 1 (set when this grid is itself PDL-launched): no early trigger -- this kernel reads
+  // the coefficient store, which the first projection of the acquisition after next overwrites, so
+  // the dependents of this grid launch only once every CTA has its C tile in shared memory (below).
+  // An ordinary (non-PDL) launch of this kernel starts after all earlier work has completed, which
+  // already orders it after every earlier read of C; its dependents may then launch at once.
+  if (!(use_tma & 2)) pdl_trigger();
   for (int i = threadIdx.x; i < Sx; i += blockDim.x) stw[i] = __ldg(tw + i);
   for (int j = threadIdx.x; j < n_vx; j += blockDim.x) {
     const int v = __ldg(col_vx + j);
     sslot[j] = make_int2(fft::fslot<LOGN>(v), fft::fslot<LOGN>((Sx - v) & (Sx - 1)));
   }
-  if (use_tma && threadIdx.x == 0) {
+  if ((use_tma & 1) && threadIdx.x == 0) {
     mbar_init(&lbar, 1);
     fence_mbar_init();
   }
   pdl_wait();   // C of the projection kernels (and the uploaded row list / masks)
   const int sy = rows[r];
-  if (use_tma) {
+  if (use_tma & 1) {
     // the CTA's whole Sx x 2P slice of C in flight at once (one or two TMA boxes, pitch 2P floats =
     // the FFT's [Sx][P] layout); positions outside the pending mask are zeroed afterwards
     if (threadIdx.x == 0) {
@@ -1025,7 +1028,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
       if (!((smask[sx >> 5] >> (sx & 31)) & 1u))
         for (int pp = 0; pp < P; ++pp) x[(sx << logP) + pp] = make_float2(0.f, 0.f);
     __syncthreads();
-    pdl_trigger();   // every read of C by this CTA is complete
+    if (use_tma & 2) pdl_trigger();   // every read of C by this CTA is complete
   } else {
   if (threadIdx.x < mask_words) smask[threadIdx.x] = masks[(int64_t)r * mask_words + threadIdx.x];
   __syncthreads();
@@ -1057,7 +1060,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
     }
   }
   __syncthreads();
-  pdl_trigger();   // every read of C by this CTA is complete
+  if (use_tma & 2) pdl_trigger();   // every read of C by this CTA is complete
   }
   fft::fft_seq<LOGN>(x, stw, logP);
   const float hs = 0.5f * scale;
@@ -1364,7 +1367,7 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
                                 (uint32_t)std::min(p.Sx, 256));
       return launch_pdl(rowfft_kernel<LOGN>, grid, dim3(nt), smem, st, rowfft_pdl, (const float*)p.d_Call, rows, masks,
                         p.mask_words, (const float2*)p.d_twx, (const int32_t*)p.d_col_vx, p.d_R, logP, p.Sy, p.K,
-                        p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, tma ? 1 : 0);
+                        p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0));
     });
   }
   {

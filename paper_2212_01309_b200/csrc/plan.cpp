@@ -366,6 +366,7 @@ wdd_status stage_rows(Plan& p, const std::vector<int32_t>& rows_in) {
   }
   Prof pr(p, kSlotRowDft, p.stream);
   CUDA_TRY(launch_rowdft(p, dr, dm, n_rows, p.stream));
+  p.c_read_since_swap = true;
   return WDD_OK;
 }
 
@@ -435,6 +436,7 @@ wdd_status form_G(Plan& p) {
   if (s != WDD_OK) return s;
   const int32_t* dr = static_cast<const int32_t*>(d);
   CUDA_TRY(launch_rowdft(p, dr, reinterpret_cast<const uint32_t*>(dr + mask_off), n_rows, p.stream));
+  p.c_read_since_swap = true;
   CUDA_TRY(launch_flush(p, dr, n_rows, /*overwrite*/ true, p.stream, false));
   return WDD_OK;
 }
@@ -882,9 +884,15 @@ wdd_status wdd_reset(wdd_plan_t plan) {
   std::fill(p.pending.begin(), p.pending.end(), 0u);
   if (p.d_Call_alt && p.frames_ingested > 0) {
     // the previous acquisition's flush / readout may still read the current store: the next
-    // acquisition writes the other one, so its first projection need not wait for them
+    // acquisition writes the other one, so its first projection need not wait for them.  That
+    // store was last read by the row transform of the acquisition before the previous one; the
+    // first projection may overlap (PDL) the previous readout only if a row transform of the
+    // previous acquisition lies in between: that launch is ordered after every earlier read of C
+    // (a PDL-launched row FFT triggers its dependents only after its own C loads, an ordinary
+    // launch starts after all earlier work), and the projection is downstream of it
     std::swap(p.d_Call, p.d_Call_alt);
-    p.c_fresh = true;
+    p.c_fresh = p.c_read_since_swap;
+    p.c_read_since_swap = false;
   }
   p.frames_ingested = 0;
   return WDD_OK;

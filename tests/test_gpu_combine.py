@@ -67,7 +67,7 @@ def test_one_rank_comm_readout_matches_oracle(env, name, combine, accumulator):
     cfg, idx, fr, ref = _cached(name)
     plan = _comm_plan(wdd, cfg, combine=combine, accumulator=accumulator)
     dev = torch.from_numpy(np.ascontiguousarray(fr)).cuda()
-    b = cfg.batch or 256
+    b = min(cfg.batch or 256, cfg.S // 4)
     half = (cfg.S // 2) // b * b
     for a in range(0, half, b):
         plan.ingest(dev[a:a + b], idx[a:a + b])
