@@ -148,9 +148,10 @@ wdd_status wdd_readout_host(wdd_plan_t plan, void* complex_out_host);
 /* Release every resource of the plan (synchronises its stream first).  NULL is a no-op. */
 wdd_status wdd_destroy(wdd_plan_t plan);
 
-/* Flush staged rows and copy this rank's accumulator G (n_act x K complex64, accumulator order)
- * into G_out_dev (DEVICE, may be NULL) and the active list (flattened v = vy*Sx + vx, int32, in
- * the same order) into active_v_host (HOST, may be NULL).  *n_act receives n_act. */
+/* Flush staged rows and copy this rank's accumulator G (n_act x K complex64, accumulator order;
+ * shard plans: n_act x k_count, their coefficients only) into G_out_dev (DEVICE, may be NULL) and
+ * the active list (flattened v = vy*Sx + vx, int32, in the same order) into active_v_host (HOST,
+ * may be NULL).  *n_act receives n_act.  Collective in a shard group with a communicator. */
 wdd_status wdd_get_accumulator(wdd_plan_t plan, void* G_out_dev, int32_t* active_v_host,
                                int64_t* n_act);
 
@@ -170,6 +171,39 @@ wdd_status wdd_reset(wdd_plan_t plan);
 wdd_status wdd_nccl_get_unique_id(uint8_t id[128]);
 wdd_status wdd_set_comm(wdd_plan_t plan, int32_t nranks, int32_t rank, const uint8_t id[128]);
 
+/* ----------------------- coefficient-sharded rank groups -----------------------
+ * A plan created with opts.k_shards = n > 1, opts.k_rank = r owns the coefficient rows a in
+ * [floor(r L / n), floor((r+1) L / n)) of H(I) (k = a*L + b): its coefficient store, row staging R,
+ * accumulator G and Wiener bank hold only those k_count = (a1 - a0) L coefficients.  Every rank
+ * ingests its own frames (any partition of the scan: contiguous rows, round-robin batches) and the
+ * projection kernel stores each frame's coefficient rows of shard o straight into rank o's store
+ * (peer memory over NVLink / NVSwitch: the exchange is fused into the projection's epilogue, about
+ * 4K (n-1)/n bytes per frame against the frame's 2 Q^2).  At readout every rank flushes and reads
+ * out its own coefficients over the whole scan, o_v = sum_{k in shard} G[v,k] K_v[k], and the NCCL
+ * allreduce of o sums the shards (P:522-523 is a sum over k; P:536, P:542 merge by summation), so
+ * the per-rank readout cost is 1/n of the single-GPU one.
+ * Protocol: every rank creates the plan with the same geometry and its own k_rank, calls
+ * wdd_set_comm (all ranks), exchanges store handles (wdd_shard_store_handle -> all-gather ->
+ * wdd_set_shard_peers) and then, for each acquisition: wdd_reset (collective in a shard group),
+ * wdd_ingest of its own frames, wdd_ingest_remote of every other rank's scan positions (host
+ * bookkeeping only: those coefficients arrive from the peers), wdd_readout (collective; a barrier
+ * collective orders every rank's projections before the flush reads the store).
+ * In one process (tests, or several devices of one process) wdd_link_shards replaces the handle
+ * exchange; without a communicator the caller orders ingests before readouts (e.g. one stream or a
+ * device synchronisation) and combines wdd_readout_spectrum(..., combine = 0) itself. */
+
+/* Positions ingested by other ranks of the plan's shard group (validated like wdd_ingest: range,
+ * duplicates; the whole call is rejected on error).  Host bookkeeping only. */
+wdd_status wdd_ingest_remote(wdd_plan_t plan, const int32_t* scan_idx_host, int64_t n);
+/* IPC handle (64 bytes, cudaIpcGetMemHandle) of the plan's coefficient-store allocation. */
+wdd_status wdd_shard_store_handle(wdd_plan_t plan, uint8_t handle[64]);
+/* handles: nshard x 64 bytes, rank order (this rank's own entry is ignored); opens the peers'
+ * stores in this process (cudaIpcOpenMemHandle).  nshard / rank must match the plan's options. */
+wdd_status wdd_set_shard_peers(wdd_plan_t plan, int32_t nshard, int32_t rank, const uint8_t* handles);
+/* Single process: plans[r] is shard r of nshard (same geometry); links their stores directly
+ * (enables peer access between distinct devices). */
+wdd_status wdd_link_shards(int32_t nshard, const wdd_plan_t* plans);
+
 /* Thread-local description of the last error (never NULL). */
 const char* wdd_last_error(void);
 
@@ -182,6 +216,8 @@ typedef struct {
   int64_t frames_ingested;
   int32_t nranks, rank;
   int32_t proj_ctas_per_sm;   /* resident projection CTAs per SM (occupancy query; 2 = lean variant) */
+  int32_t k_shards, k_rank;   /* coefficient shard group (1, 0 when unsharded)                         */
+  int32_t k_lo, k_count;      /* this plan's coefficients k_lo .. k_lo + k_count - 1 (G, bank, store)  */
   int32_t reserved0;
 } wdd_plan_info;
 wdd_status wdd_get_info(wdd_plan_t plan, wdd_plan_info* info);

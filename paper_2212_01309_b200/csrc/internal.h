@@ -15,9 +15,30 @@ struct FullWddWork;   // fullwdd.cu: scratch + cuFFT plans of wdd_full_wdd, kept
 
 enum ProfSlot { kSlotProject = 0, kSlotRowDft = 1, kSlotFlush = 2, kSlotReadout = 3, kSlotFinalize = 4, kNumSlots = 5 };
 
+constexpr int kMaxShards = 8;        // coefficient shards (ranks) a projection can write to
+
+// Destinations of the projection's coefficient rows: a = n_x row of H(I) (k = a*L + b) goes to
+// shard o with alo[o] <= a < alo[o+1], at C[o] + position * K[o] + (a - alo[o]) * L.
+struct ProjDst {
+  int n = 1;
+  float* C[kMaxShards] = {};
+  int K[kMaxShards] = {};
+  int alo[kMaxShards + 1] = {};
+};
+
 struct Plan {
   // geometry
   int Sy = 0, Sx = 0, Q = 0, L = 0, K = 0, dtype = 0, normalize = 0, device = 0, combine = 0;
+  // coefficient sharding (opts.k_shards): this plan owns rows a in [a_split[shard],
+  // a_split[shard+1]) of every frame's H(I), i.e. the Kl = (a1 - a0) * L coefficients from k0; its
+  // coefficient store, R, G, bank and readout cover only those.  Unsharded: nshard = 1, Kl = K.
+  int nshard = 1, shard = 0, Kl = 0, k0 = 0;
+  std::vector<int> a_split;            // nshard + 1
+  float* peer_base[kMaxShards] = {};   // each shard's store allocation (2 x S x Kl_o), this process's view
+  bool peers_ipc[kMaxShards] = {};     // opened with cudaIpcOpenMemHandle (closed at destroy)
+  bool peers_ready = false;
+  int store_par = 0;                   // which of the two stores is current (flips at every swap)
+  float* d_Cbase = nullptr;            // the allocation holding both coefficient stores
   int64_t S = 0, n_act = 0;
   int n_vx = 0;
   double step = 0, lambda = 0, alpha = 0, defocus = 0, eps = 0, dq = 0, qa = 0, R = 0, sigma = 0;
@@ -63,6 +84,7 @@ struct Plan {
   bool c_fresh = false;               // d_Call was swapped in by the last reset (not yet written) and
                                       // its first projection may be PDL-launched (see wdd_reset)
   bool c_read_since_swap = false;     // a row transform (reader of d_Call) was launched since the last swap
+  bool barrier_since_swap = false;    // shard groups: a readout barrier collective since the last swap
   int32_t* d_act_vy = nullptr;
   int32_t* d_col_off = nullptr;
   int32_t* d_vpos = nullptr;          // n_act flattened v (scatter positions)
@@ -125,10 +147,12 @@ struct Plan {
 
 // ---- kernel launchers (kernels.cu); return cudaError_t of the launch
 // projection of n frames; C row of frame f = idx ? idx[f] : f (idx: device array or null)
-// wait_start: the kernel waits for the preceding grid before reading frames (the frames may be
-// produced by a caller kernel right before the ingest); else frames are read at once (ingest_overlap)
-cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* C, const int32_t* idx,
-                           cudaStream_t st, bool wait_start);
+// projection of n frames; scan position of frame f = idx ? idx[f] : pos0 + f (idx: device array or
+// null); coefficient rows go to `dst`.  wait_start: the kernel waits for the preceding grid before
+// reading frames (the frames may be produced by a caller kernel right before the ingest); else
+// frames are read at once (ingest_overlap)
+cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, const ProjDst& dst, const int32_t* idx,
+                           int64_t pos0, cudaStream_t st, bool wait_start);
 // cudaFuncSetAttribute once per (device, kernel, attribute, value); thread-safe
 cudaError_t func_attr_once(const void* fn, cudaFuncAttribute attr, int value);
 // row DFT (a4) of the listed scan rows from the pending positions of d_Call (masks: n_rows x
@@ -152,6 +176,9 @@ int colfft_tiles(const Plan& p);
 bool finalize_uses_fft(const Plan& p);
 // o[g] = sum_k G[g][k] W[g][k] (one warp per active v)
 cudaError_t launch_readout(const Plan& p, const float2* G, float2* o, cudaStream_t st);
+// an ordinary (non-PDL) launch of an empty kernel that triggers nothing early: every later kernel
+// starts after all earlier work on the stream has completed (around the shard barrier collective)
+cudaError_t launch_fence(cudaStream_t st);
 // image from the partial readouts op[tiles][n_act] (summed over tiles in order)
 cudaError_t launch_finalize(const Plan& p, const float2* op, int tiles, float2* out, cudaStream_t st);
 // o[g] = fixed-order sum of `tiles` partial readouts (n_act entries, accumulator order)

@@ -232,8 +232,10 @@ cudaError_t func_attr_once(const void* fn, cudaFuncAttribute attr, int value) {
 struct ProjArgs {
   const void* frames;
   int64_t n;
-  float* C;
-  const int32_t* idx;   // C row of frame f: idx ? idx[f] : f
+  int64_t pos0;         // scan position of frame f: idx ? idx[f] : pos0 + f
+  const int32_t* idx;
+  ProjDst dst;          // where coefficient row a of a frame goes: shard o with alo[o] <= a < alo[o+1]
+                        // -> C[o] + position * Kd[o] + (a - alo[o]) * L (another rank's store: peer memory)
   int g2;      // frames per stage-2 group (<= kG2; a multiple of kFPT)
   const uint4* Bpack;
   float sc1;   // acc1 -> fp16 A2 scale   (2^(eT - s))
@@ -606,6 +608,13 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
     int npend = 0;
     // accumulator row held by this thread's lane (M = 64: lanes 0-15 of each quadrant)
     const int m2 = Cfg::kM2 == 128 ? row : (lane < 16 ? quad * 16 + lane : 1 << 20);
+    // destination of this thread's coefficient row a = m2 % L (fixed for the kernel): the shard
+    // that owns it -- this rank's store or a peer's, written directly over NVLink
+    int c_own = 0;
+    while (c_own + 1 < a.dst.n && (m2 % L) >= a.dst.alo[c_own + 1]) ++c_own;
+    float* const c_base = a.dst.C[c_own];
+    const int64_t c_stride = a.dst.K[c_own];
+    const int c_off = ((m2 % L) - a.dst.alo[c_own]) * L;
     auto stage2_epilogue = [&](int64_t frame0, int64_t gi) {
       const uint32_t gb = (uint32_t)(gi % Cfg::kNB2);
       float d[Cfg::kNacc];
@@ -617,7 +626,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
       if (lane == 0) mbar_arrive(&acc2_empty[gb]);
       const int f = m2 / L, aa = m2 % L;
       const int64_t fg = frame0 + f;
-      if constexpr (Cfg::kCStage) {
+      if constexpr (Cfg::kCStage) if (a.dst.n == 1) {
         // lanes 0-15 of this warp hold rows aa0 .. aa0 + 15 of one frame (a contiguous 16 L floats
         // of C): rows into the warp's staging (16-byte chunks XOR-swizzled by row), then the warp
         // stores them as 512-byte contiguous pieces
@@ -632,7 +641,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
         const int fw = (quad * 16) / L;                      // the warp's frame (warp-uniform)
         const int64_t fgw = frame0 + fw;
         if (fw < g2 && fgw < n) {
-          float* dst = a.C + (a.idx ? (int64_t)__ldg(a.idx + fgw) : fgw) * K + ((quad * 16) % L) * L;
+          float* dst = a.dst.C[0] + (a.idx ? (int64_t)__ldg(a.idx + fgw) : a.pos0 + fgw) * K + ((quad * 16) % L) * L;
 #pragma unroll
           for (int i = 0; i < (16 * L) / 128; ++i) {
             const int e = i * 128 + lane * 4;                // float index in the warp's 16 rows
@@ -644,7 +653,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
         return;
       }
       if (f < g2 && fg < n) {
-        float* dst = a.C + (a.idx ? (int64_t)__ldg(a.idx + fg) : fg) * K + aa * L;
+        float* dst = c_base + (a.idx ? (int64_t)__ldg(a.idx + fg) : a.pos0 + fg) * c_stride + c_off;
 #pragma unroll
         for (int b = 0; b < L; b += 4) {
           float4 v = make_float4(dv(b) * a.sc2, dv(b + 1) * a.sc2, dv(b + 2) * a.sc2, dv(b + 3) * a.sc2);
@@ -726,6 +735,9 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
       tc_fence_after();
       flush_pending(cl);
     }
+    // coefficients stored into peers' stores are performed system-wide before this grid completes
+    // (the readout's barrier collective then orders them before the owner's row transform)
+    if (a.dst.n > 1) __threadfence_system();
   }
   tc_fence_before();
   __syncthreads();
@@ -768,8 +780,8 @@ static bool fft_tmap(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t
 }
 
 template <int Q, int L, bool U16>
-static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n, float* C, const int32_t* idx,
-                                    cudaStream_t st, bool wait_start) {
+static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n, const ProjDst& dst,
+                                    const int32_t* idx, int64_t pos0, cudaStream_t st, bool wait_start) {
   using Cfg = ProjCfg<Q, L, U16>;
   auto kern = project_kernel<Q, L, U16>;
   {
@@ -817,7 +829,7 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
   static const int no_wait = [] { const char* e = std::getenv("WDD_PROJ_NO_PDLWAIT"); return e ? std::atoi(e) : 0; }();
-  ProjArgs a{frames, n, C, idx, g2, reinterpret_cast<const uint4*>(p.d_Bpack), (float)p.sc1, (float)p.sc2,
+  ProjArgs a{frames, n, pos0, idx, dst, g2, reinterpret_cast<const uint4*>(p.d_Bpack), (float)p.sc1, (float)p.sc2,
              no_wait ? 0 : 1, wait_start ? 1 : 0, p.d_err};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -839,11 +851,11 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
 
 #define WDD_PROJ_CASE(QQ, LL)                                                          \
   if (p.Q == QQ && p.L == LL)                                                          \
-    return p.dtype == 0 ? launch_project_t<QQ, LL, true>(p, frames, n, C, idx, st, wait_start)     \
-                        : launch_project_t<QQ, LL, false>(p, frames, n, C, idx, st, wait_start);
+    return p.dtype == 0 ? launch_project_t<QQ, LL, true>(p, frames, n, dst, idx, pos0, st, wait_start)     \
+                        : launch_project_t<QQ, LL, false>(p, frames, n, dst, idx, pos0, st, wait_start);
 
-cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, float* C, const int32_t* idx,
-                           cudaStream_t st, bool wait_start) {
+cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, const ProjDst& dst, const int32_t* idx,
+                           int64_t pos0, cudaStream_t st, bool wait_start) {
   WDD_PROJ_CASE(32, 8) WDD_PROJ_CASE(32, 16) WDD_PROJ_CASE(32, 24) WDD_PROJ_CASE(32, 32)
   WDD_PROJ_CASE(64, 8) WDD_PROJ_CASE(64, 16) WDD_PROJ_CASE(64, 24) WDD_PROJ_CASE(64, 32)
   WDD_PROJ_CASE(128, 8) WDD_PROJ_CASE(128, 16) WDD_PROJ_CASE(128, 24) WDD_PROJ_CASE(128, 32)
@@ -1348,7 +1360,7 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
     int logP = ilog2(std::max(2, std::min(logSx <= 8 ? 16 : 32, kFftSmem / (8 * p.Sx))));
     if (knob.x >= 0) logP = std::min(logP, knob.x);
     const int nt = knob.y > 0 ? knob.y : logSx <= 8 ? 128 : 256;
-    while ((2 << logP) > p.K || p.K % (2 << logP)) --logP;
+    while ((2 << logP) > p.Kl || p.Kl % (2 << logP)) --logP;
     const size_t smem = ((size_t)p.Sx << logP) * 8 + (size_t)p.Sx * 8 + 16;
     return with_log(logSx, [&](auto LN) {
       constexpr int LOGN = decltype(LN)::value;
@@ -1357,16 +1369,16 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
                                        kFftSmem + 16384);
         if (e != cudaSuccess) return e;
       }
-      dim3 grid(p.K / (2 << logP), n_rows);
+      dim3 grid(p.Kl / (2 << logP), n_rows);
       // (with two projection CTAs per SM a PDL-launched row FFT would park its CTAs next to the
       // last projection CTAs and slow them down: launch it after the projection completes)
       static const int env_pdl = [] { const char* e = std::getenv("WDD_ROWFFT_PDL"); return e ? std::atoi(e) : -1; }();
       const bool rowfft_pdl = env_pdl >= 0 ? env_pdl != 0 : !project_is_lean(p);
       CUtensorMap tmC;
-      const bool tma = fft_tmap(&tmC, p.d_Call, (uint64_t)p.K, (uint64_t)p.S, (uint64_t)p.K * 4, 2u << logP,
+      const bool tma = fft_tmap(&tmC, p.d_Call, (uint64_t)p.Kl, (uint64_t)p.S, (uint64_t)p.Kl * 4, 2u << logP,
                                 (uint32_t)std::min(p.Sx, 256));
       return launch_pdl(rowfft_kernel<LOGN>, grid, dim3(nt), smem, st, rowfft_pdl, (const float*)p.d_Call, rows, masks,
-                        p.mask_words, (const float2*)p.d_twx, (const int32_t*)p.d_col_vx, p.d_R, logP, p.Sy, p.K,
+                        p.mask_words, (const float2*)p.d_twx, (const int32_t*)p.d_col_vx, p.d_R, logP, p.Sy, p.Kl,
                         p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0));
     });
   }
@@ -1374,8 +1386,8 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
     cudaError_t e = func_attr_once((const void*)rowdft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRdSmem);
     if (e != cudaSuccess) return e;
   }
-  dim3 grid(p.K / 64, (p.n_vx + 15) / 16, n_rows);
-  rowdft_kernel<<<grid, 256, kRdSmem, st>>>(p.d_Call, rows, masks, p.mask_words, p.d_Fx, p.d_R, p.Sx, p.Sy, p.K,
+  dim3 grid(p.Kl / 64, (p.n_vx + 15) / 16, n_rows);
+  rowdft_kernel<<<grid, 256, kRdSmem, st>>>(p.d_Call, rows, masks, p.mask_words, p.d_Fx, p.d_R, p.Sx, p.Sy, p.Kl,
                                             p.n_vx);
   return cudaGetLastError();
 }
@@ -2103,7 +2115,7 @@ static int colgemm_chunks(const Plan& p) {
   int max_mj = 0;
   for (int j = 0; j < p.n_vx; ++j) max_mj = std::max(max_mj, p.col_off[j + 1] - p.col_off[j]);
   const int ctas = p.n_vx * ((max_mj + kCgM - 1) / kCgM);
-  const int tiles = p.K / kCgNT;
+  const int tiles = p.Kl / kCgNT;
   int ch = std::max(1, std::min(tiles, (2 * p.sm_count + ctas - 1) / ctas));
   while (tiles % ch) ++ch;
   return ch;
@@ -2113,14 +2125,14 @@ static int colfft_logkt(const Plan& p) {
   static const int2 knob = env_pair("WDD_COLFFT");   // (log2 k per CTA, threads) override
   int logKT = ilog2(std::max(2, std::min(32, kFftSmem / (8 * p.Sy))));
   if (knob.x >= 0) logKT = std::min(logKT, knob.x);
-  while ((1 << logKT) > p.K || p.K % (1 << logKT)) --logKT;
+  while ((1 << logKT) > p.Kl || p.Kl % (1 << logKT)) --logKT;
   return logKT;
 }
 
 // k-tiles per y-FFT CTA (<= 2: with the TMA tile loads, 4 was 1.5% slower at Large and equal at
 // Live) keeping >= 2 waves of CTAs
 static int colfft_tpc(const Plan& p) {
-  const int tiles = p.K >> colfft_logkt(p);
+  const int tiles = p.Kl >> colfft_logkt(p);
   int tpc = 1;
   while (tpc < 2 && tpc * 2 <= tiles && tiles % (tpc * 2) == 0 && (int64_t)(tiles / (tpc * 2)) * p.n_vx >= 2 * p.sm_count)
     tpc *= 2;
@@ -2129,11 +2141,11 @@ static int colfft_tpc(const Plan& p) {
   return tpc;
 }
 
-int colfft_tiles(const Plan& p) { return (p.K >> colfft_logkt(p)) / colfft_tpc(p); }
+int colfft_tiles(const Plan& p) { return (p.Kl >> colfft_logkt(p)) / colfft_tpc(p); }
 
 // k-chunks of the pipelined GEMM flush: enough work items for ~4 per CTA
 static int rgemm_nkc(const Plan& p) {
-  const int KT = p.K / kRgNT;
+  const int KT = p.Kl / kRgNT;
   static const int env = [] { const char* e = std::getenv("WDD_RG_NKC"); return e ? std::atoi(e) : 0; }();
   if (env > 0 && KT % env == 0) return env;
   int nkc = 1;
@@ -2142,7 +2154,7 @@ static int rgemm_nkc(const Plan& p) {
 }
 
 bool rgemm_possible(const Plan& p, int n_rows) {
-  return p.rg_ready && n_rows >= 1 && n_rows <= kRgRows && p.K % kRgNT == 0 && is_pow2(p.Sx) && p.Sx >= 2 &&
+  return p.rg_ready && n_rows >= 1 && n_rows <= kRgRows && p.Kl % kRgNT == 0 && is_pow2(p.Sx) && p.Sx >= 2 &&
          p.Sx <= (1 << kFftMaxLog);
 }
 
@@ -2154,12 +2166,12 @@ cudaError_t rgemm_prepare(Plan& p) {
   for (int j = 0; j < p.n_vx; ++j)
     for (int i0 = 0; i0 < p.col_off[j + 1] - p.col_off[j]; i0 += kRgM) p.rg_items.push_back(make_int2(j, i0));
   auto enc = get_encode();
-  if (!enc || p.K % kRgNT) return cudaSuccess;   // (the FFT / DFT flushes remain)
+  if (!enc || p.Kl % kRgNT) return cudaSuccess;   // (the FFT / DFT flushes remain)
   static_assert(sizeof(RgMaps) <= sizeof(p.rg_tmap), "tensor map storage");
   RgMaps* maps = reinterpret_cast<RgMaps*>(p.rg_tmap);
   auto make = [&](CUtensorMap* tm, void* base, uint64_t rows, uint32_t box_rows) {
-    const cuuint64_t dims[2] = {(cuuint64_t)2 * p.K, (cuuint64_t)rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)p.K * sizeof(float2)};
+    const cuuint64_t dims[2] = {(cuuint64_t)2 * p.Kl, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)p.Kl * sizeof(float2)};
     const cuuint32_t box[2] = {32u, box_rows};   // 16 complex (128 B) x box_rows
     const cuuint32_t estr[2] = {1u, 1u};
     return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -2184,7 +2196,7 @@ static cudaError_t launch_rgemm(const Plan& p, const int32_t* rows, int n_rows, 
   const int nkc = rgemm_nkc(p);
   RgArgs a{(const float2*)p.d_R, rows, n_rows, (const float2*)p.d_twy, p.Sy,
            (float)(1.0 / std::sqrt((double)p.Sy)), (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy,
-           (const int2*)p.d_rg_items, (int)p.rg_items.size(), nkc, p.d_G, p.d_opart, (int64_t)p.n_act, p.K,
+           (const int2*)p.d_rg_items, (int)p.rg_items.size(), nkc, p.d_G, p.d_opart, (int64_t)p.n_act, p.Kl,
            (!overwrite && !o_only) ? 1 : 0, o_only ? 0 : 1, row0};
   const int64_t work = (int64_t)p.rg_items.size() * nkc;
   cudaLaunchConfig_t cfg = {};
@@ -2217,7 +2229,7 @@ int flush_kind(const Plan& p, int n_rows, bool allow_rg) {
          : std::strcmp(e, "dft") == 0 ? 0 : -1;
   }();
   if (allow_rg && rgemm_possible(p, n_rows) && (env == -1 || env == 3)) return 3;
-  const bool gemm_ok = n_rows <= kCgRows && p.K % kCgNT == 0;
+  const bool gemm_ok = n_rows <= kCgRows && p.Kl % kCgNT == 0;
   int k;
   if (env == 2 || env == 3) k = gemm_ok ? 2 : (flush_uses_fft(p, n_rows) ? 1 : 0);
   else if (env == 1) k = flush_uses_fft(p, n_rows) ? 1 : (gemm_ok ? 2 : 0);
@@ -2251,7 +2263,7 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
     return launch_pdl(colgemm_kernel, grid, dim3(256), (size_t)kCgSmem, st, true, (const float2*)p.d_R, rows, n_rows,
                       (const float2*)p.d_twy, p.Sy, (float)(1.0 / std::sqrt((double)p.Sy)),
                       (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G, (const float2*)p.d_W,
-                      p.d_opart, (int64_t)p.n_act, p.K, (p.K / kCgNT) / ch, overwrite ? 1 : 0, o_only ? 1 : 0);
+                      p.d_opart, (int64_t)p.n_act, p.Kl, (p.Kl / kCgNT) / ch, overwrite ? 1 : 0, o_only ? 1 : 0);
   }
   if (kind == 1) {
     const int logSy = ilog2(p.Sy);
@@ -2265,25 +2277,25 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
         if (e != cudaSuccess) return e;
       }
       const int tpc = colfft_tpc(p);
-      dim3 grid((p.K >> logKT) / tpc, p.n_vx);
+      dim3 grid((p.Kl >> logKT) / tpc, p.n_vx);
       static const int2 knob = env_pair("WDD_COLFFT");
       // L2 prefetch of the output stage's rows: Large readout 339 -> 333 us, Box 3.77 -> 3.65 ms;
       // none at Medium (-0.15%: fewer load rounds per tile), so only from Sy = 256
       static const bool pf_on = [] { const char* e = std::getenv("WDD_COLFFT_PF"); return !(e && std::atoi(e) == 0); }();
       CUtensorMap tmR;
-      const bool tma = fft_tmap(&tmR, p.d_R, (uint64_t)p.K * 2, (uint64_t)p.n_vx * p.Sy, (uint64_t)p.K * 8,
+      const bool tma = fft_tmap(&tmR, p.d_R, (uint64_t)p.Kl * 2, (uint64_t)p.n_vx * p.Sy, (uint64_t)p.Kl * 8,
                                 2u << logKT, (uint32_t)std::min(p.Sy, 256));
       return launch_pdl(colfft_kernel<LOGN>, grid, dim3(knob.y > 0 ? knob.y : 256), smem, st, true, p.d_R, rows, n_rows,
                         (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G,
-                        (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.K,
+                        (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.Kl,
                         (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0, tpc, o_only ? 1 : 0, tmR,
                         (tma ? 1 : 0) | (pf_on && p.Sy >= 256 ? 8 : 0));
     });
   }
   if (o_only) return cudaErrorNotSupported;   // unreachable: flush_kind never picks the DFT for these
-  dim3 grid((unsigned)p.flush_tiles.size(), (p.K + 63) / 64);
+  dim3 grid((unsigned)p.flush_tiles.size(), (p.Kl + 63) / 64);
   flush_kernel<<<grid, 256, 0, st>>>(p.d_R, p.d_Fy, rows, n_rows, p.d_flush_tiles, p.d_col_off, p.d_act_vy,
-                                     p.d_G, p.Sy, p.K, overwrite ? 1 : 0);
+                                     p.d_G, p.Sy, p.Kl, overwrite ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -2314,10 +2326,17 @@ __global__ void __launch_bounds__(256) readout_kernel(const float2* __restrict__
   if (lane == 0) o[g] = make_float2(re, im);
 }
 
+__global__ void fence_kernel() {}
+
+cudaError_t launch_fence(cudaStream_t st) {
+  fence_kernel<<<1, 32, 0, st>>>();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_readout(const Plan& p, const float2* G, float2* o, cudaStream_t st) {
   const int64_t threads = p.n_act * 32;
   const unsigned blocks = (unsigned)((threads + 255) / 256);
-  readout_kernel<<<blocks, 256, 0, st>>>(G, p.d_W, p.n_act, p.K, o);
+  readout_kernel<<<blocks, 256, 0, st>>>(G, p.d_W, p.n_act, p.Kl, o);
   return cudaGetLastError();
 }
 

@@ -288,17 +288,44 @@ wdd_status validate_and_mark(Plan& p, const int32_t* idx, int64_t n) {
   return WDD_OK;
 }
 
+// Positions whose coefficients are (or, for a peer rank's frames, will be) in the current store:
+// their rows are row-transformed at the next flush.
+void mark_pending(Plan& p, const int32_t* idx, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) {
+    const int sy = idx[i] / p.Sx, sx = idx[i] % p.Sx;
+    p.row_dirty[sy] = 1;
+    p.pending[(size_t)sy * p.mask_words + (sx >> 5)] |= 1u << (sx & 31);
+    if (p.o_only) p.ingested[(size_t)sy * p.mask_words + (sx >> 5)] |= 1u << (sx & 31);
+  }
+}
+
+// The current store of shard o (this plan's or a peer's, as mapped into this process)
+float* shard_store(const Plan& p, int o) {
+  const int Ko = (p.a_split[o + 1] - p.a_split[o]) * p.L;
+  return p.peer_base[o] + (size_t)p.store_par * p.S * Ko;
+}
+
+ProjDst proj_dst(const Plan& p) {
+  ProjDst d;
+  d.n = p.nshard;
+  for (int o = 0; o < p.nshard; ++o) {
+    d.C[o] = p.nshard == 1 ? p.d_Call : shard_store(p, o);
+    d.K[o] = (p.a_split[o + 1] - p.a_split[o]) * p.L;
+    d.alo[o] = p.a_split[o];
+  }
+  d.alo[p.nshard] = p.L;
+  return d;
+}
+
 // Enqueue the projection of one chunk of already-validated frames; its coefficients land in
-// d_Call at their scan positions (the row DFT of completed rows happens at flush time).
+// the coefficient store(s) at their scan positions (the row DFT happens at flush time).
 wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, int64_t nc, bool first) {
   cudaStream_t st = p.stream;
   bool contiguous = true;
   for (int64_t i = 1; i < nc && contiguous; ++i) contiguous = idx[i] == idx[0] + i;
-  float* C = p.d_Call;
+  const ProjDst dst = proj_dst(p);
   const int32_t* d_idx = nullptr;
-  if (contiguous) {
-    C += (size_t)idx[0] * p.K;
-  } else {
+  if (!contiguous) {
     void* d = nullptr;
     wdd_status s = upload_meta(p, idx, (size_t)nc * sizeof(int32_t), &d);
     if (s != WDD_OK) return s;
@@ -309,18 +336,13 @@ wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, in
     // (frames of the first chunk of a call may come from a caller kernel enqueued right before it:
     // unless the plan was created with ingest_overlap, that launch reads them only after its
     // predecessor grid has completed; later chunks are ordered behind it)
-    CUDA_TRY(launch_project(p, frames_dev, nc, C, d_idx, st, first && !p.ingest_overlap));
+    CUDA_TRY(launch_project(p, frames_dev, nc, dst, d_idx, contiguous ? idx[0] : 0, st, first && !p.ingest_overlap));
   }
   p.c_fresh = false;
   // The row DFT of completed rows is deferred to the next flush (readout): launched per batch it
   // would sit between the PDL-chained projection launches and stall them (measured: 246 us vs
   // 162 us per Medium acquisition).
-  for (int64_t i = 0; i < nc; ++i) {
-    const int sy = idx[i] / p.Sx, sx = idx[i] % p.Sx;
-    p.row_dirty[sy] = 1;
-    p.pending[(size_t)sy * p.mask_words + (sx >> 5)] |= 1u << (sx & 31);
-    if (p.o_only) p.ingested[(size_t)sy * p.mask_words + (sx >> 5)] |= 1u << (sx & 31);
-  }
+  mark_pending(p, idx, nc);
   return WDD_OK;
 }
 
@@ -421,7 +443,7 @@ wdd_status form_G(Plan& p) {
         break;
       }
   if (rows.empty()) {
-    CUDA_TRY(cudaMemsetAsync(p.d_G, 0, (size_t)p.n_act * p.K * sizeof(float2), p.stream));
+    CUDA_TRY(cudaMemsetAsync(p.d_G, 0, (size_t)p.n_act * p.Kl * sizeof(float2), p.stream));
     return WDD_OK;
   }
   const int n_rows = (int)rows.size();
@@ -445,10 +467,24 @@ wdd_status form_G(Plan& p) {
 wdd_status materialize_G(Plan& p) {
   if (p.o_only) return form_G(p);
   if (p.G_zero) {
-    CUDA_TRY(cudaMemsetAsync(p.d_G, 0, (size_t)p.n_act * p.K * sizeof(float2), p.stream));
+    CUDA_TRY(cudaMemsetAsync(p.d_G, 0, (size_t)p.n_act * p.Kl * sizeof(float2), p.stream));
     p.G_zero = false;
     p.opart_tiles = 0;
   }
+  return WDD_OK;
+}
+
+// Shard groups: the coefficient rows of this plan's shard arrive from every rank's projections
+// (peer stores).  Before the flush reads them, every rank's earlier work must be complete: an
+// ordinary launch of an empty kernel (starts once all earlier work on this stream is done), a
+// one-element allreduce (completes once every rank has reached it), and another empty kernel
+// (later kernels start only after the collective has completed, however NCCL launches).
+wdd_status shard_barrier(Plan& p) {
+  if (p.nshard == 1 || !p.nccl) return WDD_OK;
+  CUDA_TRY(launch_fence(p.stream));
+  NCCL_TRY(ncclAllReduce(p.d_o, p.d_o, 1, ncclFloat, ncclSum, reinterpret_cast<ncclComm_t>(p.nccl), p.stream));
+  CUDA_TRY(launch_fence(p.stream));
+  p.barrier_since_swap = true;
   return WDD_OK;
 }
 
@@ -461,8 +497,9 @@ wdd_status materialize_G(Plan& p) {
 // readouts into o (n_act) and allreduces o -- exact by linearity, K x fewer bytes than G;
 // combine = 1 (north star) allreduces the partial G and runs the readout on the sum.
 wdd_status readout_spectrum(Plan& p, bool combine, const float2** op_out, int* tiles_out) {
-  wdd_status s = flush(p);
-  if (s != WDD_OK) return s;
+  wdd_status s = WDD_OK;
+  if (combine && (s = shard_barrier(p)) != WDD_OK) return s;
+  if ((s = flush(p)) != WDD_OK) return s;
   const float2* op = p.d_opart;
   int tiles = p.opart_tiles;
   if (p.o_only) {
@@ -478,7 +515,7 @@ wdd_status readout_spectrum(Plan& p, bool combine, const float2** op_out, int* t
     ncclComm_t comm = reinterpret_cast<ncclComm_t>(p.nccl);
     if (!p.o_only && p.combine == 1) {
       if ((s = materialize_G(p)) != WDD_OK) return s;
-      NCCL_TRY(ncclAllReduce(p.d_G, p.d_Gsum, (size_t)p.n_act * p.K * 2, ncclFloat, ncclSum, comm, p.stream));
+      NCCL_TRY(ncclAllReduce(p.d_G, p.d_Gsum, (size_t)p.n_act * p.Kl * 2, ncclFloat, ncclSum, comm, p.stream));
       Prof pr(p, kSlotReadout, p.stream);
       CUDA_TRY(launch_readout(p, p.d_Gsum, p.d_o, p.stream));
     } else {
@@ -501,8 +538,10 @@ void free_plan(Plan* p) {
   if (p->stream) cudaStreamSynchronize(p->stream);
   cudaDeviceSynchronize();
   if (p->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(p->nccl));
+  for (int o = 0; o < kMaxShards; ++o)
+    if (p->peers_ipc[o] && p->peer_base[o]) cudaIpcCloseMemHandle(p->peer_base[o]);
   full_wdd_release(*p);
-  void* bufs[] = {p->d_rg_items, p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Call, p->d_Call_alt,
+  void* bufs[] = {p->d_rg_items, p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Cbase,
                   p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec, p->d_img_tmp,
                   p->d_meta, p->d_stage[0], p->d_stage[1], p->d_err};
   for (void* b : bufs)
@@ -557,6 +596,10 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   if (o.accumulator != 0 && o.accumulator != 1) return fail(WDD_E_ARG, "accumulator must be 0 (G) or 1 (spectrum)");
   if (o.accumulator == 1 && (Sy < 2 || Sy > 1024 || (Sy & (Sy - 1)) != 0))
     return fail(WDD_E_ARG, "the spectrum-only accumulator needs a power-of-two Sy in [2, 1024] (got %d)", Sy);
+  const int nshard = o.k_shards <= 1 ? 1 : o.k_shards;
+  if (o.k_shards < 0 || nshard > kMaxShards || nshard > L || o.k_rank < 0 || o.k_rank >= nshard)
+    return fail(WDD_E_ARG, "k_shards = %d / k_rank = %d: need 0 <= k_rank < k_shards <= min(%d, L)", o.k_shards,
+                o.k_rank, kMaxShards);
 
   Plan* p = new Plan();
   p->Sy = Sy; p->Sx = Sx; p->Q = Q; p->L = L; p->K = K; p->S = (int64_t)Sy * Sx;
@@ -565,6 +608,12 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   p->eps = wiener_eps;
   p->o_only = o.accumulator == 1;
   p->ingest_overlap = o.ingest_overlap;
+  p->nshard = nshard;
+  p->shard = nshard > 1 ? o.k_rank : 0;
+  if (nshard > 1) p->combine = 0;   // (the shards' G are disjoint: the combine sums o)
+  for (int i = 0; i <= nshard; ++i) p->a_split.push_back(i * L / nshard);   // as even as possible
+  p->k0 = p->a_split[p->shard] * L;
+  p->Kl = (p->a_split[p->shard + 1] - p->a_split[p->shard]) * L;
   p->dq = o.det_px_rad > 0 ? o.det_px_rad / p->lambda : 1.0 / (Q * step_A);  // R17
   p->qa = p->alpha / p->lambda;                                               // R7
   p->R = p->qa / p->dq;
@@ -628,7 +677,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   // bank: built on the device once the column tables are there (below)
   ApertureIntervals apiv;
   if (!aperture_intervals(*p, ap, apiv)) return bail(fail(WDD_E_ARG, "aperture rows are not pixel intervals"));
-  const size_t nW = (size_t)p->n_act * K;
+  const size_t nW = (size_t)p->n_act * p->Kl;   // G and bank: this plan's coefficients only
 
   // device buffers
   std::vector<uint16_t> bpack;
@@ -677,9 +726,15 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ALLOC(p->d_W, nW * sizeof(float2));
   ALLOC(p->d_G, nW * sizeof(float2));
   if (p->combine == 1) ALLOC(p->d_Gsum, nW * sizeof(float2));
-  ALLOC(p->d_R, (size_t)p->n_vx * Sy * K * sizeof(float2));
-  ALLOC(p->d_Call, (size_t)p->S * K * sizeof(float));
-  if (double_c_store()) ALLOC(p->d_Call_alt, (size_t)p->S * K * sizeof(float));
+  ALLOC(p->d_R, (size_t)p->n_vx * Sy * p->Kl * sizeof(float2));
+  // the two coefficient stores in one allocation (one IPC handle for peers of a shard group)
+  const size_t c_store = (size_t)p->S * p->Kl;
+  const int n_stores = (double_c_store() || nshard > 1) ? 2 : 1;
+  ALLOC(p->d_Cbase, n_stores * c_store * sizeof(float));
+  p->d_Call = p->d_Cbase;
+  p->d_Call_alt = n_stores == 2 ? p->d_Cbase + c_store : nullptr;
+  p->peer_base[p->shard] = p->d_Cbase;
+  p->peers_ready = nshard == 1;
   ALLOC(p->d_act_vy, act.size() * 4);
   ALLOC(p->d_col_off, p->col_off.size() * 4);
   ALLOC(p->d_vpos, act.size() * 4);
@@ -717,13 +772,22 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ok = ok && cudaMemset(p->d_oacc, 0, act.size() * sizeof(float2)) == cudaSuccess &&
        cudaMemset(p->d_ones, 0xFF, (size_t)Sy * p->mask_words * sizeof(uint32_t)) == cudaSuccess &&
        cudaMemset(p->d_G, 0, nW * sizeof(float2)) == cudaSuccess &&
-       cudaMemset(p->d_Call, 0, (size_t)p->S * K * sizeof(float)) == cudaSuccess &&
-       (!p->d_Call_alt || cudaMemset(p->d_Call_alt, 0, (size_t)p->S * K * sizeof(float)) == cudaSuccess) &&
+       cudaMemset(p->d_Cbase, 0, n_stores * c_store * sizeof(float)) == cudaSuccess &&
        cudaMemset(p->d_spec, 0, (size_t)p->S * sizeof(float2)) == cudaSuccess &&
        cudaMemset(p->d_err, 0, sizeof(unsigned)) == cudaSuccess;
   if (!ok) return bail(fail(WDD_E_CUDA, "upload failed: %s", cudaGetErrorString(cudaGetLastError())));
-  {
+  if (nshard == 1) {
     const cudaError_t e = build_bank(*p, q.data(), apiv.rows.data(), apiv.ax_lo, apiv.n_axc, p->d_W, false);
+    if (e != cudaSuccess) return bail(fail(WDD_E_CUDA, "bank build: %s", cudaGetErrorString(e)));
+  } else {
+    // the whole bank into scratch, then this shard's coefficient columns [k0, k0 + Kl)
+    void* tmp = nullptr;
+    cudaError_t e = cudaMalloc(&tmp, (size_t)p->n_act * K * sizeof(float2));
+    if (e == cudaSuccess) e = build_bank(*p, q.data(), apiv.rows.data(), apiv.ax_lo, apiv.n_axc, tmp, false);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2D(p->d_W, (size_t)p->Kl * sizeof(float2), static_cast<float2*>(tmp) + p->k0, (size_t)K * sizeof(float2),
+                       (size_t)p->Kl * sizeof(float2), (size_t)p->n_act, cudaMemcpyDeviceToDevice);
+    if (tmp) cudaFree(tmp);
     if (e != cudaSuccess) return bail(fail(WDD_E_CUDA, "bank build: %s", cudaGetErrorString(e)));
   }
   if (cufftPlan2d(&p->fft, Sy, Sx, CUFFT_C2C) != CUFFT_SUCCESS) return bail(fail(WDD_E_CUDA, "cufftPlan2d failed"));
@@ -744,6 +808,7 @@ wdd_status wdd_ingest(wdd_plan_t plan, const void* frames_dev, const int32_t* sc
   if (n < 0) return fail(WDD_E_ARG, "n < 0");
   if (n == 0) return WDD_OK;
   if (!frames_dev || !scan_idx_host) return fail(WDD_E_ARG, "NULL frames or indices");
+  if (!p.peers_ready) return fail(WDD_E_STATE, "shard plan: wdd_set_shard_peers / wdd_link_shards first");
   CUDA_TRY(cudaSetDevice(p.device));
   wdd_status s = validate_and_mark(p, scan_idx_host, n);
   if (s != WDD_OK) return s;
@@ -766,6 +831,7 @@ wdd_status wdd_ingest_host(wdd_plan_t plan, const void* frames_host, const int32
   if (n == 0) return WDD_OK;
   if (!frames_host || !scan_idx_host) return fail(WDD_E_ARG, "NULL frames or indices");
   if (p.capturing) return fail(WDD_E_STATE, "wdd_ingest_host cannot be captured");
+  if (!p.peers_ready) return fail(WDD_E_STATE, "shard plan: wdd_set_shard_peers / wdd_link_shards first");
   CUDA_TRY(cudaSetDevice(p.device));
   wdd_status s = validate_and_mark(p, scan_idx_host, n);
   if (s != WDD_OK) return s;
@@ -835,6 +901,82 @@ wdd_status wdd_image_from_spectrum(wdd_plan_t plan, const void* spectrum_dev, vo
   return WDD_OK;
 }
 
+wdd_status wdd_ingest_remote(wdd_plan_t plan, const int32_t* scan_idx_host, int64_t n) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (n < 0) return fail(WDD_E_ARG, "n < 0");
+  if (n == 0) return WDD_OK;
+  if (!scan_idx_host) return fail(WDD_E_ARG, "NULL indices");
+  if (p.nshard == 1) return fail(WDD_E_STATE, "wdd_ingest_remote needs a shard plan (opts.k_shards > 1)");
+  wdd_status s = validate_and_mark(p, scan_idx_host, n);
+  if (s != WDD_OK) return s;
+  mark_pending(p, scan_idx_host, n);
+  p.frames_ingested += n;
+  return WDD_OK;
+}
+
+wdd_status wdd_shard_store_handle(wdd_plan_t plan, uint8_t handle[64]) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (!handle) return fail(WDD_E_ARG, "NULL handle");
+  if (p.nshard == 1) return fail(WDD_E_STATE, "not a shard plan");
+  CUDA_TRY(cudaSetDevice(p.device));
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+  CUDA_TRY(cudaIpcGetMemHandle(&h, p.d_Cbase));
+  std::memcpy(handle, &h, 64);
+  return WDD_OK;
+}
+
+wdd_status wdd_set_shard_peers(wdd_plan_t plan, int32_t nshard, int32_t rank, const uint8_t* handles) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (!handles) return fail(WDD_E_ARG, "NULL handles");
+  if (p.nshard == 1 || nshard != p.nshard || rank != p.shard)
+    return fail(WDD_E_ARG, "shard group (%d, %d) does not match the plan's (%d, %d)", nshard, rank, p.nshard, p.shard);
+  CUDA_TRY(cudaSetDevice(p.device));
+  for (int o = 0; o < nshard; ++o) {
+    if (o == p.shard) continue;
+    if (p.peers_ipc[o] && p.peer_base[o]) cudaIpcCloseMemHandle(p.peer_base[o]);
+    p.peers_ipc[o] = false;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + 64 * (size_t)o, 64);
+    void* d = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&d, h, cudaIpcMemLazyEnablePeerAccess));
+    p.peer_base[o] = static_cast<float*>(d);
+    p.peers_ipc[o] = true;
+  }
+  p.peers_ready = true;
+  return WDD_OK;
+}
+
+wdd_status wdd_link_shards(int32_t nshard, const wdd_plan_t* plans) {
+  if (!plans || nshard < 2 || nshard > kMaxShards) return fail(WDD_E_ARG, "need 2..%d plans", kMaxShards);
+  for (int r = 0; r < nshard; ++r) {
+    const Plan* q = P(plans[r]);
+    const Plan* q0 = P(plans[0]);
+    if (!q || q->nshard != nshard || q->shard != r || q->S != q0->S || q->L != q0->L || q->Q != q0->Q)
+      return fail(WDD_E_ARG, "plan %d is not shard %d of %d of the same geometry", r, r, nshard);
+  }
+  for (int r = 0; r < nshard; ++r) {
+    Plan& q = *P(plans[r]);
+    CUDA_TRY(cudaSetDevice(q.device));
+    for (int o = 0; o < nshard; ++o) {
+      const Plan& po = *P(plans[o]);
+      if (po.device != q.device) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(po.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          return fail(WDD_E_CUDA, "peer access %d -> %d: %s", q.device, po.device, cudaGetErrorString(e));
+        cudaGetLastError();
+      }
+      q.peer_base[o] = po.d_Cbase;
+      q.peers_ipc[o] = false;
+    }
+    q.peers_ready = true;
+  }
+  return WDD_OK;
+}
+
 wdd_status wdd_readout_host(wdd_plan_t plan, void* complex_out_host) {
   if (check_plan(plan)) return WDD_E_ARG;
   Plan& p = *P(plan);
@@ -860,10 +1002,11 @@ wdd_status wdd_get_accumulator(wdd_plan_t plan, void* G_out_dev, int32_t* active
   if (n_act) *n_act = p.n_act;
   if (active_v_host) std::memcpy(active_v_host, p.active_v.data(), p.active_v.size() * 4);
   if (G_out_dev) {
-    wdd_status s = flush(p);
+    wdd_status s = shard_barrier(p);
+    if (s == WDD_OK) s = flush(p);
     if (s == WDD_OK) s = materialize_G(p);
     if (s != WDD_OK) return s;
-    CUDA_TRY(cudaMemcpyAsync(G_out_dev, p.d_G, (size_t)p.n_act * p.K * sizeof(float2), cudaMemcpyDeviceToDevice, p.stream));
+    CUDA_TRY(cudaMemcpyAsync(G_out_dev, p.d_G, (size_t)p.n_act * p.Kl * sizeof(float2), cudaMemcpyDeviceToDevice, p.stream));
   }
   return WDD_OK;
 }
@@ -883,6 +1026,14 @@ wdd_status wdd_reset(wdd_plan_t plan) {
   std::fill(p.row_staged.begin(), p.row_staged.end(), 0);
   std::fill(p.pending.begin(), p.pending.end(), 0u);
   if (p.d_Call_alt && p.frames_ingested > 0) {
+    // shard groups: the store this acquisition is about to write (on every rank) was read by the
+    // row transforms of the acquisition before the previous one; without a readout barrier in the
+    // previous acquisition, one here orders those reads before any rank's next projection
+    if (p.nshard > 1 && !p.barrier_since_swap) {
+      wdd_status s = shard_barrier(p);
+      if (s != WDD_OK) return s;
+    }
+    p.barrier_since_swap = false;
     // the previous acquisition's flush / readout may still read the current store: the next
     // acquisition writes the other one, so its first projection need not wait for them.  That
     // store was last read by the row transform of the acquisition before the previous one; the
@@ -891,6 +1042,7 @@ wdd_status wdd_reset(wdd_plan_t plan) {
     // (a PDL-launched row FFT triggers its dependents only after its own C loads, an ordinary
     // launch starts after all earlier work), and the projection is downstream of it
     std::swap(p.d_Call, p.d_Call_alt);
+    p.store_par ^= 1;
     p.c_fresh = p.c_read_since_swap;
     p.c_read_since_swap = false;
   }
@@ -935,9 +1087,10 @@ wdd_status wdd_get_info(wdd_plan_t plan, wdd_plan_info* info) {
   i.Sy = p.Sy; i.Sx = p.Sx; i.Q = p.Q; i.L = p.L; i.K = p.K; i.n_vx = p.n_vx; i.dtype = p.dtype;
   i.normalize = p.normalize; i.n_act = p.n_act; i.dq = p.dq; i.q_alpha = p.qa; i.R_px = p.R;
   i.sigma_px = p.sigma; i.wavelength_A = p.lambda; i.step_A = p.step; i.eps = p.eps;
-  i.bytes_G = p.n_act * p.K * 8; i.bytes_bank = i.bytes_G; i.bytes_R = (int64_t)p.n_vx * p.Sy * p.K * 8;
-  i.bytes_C = p.chunk_cap * p.K * 4; i.frames_ingested = p.frames_ingested; i.nranks = p.nranks; i.rank = p.rank;
+  i.bytes_G = p.n_act * p.Kl * 8; i.bytes_bank = i.bytes_G; i.bytes_R = (int64_t)p.n_vx * p.Sy * p.Kl * 8;
+  i.bytes_C = p.S * p.Kl * 4; i.frames_ingested = p.frames_ingested; i.nranks = p.nranks; i.rank = p.rank;
   i.proj_ctas_per_sm = project_occupancy(p);
+  i.k_shards = p.nshard; i.k_rank = p.shard; i.k_lo = p.k0; i.k_count = p.Kl;
   *info = i;
   return WDD_OK;
 }
@@ -983,8 +1136,12 @@ wdd_status wdd_project(wdd_plan_t plan, const void* frames_dev, int64_t n, void*
   if (n < 0 || (n > 0 && (!frames_dev || !C_out_dev))) return fail(WDD_E_ARG, "bad arguments");
   CUDA_TRY(cudaSetDevice(p.device));
   Prof pr(p, kSlotProject, reinterpret_cast<cudaStream_t>(stream));
-  CUDA_TRY(launch_project(p, frames_dev, n, static_cast<float*>(C_out_dev), nullptr,
-                          reinterpret_cast<cudaStream_t>(stream), /*wait_start*/ true));
+  ProjDst d;
+  d.C[0] = static_cast<float*>(C_out_dev);
+  d.K[0] = p.K;
+  d.alo[1] = p.L;
+  CUDA_TRY(launch_project(p, frames_dev, n, d, nullptr, 0, reinterpret_cast<cudaStream_t>(stream),
+                          /*wait_start*/ true));
   return WDD_OK;
 }
 

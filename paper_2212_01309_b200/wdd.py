@@ -45,7 +45,9 @@ class _Info(ctypes.Structure):
                 ("wavelength_A", ctypes.c_double), ("step_A", ctypes.c_double), ("eps", ctypes.c_double),
                 ("bytes_G", ctypes.c_int64), ("bytes_bank", ctypes.c_int64), ("bytes_R", ctypes.c_int64),
                 ("bytes_C", ctypes.c_int64), ("frames_ingested", ctypes.c_int64), ("nranks", ctypes.c_int32),
-                ("rank", ctypes.c_int32), ("proj_ctas_per_sm", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
+                ("rank", ctypes.c_int32), ("proj_ctas_per_sm", ctypes.c_int32), ("k_shards", ctypes.c_int32),
+                ("k_rank", ctypes.c_int32), ("k_lo", ctypes.c_int32), ("k_count", ctypes.c_int32),
+                ("reserved0", ctypes.c_int32)]
 
 
 _lib = None
@@ -69,6 +71,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "wdd_readout_spectrum": [P, V, I32],
             "wdd_image_from_spectrum": [P, V, V],
             "wdd_check": [P],
+            "wdd_ingest_remote": [P, ctypes.POINTER(I32), I64],
+            "wdd_shard_store_handle": [P, ctypes.c_char_p],
+            "wdd_set_shard_peers": [P, I32, I32, ctypes.c_char_p],
+            "wdd_link_shards": [I32, ctypes.POINTER(P)],
             "wdd_destroy": [P],
             "wdd_get_accumulator": [P, V, ctypes.POINTER(I32), ctypes.POINTER(I64)],
             "wdd_full_wdd": [P, V, V, V],
@@ -131,6 +137,13 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def link_shards(plans):
+    """Link the coefficient stores of plans[r] = shard r of len(plans) in this process
+    (wdd_link_shards): each plan's projection then writes the other shards' coefficients directly."""
+    arr = (ctypes.c_void_p * len(plans))(*[p._h.value for p in plans])
+    _check(load_library().wdd_link_shards(len(plans), arr))
+
+
 class Plan:
     """A Live-WDD plan (wdd_plan_create ... wdd_destroy)."""
 
@@ -163,6 +176,7 @@ class Plan:
         self.device = int(device)
         i = self.info()
         self.Sy, self.Sx, self.Q, self.L, self.K, self.n_act = i["Sy"], i["Sx"], i["Q"], i["L"], i["K"], i["n_act"]
+        self.k_lo, self.k_count = i["k_lo"], i["k_count"]
 
     @classmethod
     def from_config(cls, cfg, **kw):
@@ -260,8 +274,10 @@ class Plan:
         return out
 
     def get_accumulator(self):
+        """(G, active v): G is n_act x K complex64 (shard plans: n_act x k_count, coefficients
+        k_lo .. k_lo + k_count - 1)."""
         import torch
-        G = torch.empty((self.n_act, self.K), dtype=torch.complex64, device=f"cuda:{self.device}")
+        G = torch.empty((self.n_act, self.k_count), dtype=torch.complex64, device=f"cuda:{self.device}")
         act = np.empty(self.n_act, dtype=np.int32)
         n = ctypes.c_int64()
         _check(self._lib.wdd_get_accumulator(self._h, _ptr(G), act.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
@@ -280,6 +296,23 @@ class Plan:
 
     def set_comm(self, nranks: int, rank: int, uid: bytes):
         _check(self._lib.wdd_set_comm(self._h, int(nranks), int(rank), uid))
+
+    # ---- coefficient-sharded rank groups
+    def ingest_remote(self, scan_idx):
+        """Positions another rank of the shard group ingests (host bookkeeping only)."""
+        idx = _idx(scan_idx)
+        _check(self._lib.wdd_ingest_remote(self._h, idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(idx)))
+
+    def shard_store_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _check(self._lib.wdd_shard_store_handle(self._h, buf))
+        return buf.raw
+
+    def set_shard_peers(self, nshard: int, rank: int, handles):
+        blob = b"".join(bytes(h) if h is not None else bytes(64) for h in handles)
+        if len(blob) != 64 * nshard:
+            raise ValueError("need one 64-byte handle per shard")
+        _check(self._lib.wdd_set_shard_peers(self._h, int(nshard), int(rank), blob))
 
     # ---- introspection / test hooks
     def info(self) -> dict:

@@ -94,8 +94,9 @@ def test_overlapped_acquisitions_without_wide_first_launch():
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = ("import torch, paper_2212_01309_b200 as w; from synth import CONFIGS; "
-            "import tests.test_gpu_overlap as t; "
+    code = ("import importlib.util, torch, paper_2212_01309_b200 as w; from synth import CONFIGS; "
+            "s = importlib.util.spec_from_file_location('ovl', 'tests/test_gpu_overlap.py'); "
+            "t = importlib.util.module_from_spec(s); s.loader.exec_module(t); "
             "t._check_overlap(torch, w, CONFIGS['medium'].with_(Sy=32, Sx=32), 256, 12); "
             "t._check_overlap(torch, w, CONFIGS['medium'], 512, 4); print('ok')")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=900,
