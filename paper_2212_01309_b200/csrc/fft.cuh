@@ -77,13 +77,11 @@ template <int LOGN> struct Split {
   static constexpr int N1 = 1 << L1, N2 = 1 << L2;
 };
 
-// Slot holding frequency f = k1 + N1 k2 after fft_seq<LOGN>: row k1 of the [N1][N2] output, column
-// k2 rotated by k1 (the skew keeps a warp's accesses to 2-4 consecutive rows on distinct banks).
+// Slot holding frequency f after fft_seq<LOGN>.
 template <int LOGN>
-__host__ __device__ __forceinline__ int fslot(int f) {
+__device__ __forceinline__ int fslot(int f) {
   using S = Split<LOGN>;
-  const int k1 = f & (S::N1 - 1), k2 = f >> S::L1;
-  return S::N2 * k1 + ((k2 + k1) & (S::N2 - 1));
+  return S::N2 * (f & (S::N1 - 1)) + (f >> S::L1);
 }
 
 // Forward DFT (unnormalised, e^{-2 pi i}) of 2^logc interleaved sequences of length N = 2^LOGN
@@ -91,9 +89,6 @@ __host__ __device__ __forceinline__ int fslot(int f) {
 // addresses).  Input in natural order; frequency f ends at slot fslot<LOGN>(f).  tw = the full
 // table tw[m] = exp(-2 pi i m / N), m < N, in shared memory (only the step-2 twiddles W_N^{n2 k1}
 // read it).  Starts and ends with the block synchronised.
-// Between the steps and in the output, element (k1, n) of the [N1][N2] layout sits in column
-// (n + k1) mod N2: step 2 (one thread per k1) then reads and writes rows k1 .. k1+3 of a warp on
-// alternating bank halves instead of all on the same banks (rows are N2 * cnt * 8 bytes apart).
 template <int LOGN>
 __device__ __forceinline__ void fft_seq(float2* x, const float2* tw, int logc) {
   using S = Split<LOGN>;
@@ -110,7 +105,7 @@ __device__ __forceinline__ void fft_seq(float2* x, const float2* tw, int logc) {
       for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], tw[n2 * k1]);
     }
 #pragma unroll
-    for (int k1 = 0; k1 < N1; ++k1) x[((N2 * k1 + ((n2 + k1) & (N2 - 1))) << logc) + c] = v[k1];
+    for (int k1 = 0; k1 < N1; ++k1) x[((N2 * k1 + n2) << logc) + c] = v[k1];
   }
   __syncthreads();
   if (N2 > 1) {
@@ -118,10 +113,10 @@ __device__ __forceinline__ void fft_seq(float2* x, const float2* tw, int logc) {
       const int c = t & (cnt - 1), k1 = t >> logc;
       float2 v[N2];
 #pragma unroll
-      for (int n2 = 0; n2 < N2; ++n2) v[n2] = x[((N2 * k1 + ((n2 + k1) & (N2 - 1))) << logc) + c];
+      for (int n2 = 0; n2 < N2; ++n2) v[n2] = x[((N2 * k1 + n2) << logc) + c];
       dft_reg<S::L2>(v);
 #pragma unroll
-      for (int k2 = 0; k2 < N2; ++k2) x[((N2 * k1 + ((k2 + k1) & (N2 - 1))) << logc) + c] = v[k2];
+      for (int k2 = 0; k2 < N2; ++k2) x[((N2 * k1 + k2) << logc) + c] = v[k2];
     }
     __syncthreads();
   }

@@ -1236,12 +1236,10 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   const int64_t K2 = K >> 1;
   for (int ib = 0; ib < mj; ib += rpp * 4) {             // block-uniform trip count (shuffles)
     float4 o[4], w[4];
-    int iu[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int ii = ib + u * rpp + rs;
-      iu[u] = ii < mj ? sidx[ii] : 0;
-      const int64_t gi = (int64_t)(g0 + iu[u]) * K2 + (k0 >> 1) + pp;
+      const int64_t gi = (int64_t)(g0 + (ii < mj ? sidx[ii] : 0)) * K2 + (k0 >> 1) + pp;
       w[u] = ii < mj ? __ldg(W4 + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
       o[u] = (ii < mj && !overwrite && !o_only) ? G4[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -1250,11 +1248,12 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
       if (ib + u * rpp >= mj) break;                     // block-uniform
       const int ii = ib + u * rpp + rs;
       float2 d = make_float2(0.f, 0.f);
+      const int i = ii < mj ? sidx[ii] : 0;
       if (ii < mj) {
         const float4 z = *reinterpret_cast<const float4*>(x + (svy[ii] << logKT) + 2 * pp);
         const float4 gn = make_float4(fmaf(z.x, scale, o[u].x), fmaf(z.y, scale, o[u].y), fmaf(z.z, scale, o[u].z),
                                       fmaf(z.w, scale, o[u].w));
-        if (!o_only) G4[(int64_t)(g0 + iu[u]) * K2 + (k0 >> 1) + pp] = gn;
+        if (!o_only) G4[(int64_t)(g0 + i) * K2 + (k0 >> 1) + pp] = gn;
         d.x = fmaf(gn.x, w[u].x, fmaf(-gn.y, w[u].y, fmaf(gn.z, w[u].z, -gn.w * w[u].w)));
         d.y = fmaf(gn.x, w[u].y, fmaf(gn.y, w[u].x, fmaf(gn.z, w[u].w, gn.w * w[u].z)));
       }
@@ -1262,7 +1261,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
         d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
         d.y += __shfl_xor_sync(0xffffffffu, d.y, off);
       }
-      if (pp == 0 && ii < mj) { sdot[iu[u]].x += d.x; sdot[iu[u]].y += d.y; }
+      if (pp == 0 && ii < mj) { sdot[i].x += d.x; sdot[i].y += d.y; }
     }
   }
   }
@@ -2157,13 +2156,13 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
   if (warp == 1) tmem_dealloc<kRgTmemCols>(tbase);
 }
 
-// Output orders of the FFT kernels (fft.cuh's skewed slot layout): the row FFT's active columns
+// Output orders of the FFT kernels: the row FFT's active columns
 // sorted by the output slot of their vx, and within each column the active rows sorted by the slot
 // of their vy, so that consecutive threads of the output stages read consecutive slots.
+// slot of frequency f in fft_seq's output (fft::fslot)
 static int fslot_host(int logn, int f) {
-  const int L1 = (logn + 1) / 2, N1 = 1 << L1, N2 = 1 << (logn - L1);
-  const int k1 = f & (N1 - 1), k2 = f >> L1;
-  return N2 * k1 + ((k2 + k1) & (N2 - 1));
+  const int L1 = (logn + 1) / 2, N2 = 1 << (logn - L1);
+  return N2 * (f & ((1 << L1) - 1)) + (f >> L1);
 }
 
 cudaError_t fft_tables(Plan& p) {
