@@ -86,8 +86,6 @@ struct Plan {
   bool c_read_since_swap = false;     // a row transform (reader of d_Call) was launched since the last swap
   bool barrier_since_swap = false;    // shard groups: a readout barrier collective since the last swap
   int32_t* d_act_vy = nullptr;
-  int32_t* d_col_perm = nullptr;      // n_vx: row-FFT output order (columns by output slot)
-  int32_t* d_act_perm = nullptr;      // n_act: y-FFT output order within each column (rows by slot)
   int32_t* d_col_off = nullptr;
   int32_t* d_vpos = nullptr;          // n_act flattened v (scatter positions)
   int2* d_flush_tiles = nullptr;
@@ -174,7 +172,6 @@ int flush_kind(const Plan& p, int n_rows, bool allow_rg = true);   // 3 pipeline
 int flush_tiles(const Plan& p, int n_rows, int kind = -1);   // partial-readout tiles a flush writes (0: none)
 bool rgemm_possible(const Plan& p, int n_rows);
 cudaError_t rgemm_prepare(Plan& p);   // tensor maps + item table of the pipelined GEMM flush
-cudaError_t fft_tables(Plan& p);      // output-order tables of the FFT kernels (device)
 int colfft_tiles(const Plan& p);
 bool finalize_uses_fft(const Plan& p);
 // o[g] = sum_k G[g][k] W[g][k] (one warp per active v)

@@ -97,10 +97,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // columns) so that one CTA's pipeline fill / drain overlaps the other's streaming.
 constexpr bool kLeanAllowed = WDD_LEAN != 0;   // per configuration: lean only where it fits
 constexpr int kConv = 128;          // threads per converter group (2 groups: even / odd chunks)
-#ifndef WDD_LEAN_SMEM
-#define WDD_LEAN_SMEM (110 * 1024)
-#endif
-constexpr int kLeanSmem = WDD_LEAN_SMEM;   // shared-memory budget of a lean (two CTAs per SM) projection CTA
+constexpr int kLeanSmem = 110 * 1024;   // shared-memory budget of a lean (two CTAs per SM) projection CTA
 constexpr uint32_t kLBO = 2064;     // no-swizzle K-major: bytes between K-adjacent core matrices of a
                                     // 128-row operand (16 row groups x 128 B + 16 B bank-rotation pad)
 
@@ -789,7 +786,6 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
   auto kern = project_kernel<Q, L, U16>;
   {
     cudaError_t e = func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::smem);
-    if (e == cudaSuccess) e = func_attr_once((const void*)kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
   }
   if (n <= 0) return cudaSuccess;
@@ -907,7 +903,6 @@ int project_occupancy(const Plan& p) {
     if (p.dtype == 0) {                                                                              \
       using C = ProjCfg<QQ, LL, true>;                                                               \
       func_attr_once((const void*)project_kernel<QQ, LL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem); \
-      func_attr_once((const void*)project_kernel<QQ, LL, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100); \
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, project_kernel<QQ, LL, true>, C::kThreads, C::smem); \
     } else {                                                                                         \
       using C = ProjCfg<QQ, LL, false>;                                                              \
@@ -1002,64 +997,50 @@ template <int LOGN>
 __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MINB_LARGE) rowfft_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
                                                      const uint32_t* __restrict__ masks, int mask_words,
                                                      const float2* __restrict__ tw, const int32_t* __restrict__ col_vx,
-                                                     const int32_t* __restrict__ col_perm, float2* __restrict__ R,
-                                                     int logP, int Sy, int K, int n_vx, int n_rows,
+                                                     float2* __restrict__ R, int logP, int Sy, int K, int n_vx,
                                                      float scale, const __grid_constant__ CUtensorMap tmC, int use_tma) {
-  // CTA loops over tiles (one pending scan row x 2P coefficients): the twiddle table and the
-  // output slot table are set up once per CTA, not per tile
   constexpr int Sx = 1 << LOGN;
   constexpr int kBY = Sx < 256 ? Sx : 256;   // rows per TMA box
   extern __shared__ __align__(16) float2 fsm[];
   __shared__ uint32_t smask[(Sx + 31) / 32];
-  __shared__ int2 sslot[Sx];             // (slot of v, slot of -v), active columns in slot order
-  __shared__ int sj[Sx];                 // ... and their column index j
+  __shared__ int2 sslot[Sx];             // (slot of v, slot of -v) per active column j
   __shared__ __align__(8) uint64_t lbar;
   const int P = 1 << logP;
   float2* x = fsm;                       // [Sx][P]
   float2* stw = fsm + (Sx << logP);      // [Sx] twiddles
-  const int ktiles = K >> (logP + 1), n_tiles = ktiles * n_rows;
+  const int r = blockIdx.y, k0 = blockIdx.x * 2 * P;
   // use_tma bit 1 (set when this grid is itself PDL-launched): no early trigger -- this kernel reads
   // the coefficient store, which the first projection of the acquisition after next overwrites, so
-  // the dependents of this grid launch only once every CTA has its last C tile in shared memory.
+  // the dependents of this grid launch only once every CTA has its C tile in shared memory (below).
   // An ordinary (non-PDL) launch of this kernel starts after all earlier work has completed, which
   // already orders it after every earlier read of C; its dependents may then launch at once.
   if (!(use_tma & 2)) pdl_trigger();
   for (int i = threadIdx.x; i < Sx; i += blockDim.x) stw[i] = __ldg(tw + i);
-  // output order: columns sorted by the slot of their frequency (host table), so that a warp's
-  // (column, coefficient) reads hit consecutive slots of the FFT output
-  for (int q = threadIdx.x; q < n_vx; q += blockDim.x) {
-    const int j = __ldg(col_perm + q), v = __ldg(col_vx + j);
-    sslot[q] = make_int2(fft::fslot<LOGN>(v), fft::fslot<LOGN>((Sx - v) & (Sx - 1)));
-    sj[q] = j;
+  for (int j = threadIdx.x; j < n_vx; j += blockDim.x) {
+    const int v = __ldg(col_vx + j);
+    sslot[j] = make_int2(fft::fslot<LOGN>(v), fft::fslot<LOGN>((Sx - v) & (Sx - 1)));
   }
   if ((use_tma & 1) && threadIdx.x == 0) {
     mbar_init(&lbar, 1);
     fence_mbar_init();
   }
   pdl_wait();   // C of the projection kernels (and the uploaded row list / masks)
-  if ((use_tma & 2) && (int)blockIdx.x >= n_tiles) pdl_trigger();
-  uint32_t it = 0;
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
-  const int r = tile / ktiles, k0 = (tile - r * ktiles) * 2 * P;
-  const bool last = tile + (int)gridDim.x >= n_tiles;
   const int sy = rows[r];
-  __syncthreads();                       // x and smask free (previous tile's output stage done)
   if (use_tma & 1) {
-    // the tile's whole Sx x 2P slice of C in flight at once (one or more TMA boxes, pitch 2P floats =
+    // the CTA's whole Sx x 2P slice of C in flight at once (one or two TMA boxes, pitch 2P floats =
     // the FFT's [Sx][P] layout); positions outside the pending mask are zeroed afterwards
     if (threadIdx.x == 0) {
-      fence_proxy_async_smem();          // generic accesses of x before the async refill
       mbar_arrive_expect_tx(&lbar, (uint32_t)(Sx * P * 8));
       for (int b = 0; b < Sx / kBY; ++b) tma_load_2d(x + ((b * kBY) << logP), &tmC, k0, sy * Sx + b * kBY, &lbar);
     }
     if (threadIdx.x < mask_words) smask[threadIdx.x] = masks[(int64_t)r * mask_words + threadIdx.x];
     __syncthreads();
-    mbar_wait(&lbar, it & 1u);
+    mbar_wait(&lbar, 0);
     for (int sx = threadIdx.x; sx < Sx; sx += blockDim.x)
       if (!((smask[sx >> 5] >> (sx & 31)) & 1u))
         for (int pp = 0; pp < P; ++pp) x[(sx << logP) + pp] = make_float2(0.f, 0.f);
     __syncthreads();
-    if ((use_tma & 2) && last) pdl_trigger();   // every read of C by this CTA is complete
+    if (use_tma & 2) pdl_trigger();   // every read of C by this CTA is complete
   } else {
   if (threadIdx.x < mask_words) smask[threadIdx.x] = masks[(int64_t)r * mask_words + threadIdx.x];
   __syncthreads();
@@ -1091,17 +1072,16 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
     }
   }
   __syncthreads();
-  if ((use_tma & 2) && last) pdl_trigger();   // every read of C by this CTA is complete
+  if (use_tma & 2) pdl_trigger();   // every read of C by this CTA is complete
   }
   fft::fft_seq<LOGN>(x, stw, logP);
   const float hs = 0.5f * scale;
   for (int e = threadIdx.x; e < (n_vx << logP); e += blockDim.x) {
-    const int q = e >> logP, pp = e & (P - 1);
-    const int2 sl = sslot[q];
+    const int j = e >> logP, pp = e & (P - 1);
+    const int2 sl = sslot[j];
     const float2 z = x[(sl.x << logP) + pp], zm = x[(sl.y << logP) + pp];
     const float4 o = make_float4((z.x + zm.x) * hs, (z.y - zm.y) * hs, (z.y + zm.y) * hs, (zm.x - z.x) * hs);
-    *reinterpret_cast<float4*>(R + ((int64_t)sj[q] * Sy + sy) * K + k0 + 2 * pp) = o;
-  }
+    *reinterpret_cast<float4*>(R + ((int64_t)j * Sy + sy) * K + k0 + 2 * pp) = o;
   }
 }
 
@@ -1115,16 +1095,12 @@ template <int LOGN>
 __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MINB_LARGE) colfft_kernel(const float2* __restrict__ R, const int32_t* __restrict__ rows,
                                                      int n_rows, const float2* __restrict__ tw,
                                                      const int32_t* __restrict__ col_off,
-                                                     const int32_t* __restrict__ act_vy,
-                                                     const int32_t* __restrict__ act_perm, int n_vx,
-                                                     float2* __restrict__ G,
+                                                     const int32_t* __restrict__ act_vy, float2* __restrict__ G,
                                                      const float2* __restrict__ W, float2* __restrict__ opart,
                                                      int64_t n_act, int logKT, int K, float scale, int overwrite,
                                                      int tpc, int o_only, const __grid_constant__ CUtensorMap tmR,
                                                      int use_tma) {
-  // use_tma: bit 0 = R tiles by TMA, bit 3 = L2 prefetch of the output stage's W / G rows.
-  // Work item = (active column j, group g of tpc k-tiles); a CTA takes a contiguous run of items
-  // (columns outer), so the column's row tables are set up once per column, the twiddles once.
+  // use_tma: bit 0 = R tiles by TMA, bit 3 = L2 prefetch of the output stage's W / G rows
   constexpr int Sy = 1 << LOGN;
   constexpr int kBY = Sy < 256 ? Sy : 256;   // rows per TMA box
   extern __shared__ __align__(16) float2 fsm[];
@@ -1132,17 +1108,18 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   __shared__ int srow[Sy];                // staged rows
   __shared__ uint8_t sstaged[Sy];         // row staged (TMA path: the others are zeroed)
   __shared__ __align__(8) uint64_t lbar;
-  __shared__ int svy[Sy];                 // slot of the column's active vy, in slot order ...
-  __shared__ int sidx[Sy];                // ... and their row index within the column
-  __shared__ float2 sdot[Sy];             // per-row readout partial over the item's k-tiles
+  __shared__ int svy[Sy];                 // slot of each active vy of column j
+  __shared__ float2 sdot[Sy];             // per-row readout partial over this CTA's k-tiles
   float2* x = fsm;                       // [Sy][KT]
   float2* stw = fsm + (Sy << logKT);     // [Sy] twiddles
-  const int groups = (K >> logKT) / tpc;
-  const int64_t n_items = (int64_t)n_vx * groups;
-  const int64_t per = (n_items + gridDim.x - 1) / gridDim.x;
-  const int64_t it0 = (int64_t)blockIdx.x * per, it1 = min(n_items, it0 + per);
+  const int j = blockIdx.y;
   pdl_trigger();
+  const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
   for (int i = threadIdx.x; i < Sy; i += blockDim.x) stw[i] = __ldg(tw + i);
+  for (int i = threadIdx.x; i < mj; i += blockDim.x) {
+    svy[i] = fft::fslot<LOGN>(__ldg(act_vy + g0 + i));
+    sdot[i] = make_float2(0.f, 0.f);
+  }
   if (use_tma & 1) {
     for (int i = threadIdx.x; i < Sy; i += blockDim.x) sstaged[i] = n_rows < Sy ? 0 : 1;
     if (threadIdx.x == 0) {
@@ -1156,25 +1133,8 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     __syncthreads();
     for (int i = threadIdx.x; i < n_rows; i += blockDim.x) sstaged[srow[i]] = 1;
   }
-  int jcur = -1, g0 = 0, mj = 0;
-  uint32_t ld = 0;                                     // TMA loads issued (barrier phase)
-  for (int64_t item = it0; item < it1; ++item) {
-  const int j = (int)(item / groups), grp = (int)(item - (int64_t)j * groups);
-  __syncthreads();                                     // previous item's readout partials written
-  if (j != jcur) {
-    jcur = j;
-    g0 = __ldg(col_off + j);
-    mj = __ldg(col_off + j + 1) - g0;
-    // rows in slot order (host table): a warp's output reads hit consecutive slots
-    for (int ii = threadIdx.x; ii < mj; ii += blockDim.x) {
-      const int i = __ldg(act_perm + g0 + ii);
-      svy[ii] = fft::fslot<LOGN>(__ldg(act_vy + g0 + i));
-      sidx[ii] = i;
-    }
-  }
-  for (int i = threadIdx.x; i < mj; i += blockDim.x) sdot[i] = make_float2(0.f, 0.f);
   for (int t = 0; t < tpc; ++t) {
-  const int k0 = (grp * tpc + t) * KT;
+  const int k0 = (blockIdx.x * tpc + t) * KT;
   const int hKT = KT >> 1, lh = logKT - 1;             // 16-byte pieces per row
   if (use_tma & 1) {
     // the Sy x KT tile of R[j] in flight at once (pitch KT complex = the FFT's [Sy][KT] layout);
@@ -1186,13 +1146,11 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
       for (int b = 0; b < Sy / kBY; ++b)
         tma_load_2d(x + ((b * kBY) << logKT), &tmR, 2 * k0, j * Sy + b * kBY, &lbar);
     }
-    mbar_wait(&lbar, ld & 1u);
-    ++ld;
+    mbar_wait(&lbar, (uint32_t)(t & 1));
     if (n_rows < Sy)
       for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x)
         if (!sstaged[e >> logKT]) x[e] = make_float2(0.f, 0.f);
   } else {
-  __syncthreads();                                     // x free (previous tile)
   if (n_rows < Sy)
     for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x) x[e] = make_float2(0.f, 0.f);
   __syncthreads();
@@ -1228,8 +1186,8 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   }
   __syncthreads();
   fft::fft_seq<LOGN>(x, stw, logKT);
-  // Output: thread = (row, coefficient pair p), rows in slot order; G (+)= X / sqrt(Sy) for the
-  // column's active vy, and the tile's share of sum_k G K_v reduced over the hKT threads of the row.
+  // Output: thread = (row slot, coefficient pair p); G (+)= X / sqrt(Sy) for the column's active
+  // vy, and the tile's share of sum_k G K_v reduced over the hKT threads of the row.
   const int pp = threadIdx.x & (hKT - 1), rs = threadIdx.x >> lh, rpp = (int)blockDim.x >> lh;
   float4* G4 = reinterpret_cast<float4*>(G);
   const float4* W4 = reinterpret_cast<const float4*>(W);
@@ -1238,19 +1196,18 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     float4 o[4], w[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int ii = ib + u * rpp + rs;
-      const int64_t gi = (int64_t)(g0 + (ii < mj ? sidx[ii] : 0)) * K2 + (k0 >> 1) + pp;
-      w[u] = ii < mj ? __ldg(W4 + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
-      o[u] = (ii < mj && !overwrite && !o_only) ? G4[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int i = ib + u * rpp + rs;
+      const int64_t gi = (int64_t)(g0 + i) * K2 + (k0 >> 1) + pp;
+      w[u] = i < mj ? __ldg(W4 + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
+      o[u] = (i < mj && !overwrite && !o_only) ? G4[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (ib + u * rpp >= mj) break;                     // block-uniform
-      const int ii = ib + u * rpp + rs;
+      const int i = ib + u * rpp + rs;
       float2 d = make_float2(0.f, 0.f);
-      const int i = ii < mj ? sidx[ii] : 0;
-      if (ii < mj) {
-        const float4 z = *reinterpret_cast<const float4*>(x + (svy[ii] << logKT) + 2 * pp);
+      if (i < mj) {
+        const float4 z = *reinterpret_cast<const float4*>(x + (svy[i] << logKT) + 2 * pp);
         const float4 gn = make_float4(fmaf(z.x, scale, o[u].x), fmaf(z.y, scale, o[u].y), fmaf(z.z, scale, o[u].z),
                                       fmaf(z.w, scale, o[u].w));
         if (!o_only) G4[(int64_t)(g0 + i) * K2 + (k0 >> 1) + pp] = gn;
@@ -1261,13 +1218,12 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
         d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
         d.y += __shfl_xor_sync(0xffffffffu, d.y, off);
       }
-      if (pp == 0 && ii < mj) { sdot[i].x += d.x; sdot[i].y += d.y; }
+      if (pp == 0 && i < mj) { sdot[i].x += d.x; sdot[i].y += d.y; }
     }
   }
+  __syncthreads();   // x reused by the next k-tile; sdot settled
   }
-  __syncthreads();   // sdot settled
-  for (int i = threadIdx.x; i < mj; i += blockDim.x) opart[(int64_t)grp * n_act + g0 + i] = sdot[i];
-  }
+  for (int i = threadIdx.x; i < mj; i += blockDim.x) opart[(int64_t)blockIdx.x * n_act + g0 + i] = sdot[i];
 }
 
 static int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
@@ -1413,8 +1369,7 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
                                        kFftSmem + 16384);
         if (e != cudaSuccess) return e;
       }
-      const int n_tiles = (p.Kl / (2 << logP)) * n_rows;
-      const int grid = std::max(1, std::min(n_tiles, p.sm_count * (LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MINB_LARGE) * 4));
+      dim3 grid(p.Kl / (2 << logP), n_rows);
       // (with two projection CTAs per SM a PDL-launched row FFT would park its CTAs next to the
       // last projection CTAs and slow them down: launch it after the projection completes)
       static const int env_pdl = [] { const char* e = std::getenv("WDD_ROWFFT_PDL"); return e ? std::atoi(e) : -1; }();
@@ -1422,10 +1377,9 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
       CUtensorMap tmC;
       const bool tma = fft_tmap(&tmC, p.d_Call, (uint64_t)p.Kl, (uint64_t)p.S, (uint64_t)p.Kl * 4, 2u << logP,
                                 (uint32_t)std::min(p.Sx, 256));
-      return launch_pdl(rowfft_kernel<LOGN>, dim3(grid), dim3(nt), smem, st, rowfft_pdl, (const float*)p.d_Call, rows,
-                        masks, p.mask_words, (const float2*)p.d_twx, (const int32_t*)p.d_col_vx,
-                        (const int32_t*)p.d_col_perm, p.d_R, logP, p.Sy, p.Kl, p.n_vx, n_rows,
-                        (float)(1.0 / std::sqrt((double)p.Sx)), tmC, (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0));
+      return launch_pdl(rowfft_kernel<LOGN>, grid, dim3(nt), smem, st, rowfft_pdl, (const float*)p.d_Call, rows, masks,
+                        p.mask_words, (const float2*)p.d_twx, (const int32_t*)p.d_col_vx, p.d_R, logP, p.Sy, p.Kl,
+                        p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0));
     });
   }
   {
@@ -2156,42 +2110,6 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
   if (warp == 1) tmem_dealloc<kRgTmemCols>(tbase);
 }
 
-// Output orders of the FFT kernels: the row FFT's active columns
-// sorted by the output slot of their vx, and within each column the active rows sorted by the slot
-// of their vy, so that consecutive threads of the output stages read consecutive slots.
-// slot of frequency f in fft_seq's output (fft::fslot)
-static int fslot_host(int logn, int f) {
-  const int L1 = (logn + 1) / 2, N2 = 1 << (logn - L1);
-  return N2 * (f & ((1 << L1) - 1)) + (f >> L1);
-}
-
-cudaError_t fft_tables(Plan& p) {
-  std::vector<int32_t> cperm(p.n_vx), aperm(p.n_act);
-  for (int j = 0; j < p.n_vx; ++j) cperm[j] = j;
-  if (is_pow2(p.Sx) && p.Sx <= (1 << kFftMaxLog)) {
-    const int l = ilog2(p.Sx);
-    std::stable_sort(cperm.begin(), cperm.end(), [&](int a, int b) {
-      return fslot_host(l, p.col_vx[a]) < fslot_host(l, p.col_vx[b]);
-    });
-  }
-  for (int j = 0; j < p.n_vx; ++j) {
-    const int g0 = p.col_off[j], mj = p.col_off[j + 1] - g0;
-    int32_t* q = aperm.data() + g0;
-    for (int i = 0; i < mj; ++i) q[i] = i;
-    if (is_pow2(p.Sy) && p.Sy <= (1 << kFftMaxLog)) {
-      const int l = ilog2(p.Sy);
-      std::stable_sort(q, q + mj, [&](int a, int b) {
-        return fslot_host(l, p.act_vy[g0 + a]) < fslot_host(l, p.act_vy[g0 + b]);
-      });
-    }
-  }
-  cudaError_t e = cudaMalloc(&p.d_col_perm, cperm.size() * sizeof(int32_t));
-  if (e == cudaSuccess) e = cudaMalloc(&p.d_act_perm, aperm.size() * sizeof(int32_t));
-  if (e == cudaSuccess) e = cudaMemcpy(p.d_col_perm, cperm.data(), cperm.size() * 4, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(p.d_act_perm, aperm.data(), aperm.size() * 4, cudaMemcpyHostToDevice);
-  return e;
-}
-
 // k-chunks of the GEMM flush: enough CTAs to fill two waves of the GPU
 static int colgemm_chunks(const Plan& p) {
   int max_mj = 0;
@@ -2359,9 +2277,7 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
         if (e != cudaSuccess) return e;
       }
       const int tpc = colfft_tpc(p);
-      const int64_t n_items = (int64_t)((p.Kl >> logKT) / tpc) * p.n_vx;
-      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n_items, (int64_t)p.sm_count *
-                                                   (LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MINB_LARGE) * 4));
+      dim3 grid((p.Kl >> logKT) / tpc, p.n_vx);
       static const int2 knob = env_pair("WDD_COLFFT");
       // L2 prefetch of the output stage's rows: Large readout 339 -> 333 us, Box 3.77 -> 3.65 ms;
       // none at Medium (-0.15%: fewer load rounds per tile), so only from Sy = 256
@@ -2369,9 +2285,8 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
       CUtensorMap tmR;
       const bool tma = fft_tmap(&tmR, p.d_R, (uint64_t)p.Kl * 2, (uint64_t)p.n_vx * p.Sy, (uint64_t)p.Kl * 8,
                                 2u << logKT, (uint32_t)std::min(p.Sy, 256));
-      return launch_pdl(colfft_kernel<LOGN>, dim3(grid), dim3(knob.y > 0 ? knob.y : 256), smem, st, true, p.d_R, rows,
-                        n_rows, (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy,
-                        (const int32_t*)p.d_act_perm, p.n_vx, p.d_G,
+      return launch_pdl(colfft_kernel<LOGN>, grid, dim3(knob.y > 0 ? knob.y : 256), smem, st, true, p.d_R, rows, n_rows,
+                        (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G,
                         (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.Kl,
                         (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0, tpc, o_only ? 1 : 0, tmR,
                         (tma ? 1 : 0) | (pf_on && p.Sy >= 256 ? 8 : 0));

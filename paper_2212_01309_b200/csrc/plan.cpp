@@ -541,7 +541,7 @@ void free_plan(Plan* p) {
   for (int o = 0; o < kMaxShards; ++o)
     if (p->peers_ipc[o] && p->peer_base[o]) cudaIpcCloseMemHandle(p->peer_base[o]);
   full_wdd_release(*p);
-  void* bufs[] = {p->d_rg_items, p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Cbase, p->d_col_perm, p->d_act_perm,
+  void* bufs[] = {p->d_rg_items, p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Cbase,
                   p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec, p->d_img_tmp,
                   p->d_meta, p->d_stage[0], p->d_stage[1], p->d_err};
   for (void* b : bufs)
@@ -741,7 +741,6 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ALLOC(p->d_flush_tiles, p->flush_tiles.size() * sizeof(int2));
   ALLOC(p->d_o, act.size() * sizeof(float2));
   if (rgemm_prepare(*p) != cudaSuccess) return bail(fail(WDD_E_CUDA, "GEMM flush setup failed"));
-  if (fft_tables(*p) != cudaSuccess) return bail(fail(WDD_E_NOMEM, "FFT order tables"));
   p->opart_cap = std::max({1, colfft_tiles(*p), flush_tiles(*p, 1 << 20), p->rg_ready ? flush_tiles(*p, 64, 3) : 1});
   ALLOC(p->d_opart, (size_t)p->opart_cap * act.size() * sizeof(float2));
   ALLOC(p->d_gidx, (size_t)p->S * sizeof(int32_t));
