@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc2_empty[gb]);
-      const int f = m2 / L, aa = m2 % L;
+      const int f = m2 / L;
       const int64_t fg = frame0 + f;
       if constexpr (Cfg::kCStage) if (a.dst.n == 1) {
         // lanes 0-15 of this warp hold rows aa0 .. aa0 + 15 of one frame (a contiguous 16 L floats
