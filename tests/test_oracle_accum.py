@@ -85,17 +85,17 @@ def test_accumulate_at_equals_fft_rows():
     assert np.max(np.abs(O.accumulate_at(C, idx, v, Sy, Sx) - O.accumulate_fft(C, idx, Sy, Sx)[v])) < 1e-12
 
 
-def test_scan_phase_large_indices_exact_reduction():
-    # At 1024 x 1024 the integer-reduced phase must agree with the explicitly reduced angle
-    # (vy*sy mod Sy is exact in int64), and |f_s[v]| = 1/sqrt(S) for every entry.
+def test_scan_phase_large_indices_equals_fft_of_impulse():
+    # f_s[v] at 1024 x 1024 against an independent computation: the unitary 2-D FFT of
+    # a unit impulse at scan position s is exactly the column f_s of F_2D; checked at every v for
+    # scan positions near the ends of both axes (large products vy*sy, integer angle reduction).
     Sy = Sx = 1024
-    v = np.array([1023 * Sx + 1023, 511 * Sx + 3, 0])
-    s = np.array([1023 * Sx + 1022, 7, 1024 * 1024 - 1])
-    f = O.scan_phase(v, s, Sy, Sx)
-    assert np.allclose(np.abs(f), 1.0 / 1024, rtol=0, atol=1e-15)
-    vy, vx, sy, sx = v[:, None] // Sx, v[:, None] % Sx, s[None] // Sx, s[None] % Sx
-    ang = 2 * np.pi * ((vy * sy % Sy) / Sy + (vx * sx % Sx) / Sx)
-    assert np.max(np.abs(f - np.exp(-1j * ang) / 1024)) < 1e-15
+    for s in (1023 * Sx + 1022, 7, 1024 * 1024 - 1, 511 * Sx + 513):
+        imp = np.zeros((Sy, Sx))
+        imp[s // Sx, s % Sx] = 1.0
+        ref = np.fft.fft2(imp, norm="ortho").reshape(-1)
+        f = O.scan_phase(np.arange(Sy * Sx), [s], Sy, Sx)[:, 0]
+        assert np.max(np.abs(f - ref)) < 1e-15
 
 
 def test_project_events_equals_dense_projection():

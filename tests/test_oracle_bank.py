@@ -56,6 +56,35 @@ def test_active_set_equals_brute_force_over_all_frequencies():
     assert np.array_equal(O.active_set(g, cfg.Sy, cfg.Sx), np.array(brute))
 
 
+@pytest.mark.parametrize("name", ["medium", "large", "live", "box"])
+def test_active_set_equals_aperture_self_correlation(name):
+    # An independent construction of the exact active set (R9): in units of the scan
+    # frequency, the shift q_hat_v is v~ Q / S detector pixels (R8), an integer on the grid refined by
+    # F = S / Q.  There, v is active iff v~ = d - a for an aperture pixel a (coarse pixels, scaled by
+    # F) and a point d of the aperture disc (fine grid): the support of the cross-correlation of the
+    # two indicator arrays, computed by FFT convolution -- no per-v pixel test as in active_set.
+    from scipy.signal import fftconvolve
+    cfg = CONFIGS[name]
+    g = O.geometry(cfg)
+    assert cfg.Sy == cfg.Sx and cfg.Sy % cfg.Q == 0
+    F = cfg.Sy // cfg.Q
+    Rf = g.R * F                                            # disc radius on the fine grid
+    h = int(np.ceil(Rf)) + 1
+    w = np.arange(-h, h + 1)
+    D = (w[:, None] ** 2 + w[None, :] ** 2 <= Rf * Rf).astype(np.float64)
+    A = np.zeros_like(D)
+    u = np.arange(cfg.Q) - cfg.Q // 2                      # coarse pixel coordinates
+    uu = u[np.abs(u) * F <= h]
+    inside = uu[:, None] ** 2 + uu[None, :] ** 2 <= g.R * g.R
+    iy, ix = np.nonzero(inside)
+    A[uu[iy] * F + h, uu[ix] * F + h] = 1.0
+    corr = fftconvolve(D, A[::-1, ::-1])                    # corr[t] = sum_a A[a] D[a + t]
+    ty, tx = np.nonzero(corr > 0.5)
+    ty, tx = ty - 2 * h, tx - 2 * h
+    v = np.sort((ty % cfg.Sy) * cfg.Sx + (tx % cfg.Sx))
+    assert np.array_equal(v, O.active_set(g, cfg.Sy, cfg.Sx))
+
+
 @pytest.mark.parametrize("name,n_act", [("tiny", 517), ("medium", 7425), ("large", 29593)])
 def test_active_set_counts_and_symmetry(name, n_act):
     # Counts recorded in SURVEY.md Appendix A E6 (exact discrete test).  Symmetry: Y_{-v}(q) =
