@@ -437,7 +437,7 @@ def main():
     for _ in range(2):
         plan.graph_launch(h_ing, stream)
     torch.cuda.synchronize()
-    reps = max(3, min(args.steps, 10 if n_own >= 1 << 18 else 100))
+    reps = max(3, min(args.steps, 10 if cfg.S >= 1 << 18 else 100))   # (same on every rank)
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(stream)
     for _ in range(reps):

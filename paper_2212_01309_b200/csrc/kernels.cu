@@ -97,7 +97,10 @@ __device__ __forceinline__ unsigned long long gtime() {
 // columns) so that one CTA's pipeline fill / drain overlaps the other's streaming.
 constexpr bool kLeanAllowed = WDD_LEAN != 0;   // per configuration: lean only where it fits
 constexpr int kConv = 128;          // threads per converter group (2 groups: even / odd chunks)
-constexpr int kLeanSmem = 110 * 1024;   // shared-memory budget of a lean (two CTAs per SM) projection CTA
+#ifndef WDD_LEAN_SMEM
+#define WDD_LEAN_SMEM 115200          // two CTAs and their 1 KB reservations in the 227 KB carveout
+#endif
+constexpr int kLeanSmem = WDD_LEAN_SMEM;   // shared-memory budget of a lean (two CTAs per SM) projection CTA
 constexpr uint32_t kLBO = 2064;     // no-swizzle K-major: bytes between K-adjacent core matrices of a
                                     // 128-row operand (16 row groups x 128 B + 16 B bank-rotation pad)
 
@@ -160,18 +163,24 @@ struct ProjCfgT {
   // instead of 16-byte pieces of 16 rows) where it fits: Q = 128, L = 32 (C is 1/8 of the bytes)
   static constexpr bool kCStage = Q == 128 && L == 32 && kM2 == 64;
   static constexpr int kCStageB = kCStage ? 4 * 16 * L * 4 : 0;
-  static constexpr int kFixed = (U16 ? 0 : 2 * kSlot) + align_up(kNB2 * 2 * kA2, 1024) + align_up(kB, 1024) + kCStageB + 512;
+  // with a single A2 image the staging aliases it: the stage-2 epilogue runs between the wait for
+  // the stage-2 MMAs (A2 free) and the next group's T writes (after an epilogue-wide barrier)
+  static constexpr bool kCAlias = kCStage && kNB2 == 1 && kCStageB <= 2 * kA2;
+  // shared memory besides the raw ring: A2 images, B image, C staging, the barriers and meta words
+  // of the other rings; each raw slot adds its two barriers and a meta word (kNSraw below)
+  static constexpr int kFixed = (U16 ? 0 : 2 * kSlot) + align_up(kNB2 * 2 * kA2, 1024) + align_up(kB, 1024) +
+                                (kCAlias ? 0 : kCStageB) + 8 * (2 * kNA + 2 * 2 + 3 * kNB2 + 3) + 4 * kNA + 80;
   // (lean: two CTAs and their per-CTA reservation must share the SM's 228 KB -- 110 KB each leaves
   // room; measured: 112.3 KB CTAs did not co-reside.  Two converter groups need an even ring.)
-  static constexpr int kNSraw = (((LEAN ? kLeanSmem : 232448) - kFixed) / kSlot) & (kNGroups == 2 ? ~1 : ~0);
+  static constexpr int kNSraw = (((LEAN ? kLeanSmem : 232448) - kFixed) / (kSlot + 8 * 2 + 4)) & (kNGroups == 2 ? ~1 : ~0);
   static constexpr int kNSfit = kNSraw < 2 ? 2 : kNSraw;   // (lean: configs that do not fit run 1 CTA/SM)
   static constexpr int kNS = kNSfit < WDD_NS ? kNSfit : WDD_NS;  // raw ring (even: group = job parity)
   static constexpr int off_ring = 0;
   static constexpr int off_P1 = off_ring + kNS * kSlot;   // f32 path only
   static constexpr int off_A2 = off_P1 + (U16 ? 0 : 2 * kSlot);
   static constexpr int off_B = off_A2 + align_up(kNB2 * 2 * kA2, 1024);
-  static constexpr int off_C = off_B + align_up(kB, 1024);
-  static constexpr int off_bar = off_C + kCStageB;
+  static constexpr int off_C = kCAlias ? off_A2 : off_B + align_up(kB, 1024);
+  static constexpr int off_bar = off_B + align_up(kB, 1024) + (kCAlias ? 0 : kCStageB);
   static constexpr int kBars = 2 * kNS + 2 * kNA + 2 * kNAcc + 3 * kNB2 + 3;
   static constexpr int off_misc = off_bar + 8 * kBars;    // meta[kNS+kNA], wflag[2 groups][2][4], tmem slot
   static constexpr int smem = off_misc + 4 * (kNS + kNA) + 64 + 16;
@@ -184,8 +193,10 @@ struct ProjCfgT {
 template <int Q, int L, bool U16>
 struct ProjCfgSel {
   using LeanCfg = ProjCfgT<Q, L, U16, true>;
+  // (Q = 256, L = 32 would fit a three-slot lean CTA, but measured slower than the full variant's
+  // eight slots and two converter groups: Live step 0.78 vs 0.81 of its roofline)
   static constexpr bool lean = kLeanAllowed && LeanCfg::smem <= kLeanSmem && LeanCfg::kTmemUsed <= 256 &&
-                               LeanCfg::kNSraw >= 3;
+                               LeanCfg::kNSraw >= 3 && !(Q == 256 && L == 32);
   using type = typename std::conditional<lean, LeanCfg, ProjCfgT<Q, L, U16, false>>::type;
 };
 template <int Q, int L, bool U16>
@@ -692,6 +703,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
           mbar_wait(&s2_done[ab], ((c2 / Cfg::kNB2) - 1) & 1u);
           tc_fence_after();
           flush_pending(c2 - Cfg::kNB2);
+          if constexpr (Cfg::kCAlias) named_sync(2, 128);   // every warp's C staging (in A2) read out
         }
         // A2 element (m = f*L + a, k), MN-major: (m/8)*kSBO2 + (k/8)*128 + (k%8)*16 + (m%8)*2
         int f, k;
@@ -786,6 +798,7 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
   auto kern = project_kernel<Q, L, U16>;
   {
     cudaError_t e = func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::smem);
+    if (e == cudaSuccess) e = func_attr_once((const void*)kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
   }
   if (n <= 0) return cudaSuccess;

@@ -183,6 +183,36 @@ def test_full_geometry_row_subset(env, name, n, rows, step):
     assert rel(G[[pos[int(v)] for v in v_s]], G_ref) < TOL
 
 
+def test_group_with_one_rank_communicators(env):
+    # every plan of the group has a (one-rank) NCCL communicator, so readouts and accumulator reads
+    # take the shard-group path: the barrier collective (empty ordinary kernel, one-element
+    # allreduce, empty kernel) before the flush, and the allreduce of o -- the identity on one rank,
+    # so each plan still returns its own shard's spectrum; their sum is the oracle's
+    torch, wdd = env
+    cfg = CONFIGS["medium"]
+    idx = np.arange(cfg.S)
+    fr = Acquisition(cfg).frames_parallel(idx)
+    dev = torch.from_numpy(fr).cuda()
+    plans = _group(wdd, cfg, 2)
+    for p in plans:
+        p.set_comm(1, 0, wdd.nccl_unique_id())
+    for k in range(2):                                  # two acquisitions: resets swap the stores
+        for p in plans:
+            p.reset()
+        for b, a in enumerate(range(0, cfg.S, 512)):
+            _ingest(plans, b % 2, dev[a:a + 512], idx[a:a + 512])
+        spec = sum(p.readout_spectrum().to(torch.complex128) for p in plans)
+        imgs = [p.readout() for p in plans]
+        ref = _oracle(cfg, fr, idx)
+        assert rel(spec.cpu().numpy(), ref["o"]) < TOL, k
+        G, act = _G(plans)
+        assert rel(G, ref["G"][act]) < TOL, k
+        # each plan's image is the image of its own shard's spectrum
+        for p, im in zip(plans, imgs):
+            own = p.readout_spectrum(combine=False)
+            assert rel(im.cpu().numpy(), p.image_from_spectrum(own).cpu().numpy()) < 1e-6
+
+
 def test_shard_errors(env):
     torch, wdd = env
     cfg = CONFIGS["tiny"]
