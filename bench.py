@@ -483,8 +483,9 @@ def main():
 
     peaks, peak_src = _peaks()
     info = plan.info()
-    # wdd_ingest launches one projection per 8 192 frames of a call (the plan's chunk size)
-    n_launch = sum(-(-len(s[2]) // 8192) for s in own)
+    # wdd_ingest launches one projection per call over contiguous scan positions (all of bench.py's
+    # batches are contiguous runs)
+    n_launch = len(own)
     bytes_per_launch = n_own / n_launch * (fb + cfg.K * 4)     # frames read + C written (per launch)
     proj_ms_launch = proj_ms_step / n_launch
     achieved = bytes_per_launch / (proj_ms_launch * 1e-3) / 1e9

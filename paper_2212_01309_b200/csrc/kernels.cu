@@ -507,6 +507,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
 #pragma unroll
             for (int q = 0; q < kW; ++q) w[q] = magic_half2(w[q] & 0x03FF03FFu) | 0u;
             mbar_wait(&a_empty[aslot], aphase ^ 1u);
+            if (ct == 0) TRACE(13, aslot);
             tc_fence_after();
 #pragma unroll
             for (int q = 0; q < kW; q += 16) tmem_st16(tbase + lane_addr + Cfg::tA + aslot * Cfg::kACols + q, w + q);
@@ -701,8 +702,10 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
         const uint32_t ab = c2 % Cfg::kNB2;
         if (tt % tph == 0 && c2 >= (uint32_t)Cfg::kNB2) {   // A2 image ab is free once chunk c2 - kNB2 is done
           mbar_wait(&s2_done[ab], ((c2 / Cfg::kNB2) - 1) & 1u);
+          if (et == 0) TRACE(14, tile);
           tc_fence_after();
           flush_pending(c2 - Cfg::kNB2);
+          if (et == 0) TRACE(15, tile);
           if constexpr (Cfg::kCAlias) named_sync(2, 128);   // every warp's C staging (in A2) read out
         }
         // A2 element (m = f*L + a, k), MN-major: (m/8)*kSBO2 + (k/8)*128 + (k%8)*16 + (m%8)*2

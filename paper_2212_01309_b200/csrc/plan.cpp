@@ -212,6 +212,8 @@ struct Prof {
   }
 };
 
+constexpr int64_t kMaxLaunchFrames = 1 << 20;   // frames of one projection launch (contiguous calls)
+
 // Two coefficient stores (WDD_C_DOUBLE=0: one; the first projection of every acquisition then waits
 // for the previous readout).
 bool double_c_store() {
@@ -814,8 +816,14 @@ wdd_status wdd_ingest(wdd_plan_t plan, const void* frames_dev, const int32_t* sc
   if (s != WDD_OK) return s;
   use_stream(p, reinterpret_cast<cudaStream_t>(stream));
   const size_t fb = frame_bytes(p);
-  for (int64_t c0 = 0; c0 < n; c0 += p.chunk_cap) {
-    const int64_t nc = std::min<int64_t>(p.chunk_cap, n - c0);
+  // a call over a contiguous run of scan positions is one projection launch (no index upload):
+  // each CTA then streams many frames, and its pipeline fill / drain is paid once per call
+  // (Large: 0.70 -> see DESIGN.md); scattered indices go in chunks of the metadata slot size
+  bool contiguous = true;
+  for (int64_t i = 1; i < n && contiguous; ++i) contiguous = scan_idx_host[i] == scan_idx_host[0] + i;
+  const int64_t cap = contiguous ? std::max<int64_t>(p.chunk_cap, kMaxLaunchFrames) : p.chunk_cap;
+  for (int64_t c0 = 0; c0 < n; c0 += cap) {
+    const int64_t nc = std::min<int64_t>(cap, n - c0);
     s = enqueue_chunk(p, static_cast<const uint8_t*>(frames_dev) + (size_t)c0 * fb, scan_idx_host + c0, nc, c0 == 0);
     if (s != WDD_OK) return s;
   }

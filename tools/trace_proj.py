@@ -7,7 +7,8 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 NAMES = {2: "prod issue TMA", 3: "conv raw landed", 4: "conv A full", 5: "mma1 A ready",
-         6: "mma1 acc free", 8: "epi acc1 full", 10: "epi A2 written", 11: "epi a2_full", 12: "mma2 start"}
+         6: "mma1 acc free", 8: "epi acc1 full", 10: "epi A2 written", 11: "epi a2_full", 12: "mma2 start",
+         13: "conv A slot free", 14: "epi s2 done", 15: "epi C stored"}
 
 
 def main():
@@ -32,7 +33,7 @@ def main():
     ev = sorted((v >> 16, (v >> 8) & 0xff, v & 0xff) for v in buf[:k] if v)
     t0 = ev[0][0]
     w0 = int(sys.argv[3]) if len(sys.argv) > 3 else 0
-    for t, c, j in ev[w0:w0 + 120]:
+    for t, c, j in ev[w0:w0 + 100000]:
         print(f"{(t - t0) / 1000:9.3f} us  {NAMES.get(c, c):18s} {j}")
     for c in sorted(NAMES):
         ts = [t for t, cc, _ in ev if cc == c]
