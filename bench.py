@@ -457,18 +457,31 @@ def main():
     torch.cuda.synchronize()
     lat_ing = np.array([a.elapsed_time(b) for a, b in evs["ingest"]]) * 1e3
     lat_rd = np.array([a.elapsed_time(b) for a, b in evs["readout"]]) * 1e3
-    iso = []
-    for k in range(5):
-        plan.reset()
-        s = own[min(k, len(own) - 1)]
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        plan.ingest(frames_of(s[1], len(s[2])), s[2], stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        iso.append(e0.elapsed_time(e1) * 1e3)
-    plan.reset()
+    def isolated(pl):
+        # a lone batch on an idle GPU (the second batch of an acquisition: not the wide first launch)
+        t = []
+        for k in range(5):
+            pl.reset()
+            s0, s = own[0], own[min(1, len(own) - 1)]
+            if s is not s0:
+                pl.ingest(frames_of(s0[1], len(s0[2])), s0[2], stream)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            pl.ingest(frames_of(s[1], len(s[2])), s[2], stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t.append(e0.elapsed_time(e1) * 1e3)
+        pl.reset()
+        return t
+    iso = isolated(plan) if not kshard else [float("nan")]
+    iso_spread = [float("nan")]
+    if world == 1:
+        # the same on a plan with the latency grid (opts.ingest_spread = 1)
+        lp = wdd.Plan.from_config(cfg, device=local, ingest_overlap=True, accumulator=args.accumulator,
+                                  ingest_spread=True)
+        iso_spread = isolated(lp)
+        lp.close()
 
     # ---- per-kernel device times (eager, event pairs around every launch: isolated-launch costs)
     plan.profile_enable(True)
@@ -568,11 +581,14 @@ def main():
             "latency": {
                 "ingest_batch_us": {"p50": float(np.percentile(lat_ing, 50)), "p99": float(np.percentile(lat_ing, 99)),
                                     "max": float(lat_ing.max()), "n": int(len(lat_ing)), "frames": batch},
-                "isolated_batch_us": {"median": float(np.median(iso)), "n": len(iso), "frames": len(own[0][2])},
+                "isolated_batch_us": {"median": float(np.median(iso)), "n": len(iso),
+                                      "frames": len(own[min(1, len(own) - 1)][2]),
+                                      "latency_grid_median": float(np.median(iso_spread))},
                 "readout_us": {"p50": float(np.percentile(lat_rd, 50)), "max": float(lat_rd.max()),
                                "n": int(len(lat_rd))},
                 "how": "CUDA events around each call of one eager acquisition (ingest_batch, readout); "
-                       "isolated_batch: one batch on an idle GPU after a sync"},
+                       "isolated_batch: one batch on an idle GPU after a sync (default throughput grid, "
+                       "and on a plan with the latency grid, opts.ingest_spread = 1)"},
             "kernels_isolated": kern,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(cfg.S * fb),
                     "d2h_bytes_per_step": int(cfg.S * 8 * n_read)},

@@ -84,7 +84,11 @@ typedef struct {
                             k_rank of n (contiguous, as even as possible, n <= L) -- its coefficient
                             store, R staging, G and bank hold only those k; see wdd_set_shard_peers */
   int32_t k_rank;        /* this plan's shard, 0 <= k_rank < k_shards                              */
-  int32_t reserved[3];   /* must be zero                                                      */
+  int32_t ingest_spread; /* 0 (default) = throughput grid: ~0.5-1 MiB of frames per projection CTA,
+                            so consecutive (PDL-chained) batches stream side by side on the SMs;
+                            1 = latency grid: every launch spread over all SMs (a lone batch on an
+                            idle GPU finishes sooner; chained small batches lose overlap)          */
+  int32_t reserved[2];   /* must be zero                                                      */
 } wdd_plan_opts;
 
 /* Plan creation (host, blocking): derives dq, R, sigma; computes in float64 the basis Psi,

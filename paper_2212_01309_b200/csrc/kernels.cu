@@ -825,6 +825,7 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
   // launches of the following batches find a full machine instead of ramping up one grid at a time
   static const int wide_first = [] { const char* e = std::getenv("WDD_PROJ_WIDE_FIRST"); return e ? std::atoi(e) : 1; }();
   if (wide_first && p.frames_ingested == 0 && env_frames < 0) min_frames = 1;
+  if (p.ingest_spread) min_frames = 1;                 // latency grid (opts.ingest_spread)
   if (min_frames > 0) g2 = Cfg::kG2;
   const int64_t groups = (n + g2 - 1) / g2;
   int grid = (int)std::min<int64_t>(groups, (int64_t)p.sm_count * Cfg::kMinBlocks);
@@ -1707,7 +1708,10 @@ constexpr int kRgPlaneB = (kRgN / 8) * (kRgRows / 8) * 128;  // 8 KB: element (n
 constexpr int kRgStB = 2 * kRgPlaneB;                        // 16 KB = the fp32 R tile (two 128-B halves x 64 rows)
 constexpr int kRgHalfR = kRgRows * 128;                      // 8 KB: one 16-coefficient half of the R tile
 constexpr int kRgM = 128;
-constexpr int kRgNB = 2;                                     // B ring depth (MMA tiles)
+#ifndef WDD_RG_NB
+#define WDD_RG_NB 2
+#endif
+constexpr int kRgNB = WDD_RG_NB;                             // B ring depth (MMA tiles)
 constexpr int kRgBoxGW = kRgM * 128;                         // 16 KB: 128 rows x 16 complex
 constexpr int kRgStWG = 2 * kRgBoxGW;                        // 32 KB: W box + G box of one half tile
 #ifndef WDD_RG_NWG

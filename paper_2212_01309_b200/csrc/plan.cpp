@@ -583,6 +583,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   for (int r : o.reserved)
     if (r) return fail(WDD_E_ARG, "opts.reserved must be zero");
   if (o.ingest_overlap != 0 && o.ingest_overlap != 1) return fail(WDD_E_ARG, "ingest_overlap must be 0 or 1");
+  if (o.ingest_spread != 0 && o.ingest_spread != 1) return fail(WDD_E_ARG, "ingest_spread must be 0 or 1");
   const int Sy = scan_shape[0], Sx = scan_shape[1], Q = det_shape[0];
   if (Sy < 2 || Sx < 2 || (int64_t)Sy * Sx > (1ll << 30)) return fail(WDD_E_ARG, "scan shape %d x %d unsupported", Sy, Sx);
   if (det_shape[1] != Q || !(Q == 32 || Q == 64 || Q == 128 || Q == 256))
@@ -610,6 +611,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   p->eps = wiener_eps;
   p->o_only = o.accumulator == 1;
   p->ingest_overlap = o.ingest_overlap;
+  p->ingest_spread = o.ingest_spread;
   p->nshard = nshard;
   p->shard = nshard > 1 ? o.k_rank : 0;
   if (nshard > 1) p->combine = 0;   // (the shards' G are disjoint: the combine sums o)

@@ -34,7 +34,8 @@ class _Opts(ctypes.Structure):
     _fields_ = [("det_px_rad", ctypes.c_double), ("sigma_px", ctypes.c_double),
                 ("dtype", ctypes.c_int32), ("normalize", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("combine", ctypes.c_int32), ("accumulator", ctypes.c_int32), ("ingest_overlap", ctypes.c_int32),
-                ("k_shards", ctypes.c_int32), ("k_rank", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("k_shards", ctypes.c_int32), ("k_rank", ctypes.c_int32), ("ingest_spread", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class _Info(ctypes.Structure):
@@ -151,7 +152,7 @@ class Plan:
                  semiangle_rad: float, defocus_A: float = 0.0, wiener_eps: float = 1e-3, *,
                  dtype: str = "u16", normalize: bool = False, device: int = 0, sigma_px: float = 0.0,
                  det_px_rad: float = 0.0, combine: int = 0, accumulator: str = "G",
-                 ingest_overlap: bool = False, k_shards: int = 0, k_rank: int = 0):
+                 ingest_overlap: bool = False, k_shards: int = 0, k_rank: int = 0, ingest_spread: bool = False):
         lib = load_library()
         scan = (ctypes.c_int32 * 2)(*[int(v) for v in scan_shape])
         det = (ctypes.c_int32 * 2)(*[int(v) for v in det_shape])
@@ -167,6 +168,7 @@ class Plan:
         opts.ingest_overlap = int(bool(ingest_overlap))
         opts.k_shards = int(k_shards)
         opts.k_rank = int(k_rank)
+        opts.ingest_spread = int(bool(ingest_spread))
         h = ctypes.c_void_p()
         _check(lib.wdd_plan_create(scan, float(step_A), det, int(K), ctypes.byref(probe), float(wiener_eps),
                                    ctypes.byref(opts), ctypes.byref(h)))
