@@ -169,6 +169,12 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
 // o_acc += sum of `tiles` partial readouts (spectrum-only plans)
 cudaError_t launch_oacc(const Plan& p, int tiles, cudaStream_t st);
 bool flush_uses_fft(const Plan& p, int n_rows);
+// a4 + a5 + a6 in one cluster kernel (scans up to 256 x 256): row FFT, y-FFT, G update and the
+// partial readouts (fused_tiles of them), R never materialised; rows / masks as launch_rowdft
+bool fused_possible(const Plan& p);
+int fused_tiles(const Plan& p);
+cudaError_t launch_fft2(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, bool overwrite,
+                        bool o_only, cudaStream_t st);
 int flush_kind(const Plan& p, int n_rows, bool allow_rg = true);   // 3 pipelined GEMM, 2 GEMM, 1 FFT, 0 DFT matrix
 int flush_tiles(const Plan& p, int n_rows, int kind = -1);   // partial-readout tiles a flush writes (0: none)
 bool rgemm_possible(const Plan& p, int n_rows);

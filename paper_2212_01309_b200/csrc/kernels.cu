@@ -2320,6 +2320,193 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
 }
 
 // =====================================================================================
+// a4 + a5 + a6 fused for scans up to 256 x 256: the whole 2-D scan DFT of a group of coefficients
+// in one thread-block cluster, so the row-DFT staging R never goes through HBM (the row FFT + y-FFT
+// pair moves 16 n_vx K / Sx bytes per frame through R otherwise).
+//   CTA r of the cluster owns scan rows [r RB, (r+1) RB) for the row pass: the 2 NP coefficients
+//   k0 .. k0 + 2NP - 1 of every position, packed as NP complex sequences (z = C_k + i C_k+1), are
+//   read from the coefficient store (pending positions only; the rest are zeros), FFT'd along x
+//   (fft_seq), and kept in shared memory.  After a cluster barrier, CTA r takes the active columns
+//   [r n_vx / CS, (r+1) n_vx / CS): it gathers each column's row transforms from all CTAs of the
+//   cluster through distributed shared memory (X_k = (Z[v] + conj Z[-v]) / 2, X_k+1 = (Z[v] -
+//   conj Z[-v]) / 2i, the real-pair split of rowfft_kernel), FFTs them along y, updates G (+)= X
+//   for the column's active vy and writes the Wiener readout partial of its 2 NP coefficients,
+//   opart[group][v] = sum_k G[v][k] K_v[k].  Exact like the two-kernel form (same
+//   transforms, same order of the additions in G; the partial readouts are summed over groups).
+// =====================================================================================
+template <int LX, int LY, int CS, int NP>
+__global__ void __launch_bounds__(256) fft2_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
+                                                   const uint32_t* __restrict__ masks, int n_rows, int mask_words,
+                                                   const float2* __restrict__ twx, const float2* __restrict__ twy,
+                                                   const int32_t* __restrict__ col_vx,
+                                                   const int32_t* __restrict__ col_off,
+                                                   const int32_t* __restrict__ act_vy, int n_vx,
+                                                   float2* __restrict__ G, const float2* __restrict__ W,
+                                                   float2* __restrict__ opart, int64_t n_act, int K, float sx_scale,
+                                                   float sy_scale, int overwrite, int o_only, int late_trigger) {
+  constexpr int SX = 1 << LX, SY = 1 << LY;
+  constexpr int LCS = CS == 8 ? 3 : CS == 4 ? 2 : CS == 2 ? 1 : 0;
+  constexpr int RB = SY / CS, LRB = LY - LCS;
+  constexpr int LCNT = LRB + (NP == 2 ? 1 : 0), CNT = 1 << LCNT;    // row-pass sequences (row, pair)
+  constexpr int CB = 8;                                               // columns per column-pass batch
+  constexpr int LCNT2 = 3 + (NP == 2 ? 1 : 0) + 1, CNT2 = 1 << LCNT2; // (column, pair, k / k+1)
+  static_assert(CNT2 == CB * NP * 2, "column batch");
+  extern __shared__ __align__(16) float2 fsm[];
+  float2* xr = fsm;                        // [SX][CNT]
+  float2* xc = xr + SX * CNT;              // [SY][CNT2]
+  float2* stx = xc + SY * CNT2;            // [SX]
+  float2* sty = stx + SX;                  // [SY]
+  __shared__ int sli[SY];                  // row -> index in the flush's row list, or -1
+  __shared__ int2 scs[CB];                 // batch column: (slot of v, slot of -v)
+  __shared__ int sgo[CB + 1];              // batch column: first accumulator row, then a prefix end
+  cg::cluster_group cluster = cg::this_cluster();
+  const int r = (int)cluster.block_rank();
+  const int k0 = blockIdx.y * 2 * NP;
+  const int tid = threadIdx.x;
+  if (!late_trigger) pdl_trigger();
+  for (int i = tid; i < SX; i += blockDim.x) stx[i] = __ldg(twx + i);
+  for (int i = tid; i < SY; i += blockDim.x) { sty[i] = __ldg(twy + i); sli[i] = -1; }
+  pdl_wait();   // C of the projections (and the uploaded row list / masks)
+  __syncthreads();
+  for (int i = tid; i < n_rows; i += blockDim.x) sli[__ldg(rows + i)] = i;
+  __syncthreads();
+  // ---- row pass: load this CTA's rows (sequence index fastest: conflict-free smem stores)
+  for (int e = tid; e < RB * SX; e += blockDim.x) {
+    const int i = e % RB, sx = e / RB, sy = r * RB + i;
+    const int li = sli[sy];
+    const bool ok = li >= 0 && ((__ldg(masks + (int64_t)li * mask_words + (sx >> 5)) >> (sx & 31)) & 1u);
+    const float* src = C + ((int64_t)sy * SX + sx) * K + k0;
+    if constexpr (NP == 2) {
+      const float4 v = ok ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      xr[sx * CNT + 2 * i] = make_float2(v.x, v.y);
+      xr[sx * CNT + 2 * i + 1] = make_float2(v.z, v.w);
+    } else {
+      const float2 v = ok ? __ldg(reinterpret_cast<const float2*>(src)) : make_float2(0.f, 0.f);
+      xr[sx * CNT + i] = v;
+    }
+  }
+  __syncthreads();
+  if (late_trigger) pdl_trigger();   // every read of C by this CTA is complete
+  fft::fft_seq<LX>(xr, stx, LCNT);
+  cluster.sync();                    // every CTA's row transforms are complete
+  // ---- column pass over this CTA's share of the active columns
+  const int jlo = (int)((int64_t)r * n_vx / CS), jhi = (int)((int64_t)(r + 1) * n_vx / CS);
+  const float hs = 0.5f * sx_scale;
+  for (int jb0 = jlo; jb0 < jhi; jb0 += CB) {
+    const int nb = min(CB, jhi - jb0);
+    if (tid < CB) {
+      if (tid < nb) {
+        const int v = __ldg(col_vx + jb0 + tid);
+        scs[tid] = make_int2(fft::fslot<LX>(v), fft::fslot<LX>((SX - v) & (SX - 1)));
+      }
+    }
+    if (tid == 0) {
+      sgo[0] = 0;
+      for (int b = 0; b < nb; ++b) sgo[b + 1] = sgo[b] + (__ldg(col_off + jb0 + b + 1) - __ldg(col_off + jb0 + b));
+    }
+    __syncthreads();
+    // gather X_k, X_k+1 of the batch's columns for every scan row from the owning CTA (DSMEM)
+    for (int e = tid; e < SY * CB * NP; e += blockDim.x) {
+      const int q = e % (CB * NP), sy = e / (CB * NP);
+      const int jb = q / NP, p = q - jb * NP;
+      float2 x0 = make_float2(0.f, 0.f), x1 = x0;
+      if (jb < nb) {
+        const float2* src = cluster.map_shared_rank(xr, sy / RB);
+        const int c = (sy % RB) * NP + p;
+        const int2 sl = scs[jb];
+        const float2 z = src[(sl.x << LCNT) + c], zm = src[(sl.y << LCNT) + c];
+        x0 = make_float2((z.x + zm.x) * hs, (z.y - zm.y) * hs);
+        x1 = make_float2((z.y + zm.y) * hs, (zm.x - z.x) * hs);
+      }
+      xc[sy * CNT2 + 2 * q] = x0;
+      xc[sy * CNT2 + 2 * q + 1] = x1;
+    }
+    __syncthreads();
+    fft::fft_seq<LY>(xc, sty, LCNT2);
+    // output: thread = one active (vy, column) of the batch, all 2 NP coefficients: G (+)= X, and
+    // the readout partial of these coefficients
+    const int tot = sgo[nb];
+    for (int f = tid; f < tot; f += blockDim.x) {
+      int jb = 0;
+      while (jb + 1 < nb && f >= sgo[jb + 1]) ++jb;
+      const int64_t g = __ldg(col_off + jb0 + jb) + (f - sgo[jb]);
+      const int slot = fft::fslot<LY>(__ldg(act_vy + g));
+      const float2* xs = xc + slot * CNT2 + jb * 2 * NP;
+      float2* Gr = G + g * K + k0;
+      const float2* Wr = W + g * K + k0;
+      float2 d = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int e2 = 0; e2 < 2 * NP; ++e2) {
+        const float2 w = __ldg(Wr + e2);
+        const float2 o = (overwrite || o_only) ? make_float2(0.f, 0.f) : Gr[e2];
+        const float2 z = xs[e2];
+        const float2 gn = make_float2(fmaf(z.x, sy_scale, o.x), fmaf(z.y, sy_scale, o.y));
+        if (!o_only) Gr[e2] = gn;
+        d.x = fmaf(gn.x, w.x, fmaf(-gn.y, w.y, d.x));
+        d.y = fmaf(gn.x, w.y, fmaf(gn.y, w.x, d.y));
+      }
+      opart[(int64_t)blockIdx.y * n_act + g] = d;
+    }
+    __syncthreads();                 // xc and the batch tables reused
+  }
+  cluster.sync();                    // no CTA leaves while others may still read its row transforms
+}
+
+// Fused 2-D flush geometry: square power-of-two scans from 32 to 256; two coefficient pairs per
+// cluster up to 128, one at 256; cluster size from 64 KB of row transforms per CTA.
+bool fused_possible(const Plan& p) {
+  static const bool off = [] { const char* e = std::getenv("WDD_FUSED"); return e && std::atoi(e) == 0; }();
+  return !off && p.Sx == p.Sy && is_pow2(p.Sx) && p.Sx >= 32 && p.Sx <= 256 && p.Kl % 4 == 0;
+}
+
+static int fused_np(const Plan& p) { return p.Sx <= 128 ? 2 : 1; }
+
+int fused_tiles(const Plan& p) { return p.Kl / (2 * fused_np(p)); }
+
+template <int LX, int CS, int NP>
+static cudaError_t launch_fft2_t(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, bool overwrite,
+                                 bool o_only, cudaStream_t st) {
+  constexpr int SX = 1 << LX, RB = SX / CS;
+  constexpr int CNT = RB * NP, CNT2 = 8 * NP * 2;
+  constexpr size_t smem = (size_t)(SX * CNT + SX * CNT2 + 2 * SX) * sizeof(float2);
+  auto kern = fft2_kernel<LX, LX, CS, NP>;
+  cudaError_t e = func_attr_once((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const bool pdl = !project_is_lean(p);   // (as the row FFT: see launch_rowdft)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS, p.Kl / (2 * NP));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, (const float*)p.d_Call, rows, masks, n_rows, p.mask_words,
+                            (const float2*)p.d_twx, (const float2*)p.d_twy, (const int32_t*)p.d_col_vx,
+                            (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.n_vx, p.d_G,
+                            (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, p.Kl,
+                            (float)(1.0 / std::sqrt((double)p.Sx)), (float)(1.0 / std::sqrt((double)p.Sy)),
+                            overwrite ? 1 : 0, o_only ? 1 : 0, pdl ? 1 : 0);
+}
+
+cudaError_t launch_fft2(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, bool overwrite,
+                        bool o_only, cudaStream_t st) {
+  switch (p.Sx) {
+    case 32: return launch_fft2_t<5, 1, 2>(p, rows, masks, n_rows, overwrite, o_only, st);
+    case 64: return launch_fft2_t<6, 1, 2>(p, rows, masks, n_rows, overwrite, o_only, st);
+    case 128: return launch_fft2_t<7, 4, 2>(p, rows, masks, n_rows, overwrite, o_only, st);
+    case 256: return launch_fft2_t<8, 8, 1>(p, rows, masks, n_rows, overwrite, o_only, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// =====================================================================================
 // Readout (a6): o_v = sum_k G[v][k] W[v][k], one warp per active v
 // =====================================================================================
 __global__ void __launch_bounds__(256) readout_kernel(const float2* __restrict__ G, const float2* __restrict__ W,

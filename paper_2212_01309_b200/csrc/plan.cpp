@@ -356,9 +356,10 @@ size_t frame_bytes(const Plan& p) { return (size_t)p.Q * p.Q * (p.dtype == 0 ? 2
 // read as zeros, so the coefficient store never needs clearing (each scan position is ingested at
 // most once per reset).  A contiguous range of complete rows (offline scans, live scans in scan
 // order) needs no upload: the rows are a slice of the plan's device iota and the masks all-ones.
-wdd_status stage_rows(Plan& p, const std::vector<int32_t>& rows_in) {
+// Row list + per-row pending masks of a row transform (device pointers *dr / *dm; the bookkeeping:
+// the rows' pending positions are consumed).  A contiguous range of complete rows needs no upload.
+wdd_status row_blob(Plan& p, const std::vector<int32_t>& rows_in, const int32_t** dr_out, const uint32_t** dm_out) {
   const int n_rows = (int)rows_in.size();
-  if (n_rows == 0) return WDD_OK;
   std::vector<int32_t> blob(rows_in);
   const size_t mask_off = ((size_t)n_rows + 3) / 4 * 4;
   blob.resize(mask_off + (size_t)n_rows * p.mask_words, 0);
@@ -374,20 +375,28 @@ wdd_status stage_rows(Plan& p, const std::vector<int32_t>& rows_in) {
       m = 0;
     }
     p.row_dirty[sy] = 0;
-    p.row_staged[sy] = 1;
   }
+  if (simple) {
+    *dr_out = p.d_iota + blob[0];
+    *dm_out = p.d_ones;
+    return WDD_OK;
+  }
+  void* d = nullptr;
+  wdd_status s = upload_meta(p, blob.data(), blob.size() * sizeof(int32_t), &d);
+  if (s != WDD_OK) return s;
+  *dr_out = static_cast<const int32_t*>(d);
+  *dm_out = reinterpret_cast<const uint32_t*>(*dr_out + mask_off);
+  return WDD_OK;
+}
+
+wdd_status stage_rows(Plan& p, const std::vector<int32_t>& rows_in) {
+  const int n_rows = (int)rows_in.size();
+  if (n_rows == 0) return WDD_OK;
   const int32_t* dr = nullptr;
   const uint32_t* dm = nullptr;
-  if (simple) {
-    dr = p.d_iota + blob[0];
-    dm = p.d_ones;
-  } else {
-    void* d = nullptr;
-    wdd_status s = upload_meta(p, blob.data(), blob.size() * sizeof(int32_t), &d);
-    if (s != WDD_OK) return s;
-    dr = static_cast<const int32_t*>(d);
-    dm = reinterpret_cast<const uint32_t*>(dr + mask_off);
-  }
+  wdd_status s = row_blob(p, rows_in, &dr, &dm);
+  if (s != WDD_OK) return s;
+  for (int32_t sy : rows_in) p.row_staged[sy] = 1;
   Prof pr(p, kSlotRowDft, p.stream);
   CUDA_TRY(launch_rowdft(p, dr, dm, n_rows, p.stream));
   p.c_read_since_swap = true;
@@ -400,6 +409,26 @@ wdd_status flush(Plan& p) {
   std::vector<int32_t> rows;
   for (int sy = 0; sy < p.Sy; ++sy)
     if (p.row_dirty[sy]) rows.push_back(sy);
+  if (!rows.empty() && flush_kind(p, (int)rows.size()) == 1 && fused_possible(p)) {
+    // the whole flush (row FFT, y-FFT, G update, partial readouts) in one cluster kernel
+    const int32_t* dr = nullptr;
+    const uint32_t* dm = nullptr;
+    wdd_status s = row_blob(p, rows, &dr, &dm);
+    if (s != WDD_OK) return s;
+    {
+      Prof pr(p, kSlotFlush, p.stream);
+      CUDA_TRY(launch_fft2(p, dr, dm, (int)rows.size(), p.G_zero, p.o_only, p.stream));
+    }
+    p.c_read_since_swap = true;
+    if (p.o_only) {
+      Prof pr(p, kSlotReadout, p.stream);
+      CUDA_TRY(launch_oacc(p, fused_tiles(p), p.stream));
+      return WDD_OK;
+    }
+    p.G_zero = false;
+    p.opart_tiles = fused_tiles(p);
+    return WDD_OK;
+  }
   wdd_status s = stage_rows(p, rows);
   if (s != WDD_OK) return s;
   rows.clear();
@@ -745,7 +774,8 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ALLOC(p->d_flush_tiles, p->flush_tiles.size() * sizeof(int2));
   ALLOC(p->d_o, act.size() * sizeof(float2));
   if (rgemm_prepare(*p) != cudaSuccess) return bail(fail(WDD_E_CUDA, "GEMM flush setup failed"));
-  p->opart_cap = std::max({1, colfft_tiles(*p), flush_tiles(*p, 1 << 20), p->rg_ready ? flush_tiles(*p, 64, 3) : 1});
+  p->opart_cap = std::max({1, colfft_tiles(*p), flush_tiles(*p, 1 << 20), p->rg_ready ? flush_tiles(*p, 64, 3) : 1,
+                           fused_possible(*p) ? fused_tiles(*p) : 1});
   ALLOC(p->d_opart, (size_t)p->opart_cap * act.size() * sizeof(float2));
   ALLOC(p->d_gidx, (size_t)p->S * sizeof(int32_t));
   ALLOC(p->d_oacc, act.size() * sizeof(float2));

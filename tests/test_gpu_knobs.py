@@ -1,9 +1,13 @@
 """GPU checks of the alternative code paths behind the library's environment knobs (DESIGN.md
 "Tuning knobs"; each knob is read once per process, so every variant runs in its own process).
 
-* Pure data-movement alternatives must give bit-identical images: the FFT kernels' TMA tile loads
-  against per-thread vector loads (WDD_FFT_TMA=0) and the y-FFT's L2 prefetch (WDD_COLFFT_PF=0).
-  Both read the same bytes into the same shared-memory layout and run the same arithmetic.
+* The fused one-cluster 2-D flush (default up to 256 x 256 scans) against the two-kernel row FFT +
+  y-FFT through the R staging (WDD_FUSED=0): the same transforms in the same order, so G is
+  bit-identical.
+* Pure data-movement alternatives of the two-kernel flush must give bit-identical images: the FFT
+  kernels' TMA tile loads against per-thread vector loads (WDD_FFT_TMA=0) and the y-FFT's L2
+  prefetch (WDD_COLFFT_PF=0).  Both read the same bytes into the same shared-memory layout and run
+  the same arithmetic.
 * Alternative arithmetic (image transform by cuFFT or two passes, the DFT-matrix and tensor-core
   rank-update flushes) must agree to float32 rounding of a different summation order: relative
   L2 <= 1e-5 against the default path (the oracle tolerance is 1e-4, P:815 readout).
@@ -35,8 +39,10 @@ for a in range(0, cfg.S, b):
     fr = dense_frames_torch(*sparse_events(5, idx, cfg.Q), cfg.Q, "cuda")
     plan.ingest(fr, idx.astype(np.int32))
 out = plan.readout()
+G, act = plan.get_accumulator()
 torch.cuda.synchronize()
 np.save({path!r}, out.cpu().numpy())
+np.save({path!r} + ".G.npy", G.cpu().numpy())
 """
 
 
@@ -50,7 +56,7 @@ def _run(tmp_path, name, env_extra):
     r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, path=path)], env=env, cwd=ROOT,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
-    return np.load(path)
+    return np.load(path), np.load(path + ".G.npy")
 
 
 @pytest.fixture(scope="module")
@@ -60,15 +66,30 @@ def default_image(tmp_path_factory):
     return _run(tmp_path_factory.mktemp("knobs"), "default", {})
 
 
+@pytest.fixture(scope="module")
+def two_kernel_image(tmp_path_factory):
+    # the flush as a row-FFT kernel + a y-FFT kernel through the R staging (WDD_FUSED=0)
+    return _run(tmp_path_factory.mktemp("knobs2"), "unfused", {"WDD_FUSED": "0"})
+
+
+def test_fused_flush_equals_two_kernel_flush(default_image, two_kernel_image):
+    # the one-cluster 2-D flush runs the same transforms on the same values in the same order: G is
+    # bit-identical; the partial readouts sum in another grouping (image within float32 rounding)
+    img, G = default_image
+    img2, G2 = two_kernel_image
+    assert np.array_equal(G, G2)
+    assert np.linalg.norm(img - img2) / np.linalg.norm(img2) <= 1e-6
+
+
 @pytest.mark.parametrize("env", [{"WDD_FFT_TMA": "0"}, {"WDD_COLFFT_PF": "0"}])
-def test_data_movement_variants_bit_identical(default_image, tmp_path, env):
-    img = _run(tmp_path, "v", env)
-    assert np.array_equal(img, default_image), env
+def test_data_movement_variants_bit_identical(two_kernel_image, tmp_path, env):
+    img, _ = _run(tmp_path, "v", dict(env, WDD_FUSED="0"))
+    assert np.array_equal(img, two_kernel_image[0]), env
 
 
 @pytest.mark.parametrize("env", [{"WDD_IMG": "cufft"}, {"WDD_IMG": "unfused"}, {"WDD_FLUSH": "gemm"},
                                  {"WDD_FLUSH": "dft"}])
 def test_arithmetic_variants_agree(default_image, tmp_path, env):
-    img = _run(tmp_path, "v", env)
-    err = np.linalg.norm(img - default_image) / np.linalg.norm(default_image)
+    img, _ = _run(tmp_path, "v", env)
+    err = np.linalg.norm(img - default_image[0]) / np.linalg.norm(default_image[0])
     assert err <= 1e-5, (env, err)
