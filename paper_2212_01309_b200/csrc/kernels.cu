@@ -2453,10 +2453,13 @@ __global__ void __launch_bounds__(256) fft2_kernel(const float* __restrict__ C, 
 }
 
 // Fused 2-D flush geometry: square power-of-two scans from 32 to 256; two coefficient pairs per
-// cluster up to 128, one at 256; cluster size from 64 KB of row transforms per CTA.
+// cluster up to 128, one at 256; cluster size from 64 KB of row transforms per CTA.  Opt-in
+// (WDD_FUSED=1): measured slower than the two-kernel flush -- with 2-4 coefficients per cluster
+// (what fits the cluster's shared memory) every position is an 8-16 byte read at a K * 4-byte
+// stride (Medium flush 78 vs 38 us, Large 1.37 vs 0.32 ms; profiles/README.md).
 bool fused_possible(const Plan& p) {
-  static const bool off = [] { const char* e = std::getenv("WDD_FUSED"); return e && std::atoi(e) == 0; }();
-  return !off && p.Sx == p.Sy && is_pow2(p.Sx) && p.Sx >= 32 && p.Sx <= 256 && p.Kl % 4 == 0;
+  static const bool on = [] { const char* e = std::getenv("WDD_FUSED"); return e && std::atoi(e) == 1; }();
+  return on && p.Sx == p.Sy && is_pow2(p.Sx) && p.Sx >= 32 && p.Sx <= 256 && p.Kl % 4 == 0;
 }
 
 static int fused_np(const Plan& p) { return p.Sx <= 128 ? 2 : 1; }

@@ -1,8 +1,8 @@
 """GPU checks of the alternative code paths behind the library's environment knobs (DESIGN.md
 "Tuning knobs"; each knob is read once per process, so every variant runs in its own process).
 
-* The fused one-cluster 2-D flush (default up to 256 x 256 scans) against the two-kernel row FFT +
-  y-FFT through the R staging (WDD_FUSED=0): the same transforms in the same order, so G is
+* The opt-in fused one-cluster 2-D flush (WDD_FUSED=1, scans up to 256 x 256) against the default
+  two-kernel row FFT + y-FFT through the R staging: the same transforms in the same order, so G is
   bit-identical.
 * Pure data-movement alternatives of the two-kernel flush must give bit-identical images: the FFT
   kernels' TMA tile loads against per-thread vector loads (WDD_FFT_TMA=0) and the y-FFT's L2
@@ -66,25 +66,20 @@ def default_image(tmp_path_factory):
     return _run(tmp_path_factory.mktemp("knobs"), "default", {})
 
 
-@pytest.fixture(scope="module")
-def two_kernel_image(tmp_path_factory):
-    # the flush as a row-FFT kernel + a y-FFT kernel through the R staging (WDD_FUSED=0)
-    return _run(tmp_path_factory.mktemp("knobs2"), "unfused", {"WDD_FUSED": "0"})
-
-
-def test_fused_flush_equals_two_kernel_flush(default_image, two_kernel_image):
-    # the one-cluster 2-D flush runs the same transforms on the same values in the same order: G is
-    # bit-identical; the partial readouts sum in another grouping (image within float32 rounding)
+def test_fused_flush_equals_two_kernel_flush(default_image, tmp_path):
+    # the opt-in one-cluster 2-D flush (WDD_FUSED=1) runs the same transforms on the same values in
+    # the same order as the row FFT + y-FFT pair: G is bit-identical; the partial readouts sum in
+    # another grouping (image within float32 rounding)
     img, G = default_image
-    img2, G2 = two_kernel_image
+    img2, G2 = _run(tmp_path, "fused", {"WDD_FUSED": "1"})
     assert np.array_equal(G, G2)
-    assert np.linalg.norm(img - img2) / np.linalg.norm(img2) <= 1e-6
+    assert np.linalg.norm(img - img2) / np.linalg.norm(img) <= 1e-6
 
 
 @pytest.mark.parametrize("env", [{"WDD_FFT_TMA": "0"}, {"WDD_COLFFT_PF": "0"}])
-def test_data_movement_variants_bit_identical(two_kernel_image, tmp_path, env):
-    img, _ = _run(tmp_path, "v", dict(env, WDD_FUSED="0"))
-    assert np.array_equal(img, two_kernel_image[0]), env
+def test_data_movement_variants_bit_identical(default_image, tmp_path, env):
+    img, _ = _run(tmp_path, "v", env)
+    assert np.array_equal(img, default_image[0]), env
 
 
 @pytest.mark.parametrize("env", [{"WDD_IMG": "cufft"}, {"WDD_IMG": "unfused"}, {"WDD_FLUSH": "gemm"},
