@@ -474,8 +474,8 @@ def main():
             t.append(e0.elapsed_time(e1) * 1e3)
         pl.reset()
         return t
-    iso = isolated(plan) if not kshard else [float("nan")]
-    iso_spread = [float("nan")]
+    iso = isolated(plan) if not kshard else None          # (resets are collective in a shard group)
+    iso_spread = None
     if world == 1:
         # the same on a plan with the latency grid (opts.ingest_spread = 1)
         lp = wdd.Plan.from_config(cfg, device=local, ingest_overlap=True, accumulator=args.accumulator,
@@ -581,9 +581,9 @@ def main():
             "latency": {
                 "ingest_batch_us": {"p50": float(np.percentile(lat_ing, 50)), "p99": float(np.percentile(lat_ing, 99)),
                                     "max": float(lat_ing.max()), "n": int(len(lat_ing)), "frames": batch},
-                "isolated_batch_us": {"median": float(np.median(iso)), "n": len(iso),
+                "isolated_batch_us": {"median": float(np.median(iso)) if iso else None, "n": len(iso or []),
                                       "frames": len(own[min(1, len(own) - 1)][2]),
-                                      "latency_grid_median": float(np.median(iso_spread))},
+                                      "latency_grid_median": float(np.median(iso_spread)) if iso_spread else None},
                 "readout_us": {"p50": float(np.percentile(lat_rd, 50)), "max": float(lat_rd.max()),
                                "n": int(len(lat_rd))},
                 "how": "CUDA events around each call of one eager acquisition (ingest_batch, readout); "
