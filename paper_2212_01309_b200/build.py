@@ -36,7 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    tmp = LIB + ".tmp"
+    tmp = LIB + f".{os.getpid()}.tmp"      # (per-process temp: several ranks may build at once)
     extra = os.environ.get("WDD_NVCC_EXTRA", "").split()
     cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES,
            "-lcufft", "-lnccl", "-lpthread"]

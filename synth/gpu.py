@@ -29,11 +29,11 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         os.makedirs(os.path.dirname(_LIB), exist_ok=True)
         cmd = [os.environ.get("NVCC", "nvcc"), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
-               "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-o", _LIB + ".tmp", _SRC, "-lcufft"]
+               "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-o", _LIB + f".{os.getpid()}.tmp", _SRC, "-lcufft"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError("nvcc failed building libwddsim.so:\n" + res.stderr)
-        os.replace(_LIB + ".tmp", _LIB)
+        os.replace(_LIB + f".{os.getpid()}.tmp", _LIB)     # (per-process temp: ranks may build at once)
     return _LIB
 
 
