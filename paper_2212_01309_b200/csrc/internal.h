@@ -158,14 +158,17 @@ cudaError_t launch_project(const Plan& p, const void* frames, int64_t n, const P
 cudaError_t func_attr_once(const void* fn, cudaFuncAttribute attr, int value);
 // row DFT (a4) of the listed scan rows from the pending positions of d_Call (masks: n_rows x
 // mask_words bits) into R; FFT for power-of-two Sx, DFT matrix otherwise
-cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, cudaStream_t st);
+// kbase / KR: only coefficients kbase .. kbase + KR - 1, R as a [n_vx][Sy][KR] chunk (KR <= 0: all)
+cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, cudaStream_t st,
+                          int kbase = 0, int KR = 0);
 // rank update (a5) of the listed staged rows of R into G; FFT along y or DFT matrix
 // (overwrite: G is logically zero, write instead of accumulate).  The FFT form also writes the
 // per-k-tile partial Wiener readout d_opart[colfft_tiles][n_act].
 // o_only: spectrum-only plans -- no G update, the partial readouts are of this flush's increment
 // kind: flush_kind() result to use (-1: choose); row0 >= 0: the rows are row0 .. row0 + n_rows - 1
 cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st,
-                         bool o_only = false, int kind = -1, int row0 = -1);
+                         bool o_only = false, int kind = -1, int row0 = -1, int kbase = 0, int KR = 0);
+int flush_chunk(const Plan& p);   // coefficients per L2-resident R chunk of an FFT flush (Kl: none)
 // o_acc += sum of `tiles` partial readouts (spectrum-only plans)
 cudaError_t launch_oacc(const Plan& p, int tiles, cudaStream_t st);
 bool flush_uses_fft(const Plan& p, int n_rows);

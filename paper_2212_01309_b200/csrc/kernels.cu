@@ -1015,7 +1015,9 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
                                                      const uint32_t* __restrict__ masks, int mask_words,
                                                      const float2* __restrict__ tw, const int32_t* __restrict__ col_vx,
                                                      float2* __restrict__ R, int logP, int Sy, int K, int n_vx,
-                                                     float scale, const __grid_constant__ CUtensorMap tmC, int use_tma) {
+                                                     float scale, const __grid_constant__ CUtensorMap tmC, int use_tma,
+                                                     int kbase, int KR) {
+  // coefficients kbase + blockIdx.x * 2P ..; R holds the chunk kbase .. kbase + KR - 1 (row stride KR)
   constexpr int Sx = 1 << LOGN;
   constexpr int kBY = Sx < 256 ? Sx : 256;   // rows per TMA box
   extern __shared__ __align__(16) float2 fsm[];
@@ -1025,7 +1027,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
   const int P = 1 << logP;
   float2* x = fsm;                       // [Sx][P]
   float2* stw = fsm + (Sx << logP);      // [Sx] twiddles
-  const int r = blockIdx.y, k0 = blockIdx.x * 2 * P;
+  const int r = blockIdx.y, k0 = kbase + blockIdx.x * 2 * P;
   // use_tma bit 1 (set when this grid is itself PDL-launched): no early trigger -- this kernel reads
   // the coefficient store, which the first projection of the acquisition after next overwrites, so
   // the dependents of this grid launch only once every CTA has its C tile in shared memory (below).
@@ -1098,7 +1100,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
     const int2 sl = sslot[j];
     const float2 z = x[(sl.x << logP) + pp], zm = x[(sl.y << logP) + pp];
     const float4 o = make_float4((z.x + zm.x) * hs, (z.y - zm.y) * hs, (z.y + zm.y) * hs, (zm.x - z.x) * hs);
-    *reinterpret_cast<float4*>(R + ((int64_t)j * Sy + sy) * K + k0 + 2 * pp) = o;
+    *reinterpret_cast<float4*>(R + ((int64_t)j * Sy + sy) * KR + (k0 - kbase) + 2 * pp) = o;
   }
 }
 
@@ -1116,8 +1118,9 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
                                                      const float2* __restrict__ W, float2* __restrict__ opart,
                                                      int64_t n_act, int logKT, int K, float scale, int overwrite,
                                                      int tpc, int o_only, const __grid_constant__ CUtensorMap tmR,
-                                                     int use_tma) {
-  // use_tma: bit 0 = R tiles by TMA, bit 3 = L2 prefetch of the output stage's W / G rows
+                                                     int use_tma, int kbase, int KR) {
+  // use_tma: bit 0 = R tiles by TMA, bit 3 = L2 prefetch of the output stage's W / G rows.
+  // R holds the coefficient chunk kbase .. kbase + KR - 1 (row stride KR); G, W, opart are global
   constexpr int Sy = 1 << LOGN;
   constexpr int kBY = Sy < 256 ? Sy : 256;   // rows per TMA box
   extern __shared__ __align__(16) float2 fsm[];
@@ -1151,7 +1154,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     for (int i = threadIdx.x; i < n_rows; i += blockDim.x) sstaged[srow[i]] = 1;
   }
   for (int t = 0; t < tpc; ++t) {
-  const int k0 = (blockIdx.x * tpc + t) * KT;
+  const int k0 = kbase + (blockIdx.x * tpc + t) * KT, kl = k0 - kbase;
   const int hKT = KT >> 1, lh = logKT - 1;             // 16-byte pieces per row
   if (use_tma & 1) {
     // the Sy x KT tile of R[j] in flight at once (pitch KT complex = the FFT's [Sy][KT] layout);
@@ -1161,7 +1164,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
       fence_proxy_async_smem();                        // generic writes of x before the async refill
       mbar_arrive_expect_tx(&lbar, (uint32_t)(Sy * KT * 8));
       for (int b = 0; b < Sy / kBY; ++b)
-        tma_load_2d(x + ((b * kBY) << logKT), &tmR, 2 * k0, j * Sy + b * kBY, &lbar);
+        tma_load_2d(x + ((b * kBY) << logKT), &tmR, 2 * kl, j * Sy + b * kBY, &lbar);
     }
     mbar_wait(&lbar, (uint32_t)(t & 1));
     if (n_rows < Sy)
@@ -1172,7 +1175,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x) x[e] = make_float2(0.f, 0.f);
   __syncthreads();
   // staged rows of R[j] (k0 .. k0+KT), two coefficients (16 bytes) per load, kU loads in flight
-  const float4* Rj = reinterpret_cast<const float4*>(R + (int64_t)j * Sy * K + k0);
+  const float4* Rj = reinterpret_cast<const float4*>(R + (int64_t)j * Sy * KR + kl);
   const int total = n_rows << lh;
   for (int base = 0; base < total; base += kU * (int)blockDim.x) {
     float4 v[kU];
@@ -1182,7 +1185,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
       const int e = base + u * (int)blockDim.x + threadIdx.x;
       const int sy = e < total ? srow[e >> lh] : 0, h = e & (hKT - 1);
       dst[u] = e < total ? (sy << logKT) + 2 * h : -1;
-      v[u] = e < total ? __ldg(Rj + (int64_t)sy * (K >> 1) + h) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[u] = e < total ? __ldg(Rj + (int64_t)sy * (KR >> 1) + h) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -1240,7 +1243,8 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   }
   __syncthreads();   // x reused by the next k-tile; sdot settled
   }
-  for (int i = threadIdx.x; i < mj; i += blockDim.x) opart[(int64_t)blockIdx.x * n_act + g0 + i] = sdot[i];
+  const int64_t orow = blockIdx.x + kbase / (KT * tpc);
+  for (int i = threadIdx.x; i < mj; i += blockDim.x) opart[orow * n_act + g0 + i] = sdot[i];
 }
 
 static int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
@@ -1367,17 +1371,28 @@ __global__ void __launch_bounds__(256) rowdft_kernel(const float* __restrict__ C
   }
 }
 
-cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, cudaStream_t st) {
+static int rowfft_logp(const Plan& p) {
+  static const int2 knob = env_pair("WDD_ROWFFT");   // (log2 k pairs per CTA, threads) override
+  // k pairs per CTA (>= 2) and threads: up to Sx = 256, 16 pairs on 128 threads (twice the CTAs
+  // of 32 pairs on 256: +0.8% Medium, +1% Large end to end); 256 threads beyond (Live: -0.5%)
+  const int logSx = ilog2(p.Sx);
+  int logP = ilog2(std::max(2, std::min(logSx <= 8 ? 16 : 32, kFftSmem / (8 * p.Sx))));
+  if (knob.x >= 0) logP = std::min(logP, knob.x);
+  while ((2 << logP) > p.Kl || p.Kl % (2 << logP)) --logP;
+  return logP;
+}
+
+cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, cudaStream_t st,
+                          int kbase, int KR) {
+  if (KR <= 0) { kbase = 0; KR = p.Kl; }
   if (n_rows <= 0) return cudaSuccess;
   if (is_pow2(p.Sx) && p.Sx >= 2 && p.Sx <= (1 << kFftMaxLog)) {
     const int logSx = ilog2(p.Sx);
     static const int2 knob = env_pair("WDD_ROWFFT");   // (log2 k pairs per CTA, threads) override
     // k pairs per CTA (>= 2) and threads: up to Sx = 256, 16 pairs on 128 threads (twice the CTAs
     // of 32 pairs on 256: +0.8% Medium, +1% Large end to end); 256 threads beyond (Live: -0.5%)
-    int logP = ilog2(std::max(2, std::min(logSx <= 8 ? 16 : 32, kFftSmem / (8 * p.Sx))));
-    if (knob.x >= 0) logP = std::min(logP, knob.x);
+    const int logP = rowfft_logp(p);
     const int nt = knob.y > 0 ? knob.y : logSx <= 8 ? 128 : 256;
-    while ((2 << logP) > p.Kl || p.Kl % (2 << logP)) --logP;
     const size_t smem = ((size_t)p.Sx << logP) * 8 + (size_t)p.Sx * 8 + 16;
     return with_log(logSx, [&](auto LN) {
       constexpr int LOGN = decltype(LN)::value;
@@ -1386,7 +1401,7 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
                                        kFftSmem + 16384);
         if (e != cudaSuccess) return e;
       }
-      dim3 grid(p.Kl / (2 << logP), n_rows);
+      dim3 grid(KR / (2 << logP), n_rows);
       // (with two projection CTAs per SM a PDL-launched row FFT would park its CTAs next to the
       // last projection CTAs and slow them down: launch it after the projection completes)
       static const int env_pdl = [] { const char* e = std::getenv("WDD_ROWFFT_PDL"); return e ? std::atoi(e) : -1; }();
@@ -1396,7 +1411,8 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
                                 (uint32_t)std::min(p.Sx, 256));
       return launch_pdl(rowfft_kernel<LOGN>, grid, dim3(nt), smem, st, rowfft_pdl, (const float*)p.d_Call, rows, masks,
                         p.mask_words, (const float2*)p.d_twx, (const int32_t*)p.d_col_vx, p.d_R, logP, p.Sy, p.Kl,
-                        p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0));
+                        p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0),
+                        kbase, KR);
     });
   }
   {
@@ -2163,6 +2179,22 @@ static int colfft_tpc(const Plan& p) {
 
 int colfft_tiles(const Plan& p) { return (p.Kl >> colfft_logkt(p)) / colfft_tpc(p); }
 
+// Coefficient chunk of an FFT flush whose R staging stays in L2 (WDD_R_CHUNK_MB: the chunk's R
+// budget in MB; 0 = off): each chunk is a row FFT + y-FFT pair over the same R buffer, so R is
+// written and read back through L2 instead of HBM.  Returns p.Kl (no chunking) when the budget is
+// off, too small for one tile unit, or the whole R fits.
+int flush_chunk(const Plan& p) {
+  static const int mb = [] { const char* e = std::getenv("WDD_R_CHUNK_MB"); return e ? std::atoi(e) : 0; }();
+  if (mb <= 0 || !is_pow2(p.Sx) || !is_pow2(p.Sy) || p.Sx > (1 << kFftMaxLog) || p.Sy > (1 << kFftMaxLog)) return p.Kl;
+  const int a = 2 << rowfft_logp(p), b = (1 << colfft_logkt(p)) * colfft_tpc(p);
+  int unit = a;
+  while (unit % b) unit += a;                          // lcm
+  const int64_t per_k = (int64_t)p.n_vx * p.Sy * 8;
+  int KR = p.Kl;
+  while (KR > unit && (KR % 2 == 0) && (int64_t)KR * per_k > (int64_t)mb << 20 && (KR / 2) % unit == 0) KR /= 2;
+  return KR;
+}
+
 // k-chunks of the pipelined GEMM flush: enough work items for ~4 per CTA
 static int rgemm_nkc(const Plan& p) {
   const int KT = p.Kl / kRgNT;
@@ -2267,7 +2299,8 @@ int flush_tiles(const Plan& p, int n_rows, int kind) {
 }
 
 cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st, bool o_only,
-                         int kind, int row0) {
+                         int kind, int row0, int kbase, int KR) {
+  if (KR <= 0) { kbase = 0; KR = p.Kl; }
   if (n_rows <= 0) return cudaSuccess;
   if (kind < 0) kind = flush_kind(p, n_rows);
   if (kind == 3) return launch_rgemm(p, rows, n_rows, overwrite, o_only, st, row0);
@@ -2297,19 +2330,19 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
         if (e != cudaSuccess) return e;
       }
       const int tpc = colfft_tpc(p);
-      dim3 grid((p.Kl >> logKT) / tpc, p.n_vx);
+      dim3 grid((KR >> logKT) / tpc, p.n_vx);
       static const int2 knob = env_pair("WDD_COLFFT");
       // L2 prefetch of the output stage's rows: Large readout 339 -> 333 us, Box 3.77 -> 3.65 ms;
       // none at Medium (-0.15%: fewer load rounds per tile), so only from Sy = 256
       static const bool pf_on = [] { const char* e = std::getenv("WDD_COLFFT_PF"); return !(e && std::atoi(e) == 0); }();
       CUtensorMap tmR;
-      const bool tma = fft_tmap(&tmR, p.d_R, (uint64_t)p.Kl * 2, (uint64_t)p.n_vx * p.Sy, (uint64_t)p.Kl * 8,
+      const bool tma = fft_tmap(&tmR, p.d_R, (uint64_t)KR * 2, (uint64_t)p.n_vx * p.Sy, (uint64_t)KR * 8,
                                 2u << logKT, (uint32_t)std::min(p.Sy, 256));
       return launch_pdl(colfft_kernel<LOGN>, grid, dim3(knob.y > 0 ? knob.y : 256), smem, st, true, p.d_R, rows, n_rows,
                         (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G,
                         (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.Kl,
                         (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0, tpc, o_only ? 1 : 0, tmR,
-                        (tma ? 1 : 0) | (pf_on && p.Sy >= 256 ? 8 : 0));
+                        (tma ? 1 : 0) | (pf_on && p.Sy >= 256 ? 8 : 0), kbase, KR);
     });
   }
   if (o_only) return cudaErrorNotSupported;   // unreachable: flush_kind never picks the DFT for these

@@ -429,6 +429,33 @@ wdd_status flush(Plan& p) {
     p.opart_tiles = fused_tiles(p);
     return WDD_OK;
   }
+  if (!rows.empty() && flush_kind(p, (int)rows.size()) == 1 && flush_chunk(p) < p.Kl) {
+    // FFT flush in coefficient chunks whose R staging stays in L2: per chunk, the row FFT of the
+    // pending rows and the y-FFT + G update + partial readouts of the same coefficients
+    const int32_t* dr = nullptr;
+    const uint32_t* dm = nullptr;
+    wdd_status s = row_blob(p, rows, &dr, &dm);
+    if (s != WDD_OK) return s;
+    const int n_rows = (int)rows.size(), KR = flush_chunk(p);
+    const bool contig = rows.back() - rows.front() == n_rows - 1;
+    for (int kb = 0; kb < p.Kl; kb += KR) {
+      {
+        Prof pr(p, kSlotRowDft, p.stream);
+        CUDA_TRY(launch_rowdft(p, dr, dm, n_rows, p.stream, kb, KR));
+      }
+      Prof pr(p, kSlotFlush, p.stream);
+      CUDA_TRY(launch_flush(p, dr, n_rows, p.G_zero, p.stream, p.o_only, 1, contig ? rows.front() : -1, kb, KR));
+    }
+    p.c_read_since_swap = true;
+    if (p.o_only) {
+      Prof pr(p, kSlotReadout, p.stream);
+      CUDA_TRY(launch_oacc(p, flush_tiles(p, n_rows, 1), p.stream));
+      return WDD_OK;
+    }
+    p.G_zero = false;
+    p.opart_tiles = flush_tiles(p, n_rows, 1);
+    return WDD_OK;
+  }
   wdd_status s = stage_rows(p, rows);
   if (s != WDD_OK) return s;
   rows.clear();
