@@ -20,11 +20,13 @@ def main():
     from synth import CONFIGS
     cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "medium"]
     batch = int(sys.argv[2]) if len(sys.argv) > 2 else (cfg.batch or 512)
-    n = min(cfg.S, 16384)
+    n = min(cfg.S, int(sys.argv[3]) if len(sys.argv) > 3 else 16384)
     lib = wdd.load_library()
     lib.wdd_trace_ctas.restype = ctypes.c_int
     rng = np.random.default_rng(0)
-    fr = rng.poisson(0.2, size=(n, cfg.Q, cfg.Q)).astype(np.uint16)
+    fr = rng.poisson(0.2, size=(min(n, 16384), cfg.Q, cfg.Q)).astype(np.uint16)
+    if n > len(fr):
+        fr = np.concatenate([fr] * (n // len(fr)))
     dev = torch.from_numpy(fr).cuda()
     idx = np.arange(n, dtype=np.int32)
     plan = wdd.Plan.from_config(cfg, ingest_overlap=True)
