@@ -98,7 +98,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 constexpr bool kLeanAllowed = WDD_LEAN != 0;   // per configuration: lean only where it fits
 constexpr int kConv = 128;          // threads per converter group (2 groups: even / odd chunks)
 #ifndef WDD_LEAN_SMEM
-#define WDD_LEAN_SMEM 115200          // two CTAs and their 1 KB reservations in the 227 KB carveout
+#define WDD_LEAN_SMEM (110 * 1024)    // two CTAs per SM (measured: 112.3 KB and 114 968 B CTAs ran one per SM)
 #endif
 constexpr int kLeanSmem = WDD_LEAN_SMEM;   // shared-memory budget of a lean (two CTAs per SM) projection CTA
 constexpr uint32_t kLBO = 2064;     // no-swizzle K-major: bytes between K-adjacent core matrices of a
