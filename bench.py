@@ -329,16 +329,36 @@ def main():
         p0 = a % pool_n
         return pool[p0:p0 + n]
 
-    plan = wdd.Plan.from_config(cfg, device=local, ingest_overlap=True, accumulator=args.accumulator,
-                                k_shards=world if kshard else 0, k_rank=rank if kshard else 0)
-    if world > 1:
-        obj = [wdd.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        plan.set_comm(world, rank, obj[0])
-        if kshard:
-            hs = [None] * world
-            dist.all_gather_object(hs, plan.shard_store_handle())
+    def make_plan(sharded):
+        pl = wdd.Plan.from_config(cfg, device=local, ingest_overlap=True, accumulator=args.accumulator,
+                                  k_shards=world if sharded else 0, k_rank=rank if sharded else 0)
+        if world > 1:
+            obj = [wdd.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            pl.set_comm(world, rank, obj[0])
+        return pl
+
+    plan = make_plan(kshard)
+    combine_note = None
+    if kshard:
+        # map the peers' coefficient stores (CUDA IPC); if any rank cannot, every rank falls back to
+        # the partial-accumulator combine (recorded in the JSON line)
+        hs = [None] * world
+        dist.all_gather_object(hs, plan.shard_store_handle())
+        err = None
+        try:
             plan.set_shard_peers(world, rank, hs)
+        except wdd.WddError as e:
+            err = str(e)
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        if any(errs):
+            combine_note = "kshard peer mapping failed, partial combine used: " + next(e for e in errs if e)
+            print(combine_note, file=sys.stderr, flush=True)
+            plan.close()
+            kshard, combine = False, "partial"
+            schedule = _schedule(cfg, world, rank, batch, partition)
+            plan = make_plan(False)
     out = torch.empty((cfg.Sy, cfg.Sx), dtype=torch.complex64, device=f"cuda:{local}")
     stream = torch.cuda.Stream(device=local)      # graphs cannot capture the legacy default stream
     torch.cuda.synchronize()
@@ -567,7 +587,7 @@ def main():
                        "K": cfg.K, "batch": batch, "global_batch": cfg.S,
                        "parallelism": f"{'batches round-robin' if partition == 'rr' else 'rows'}/{world}"
                                       + (f", coefficient shards/{world} (P2P)" if kshard else ""),
-                       "combine": combine, "accumulator": args.accumulator,
+                       "combine": combine, "combine_note": combine_note, "accumulator": args.accumulator,
                        "readouts_per_step": n_read,
                        "l2": f"inputs larger than L2: frame pool {pool_n * fb / 2**30:.2f} GiB cycled",
                        "graph": not args.no_graph, "acquisitions_per_graph": None if args.no_graph else A},
