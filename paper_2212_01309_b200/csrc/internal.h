@@ -45,6 +45,7 @@ struct Plan {
   double b_scale = 1.0;  // power-of-two prescale of the fp16 basis operand (2^s)
   double sc1 = 1.0, sc2 = 1.0;  // projection epilogue scales: 2^(eT-s), 2^(-s-eT)
   int sm_count = 148;
+  mutable int last_proj_grid = 0;   // CTAs of the latest projection launch (launch_rowdft's PDL choice)
   int ingest_spread = 0;              // 1: every projection launch over all SMs (latency grid)
   int ingest_overlap = 0;             // 1: frames are complete before the previous library call on the stream
                                       // (projection reads them before its predecessor grid completes)

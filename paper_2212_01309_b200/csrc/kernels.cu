@@ -863,6 +863,7 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
   // overlaps its predecessor, the previous readout, programmatically.  Later launches of the
   // acquisition write disjoint scan positions and always overlap their predecessors.
   cfg.numAttrs = (p.frames_ingested == 0 && !p.c_fresh) ? 0 : 1;
+  p.last_proj_grid = grid;
   return cudaLaunchKernelEx(&cfg, kern, a, tmap);
 }
 
@@ -1403,9 +1404,12 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
       }
       dim3 grid(KR / (2 << logP), n_rows);
       // (with two projection CTAs per SM a PDL-launched row FFT would park its CTAs next to the
-      // last projection CTAs and slow them down: launch it after the projection completes)
+      // last projection CTAs and slow them down: launch it after the projection completes -- unless
+      // that projection ran fewer CTAs than SMs, where the parked CTAs take idle SMs and the launch
+      // overlaps the projection's tail: Medium's 512-frame batches, 32 CTAs each, +1.6% end to end;
+      // Box's and Large's full-width last batches -0.4% with PDL, tools/experiments/exp_rowpdl.sh)
       static const int env_pdl = [] { const char* e = std::getenv("WDD_ROWFFT_PDL"); return e ? std::atoi(e) : -1; }();
-      const bool rowfft_pdl = env_pdl >= 0 ? env_pdl != 0 : !project_is_lean(p);
+      const bool rowfft_pdl = env_pdl >= 0 ? env_pdl != 0 : !project_is_lean(p) || p.last_proj_grid < p.sm_count;
       CUtensorMap tmC;
       const bool tma = fft_tmap(&tmC, p.d_Call, (uint64_t)p.Kl, (uint64_t)p.S, (uint64_t)p.Kl * 4, 2u << logP,
                                 (uint32_t)std::min(p.Sx, 256));
