@@ -281,6 +281,10 @@ def main():
     ap.add_argument("--combine", default="auto", choices=["auto", "kshard", "partial"])
     ap.add_argument("--accumulator", default="G", choices=["G", "spectrum"])
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--readout-async", type=int, default=-1, choices=[-1, 0, 1],
+                    help="pipelined acquisitions: readouts on the plan's readout stream (opts.readout_async); "
+                         "-1 = on for large / live, where the readout overlapping the next projections gains "
+                         "(Large +4%%, Live +2%%; Box even, Medium -2%%: tools/experiments/exp_roasync*.sh)")
     ap.add_argument("--acq-per-graph", type=int, default=0,
                     help="acquisitions per captured graph (0: 4 for small scans, 1 beyond)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -288,6 +292,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.readout_async < 0:
+        args.readout_async = int(args.config in ("large", "live"))
 
     import torch
     import torch.distributed as dist
@@ -331,7 +337,8 @@ def main():
 
     def make_plan(sharded):
         pl = wdd.Plan.from_config(cfg, device=local, ingest_overlap=True, accumulator=args.accumulator,
-                                  k_shards=world if sharded else 0, k_rank=rank if sharded else 0)
+                                  k_shards=world if sharded else 0, k_rank=rank if sharded else 0,
+                                  readout_async=bool(args.readout_async) and not sharded)
         if world > 1:
             obj = [wdd.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
@@ -382,7 +389,7 @@ def main():
                 if events is not None:
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
-                plan.readout(out)
+                plan.readout(out, wait=events is not None)
                 if events is not None:
                     e1.record(stream)
                     events["readout"].append((e0, e1))
@@ -408,11 +415,12 @@ def main():
         if args.no_graph:
             for _ in range(n):
                 step_eager()
-            return
-        for _ in range(n // A):
-            plan.graph_launch(graph_for(A), stream)
-        if n % A:
-            plan.graph_launch(graph_for(n % A), stream)
+        else:
+            for _ in range(n // A):
+                plan.graph_launch(graph_for(A), stream)
+            if n % A:
+                plan.graph_launch(graph_for(n % A), stream)
+        plan.readout_wait(stream)     # (pipelined readouts: the last one completes inside the timed region)
 
     warmup = max(3, args.warmup)
     if not args.no_graph:
@@ -590,7 +598,8 @@ def main():
                        "combine": combine, "combine_note": combine_note, "accumulator": args.accumulator,
                        "readouts_per_step": n_read,
                        "l2": f"inputs larger than L2: frame pool {pool_n * fb / 2**30:.2f} GiB cycled",
-                       "graph": not args.no_graph, "acquisitions_per_graph": None if args.no_graph else A},
+                       "graph": not args.no_graph, "acquisitions_per_graph": None if args.no_graph else A,
+                       "readout_async": plan.readout_async},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": _traffic(cfg.name),
                          "kernel": "project_kernel", "peak_source": peak_src,

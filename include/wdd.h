@@ -88,7 +88,19 @@ typedef struct {
                             so consecutive (PDL-chained) batches stream side by side on the SMs;
                             1 = latency grid: every launch spread over all SMs (a lone batch on an
                             idle GPU finishes sooner; chained small batches lose overlap)          */
-  int32_t reserved[2];   /* must be zero                                                      */
+  int32_t readout_async; /* 0 (default) = readouts run on the plan stream.  1 = pipelined acquisitions:
+                            wdd_readout / wdd_readout_spectrum / wdd_get_accumulator /
+                            wdd_image_from_spectrum run on the plan's own readout stream, which first
+                            waits for everything enqueued on the plan stream so far; the plan stream
+                            goes on with the next ingests (the next acquisition, in the other
+                            coefficient store) while the readout runs.  The output is valid once
+                            wdd_readout_wait has ordered a stream after it (or after wdd_sync).  The
+                            library orders its own hazards: a reset waits for the last readout of the
+                            store it swaps in (spectrum-only plans: for the last readout), and
+                            consecutive readouts share the readout stream (with a communicator, so do
+                            all of the plan's collectives).  Not in a shard group (its reset barrier
+                            is a collective on the plan stream): WDD_E_STATE at create.            */
+  int32_t reserved[1];   /* must be zero                                                      */
 } wdd_plan_opts;
 
 /* Plan creation (host, blocking): derives dq, R, sigma; computes in float64 the basis Psi,
@@ -125,10 +137,17 @@ wdd_status wdd_ingest_host(wdd_plan_t plan, const void* frames_host, const int32
  * flush staged rows into G, o_v = sum_k G[v,k] K_v[k] for active v (0 elsewhere), multi-rank
  * combine, O = conj(IDFT2_unitary(o)) [/ sqrt(o_0)].
  *   complex_out_dev  DEVICE buffer of Sy*Sx interleaved float2 (complex64), row-major [sy][sx].
- * Enqueued on the plan stream; the caller synchronises that stream before reading.
+ * Enqueued on the plan stream (opts.readout_async: on the readout stream, see wdd_readout_wait);
+ * the caller synchronises that stream before reading.
  * Multi-rank (after wdd_set_comm) this is collective: every rank must call it, and every rank
  * receives the same image.  Two readouts with no ingest in between give identical bytes. */
 wdd_status wdd_readout(wdd_plan_t plan, void* complex_out_dev);
+
+/* Order `stream` (cudaStream_t, 0 = legacy default stream) after the plan's latest readout-family
+ * call, so work enqueued there may read its output.  With opts.readout_async = 0 the readouts are
+ * already on the plan stream and this only orders `stream` after the plan stream.  Never blocks
+ * the host. */
+wdd_status wdd_readout_wait(wdd_plan_t plan, void* stream);
 
 /* The readout's spectrum instead of the image: o_v = sum_k G[v,k] K_v[k] at the active v, 0
  * elsewhere (Sy*Sx complex64, image order v = vy*Sx + vx, FFT order per axis), DEVICE buffer.

@@ -127,6 +127,14 @@ struct Plan {
   cufftHandle fft = 0;
   bool fft_ok = false;
   cudaStream_t stream = nullptr;      // plan stream (last ingest)
+  // pipelined readouts (opts.readout_async): readout-family calls run on ro_stream, forked from
+  // the plan stream (ro_fork); ro_done[par] = the latest readout that read coefficient store par,
+  // ro_last = the latest readout; *_valid: recorded in the current context (eagerly, or inside the
+  // capture in progress -- a capture's records are joined at capture end and then forgotten)
+  int readout_async = 0;
+  cudaStream_t ro_stream = nullptr;
+  cudaEvent_t ro_fork = nullptr, ro_fork_sync = nullptr, ro_last = nullptr, ro_done[2] = {nullptr, nullptr};
+  bool ro_last_valid = false, ro_done_valid[2] = {false, false};
 
   // multi-rank
   void* nccl = nullptr;

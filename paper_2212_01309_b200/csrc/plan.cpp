@@ -240,6 +240,37 @@ void use_stream(Plan& p, cudaStream_t st) {
   p.stream = st;
 }
 
+// Readout-family calls of a plan with opts.readout_async: the scope forks the readout stream off
+// the plan stream (everything enqueued so far, i.e. every projection the readout reads, comes
+// first), points p.stream at it for the calls inside, and records the completion events the
+// plan stream's later hazards wait for (wdd_reset, wdd_graph_launch, wdd_readout_wait).
+struct RoScope {
+  Plan& p;
+  cudaStream_t saved = nullptr;
+  bool on = false;
+  wdd_status status = WDD_OK;
+  explicit RoScope(Plan& q) : p(q) {
+    if (!p.readout_async) return;
+    if (cudaEventRecord(p.ro_fork, p.stream) != cudaSuccess || cudaStreamWaitEvent(p.ro_stream, p.ro_fork, 0) != cudaSuccess) {
+      status = fail(WDD_E_CUDA, "readout stream fork: %s", cudaGetErrorString(cudaGetLastError()));
+      return;
+    }
+    saved = p.stream;
+    p.stream = p.ro_stream;
+    on = true;
+  }
+  ~RoScope() {
+    if (!on) return;
+    const int par = p.d_Call_alt ? p.store_par : 0;
+    if (cudaEventRecord(p.ro_done[par], p.ro_stream) == cudaSuccess) p.ro_done_valid[par] = true;
+    if (cudaEventRecord(p.ro_last, p.ro_stream) == cudaSuccess) p.ro_last_valid = true;
+    p.stream = saved;
+  }
+};
+
+// stream waits for an event if it was recorded in the current context
+cudaError_t wait_if(cudaStream_t st, cudaEvent_t e, bool valid) { return valid ? cudaStreamWaitEvent(st, e, 0) : cudaSuccess; }
+
 wdd_status upload_meta(Plan& p, const void* host, size_t bytes, void** dev_out) {
   if (bytes > p.meta_slot_bytes) return fail(WDD_E_ARG, "metadata too large");
   if (p.capturing) {
@@ -594,6 +625,7 @@ void free_plan(Plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
   if (p->stream) cudaStreamSynchronize(p->stream);
+  if (p->ro_stream) cudaStreamSynchronize(p->ro_stream);
   cudaDeviceSynchronize();
   if (p->nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(p->nccl));
   for (int o = 0; o < kMaxShards; ++o)
@@ -616,6 +648,9 @@ void free_plan(Plan* p) {
     if (e) cudaEventDestroy(e);
   for (auto e : p->ev_pool) cudaEventDestroy(e);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  for (cudaEvent_t e : {p->ro_fork, p->ro_last, p->ro_done[0], p->ro_done[1], p->ro_fork_sync})
+    if (e) cudaEventDestroy(e);
+  if (p->ro_stream) cudaStreamDestroy(p->ro_stream);
   if (p->fft_ok) cufftDestroy(p->fft);
   delete p;
 }
@@ -640,6 +675,8 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
     if (r) return fail(WDD_E_ARG, "opts.reserved must be zero");
   if (o.ingest_overlap != 0 && o.ingest_overlap != 1) return fail(WDD_E_ARG, "ingest_overlap must be 0 or 1");
   if (o.ingest_spread != 0 && o.ingest_spread != 1) return fail(WDD_E_ARG, "ingest_spread must be 0 or 1");
+  if (o.readout_async != 0 && o.readout_async != 1) return fail(WDD_E_ARG, "readout_async must be 0 or 1");
+  if (o.readout_async && o.k_shards > 1) return fail(WDD_E_STATE, "readout_async is not available in a shard group");
   const int Sy = scan_shape[0], Sx = scan_shape[1], Q = det_shape[0];
   if (Sy < 2 || Sx < 2 || (int64_t)Sy * Sx > (1ll << 30)) return fail(WDD_E_ARG, "scan shape %d x %d unsupported", Sy, Sx);
   if (det_shape[1] != Q || !(Q == 32 || Q == 64 || Q == 128 || Q == 256))
@@ -668,6 +705,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   p->o_only = o.accumulator == 1;
   p->ingest_overlap = o.ingest_overlap;
   p->ingest_spread = o.ingest_spread;
+  p->readout_async = o.readout_async;
   p->nshard = nshard;
   p->shard = nshard > 1 ? o.k_rank : 0;
   if (nshard > 1) p->combine = 0;   // (the shards' G are disjoint: the combine sums o)
@@ -821,6 +859,10 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(fail(WDD_E_CUDA, "event"));
   for (auto& e : p->copy_ev)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return bail(fail(WDD_E_CUDA, "event"));
+  for (cudaEvent_t* e : {&p->ro_fork, &p->ro_last, &p->ro_done[0], &p->ro_done[1], &p->ro_fork_sync})
+    if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return bail(fail(WDD_E_CUDA, "event"));
+  if (p->readout_async && cudaStreamCreateWithFlags(&p->ro_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(WDD_E_CUDA, "readout stream"));
   auto up = [&](void* d, const void* h, size_t b) { return cudaMemcpy(d, h, b, cudaMemcpyHostToDevice) == cudaSuccess; };
   bool ok = up(p->d_Bpack, bpack.data(), bpack.size() * 2) && up(p->d_psi, psi32.data(), psi32.size() * 4) &&
             up(p->d_Fx, Fx.data(), Fx.size() * sizeof(float2)) && up(p->d_Fy, Fy.data(), Fy.size() * sizeof(float2)) &&
@@ -934,6 +976,8 @@ wdd_status wdd_readout(wdd_plan_t plan, void* complex_out_dev) {
   Plan& p = *P(plan);
   if (!complex_out_dev) return fail(WDD_E_ARG, "NULL output");
   CUDA_TRY(cudaSetDevice(p.device));
+  RoScope ro(p);
+  if (ro.status != WDD_OK) return ro.status;
   const float2* op = nullptr;
   int tiles = 0;
   wdd_status s = readout_spectrum(p, /*combine*/ true, &op, &tiles);
@@ -948,6 +992,8 @@ wdd_status wdd_readout_spectrum(wdd_plan_t plan, void* spectrum_out_dev, int32_t
   Plan& p = *P(plan);
   if (!spectrum_out_dev) return fail(WDD_E_ARG, "NULL output");
   CUDA_TRY(cudaSetDevice(p.device));
+  RoScope ro(p);
+  if (ro.status != WDD_OK) return ro.status;
   const float2* op = nullptr;
   int tiles = 0;
   wdd_status s = readout_spectrum(p, combine != 0, &op, &tiles);
@@ -963,6 +1009,8 @@ wdd_status wdd_image_from_spectrum(wdd_plan_t plan, const void* spectrum_dev, vo
   if (!spectrum_dev || !complex_out_dev) return fail(WDD_E_ARG, "NULL buffer");
   if (spectrum_dev == complex_out_dev) return fail(WDD_E_ARG, "spectrum and image must not alias");
   CUDA_TRY(cudaSetDevice(p.device));
+  RoScope ro(p);
+  if (ro.status != WDD_OK) return ro.status;
   Prof pr(p, kSlotFinalize, p.stream);
   CUDA_TRY(launch_image(p, static_cast<const float2*>(spectrum_dev), static_cast<float2*>(complex_out_dev), p.stream));
   return WDD_OK;
@@ -1054,6 +1102,7 @@ wdd_status wdd_readout_host(wdd_plan_t plan, void* complex_out_host) {
   CUDA_TRY(cudaMallocAsync(&d, (size_t)p.S * sizeof(float2), p.stream));
   wdd_status s = wdd_readout(plan, d);
   if (s == WDD_OK) {
+    CUDA_TRY(wait_if(p.stream, p.ro_last, p.readout_async && p.ro_last_valid));
     CUDA_TRY(cudaMemcpyAsync(complex_out_host, d, (size_t)p.S * sizeof(float2), cudaMemcpyDeviceToHost, p.stream));
   }
   cudaFreeAsync(d, p.stream);
@@ -1069,6 +1118,8 @@ wdd_status wdd_get_accumulator(wdd_plan_t plan, void* G_out_dev, int32_t* active
   if (n_act) *n_act = p.n_act;
   if (active_v_host) std::memcpy(active_v_host, p.active_v.data(), p.active_v.size() * 4);
   if (G_out_dev) {
+    RoScope ro(p);
+    if (ro.status != WDD_OK) return ro.status;
     wdd_status s = shard_barrier(p);
     if (s == WDD_OK) s = flush(p);
     if (s == WDD_OK) s = materialize_G(p);
@@ -1083,6 +1134,9 @@ wdd_status wdd_reset(wdd_plan_t plan) {
   Plan& p = *P(plan);
   CUDA_TRY(cudaSetDevice(p.device));
   p.G_zero = true;          // the next flush writes G instead of accumulating (no clearing pass)
+  // (pipelined readouts: the running spectrum below, and a single coefficient store, are still
+  // read by the last readout)
+  if (p.readout_async && (p.o_only || !p.d_Call_alt)) CUDA_TRY(wait_if(p.stream, p.ro_last, p.ro_last_valid));
   if (p.o_only) CUDA_TRY(cudaMemsetAsync(p.d_oacc, 0, (size_t)p.n_act * sizeof(float2), p.stream));
   std::fill(p.ingested.begin(), p.ingested.end(), 0u);
   p.opart_tiles = 0;
@@ -1110,6 +1164,8 @@ wdd_status wdd_reset(wdd_plan_t plan) {
     // launch starts after all earlier work), and the projection is downstream of it
     std::swap(p.d_Call, p.d_Call_alt);
     p.store_par ^= 1;
+    // pipelined readouts: the store swapped in is free once the last readout that read it is done
+    if (p.readout_async) CUDA_TRY(wait_if(p.stream, p.ro_done[p.store_par], p.ro_done_valid[p.store_par]));
     p.c_fresh = p.c_read_since_swap;
     p.c_read_since_swap = false;
   }
@@ -1263,6 +1319,8 @@ wdd_status wdd_capture_begin(wdd_plan_t plan, void* stream) {
   }
   use_stream(p, reinterpret_cast<cudaStream_t>(stream));
   CUDA_TRY(cudaStreamSynchronize(p.stream));
+  if (p.ro_stream) CUDA_TRY(cudaStreamSynchronize(p.ro_stream));
+  p.ro_last_valid = p.ro_done_valid[0] = p.ro_done_valid[1] = false;   // (eager readouts all done)
   CUDA_TRY(cudaStreamBeginCapture(p.stream, cudaStreamCaptureModeThreadLocal));
   p.capturing = true;
   return WDD_OK;
@@ -1273,8 +1331,14 @@ wdd_status wdd_capture_end(wdd_plan_t plan, int64_t* graph_handle) {
   Plan& p = *P(plan);
   if (!p.capturing) return fail(WDD_E_STATE, "not capturing");
   p.capturing = false;
+  // join the readout stream's captured work (a capture must end with every forked stream joined;
+  // a replay of the graph therefore completes only after its last readout)
+  const cudaError_t je = wait_if(p.stream, p.ro_last, p.readout_async && p.ro_last_valid);
+  p.ro_last_valid = p.ro_done_valid[0] = p.ro_done_valid[1] = false;
   cudaGraph_t g = nullptr;
-  CUDA_TRY(cudaStreamEndCapture(p.stream, &g));
+  const cudaError_t ee = cudaStreamEndCapture(p.stream, &g);
+  CUDA_TRY(je);
+  CUDA_TRY(ee);
   cudaGraphExec_t ex = nullptr;
   cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
   cudaGraphDestroy(g);
@@ -1291,6 +1355,8 @@ wdd_status wdd_graph_launch(wdd_plan_t plan, int64_t graph_handle, void* stream)
   if (graph_handle < 0 || graph_handle >= (int64_t)p.graphs.size()) return fail(WDD_E_ARG, "bad graph handle");
   CUDA_TRY(cudaSetDevice(p.device));
   use_stream(p, reinterpret_cast<cudaStream_t>(stream));
+  // (a replayed acquisition may swap in the store an eager readout still reads)
+  CUDA_TRY(wait_if(p.stream, p.ro_last, p.readout_async && p.ro_last_valid));
   CUDA_TRY(cudaGraphLaunch(p.graphs[(size_t)graph_handle], p.stream));
   return WDD_OK;
 }
@@ -1301,6 +1367,7 @@ wdd_status wdd_check(wdd_plan_t plan) {
   if (p.capturing) return fail(WDD_E_STATE, "wdd_check cannot be captured");
   CUDA_TRY(cudaSetDevice(p.device));
   CUDA_TRY(cudaStreamSynchronize(p.stream));
+  if (p.ro_stream) CUDA_TRY(cudaStreamSynchronize(p.ro_stream));
   unsigned f = 0;
   CUDA_TRY(cudaMemcpy(&f, p.d_err, sizeof f, cudaMemcpyDeviceToHost));
   if (f) {
@@ -1317,6 +1384,24 @@ wdd_status wdd_sync(wdd_plan_t plan) {
   CUDA_TRY(cudaSetDevice(p.device));
   CUDA_TRY(cudaStreamSynchronize(p.stream));
   if (p.copy_stream) CUDA_TRY(cudaStreamSynchronize(p.copy_stream));
+  if (p.ro_stream) CUDA_TRY(cudaStreamSynchronize(p.ro_stream));
+  return WDD_OK;
+}
+
+wdd_status wdd_readout_wait(wdd_plan_t plan, void* stream) {
+  if (check_plan(plan)) return WDD_E_ARG;
+  Plan& p = *P(plan);
+  if (p.capturing) return fail(WDD_E_STATE, "wdd_readout_wait cannot be captured");
+  CUDA_TRY(cudaSetDevice(p.device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (p.readout_async && p.ro_last_valid) {
+    CUDA_TRY(cudaStreamWaitEvent(st, p.ro_last, 0));
+  } else if (st != p.stream) {
+    // synchronous readouts (or a replayed graph, whose readouts joined the plan stream): order
+    // `stream` after the plan stream
+    CUDA_TRY(cudaEventRecord(p.ro_fork_sync, p.stream));
+    CUDA_TRY(cudaStreamWaitEvent(st, p.ro_fork_sync, 0));
+  }
   return WDD_OK;
 }
 

@@ -35,7 +35,7 @@ class _Opts(ctypes.Structure):
                 ("dtype", ctypes.c_int32), ("normalize", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("combine", ctypes.c_int32), ("accumulator", ctypes.c_int32), ("ingest_overlap", ctypes.c_int32),
                 ("k_shards", ctypes.c_int32), ("k_rank", ctypes.c_int32), ("ingest_spread", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("readout_async", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class _Info(ctypes.Structure):
@@ -70,6 +70,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "wdd_readout": [P, V],
             "wdd_readout_host": [P, V],
             "wdd_readout_spectrum": [P, V, I32],
+            "wdd_readout_wait": [P, V],
             "wdd_image_from_spectrum": [P, V, V],
             "wdd_check": [P],
             "wdd_ingest_remote": [P, ctypes.POINTER(I32), I64],
@@ -152,7 +153,8 @@ class Plan:
                  semiangle_rad: float, defocus_A: float = 0.0, wiener_eps: float = 1e-3, *,
                  dtype: str = "u16", normalize: bool = False, device: int = 0, sigma_px: float = 0.0,
                  det_px_rad: float = 0.0, combine: int = 0, accumulator: str = "G",
-                 ingest_overlap: bool = False, k_shards: int = 0, k_rank: int = 0, ingest_spread: bool = False):
+                 ingest_overlap: bool = False, k_shards: int = 0, k_rank: int = 0, ingest_spread: bool = False,
+                 readout_async: bool = False):
         lib = load_library()
         scan = (ctypes.c_int32 * 2)(*[int(v) for v in scan_shape])
         det = (ctypes.c_int32 * 2)(*[int(v) for v in det_shape])
@@ -169,12 +171,14 @@ class Plan:
         opts.k_shards = int(k_shards)
         opts.k_rank = int(k_rank)
         opts.ingest_spread = int(bool(ingest_spread))
+        opts.readout_async = int(bool(readout_async))
         h = ctypes.c_void_p()
         _check(lib.wdd_plan_create(scan, float(step_A), det, int(K), ctypes.byref(probe), float(wiener_eps),
                                    ctypes.byref(opts), ctypes.byref(h)))
         self._h = h
         self._lib = lib
         self.dtype = dtype
+        self.readout_async = bool(readout_async)
         self.device = int(device)
         i = self.info()
         self.Sy, self.Sx, self.Q, self.L, self.K, self.n_act = i["Sy"], i["Sx"], i["Q"], i["L"], i["K"], i["n_act"]
@@ -234,30 +238,43 @@ class Plan:
         _check(self._lib.wdd_ingest_host(self._h, _ptr(frames), idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                          len(idx), _stream(stream)))
 
-    def readout(self, out=None):
+    def readout(self, out=None, wait: bool = True):
+        """The image (Sy x Sx complex64).  readout_async plans: wait=True orders torch's current
+        stream after the readout; wait=False leaves that to a later readout_wait (pipelining)."""
         import torch
         if out is None:
             out = torch.empty((self.Sy, self.Sx), dtype=torch.complex64, device=f"cuda:{self.device}")
         self._check_out(out)
         _check(self._lib.wdd_readout(self._h, _ptr(out)))
+        self._maybe_wait(wait)
         return out
 
-    def readout_spectrum(self, out=None, combine: bool = True):
+    def readout_wait(self, stream=None):
+        """Order `stream` (default: torch's current stream) after the latest readout-family call."""
+        _check(self._lib.wdd_readout_wait(self._h, _stream(stream)))
+
+    def _maybe_wait(self, wait: bool):
+        if wait and self.readout_async and not getattr(self, "_capturing", False):
+            self.readout_wait()
+
+    def readout_spectrum(self, out=None, combine: bool = True, wait: bool = True):
         """o_v (Sy x Sx complex64, FFT order, 0 at inactive v): combined over ranks, or this rank's own."""
         import torch
         if out is None:
             out = torch.empty((self.Sy, self.Sx), dtype=torch.complex64, device=f"cuda:{self.device}")
         self._check_out(out)
         _check(self._lib.wdd_readout_spectrum(self._h, _ptr(out), int(bool(combine))))
+        self._maybe_wait(wait)
         return out
 
-    def image_from_spectrum(self, spectrum, out=None):
+    def image_from_spectrum(self, spectrum, out=None, wait: bool = True):
         import torch
         self._check_out(spectrum)
         if out is None:
             out = torch.empty((self.Sy, self.Sx), dtype=torch.complex64, device=f"cuda:{self.device}")
         self._check_out(out)
         _check(self._lib.wdd_image_from_spectrum(self._h, _ptr(spectrum), _ptr(out)))
+        self._maybe_wait(wait)
         return out
 
     def check(self):
@@ -284,6 +301,7 @@ class Plan:
         n = ctypes.c_int64()
         _check(self._lib.wdd_get_accumulator(self._h, _ptr(G), act.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                              ctypes.byref(n)))
+        self._maybe_wait(True)
         return G, act
 
     def active_set(self) -> np.ndarray:
@@ -367,9 +385,11 @@ class Plan:
     # ---- CUDA graphs (capture a fixed sequence, replay its device work)
     def capture_begin(self, stream=None):
         _check(self._lib.wdd_capture_begin(self._h, _stream(stream)))
+        self._capturing = True
 
     def capture_end(self) -> int:
         h = ctypes.c_int64()
+        self._capturing = False
         _check(self._lib.wdd_capture_end(self._h, ctypes.byref(h)))
         return h.value
 

@@ -3,7 +3,9 @@ stores, so the next acquisition's first projection is launched programmatically 
 previous acquisition's readout instead of after it.  The readouts must be bit-identical to the
 same acquisitions run one at a time with a device synchronisation in between (same kernels, same
 arithmetic: any race on the coefficient store, R, G or the partial readouts shows up as a
-difference), both eagerly and inside one captured CUDA graph (bench.py's step graph)."""
+difference), both eagerly and inside one captured CUDA graph (bench.py's step graph).  Plans with
+readout_async run each readout on their readout stream while the plan stream goes on with the
+next acquisition: the same bit-identity must hold."""
 import numpy as np
 import pytest
 
@@ -22,20 +24,23 @@ def env():
     return torch, wdd
 
 
-def _check_overlap(torch, wdd, cfg, batch, n_acq):
+def _check_overlap(torch, wdd, cfg, batch, n_acq, readout_async=False, accumulator="G", cadence=0):
     from synth.sparse import dense_frames_torch, sparse_events
     idx = np.arange(cfg.S)
     b = batch
     acqs = [dense_frames_torch(*sparse_events(seed, idx, cfg.Q), cfg.Q, "cuda") for seed in range(11, 11 + n_acq)]
-    plan = wdd.Plan.from_config(cfg, ingest_overlap=True)
+    plan = wdd.Plan.from_config(cfg, ingest_overlap=True, readout_async=readout_async, accumulator=accumulator)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
 
     def acquire(fr, out):
+        # cadence > 0: a readout (into out, overwritten) after every `cadence` batches as well
         plan.reset()
-        for a in range(0, cfg.S, b):
+        for i, a in enumerate(range(0, cfg.S, b)):
             plan.ingest(fr[a:a + b], idx[a:a + b].astype(np.int32), stream)
-        plan.readout(out)
+            if cadence and (i + 1) % cadence == 0 and a + b < cfg.S:
+                plan.readout(out, wait=False)
+        plan.readout(out, wait=False)
 
     iso = []
     for fr in acqs:
@@ -44,6 +49,15 @@ def _check_overlap(torch, wdd, cfg, batch, n_acq):
         torch.cuda.synchronize()
         iso.append(out.cpu().numpy())
     assert not np.array_equal(iso[0], iso[1])
+    if readout_async and not cadence:   # the pipelined plan's isolated images are the ordinary plan's
+        ref = wdd.Plan.from_config(cfg, ingest_overlap=True, accumulator=accumulator)
+        ref.reset()
+        for a in range(0, cfg.S, b):
+            ref.ingest(acqs[0][a:a + b], idx[a:a + b].astype(np.int32), stream)
+        img = ref.readout()
+        torch.cuda.synchronize()
+        assert np.array_equal(img.cpu().numpy(), iso[0])
+        ref.close()
 
     # eager, no synchronisation between the acquisitions
     outs = [torch.empty((cfg.Sy, cfg.Sx), dtype=torch.complex64, device="cuda") for _ in acqs]
@@ -85,6 +99,19 @@ def test_many_small_overlapped_acquisitions(env, Sy, Sx, batch):
     # C tiles are in shared memory)
     torch, wdd = env
     _check_overlap(torch, wdd, CONFIGS["medium"].with_(Sy=Sy, Sx=Sx), batch, 12)
+
+
+@pytest.mark.parametrize("name,Sy,batch,acc,cadence", [("medium", 128, 512, "G", 0), ("medium", 128, 512, "G", 8),
+                                                        ("medium", 128, 512, "spectrum", 4), ("medium", 2, 1, "G", 0),
+                                                        ("medium", 32, 256, "G", 1), ("large", 256, 16384, "G", 0)])
+def test_pipelined_readouts_match_isolated(env, name, Sy, batch, acc, cadence):
+    # readout_async: each readout runs on the plan's readout stream while the next acquisition's
+    # projections run on the plan stream (mid-acquisition readouts too, Live cadence)
+    torch, wdd = env
+    cfg = CONFIGS[name]
+    cfg = cfg.with_(Sy=Sy, Sx=Sy) if Sy != cfg.Sy else cfg
+    _check_overlap(torch, wdd, cfg, batch, 12 if cfg.S <= 1024 else 4, readout_async=True, accumulator=acc,
+                   cadence=cadence)
 
 
 def test_overlapped_acquisitions_without_wide_first_launch():
