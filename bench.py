@@ -532,13 +532,15 @@ def main():
     achieved = bytes_per_launch / (proj_ms_launch * 1e-3) / 1e9
     share = proj_ms_step / ms_step
     # whole-step algorithmic roofline (SURVEY §8(d) bytes per frame; every stage is HBM-bound):
-    # frame + C write/read (8K) + R staging write/read (16 n_vx K / Sx) + per readout the bank read
-    # (8 n_act K) and the G traffic (first flush: write; later flushes: read + write; spectrum-only
-    # accumulator: none)
+    # frame + C write/read (8K) + R staging write/read (16 n_r K / Sx, n_r = the staged columns: the
+    # n_vh primary columns of the Hermitian half plane for FFT flushes, all n_vx for the Live
+    # cadence's GEMM flushes) + per readout the bank read (8 n_act K) and the G traffic (first
+    # flush: write; later flushes: read + write; spectrum-only accumulator: none)
     n_read = sum(1 for s in schedule if s[0] == "readout")
     n_act, n_vx = info["n_act"], info["n_vx"]
+    n_r = n_vx if (cfg.readout_rows or not info["n_vh"]) else info["n_vh"]
     g_passes = n_read + (2 * n_read - 1 if args.accumulator == "G" else 0)
-    b_frame = fb + 8 * cfg.K + 16 * n_vx * cfg.K / cfg.Sx + 8 * n_act * cfg.K * g_passes / cfg.S
+    b_frame = fb + 8 * cfg.K + 16 * n_r * cfg.K / cfg.Sx + 8 * n_act * cfg.K * g_passes / cfg.S
     roof_fps = world * peaks["hbm_gbs"] * 1e9 / b_frame
 
     # ---- end to end through the public API: frames from pinned host memory (H2D inside the timed

@@ -241,7 +241,8 @@ typedef struct {
   int32_t proj_ctas_per_sm;   /* resident projection CTAs per SM (occupancy query; 2 = lean variant) */
   int32_t k_shards, k_rank;   /* coefficient shard group (1, 0 when unsharded)                         */
   int32_t k_lo, k_count;      /* this plan's coefficients k_lo .. k_lo + k_count - 1 (G, bank, store)  */
-  int32_t reserved0;
+  int32_t n_vh;               /* primary scan-frequency columns of the Hermitian half-plane FFT flush
+                                 (vx <= Sx/2; 0 = the active set is not symmetric, full plane)         */
 } wdd_plan_info;
 wdd_status wdd_get_info(wdd_plan_t plan, wdd_plan_info* info);
 

@@ -73,6 +73,13 @@ struct Plan {
   float2* d_twx = nullptr;            // Sx FFT twiddles exp(-2 pi i m / Sx), m < Sx
   float2* d_twy = nullptr;            // Sy FFT twiddles exp(-2 pi i m / Sy), m < Sy
   int32_t* d_col_vx = nullptr;        // n_vx active vx, ascending
+  // Hermitian half plane (the active set is symmetric under v -> -v, power-of-two Sx): the row
+  // FFT writes only the n_vh primary columns (vx <= Sx/2) to R, the y-FFT writes each primary
+  // column's mirror from the same transform (colfft_kernel); r_half is set per flush (FFT flushes)
+  int n_vh = 0;                       // 0: not available
+  int32_t* d_col_vx_half = nullptr;   // n_vh primary vx
+  int2* d_half_map = nullptr;         // n_vh (accumulator column of vx, of -vx or -1)
+  mutable bool r_half = false;
   float2* d_W = nullptr;              // n_act * K
   float2* d_G = nullptr;              // n_act * K
   float2* d_Gsum = nullptr;           // n_act * K (combine = 1 only)
@@ -181,6 +188,7 @@ int flush_chunk(const Plan& p);   // coefficients per L2-resident R chunk of an 
 // o_acc += sum of `tiles` partial readouts (spectrum-only plans)
 cudaError_t launch_oacc(const Plan& p, int tiles, cudaStream_t st);
 bool flush_uses_fft(const Plan& p, int n_rows);
+bool rowfft_applies(const Plan& p);   // the row transform is rowfft_kernel (power-of-two Sx <= 1024)
 // a4 + a5 + a6 in one cluster kernel (scans up to 256 x 256): row FFT, y-FFT, G update and the
 // partial readouts (fused_tiles of them), R never materialised; rows / masks as launch_rowdft
 bool fused_possible(const Plan& p);

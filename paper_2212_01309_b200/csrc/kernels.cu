@@ -1119,9 +1119,15 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
                                                      const float2* __restrict__ W, float2* __restrict__ opart,
                                                      int64_t n_act, int logKT, int K, float scale, int overwrite,
                                                      int tpc, int o_only, const __grid_constant__ CUtensorMap tmR,
-                                                     int use_tma, int kbase, int KR) {
+                                                     int use_tma, int kbase, int KR, const int2* __restrict__ hmap) {
   // use_tma: bit 0 = R tiles by TMA, bit 3 = L2 prefetch of the output stage's W / G rows.
-  // R holds the coefficient chunk kbase .. kbase + KR - 1 (row stride KR); G, W, opart are global
+  // R holds the coefficient chunk kbase .. kbase + KR - 1 (row stride KR); G, W, opart are global.
+  // hmap (Hermitian half plane, NULL = off): R holds only the primary columns (vx <= Sx/2); CTA
+  // column blockIdx.y is R column jr, accumulator column hmap[jr].x, and hmap[jr].y the column of
+  // -vx (-1: self-mirror).  The coefficients are real, so G[(-vy, -vx)][k] = conj G[(vy, vx)][k]
+  // (the scan DFT of a real sequence, eq:outer_prod P:424): the mirror column's active rows are
+  // written from the same transform, X[-vy] conjugated -- half the row-FFT output, R traffic
+  // and y-FFTs.
   constexpr int Sy = 1 << LOGN;
   constexpr int kBY = Sy < 256 ? Sy : 256;   // rows per TMA box
   extern __shared__ __align__(16) float2 fsm[];
@@ -1131,15 +1137,28 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   __shared__ __align__(8) uint64_t lbar;
   __shared__ int svy[Sy];                 // slot of each active vy of column j
   __shared__ float2 sdot[Sy];             // per-row readout partial over this CTA's k-tiles
+  __shared__ int svm[Sy];                 // the same for the mirror column (slot of -vy)
+  __shared__ float2 sdm[Sy];
   float2* x = fsm;                       // [Sy][KT]
   float2* stw = fsm + (Sy << logKT);     // [Sy] twiddles
-  const int j = blockIdx.y;
+  const int jr = blockIdx.y;              // column of R
+  int j = jr, jm = -1;
+  if (hmap) {
+    const int2 h = __ldg(hmap + jr);
+    j = h.x;
+    jm = h.y;
+  }
   pdl_trigger();
   const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
+  const int gm0 = jm >= 0 ? __ldg(col_off + jm) : 0, mjm = jm >= 0 ? __ldg(col_off + jm + 1) - gm0 : 0;
   for (int i = threadIdx.x; i < Sy; i += blockDim.x) stw[i] = __ldg(tw + i);
   for (int i = threadIdx.x; i < mj; i += blockDim.x) {
     svy[i] = fft::fslot<LOGN>(__ldg(act_vy + g0 + i));
     sdot[i] = make_float2(0.f, 0.f);
+  }
+  for (int i = threadIdx.x; i < mjm; i += blockDim.x) {
+    svm[i] = fft::fslot<LOGN>((Sy - __ldg(act_vy + gm0 + i)) & (Sy - 1));
+    sdm[i] = make_float2(0.f, 0.f);
   }
   if (use_tma & 1) {
     for (int i = threadIdx.x; i < Sy; i += blockDim.x) sstaged[i] = n_rows < Sy ? 0 : 1;
@@ -1165,7 +1184,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
       fence_proxy_async_smem();                        // generic writes of x before the async refill
       mbar_arrive_expect_tx(&lbar, (uint32_t)(Sy * KT * 8));
       for (int b = 0; b < Sy / kBY; ++b)
-        tma_load_2d(x + ((b * kBY) << logKT), &tmR, 2 * kl, j * Sy + b * kBY, &lbar);
+        tma_load_2d(x + ((b * kBY) << logKT), &tmR, 2 * kl, jr * Sy + b * kBY, &lbar);
     }
     mbar_wait(&lbar, (uint32_t)(t & 1));
     if (n_rows < Sy)
@@ -1176,7 +1195,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x) x[e] = make_float2(0.f, 0.f);
   __syncthreads();
   // staged rows of R[j] (k0 .. k0+KT), two coefficients (16 bytes) per load, kU loads in flight
-  const float4* Rj = reinterpret_cast<const float4*>(R + (int64_t)j * Sy * KR + kl);
+  const float4* Rj = reinterpret_cast<const float4*>(R + (int64_t)jr * Sy * KR + kl);
   const int total = n_rows << lh;
   for (int base = 0; base < total; base += kU * (int)blockDim.x) {
     float4 v[kU];
@@ -1198,9 +1217,9 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     // dependent load rounds then wait on L2, not DRAM
     const int lpr = KT >= 16 ? KT >> 4 : 1;            // 128-byte lines per row segment
     const bool pg = !overwrite && !o_only;
-    for (int e = threadIdx.x; e < mj * lpr; e += blockDim.x) {
+    for (int e = threadIdx.x; e < (mj + mjm) * lpr; e += blockDim.x) {
       const int i = e / lpr, l = e - i * lpr;
-      const int64_t off = (int64_t)(g0 + i) * K + k0 + 16 * l;
+      const int64_t off = (int64_t)(i < mj ? g0 + i : gm0 + i - mj) * K + k0 + 16 * l;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(W + off));
       if (pg) asm volatile("prefetch.global.L2 [%0];" ::"l"(G + off));
     }
@@ -1213,25 +1232,31 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   float4* G4 = reinterpret_cast<float4*>(G);
   const float4* W4 = reinterpret_cast<const float4*>(W);
   const int64_t K2 = K >> 1;
-  for (int ib = 0; ib < mj; ib += rpp * 4) {             // block-uniform trip count (shuffles)
+  // pass 0: column j; pass 1 (half plane): the mirror column, X[-vy] conjugated
+  for (int pass = 0; pass < (mjm > 0 ? 2 : 1); ++pass) {
+  const int gc = pass ? gm0 : g0, mc = pass ? mjm : mj;
+  const int* sv = pass ? svm : svy;
+  float2* sd = pass ? sdm : sdot;
+  const float cs = pass ? -scale : scale;                // imaginary parts: conjugate
+  for (int ib = 0; ib < mc; ib += rpp * 4) {             // block-uniform trip count (shuffles)
     float4 o[4], w[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int i = ib + u * rpp + rs;
-      const int64_t gi = (int64_t)(g0 + i) * K2 + (k0 >> 1) + pp;
-      w[u] = i < mj ? __ldg(W4 + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
-      o[u] = (i < mj && !overwrite && !o_only) ? G4[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int64_t gi = (int64_t)(gc + i) * K2 + (k0 >> 1) + pp;
+      w[u] = i < mc ? __ldg(W4 + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
+      o[u] = (i < mc && !overwrite && !o_only) ? G4[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      if (ib + u * rpp >= mj) break;                     // block-uniform
+      if (ib + u * rpp >= mc) break;                     // block-uniform
       const int i = ib + u * rpp + rs;
       float2 d = make_float2(0.f, 0.f);
-      if (i < mj) {
-        const float4 z = *reinterpret_cast<const float4*>(x + (svy[i] << logKT) + 2 * pp);
-        const float4 gn = make_float4(fmaf(z.x, scale, o[u].x), fmaf(z.y, scale, o[u].y), fmaf(z.z, scale, o[u].z),
-                                      fmaf(z.w, scale, o[u].w));
-        if (!o_only) G4[(int64_t)(g0 + i) * K2 + (k0 >> 1) + pp] = gn;
+      if (i < mc) {
+        const float4 z = *reinterpret_cast<const float4*>(x + (sv[i] << logKT) + 2 * pp);
+        const float4 gn = make_float4(fmaf(z.x, scale, o[u].x), fmaf(z.y, cs, o[u].y), fmaf(z.z, scale, o[u].z),
+                                      fmaf(z.w, cs, o[u].w));
+        if (!o_only) G4[(int64_t)(gc + i) * K2 + (k0 >> 1) + pp] = gn;
         d.x = fmaf(gn.x, w[u].x, fmaf(-gn.y, w[u].y, fmaf(gn.z, w[u].z, -gn.w * w[u].w)));
         d.y = fmaf(gn.x, w[u].y, fmaf(gn.y, w[u].x, fmaf(gn.z, w[u].w, gn.w * w[u].z)));
       }
@@ -1239,13 +1264,15 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
         d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
         d.y += __shfl_xor_sync(0xffffffffu, d.y, off);
       }
-      if (pp == 0 && i < mj) { sdot[i].x += d.x; sdot[i].y += d.y; }
+      if (pp == 0 && i < mc) { sd[i].x += d.x; sd[i].y += d.y; }
     }
+  }
   }
   __syncthreads();   // x reused by the next k-tile; sdot settled
   }
   const int64_t orow = blockIdx.x + kbase / (KT * tpc);
   for (int i = threadIdx.x; i < mj; i += blockDim.x) opart[orow * n_act + g0 + i] = sdot[i];
+  for (int i = threadIdx.x; i < mjm; i += blockDim.x) opart[orow * n_act + gm0 + i] = sdm[i];
 }
 
 static int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
@@ -1413,9 +1440,11 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
       CUtensorMap tmC;
       const bool tma = fft_tmap(&tmC, p.d_Call, (uint64_t)p.Kl, (uint64_t)p.S, (uint64_t)p.Kl * 4, 2u << logP,
                                 (uint32_t)std::min(p.Sx, 256));
+      // (Hermitian half plane, p.r_half: only the primary columns vx <= Sx/2 go to R)
       return launch_pdl(rowfft_kernel<LOGN>, grid, dim3(nt), smem, st, rowfft_pdl, (const float*)p.d_Call, rows, masks,
-                        p.mask_words, (const float2*)p.d_twx, (const int32_t*)p.d_col_vx, p.d_R, logP, p.Sy, p.Kl,
-                        p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0),
+                        p.mask_words, (const float2*)p.d_twx,
+                        (const int32_t*)(p.r_half ? p.d_col_vx_half : p.d_col_vx), p.d_R, logP, p.Sy, p.Kl,
+                        p.r_half ? p.n_vh : p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0),
                         kbase, KR);
     });
   }
@@ -2268,6 +2297,8 @@ static cudaError_t launch_rgemm(const Plan& p, const int32_t* rows, int n_rows, 
   return cudaLaunchKernelEx(&cfg, rgemm_kernel, a, *reinterpret_cast<const RgMaps*>(p.rg_tmap));
 }
 
+bool rowfft_applies(const Plan& p) { return is_pow2(p.Sx) && p.Sx >= 2 && p.Sx <= (1 << kFftMaxLog); }
+
 bool flush_uses_fft(const Plan& p, int n_rows) {
   // FFT along y costs ~5 Sy log2(Sy) flops per (column, k) whatever the number of staged rows r;
   // the DFT-matrix update ~8 r m_j with m_j (active vy of the column) a fraction of Sy.
@@ -2334,19 +2365,21 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
         if (e != cudaSuccess) return e;
       }
       const int tpc = colfft_tpc(p);
-      dim3 grid((KR >> logKT) / tpc, p.n_vx);
+      const bool half = p.r_half;
+      dim3 grid((KR >> logKT) / tpc, half ? p.n_vh : p.n_vx);
       static const int2 knob = env_pair("WDD_COLFFT");
       // L2 prefetch of the output stage's rows: Large readout 339 -> 333 us, Box 3.77 -> 3.65 ms;
       // none at Medium (-0.15%: fewer load rounds per tile), so only from Sy = 256
       static const bool pf_on = [] { const char* e = std::getenv("WDD_COLFFT_PF"); return !(e && std::atoi(e) == 0); }();
       CUtensorMap tmR;
-      const bool tma = fft_tmap(&tmR, p.d_R, (uint64_t)KR * 2, (uint64_t)p.n_vx * p.Sy, (uint64_t)KR * 8,
+      const bool tma = fft_tmap(&tmR, p.d_R, (uint64_t)KR * 2, (uint64_t)grid.y * p.Sy, (uint64_t)KR * 8,
                                 2u << logKT, (uint32_t)std::min(p.Sy, 256));
       return launch_pdl(colfft_kernel<LOGN>, grid, dim3(knob.y > 0 ? knob.y : 256), smem, st, true, p.d_R, rows, n_rows,
                         (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G,
                         (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.Kl,
                         (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0, tpc, o_only ? 1 : 0, tmR,
-                        (tma ? 1 : 0) | (pf_on && p.Sy >= 256 ? 8 : 0), kbase, KR);
+                        (tma ? 1 : 0) | (pf_on && p.Sy >= 256 ? 8 : 0), kbase, KR,
+                        half ? (const int2*)p.d_half_map : (const int2*)nullptr);
     });
   }
   if (o_only) return cudaErrorNotSupported;   // unreachable: flush_kind never picks the DFT for these

@@ -440,6 +440,7 @@ wdd_status flush(Plan& p) {
   std::vector<int32_t> rows;
   for (int sy = 0; sy < p.Sy; ++sy)
     if (p.row_dirty[sy]) rows.push_back(sy);
+  p.r_half = false;
   if (!rows.empty() && flush_kind(p, (int)rows.size()) == 1 && fused_possible(p)) {
     // the whole flush (row FFT, y-FFT, G update, partial readouts) in one cluster kernel
     const int32_t* dr = nullptr;
@@ -469,6 +470,7 @@ wdd_status flush(Plan& p) {
     if (s != WDD_OK) return s;
     const int n_rows = (int)rows.size(), KR = flush_chunk(p);
     const bool contig = rows.back() - rows.front() == n_rows - 1;
+    p.r_half = p.n_vh > 0;
     for (int kb = 0; kb < p.Kl; kb += KR) {
       {
         Prof pr(p, kSlotRowDft, p.stream);
@@ -487,6 +489,12 @@ wdd_status flush(Plan& p) {
     p.opart_tiles = flush_tiles(p, n_rows, 1);
     return WDD_OK;
   }
+  // (the flush form is chosen before the rows are staged: an FFT flush stages the half plane)
+  int n_stage = 0;
+  for (int sy = 0; sy < p.Sy; ++sy) n_stage += (p.row_staged[sy] || p.row_dirty[sy]) ? 1 : 0;
+  if (n_stage == 0) return WDD_OK;
+  const int kind = flush_kind(p, n_stage);
+  p.r_half = kind == 1 && p.n_vh > 0;   // (rows are staged and consumed within one flush call)
   wdd_status s = stage_rows(p, rows);
   if (s != WDD_OK) return s;
   rows.clear();
@@ -494,7 +502,6 @@ wdd_status flush(Plan& p) {
     if (p.row_staged[sy]) rows.push_back(sy);
   const int n_rows = (int)rows.size();
   if (n_rows == 0) return WDD_OK;
-  const int kind = flush_kind(p, n_rows);
   const int32_t* dr = nullptr;
   const bool contig = rows.back() - rows.front() == n_rows - 1;
   if (contig) {
@@ -546,9 +553,12 @@ wdd_status form_G(Plan& p) {
   wdd_status s = upload_meta(p, blob.data(), blob.size() * sizeof(int32_t), &d);
   if (s != WDD_OK) return s;
   const int32_t* dr = static_cast<const int32_t*>(d);
+  const int kind = flush_kind(p, n_rows);
+  p.r_half = kind == 1 && p.n_vh > 0;
   CUDA_TRY(launch_rowdft(p, dr, reinterpret_cast<const uint32_t*>(dr + mask_off), n_rows, p.stream));
   p.c_read_since_swap = true;
-  CUDA_TRY(launch_flush(p, dr, n_rows, /*overwrite*/ true, p.stream, false));
+  CUDA_TRY(launch_flush(p, dr, n_rows, /*overwrite*/ true, p.stream, false, kind));
+  p.r_half = false;
   return WDD_OK;
 }
 
@@ -631,7 +641,7 @@ void free_plan(Plan* p) {
   for (int o = 0; o < kMaxShards; ++o)
     if (p->peers_ipc[o] && p->peer_base[o]) cudaIpcCloseMemHandle(p->peer_base[o]);
   full_wdd_release(*p);
-  void* bufs[] = {p->d_rg_items, p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Cbase,
+  void* bufs[] = {p->d_rg_items, p->d_oacc, p->d_iota, p->d_ones, p->d_opart, p->d_gidx, p->d_Bpack, p->d_psi, p->d_Fx, p->d_Fy, p->d_twx, p->d_twy, p->d_col_vx, p->d_col_vx_half, p->d_half_map, p->d_W, p->d_G, p->d_Gsum, p->d_R, p->d_Cbase,
                   p->d_act_vy, p->d_col_off, p->d_vpos, p->d_flush_tiles, p->d_o, p->d_spec, p->d_img_tmp,
                   p->d_meta, p->d_stage[0], p->d_stage[1], p->d_err};
   for (void* b : bufs)
@@ -761,6 +771,33 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   p->n_vx = (int)p->col_vx.size();
   for (int j = 0; j < p->n_vx; ++j)
     for (int i0 = 0; i0 < p->col_off[j + 1] - p->col_off[j]; i0 += 32) p->flush_tiles.push_back(make_int2(j, i0));
+  // Hermitian half plane: G[-v][k] = conj G[v][k] (real coefficients), so when the active set is
+  // closed under v -> -v the FFT flush transforms only the columns vx <= Sx/2 (WDD_HALF=0: off)
+  std::vector<int32_t> half_vx;
+  std::vector<int2> half_map;
+  {
+    static const bool half_env = [] { const char* e = std::getenv("WDD_HALF"); return !(e && std::atoi(e) == 0); }();
+    bool sym = half_env && rowfft_applies(*p);
+    if (sym) {
+      std::vector<bool> on((size_t)p->S, false);
+      for (int32_t v : act) on[(size_t)v] = true;
+      for (int32_t v : act) {
+        const int vy = v / Sx, vx = v % Sx;
+        if (!on[(size_t)((Sy - vy) % Sy) * Sx + (Sx - vx) % Sx]) { sym = false; break; }
+      }
+    }
+    for (int j = 0; sym && j < p->n_vx; ++j) {
+      const int vx = p->col_vx[j];
+      if (2 * vx > Sx) continue;
+      const int mvx = (Sx - vx) % Sx;
+      int jm = -1;
+      if (mvx != vx)
+        jm = (int)(std::lower_bound(p->col_vx.begin(), p->col_vx.end(), mvx) - p->col_vx.begin());
+      half_vx.push_back(vx);
+      half_map.push_back(make_int2(j, jm));
+    }
+    if (sym) p->n_vh = (int)half_vx.size();
+  }
 
   // twiddles
   std::vector<float2> Fx, Fy;
@@ -821,6 +858,10 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ALLOC(p->d_twx, twx.size() * sizeof(float2));
   ALLOC(p->d_twy, twy.size() * sizeof(float2));
   ALLOC(p->d_col_vx, p->col_vx.size() * sizeof(int32_t));
+  if (p->n_vh) {
+    ALLOC(p->d_col_vx_half, half_vx.size() * sizeof(int32_t));
+    ALLOC(p->d_half_map, half_map.size() * sizeof(int2));
+  }
   ALLOC(p->d_W, nW * sizeof(float2));
   ALLOC(p->d_G, nW * sizeof(float2));
   if (p->combine == 1) ALLOC(p->d_Gsum, nW * sizeof(float2));
@@ -868,6 +909,8 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
             up(p->d_Fx, Fx.data(), Fx.size() * sizeof(float2)) && up(p->d_Fy, Fy.data(), Fy.size() * sizeof(float2)) &&
             up(p->d_twx, twx.data(), twx.size() * sizeof(float2)) && up(p->d_twy, twy.data(), twy.size() * sizeof(float2)) &&
             up(p->d_col_vx, p->col_vx.data(), p->col_vx.size() * sizeof(int32_t)) &&
+            (!p->n_vh || (up(p->d_col_vx_half, half_vx.data(), half_vx.size() * 4) &&
+                          up(p->d_half_map, half_map.data(), half_map.size() * sizeof(int2)))) &&
             up(p->d_act_vy, p->act_vy.data(), act.size() * 4) &&
             up(p->d_col_off, p->col_off.data(), p->col_off.size() * 4) && up(p->d_vpos, vpos.data(), act.size() * 4) &&
             up(p->d_gidx, gidx.data(), gidx.size() * 4) && up(p->d_iota, iota.data(), iota.size() * 4) &&
@@ -1214,6 +1257,7 @@ wdd_status wdd_get_info(wdd_plan_t plan, wdd_plan_info* info) {
   i.bytes_C = p.S * p.Kl * 4; i.frames_ingested = p.frames_ingested; i.nranks = p.nranks; i.rank = p.rank;
   i.proj_ctas_per_sm = project_occupancy(p);
   i.k_shards = p.nshard; i.k_rank = p.shard; i.k_lo = p.k0; i.k_count = p.Kl;
+  i.n_vh = p.n_vh;
   *info = i;
   return WDD_OK;
 }

@@ -48,7 +48,7 @@ class _Info(ctypes.Structure):
                 ("bytes_C", ctypes.c_int64), ("frames_ingested", ctypes.c_int64), ("nranks", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("proj_ctas_per_sm", ctypes.c_int32), ("k_shards", ctypes.c_int32),
                 ("k_rank", ctypes.c_int32), ("k_lo", ctypes.c_int32), ("k_count", ctypes.c_int32),
-                ("reserved0", ctypes.c_int32)]
+                ("n_vh", ctypes.c_int32)]
 
 
 _lib = None

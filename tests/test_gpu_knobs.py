@@ -1,9 +1,12 @@
 """GPU checks of the alternative code paths behind the library's environment knobs (DESIGN.md
 "Tuning knobs"; each knob is read once per process, so every variant runs in its own process).
 
-* The opt-in fused one-cluster 2-D flush (WDD_FUSED=1, scans up to 256 x 256) against the default
-  two-kernel row FFT + y-FFT through the R staging: the same transforms in the same order, so G is
-  bit-identical.
+* The opt-in fused one-cluster 2-D flush (WDD_FUSED=1, scans up to 256 x 256) against the
+  two-kernel row FFT + y-FFT through the R staging on the full plane (WDD_HALF=0): the same
+  transforms in the same order, so G is bit-identical.
+* The default Hermitian half-plane FFT flush (only vx <= Sx/2 transformed, the mirror column
+  written as the conjugate) against the full plane: G[-v] = conj G[v] holds bit-exactly in G, and
+  G and the image agree with the full plane to float32 rounding (relative L2 <= 1e-6).
 * Pure data-movement alternatives of the two-kernel flush must give bit-identical images: the FFT
   kernels' TMA tile loads against per-thread vector loads (WDD_FFT_TMA=0) and the y-FFT's L2
   prefetch (WDD_COLFFT_PF=0).  Both read the same bytes into the same shared-memory layout and run
@@ -43,6 +46,7 @@ G, act = plan.get_accumulator()
 torch.cuda.synchronize()
 np.save({path!r}, out.cpu().numpy())
 np.save({path!r} + ".G.npy", G.cpu().numpy())
+np.save({path!r} + ".act.npy", act)
 """
 
 
@@ -56,7 +60,7 @@ def _run(tmp_path, name, env_extra):
     r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, path=path)], env=env, cwd=ROOT,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
-    return np.load(path), np.load(path + ".G.npy")
+    return np.load(path), np.load(path + ".G.npy"), np.load(path + ".act.npy")
 
 
 @pytest.fixture(scope="module")
@@ -70,21 +74,43 @@ def test_fused_flush_equals_two_kernel_flush(default_image, tmp_path):
     # the opt-in one-cluster 2-D flush (WDD_FUSED=1) runs the same transforms on the same values in
     # the same order as the row FFT + y-FFT pair: G is bit-identical; the partial readouts sum in
     # another grouping (image within float32 rounding)
-    img, G = default_image
-    img2, G2 = _run(tmp_path, "fused", {"WDD_FUSED": "1"})
-    assert np.array_equal(G, G2)
+    img, G, _ = default_image
+    img_f, G_f, _ = _run(tmp_path, "full", {"WDD_HALF": "0"})
+    img2, G2, _ = _run(tmp_path, "fused", {"WDD_FUSED": "1"})
+    assert np.array_equal(G_f, G2)
+    assert np.linalg.norm(img_f - img2) / np.linalg.norm(img_f) <= 1e-6
     assert np.linalg.norm(img - img2) / np.linalg.norm(img) <= 1e-6
+
+
+def test_half_plane_flush(default_image, tmp_path):
+    # the default FFT flush writes the mirror columns as conjugates: G[-v] = conj G[v] exactly;
+    # against the full-plane flush (every column transformed) within float32 rounding
+    img, G, act = default_image
+    S_y = S_x = 256
+    pos = {int(v): i for i, v in enumerate(act)}
+    vy, vx = act // S_x, act % S_x
+    mirror = ((S_y - vy) % S_y) * S_x + (S_x - vx) % S_x
+    mi = np.array([pos[int(m)] for m in mirror])
+    # (columns vx = 0 and Sx/2 are their own mirrors: transformed whole, symmetric to rounding)
+    own = (vx == 0) | (vx == S_x // 2)
+    assert own.sum() < len(act) // 10
+    assert np.array_equal(G[mi[~own]], np.conj(G[~own]))
+    d = G[mi[own]] - np.conj(G[own])
+    assert np.linalg.norm(d) / np.linalg.norm(G[own]) <= 1e-6
+    img_f, G_f, _ = _run(tmp_path, "full", {"WDD_HALF": "0"})
+    assert np.linalg.norm(G - G_f) / np.linalg.norm(G_f) <= 1e-6
+    assert np.linalg.norm(img - img_f) / np.linalg.norm(img_f) <= 1e-6
 
 
 @pytest.mark.parametrize("env", [{"WDD_FFT_TMA": "0"}, {"WDD_COLFFT_PF": "0"}])
 def test_data_movement_variants_bit_identical(default_image, tmp_path, env):
-    img, _ = _run(tmp_path, "v", env)
+    img, _, _ = _run(tmp_path, "v", env)
     assert np.array_equal(img, default_image[0]), env
 
 
 @pytest.mark.parametrize("env", [{"WDD_IMG": "cufft"}, {"WDD_IMG": "unfused"}, {"WDD_FLUSH": "gemm"},
                                  {"WDD_FLUSH": "dft"}])
 def test_arithmetic_variants_agree(default_image, tmp_path, env):
-    img, _ = _run(tmp_path, "v", env)
+    img, _, _ = _run(tmp_path, "v", env)
     err = np.linalg.norm(img - default_image[0]) / np.linalg.norm(default_image[0])
     assert err <= 1e-5, (env, err)

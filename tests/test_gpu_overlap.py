@@ -129,3 +129,29 @@ def test_overlapped_acquisitions_without_wide_first_launch():
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=900,
                        env=dict(os.environ, WDD_PROJ_WIDE_FIRST="0"))
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_readout_async_api(env):
+    # a shard group keeps its collectives on the plan stream: rejected at create; readout(wait=True)
+    # orders torch's current stream after the readout stream (no device synchronisation in between)
+    torch, wdd = env
+    cfg = CONFIGS["medium"].with_(Sy=32, Sx=32)
+    with pytest.raises(wdd.WddError):
+        wdd.Plan.from_config(cfg, k_shards=2, k_rank=0, readout_async=True)
+    from synth.sparse import dense_frames_torch, sparse_events
+    idx = np.arange(cfg.S)
+    fr = dense_frames_torch(*sparse_events(5, idx, cfg.Q), cfg.Q, "cuda")
+    ref = wdd.Plan.from_config(cfg)
+    ref.ingest(fr, idx.astype(np.int32))
+    want = ref.readout().cpu().numpy()
+    plan = wdd.Plan.from_config(cfg, readout_async=True)
+    for _ in range(3):
+        plan.reset()
+        plan.ingest(fr, idx.astype(np.int32))
+        img = plan.readout()                  # wait=True: the copy below is stream-ordered after it
+        host = torch.empty_like(img, device="cpu").pin_memory()
+        host.copy_(img, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        assert np.array_equal(host.numpy(), want)
+    plan.close()
+    ref.close()
