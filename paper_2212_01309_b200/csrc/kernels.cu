@@ -2203,7 +2203,10 @@ static int colfft_logkt(const Plan& p) {
 static int colfft_tpc(const Plan& p) {
   const int tiles = p.Kl >> colfft_logkt(p);
   int tpc = 1;
-  while (tpc < 2 && tpc * 2 <= tiles && tiles % (tpc * 2) == 0 && (int64_t)(tiles / (tpc * 2)) * p.n_vx >= 2 * p.sm_count)
+  // (half plane: a CTA already writes two columns per k-tile; a second k-tile per CTA then makes
+  // the y-FFT re-read ~80% more than its bytes from DRAM -- Box 7.75 vs 4.03 GB, 2.13 vs 1.80 ms --
+  // and loses end to end: Box -1.3%, Large -0.7%, Medium -3%, tools/experiments/exp_tpc.sh)
+  while (!p.r_half && tpc < 2 && tpc * 2 <= tiles && tiles % (tpc * 2) == 0 && (int64_t)(tiles / (tpc * 2)) * p.n_vx >= 2 * p.sm_count)
     tpc *= 2;
   static const int env = [] { const char* e = std::getenv("WDD_COLFFT_TPC"); return e ? std::atoi(e) : 0; }();
   if (env > 0 && tiles % env == 0) tpc = env;
