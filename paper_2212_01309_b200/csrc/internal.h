@@ -200,6 +200,7 @@ int flush_tiles(const Plan& p, int n_rows, int kind = -1);   // partial-readout 
 bool rgemm_possible(const Plan& p, int n_rows);
 cudaError_t rgemm_prepare(Plan& p);   // tensor maps + item table of the pipelined GEMM flush
 int colfft_tiles(const Plan& p);
+int colfft_tiles_max(const Plan& p);   // >= colfft_tiles(p) whatever r_half
 bool finalize_uses_fft(const Plan& p);
 // o[g] = sum_k G[g][k] W[g][k] (one warp per active v)
 cudaError_t launch_readout(const Plan& p, const float2* G, float2* o, cudaStream_t st);

@@ -2214,6 +2214,8 @@ static int colfft_tpc(const Plan& p) {
 }
 
 int colfft_tiles(const Plan& p) { return (p.Kl >> colfft_logkt(p)) / colfft_tpc(p); }
+// upper bound over r_half and the knobs (one k-tile per CTA): sizes the partial-readout buffer
+int colfft_tiles_max(const Plan& p) { return p.Kl >> colfft_logkt(p); }
 
 // Coefficient chunk of an FFT flush whose R staging stays in L2 (WDD_R_CHUNK_MB: the chunk's R
 // budget in MB; 0 = off): each chunk is a row FFT + y-FFT pair over the same R buffer, so R is

@@ -880,7 +880,7 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
   ALLOC(p->d_flush_tiles, p->flush_tiles.size() * sizeof(int2));
   ALLOC(p->d_o, act.size() * sizeof(float2));
   if (rgemm_prepare(*p) != cudaSuccess) return bail(fail(WDD_E_CUDA, "GEMM flush setup failed"));
-  p->opart_cap = std::max({1, colfft_tiles(*p), flush_tiles(*p, 1 << 20), p->rg_ready ? flush_tiles(*p, 64, 3) : 1,
+  p->opart_cap = std::max({1, colfft_tiles_max(*p), flush_tiles(*p, 1 << 20), p->rg_ready ? flush_tiles(*p, 64, 3) : 1,
                            fused_possible(*p) ? fused_tiles(*p) : 1});
   ALLOC(p->d_opart, (size_t)p->opart_cap * act.size() * sizeof(float2));
   ALLOC(p->d_gidx, (size_t)p->S * sizeof(int32_t));
