@@ -403,6 +403,8 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
     // ================= stage-2 MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_f16(Cfg::kM2, Cfg::kNacc, 0, /*a_major=MN*/ 1, 0);
+      constexpr bool kLoN = Cfg::kM2 == 64 ? L % 8 == 0 : L % 16 == 0;                // N = L a valid MMA shape
+      constexpr uint32_t idesc_lo = idesc_f16(Cfg::kM2, L, 0, /*a_major=MN*/ 1, 0);   // Psi_hi columns only
       constexpr uint64_t kLoOff = (uint64_t)((L / 8) * 128) >> 4;
       const uint32_t a20 = smem_u32(sA2), b0 = smem_u32(sB);
       mbar_wait(b_full, 0);
@@ -417,13 +419,22 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
           TRACE(12, h);
           tc_fence_after();
           const uint32_t a2 = a20 + ab * 2 * Cfg::kA2;
-#pragma unroll 1
-          for (int plane = 0; plane < 2; ++plane) {
+          // (T_hi + T_lo)(Psi_hi + Psi_lo) without the T_lo Psi_lo term (<= 2^-22 of the product,
+          // below the fp32 accumulation): the lo plane multiplies Psi_hi only (N = L)
 #pragma unroll
-            for (int kk = 0; kk < Cfg::kK2 / 16; ++kk) {
-              const uint64_t ad = smem_desc_noswz(a2 + plane * Cfg::kA2 + kk * 256, 128, Cfg::kSBO2);
-              const uint64_t bd = smem_desc_noswz(b0 + (h * (Cfg::kK2 / 8) + 2 * kk) * Cfg::kLBO_B, Cfg::kLBO_B, 128);
-              mma_f16_ss(acc2, ad, bd, idesc, (h > 0 || plane > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < Cfg::kK2 / 16; ++kk) {
+            const uint64_t ad = smem_desc_noswz(a2 + kk * 256, 128, Cfg::kSBO2);
+            const uint64_t bd = smem_desc_noswz(b0 + (h * (Cfg::kK2 / 8) + 2 * kk) * Cfg::kLBO_B, Cfg::kLBO_B, 128);
+            mma_f16_ss(acc2, ad, bd, idesc, (h > 0 || kk > 0) ? 1u : 0u);
+            if constexpr (Cfg::kSplitAcc) mma_f16_ss(acc2, ad, bd + kLoOff, idesc, 1u);
+          }
+#pragma unroll
+          for (int kk = 0; kk < Cfg::kK2 / 16; ++kk) {
+            const uint64_t ad = smem_desc_noswz(a2 + Cfg::kA2 + kk * 256, 128, Cfg::kSBO2);
+            const uint64_t bd = smem_desc_noswz(b0 + (h * (Cfg::kK2 / 8) + 2 * kk) * Cfg::kLBO_B, Cfg::kLBO_B, 128);
+            if constexpr (kLoN) mma_f16_ss(acc2, ad, bd, idesc_lo, 1u);
+            else {
+              mma_f16_ss(acc2, ad, bd, idesc, 1u);
               if constexpr (Cfg::kSplitAcc) mma_f16_ss(acc2, ad, bd + kLoOff, idesc, 1u);
             }
           }
@@ -1035,24 +1046,27 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
   // An ordinary (non-PDL) launch of this kernel starts after all earlier work has completed, which
   // already orders it after every earlier read of C; its dependents may then launch at once.
   if (!(use_tma & 2)) pdl_trigger();
+  if (use_tma & 1) {
+    // the CTA's whole Sx x 2P slice of C in flight at once (one or two TMA boxes, pitch 2P floats =
+    // the FFT's [Sx][P] layout), issued before the twiddle / slot tables load so their latency
+    // overlaps the tile's; positions outside the pending mask are zeroed afterwards
+    if (threadIdx.x == 0) {
+      mbar_init(&lbar, 1);
+      fence_mbar_init();
+      pdl_wait();   // C of the projection kernels (and the uploaded row list / masks)
+      const int sy0 = rows[r];
+      mbar_arrive_expect_tx(&lbar, (uint32_t)(Sx * P * 8));
+      for (int b = 0; b < Sx / kBY; ++b) tma_load_2d(x + ((b * kBY) << logP), &tmC, k0, sy0 * Sx + b * kBY, &lbar);
+    }
+  }
   for (int i = threadIdx.x; i < Sx; i += blockDim.x) stw[i] = __ldg(tw + i);
   for (int j = threadIdx.x; j < n_vx; j += blockDim.x) {
     const int v = __ldg(col_vx + j);
     sslot[j] = make_int2(fft::fslot<LOGN>(v), fft::fslot<LOGN>((Sx - v) & (Sx - 1)));
   }
-  if ((use_tma & 1) && threadIdx.x == 0) {
-    mbar_init(&lbar, 1);
-    fence_mbar_init();
-  }
   pdl_wait();   // C of the projection kernels (and the uploaded row list / masks)
   const int sy = rows[r];
   if (use_tma & 1) {
-    // the CTA's whole Sx x 2P slice of C in flight at once (one or two TMA boxes, pitch 2P floats =
-    // the FFT's [Sx][P] layout); positions outside the pending mask are zeroed afterwards
-    if (threadIdx.x == 0) {
-      mbar_arrive_expect_tx(&lbar, (uint32_t)(Sx * P * 8));
-      for (int b = 0; b < Sx / kBY; ++b) tma_load_2d(x + ((b * kBY) << logP), &tmC, k0, sy * Sx + b * kBY, &lbar);
-    }
     if (threadIdx.x < mask_words) smask[threadIdx.x] = masks[(int64_t)r * mask_words + threadIdx.x];
     __syncthreads();
     mbar_wait(&lbar, 0);
@@ -1149,6 +1163,16 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     jm = h.y;
   }
   pdl_trigger();
+  if ((use_tma & 1) && threadIdx.x == 0) {
+    // the first k-tile's Sy x KT slice of R[j] in flight before the tables below load
+    mbar_init(&lbar, 1);
+    fence_mbar_init();
+    pdl_wait();   // R (row DFT) of the preceding kernel
+    mbar_arrive_expect_tx(&lbar, (uint32_t)(Sy * KT * 8));
+    const int kl0 = blockIdx.x * tpc * KT;
+    for (int b = 0; b < Sy / kBY; ++b)
+      tma_load_2d(x + ((b * kBY) << logKT), &tmR, 2 * kl0, jr * Sy + b * kBY, &lbar);
+  }
   const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
   const int gm0 = jm >= 0 ? __ldg(col_off + jm) : 0, mjm = jm >= 0 ? __ldg(col_off + jm + 1) - gm0 : 0;
   for (int i = threadIdx.x; i < Sy; i += blockDim.x) stw[i] = __ldg(tw + i);
@@ -1160,13 +1184,8 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     svm[i] = fft::fslot<LOGN>((Sy - __ldg(act_vy + gm0 + i)) & (Sy - 1));
     sdm[i] = make_float2(0.f, 0.f);
   }
-  if (use_tma & 1) {
+  if (use_tma & 1)
     for (int i = threadIdx.x; i < Sy; i += blockDim.x) sstaged[i] = n_rows < Sy ? 0 : 1;
-    if (threadIdx.x == 0) {
-      mbar_init(&lbar, 1);
-      fence_mbar_init();
-    }
-  }
   pdl_wait();   // R (row DFT) and G of the preceding kernels (and the uploaded row list)
   for (int i = threadIdx.x; i < n_rows; i += blockDim.x) srow[i] = __ldg(rows + i);
   if ((use_tma & 1) && n_rows < Sy) {
@@ -1180,7 +1199,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     // the Sy x KT tile of R[j] in flight at once (pitch KT complex = the FFT's [Sy][KT] layout);
     // rows not staged are zeroed afterwards
     __syncthreads();                                   // x free (previous tile), sstaged set
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && t > 0) {                   // (tile 0 was issued in the prologue)
       fence_proxy_async_smem();                        // generic writes of x before the async refill
       mbar_arrive_expect_tx(&lbar, (uint32_t)(Sy * KT * 8));
       for (int b = 0; b < Sy / kBY; ++b)
