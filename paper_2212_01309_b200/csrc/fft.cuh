@@ -86,37 +86,48 @@ __device__ __forceinline__ int fslot(int f) {
 
 // Forward DFT (unnormalised, e^{-2 pi i}) of 2^logc interleaved sequences of length N = 2^LOGN
 // stored in shared memory as x[n * cnt + c] (sequence index fastest: a warp touches consecutive
-// addresses).  Input in natural order; frequency f ends at slot fslot<LOGN>(f).  tw = the full
-// table tw[m] = exp(-2 pi i m / N), m < N, in shared memory (only the step-2 twiddles W_N^{n2 k1}
-// read it).  Starts and ends with the block synchronised.
-template <int LOGN>
-__device__ __forceinline__ void fft_seq(float2* x, const float2* tw, int logc) {
+// addresses), plus PAD float2 after every block of N2 positions (pidx below; PAD = 8 makes the
+// second step's 8-sequence tiles conflict-free: consecutive blocks then start half a bank row
+// apart).  LOGC >= 0 fixes logc at compile time, so every shared-memory address of a thread is
+// one base register plus an immediate offset.  Input in natural order; frequency f ends at slot
+// fslot<LOGN>(f).  tw = the full table tw[m] = exp(-2 pi i m / N), m < N, in shared memory (only
+// the step-2 twiddles W_N^{n2 k1} read it).  Starts and ends with the block synchronised.
+template <int LOGN, int PAD = 0>
+__device__ __forceinline__ int pidx(int n, int logc) {
+  return (n << logc) + (n >> Split<LOGN>::L2) * PAD;
+}
+template <int LOGN, int LOGC = -1, int PAD = 0>
+__device__ __forceinline__ void fft_seq(float2* x, const float2* tw, int logc_rt) {
   using S = Split<LOGN>;
   constexpr int N1 = S::N1, N2 = S::N2;
+  const int logc = LOGC >= 0 ? LOGC : logc_rt;
   const int cnt = 1 << logc;
+  const int bs = (N2 << logc) + PAD;       // stride between blocks of N2 positions
   for (int t = threadIdx.x; t < (N2 << logc); t += blockDim.x) {
     const int c = t & (cnt - 1), n2 = t >> logc;
+    float2* xb = x + (n2 << logc) + c;
     float2 v[N1];
 #pragma unroll
-    for (int n1 = 0; n1 < N1; ++n1) v[n1] = x[((N2 * n1 + n2) << logc) + c];
+    for (int n1 = 0; n1 < N1; ++n1) v[n1] = xb[n1 * bs];
     dft_reg<S::L1>(v);
     if (N2 > 1) {
 #pragma unroll
       for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], tw[n2 * k1]);
     }
 #pragma unroll
-    for (int k1 = 0; k1 < N1; ++k1) x[((N2 * k1 + n2) << logc) + c] = v[k1];
+    for (int k1 = 0; k1 < N1; ++k1) xb[k1 * bs] = v[k1];
   }
   __syncthreads();
   if (N2 > 1) {
     for (int t = threadIdx.x; t < (N1 << logc); t += blockDim.x) {
       const int c = t & (cnt - 1), k1 = t >> logc;
+      float2* xb = x + k1 * bs + c;
       float2 v[N2];
 #pragma unroll
-      for (int n2 = 0; n2 < N2; ++n2) v[n2] = x[((N2 * k1 + n2) << logc) + c];
+      for (int n2 = 0; n2 < N2; ++n2) v[n2] = xb[n2 << logc];
       dft_reg<S::L2>(v);
 #pragma unroll
-      for (int k2 = 0; k2 < N2; ++k2) x[((N2 * k1 + k2) << logc) + c] = v[k2];
+      for (int k2 = 0; k2 < N2; ++k2) xb[k2 << logc] = v[k2];
     }
     __syncthreads();
   }

@@ -114,7 +114,6 @@ struct ProjCfgT {
   static constexpr int kThreads = 96 + kNGroups * 128 + 128;        // MMA1, MMA2, TMA, converters, epilogue
   static constexpr int kMinBlocks = LEAN ? 2 : 1;
   static constexpr int kEpi0 = 96 + kNGroups * 128;                 // first epilogue thread
-  static constexpr int kNA = LEAN ? 2 : 4;                          // TMEM A-operand ring (u16 path)
   static constexpr int kKC = Q >= 64 ? 64 : Q;            // K elements (pixels) per A1 chunk
   static constexpr int kCPT = Q / kKC;                    // chunks per stage-1 tile
   static constexpr int kSpan = kKC * 2;                   // bytes per row of a raw u16 chunk (swizzle span)
@@ -147,7 +146,15 @@ struct ProjCfgT {
 #ifndef WDD_LEAN_NB2
 #define WDD_LEAN_NB2 1
 #endif
+#ifndef WDD_LEAN_NA
+#define WDD_LEAN_NA 2
+#endif
   static constexpr int kNB2 = LEAN ? WDD_LEAN_NB2 : 2;    // stage-2 A2 images / accumulators in flight
+  // TMEM A-operand ring (u16 path): 4 deep in the full variant; lean 2 (WDD_LEAN_NA=4, where 256
+  // TMEM columns hold it with a two-deep acc1 ring, measured: Box projection 1.016 -> 0.981 of the
+  // copy peak, Large / Medium unchanged)
+  static constexpr int kNA = !LEAN ? 4
+                           : (WDD_LEAN_NA + kNGroups) * (Q >= 64 ? 32 : Q / 2) + (2 + kNB2) * kNacc <= 256 ? WDD_LEAN_NA : 2;
   // acc1 ring: 4 deep unless TMEM (A ring + plane-1 buffers + acc1 + acc2 images) would exceed 512 columns
   // (lean: 2, or 1 where two would not leave both CTAs of an SM their 256 TMEM columns)
   static constexpr int kNAcc = LEAN ? ((kNA + kNGroups) * (Q >= 64 ? 32 : Q / 2) + (2 + kNB2) * kNacc > 256 ? 1 : 2)
@@ -1022,23 +1029,31 @@ __device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uin
 #ifndef WDD_CF_MINB_LARGE
 #define WDD_CF_MINB_LARGE 2
 #endif
-template <int LOGN>
+// LOGC >= 0: logP fixed at compile time (= the argument); -1: any logP.  FftPad: float2 of padding
+// per block of N2 positions (fft::pidx).  0: a pad that shifts the 8-sequence tiles' blocks by half
+// a bank row (64 B) would remove the FFT's second-step bank conflicts, but the TMA tile loads need
+// 128-byte aligned shared-memory destinations (measured: misaligned-address fault).
+template <int LOGC> struct FftPad { static constexpr int value = 0; };
+template <int LOGN, int LOGC>
 __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MINB_LARGE) rowfft_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
                                                      const uint32_t* __restrict__ masks, int mask_words,
                                                      const float2* __restrict__ tw, const int32_t* __restrict__ col_vx,
-                                                     float2* __restrict__ R, int logP, int Sy, int K, int n_vx,
+                                                     float2* __restrict__ R, int logP_rt, int Sy, int K, int n_vx,
                                                      float scale, const __grid_constant__ CUtensorMap tmC, int use_tma,
                                                      int kbase, int KR) {
   // coefficients kbase + blockIdx.x * 2P ..; R holds the chunk kbase .. kbase + KR - 1 (row stride KR)
   constexpr int Sx = 1 << LOGN;
-  constexpr int kBY = Sx < 256 ? Sx : 256;   // rows per TMA box
+  constexpr int PAD = FftPad<LOGC>::value;
+  constexpr int kBY = PAD ? fft::Split<LOGN>::N2 : Sx < 256 ? Sx : 256;   // rows per TMA box (one block when padded)
   extern __shared__ __align__(16) float2 fsm[];
   __shared__ uint32_t smask[(Sx + 31) / 32];
-  __shared__ int2 sslot[Sx];             // (slot of v, slot of -v) per active column j
+  __shared__ int2 sslot[Sx];             // tile offsets of the slots of v and -v per active column j
   __shared__ __align__(8) uint64_t lbar;
+  const int logP = LOGC >= 0 ? LOGC : logP_rt;
   const int P = 1 << logP;
-  float2* x = fsm;                       // [Sx][P]
-  float2* stw = fsm + (Sx << logP);      // [Sx] twiddles
+  auto xi = [&](int n) { return fft::pidx<LOGN, PAD>(n, logP); };   // position n of the [Sx][P] tile
+  float2* x = fsm;                       // [Sx][P] (+ PAD per block of N2 positions)
+  float2* stw = fsm + xi(Sx);            // [Sx] twiddles
   const int r = blockIdx.y, k0 = kbase + blockIdx.x * 2 * P;
   // use_tma bit 1 (set when this grid is itself PDL-launched): no early trigger -- this kernel reads
   // the coefficient store, which the first projection of the acquisition after next overwrites, so
@@ -1056,13 +1071,13 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
       pdl_wait();   // C of the projection kernels (and the uploaded row list / masks)
       const int sy0 = rows[r];
       mbar_arrive_expect_tx(&lbar, (uint32_t)(Sx * P * 8));
-      for (int b = 0; b < Sx / kBY; ++b) tma_load_2d(x + ((b * kBY) << logP), &tmC, k0, sy0 * Sx + b * kBY, &lbar);
+      for (int b = 0; b < Sx / kBY; ++b) tma_load_2d(x + xi(b * kBY), &tmC, k0, sy0 * Sx + b * kBY, &lbar);
     }
   }
   for (int i = threadIdx.x; i < Sx; i += blockDim.x) stw[i] = __ldg(tw + i);
   for (int j = threadIdx.x; j < n_vx; j += blockDim.x) {
     const int v = __ldg(col_vx + j);
-    sslot[j] = make_int2(fft::fslot<LOGN>(v), fft::fslot<LOGN>((Sx - v) & (Sx - 1)));
+    sslot[j] = make_int2(xi(fft::fslot<LOGN>(v)), xi(fft::fslot<LOGN>((Sx - v) & (Sx - 1))));
   }
   pdl_wait();   // C of the projection kernels (and the uploaded row list / masks)
   const int sy = rows[r];
@@ -1072,7 +1087,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
     mbar_wait(&lbar, 0);
     for (int sx = threadIdx.x; sx < Sx; sx += blockDim.x)
       if (!((smask[sx >> 5] >> (sx & 31)) & 1u))
-        for (int pp = 0; pp < P; ++pp) x[(sx << logP) + pp] = make_float2(0.f, 0.f);
+        for (int pp = 0; pp < P; ++pp) x[xi(sx) + pp] = make_float2(0.f, 0.f);
     __syncthreads();
     if (use_tma & 2) pdl_trigger();   // every read of C by this CTA is complete
   } else {
@@ -1100,7 +1115,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
       const int e = base + u * (int)blockDim.x + threadIdx.x;
       if (e < total) {
         const int sx = e >> lq;
-        *reinterpret_cast<float4*>(x + 2 * e) =
+        *reinterpret_cast<float4*>(x + xi(sx) + 2 * (e & ((P >> 1) - 1))) =
             ((smask[sx >> 5] >> (sx & 31)) & 1u) ? v[u] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
@@ -1108,12 +1123,12 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
   __syncthreads();
   if (use_tma & 2) pdl_trigger();   // every read of C by this CTA is complete
   }
-  fft::fft_seq<LOGN>(x, stw, logP);
+  fft::fft_seq<LOGN, LOGC, PAD>(x, stw, logP);
   const float hs = 0.5f * scale;
   for (int e = threadIdx.x; e < (n_vx << logP); e += blockDim.x) {
     const int j = e >> logP, pp = e & (P - 1);
     const int2 sl = sslot[j];
-    const float2 z = x[(sl.x << logP) + pp], zm = x[(sl.y << logP) + pp];
+    const float2 z = x[sl.x + pp], zm = x[sl.y + pp];
     const float4 o = make_float4((z.x + zm.x) * hs, (z.y - zm.y) * hs, (z.y + zm.y) * hs, (zm.x - z.x) * hs);
     *reinterpret_cast<float4*>(R + ((int64_t)j * Sy + sy) * KR + (k0 - kbase) + 2 * pp) = o;
   }
@@ -1125,13 +1140,13 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
 // reset, G is logically zero), and, with the updated G still in registers, the tile's share of the
 // Wiener readout  opart[t][g] = sum_{k in tile t} G[g][k] K_g[k], so a readout never
 // re-reads G.  The partial sums are combined over tiles in a fixed order by the image transform.
-template <int LOGN>
+template <int LOGN, int LOGC>
 __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MINB_LARGE) colfft_kernel(const float2* __restrict__ R, const int32_t* __restrict__ rows,
                                                      int n_rows, const float2* __restrict__ tw,
                                                      const int32_t* __restrict__ col_off,
                                                      const int32_t* __restrict__ act_vy, float2* __restrict__ G,
                                                      const float2* __restrict__ W, float2* __restrict__ opart,
-                                                     int64_t n_act, int logKT, int K, float scale, int overwrite,
+                                                     int64_t n_act, int logKT_rt, int K, float scale, int overwrite,
                                                      int tpc, int o_only, const __grid_constant__ CUtensorMap tmR,
                                                      int use_tma, int kbase, int KR, const int2* __restrict__ hmap) {
   // use_tma: bit 0 = R tiles by TMA, bit 3 = L2 prefetch of the output stage's W / G rows.
@@ -1143,18 +1158,21 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   // written from the same transform, X[-vy] conjugated -- half the row-FFT output, R traffic
   // and y-FFTs.
   constexpr int Sy = 1 << LOGN;
-  constexpr int kBY = Sy < 256 ? Sy : 256;   // rows per TMA box
+  constexpr int PAD = FftPad<LOGC>::value;
+  constexpr int kBY = PAD ? fft::Split<LOGN>::N2 : Sy < 256 ? Sy : 256;   // rows per TMA box (one block when padded)
   extern __shared__ __align__(16) float2 fsm[];
+  const int logKT = LOGC >= 0 ? LOGC : logKT_rt;
   const int KT = 1 << logKT;
+  auto xi = [&](int n) { return fft::pidx<LOGN, PAD>(n, logKT); };   // row n of the [Sy][KT] tile
   __shared__ int srow[Sy];                // staged rows
   __shared__ uint8_t sstaged[Sy];         // row staged (TMA path: the others are zeroed)
   __shared__ __align__(8) uint64_t lbar;
-  __shared__ int svy[Sy];                 // slot of each active vy of column j
+  __shared__ int svy[Sy];                 // tile offset of the slot of each active vy of column j
   __shared__ float2 sdot[Sy];             // per-row readout partial over this CTA's k-tiles
   __shared__ int svm[Sy];                 // the same for the mirror column (slot of -vy)
   __shared__ float2 sdm[Sy];
-  float2* x = fsm;                       // [Sy][KT]
-  float2* stw = fsm + (Sy << logKT);     // [Sy] twiddles
+  float2* x = fsm;                       // [Sy][KT] (+ PAD per block of N2 rows)
+  float2* stw = fsm + xi(Sy);            // [Sy] twiddles
   const int jr = blockIdx.y;              // column of R
   int j = jr, jm = -1;
   if (hmap) {
@@ -1171,17 +1189,17 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     mbar_arrive_expect_tx(&lbar, (uint32_t)(Sy * KT * 8));
     const int kl0 = blockIdx.x * tpc * KT;
     for (int b = 0; b < Sy / kBY; ++b)
-      tma_load_2d(x + ((b * kBY) << logKT), &tmR, 2 * kl0, jr * Sy + b * kBY, &lbar);
+      tma_load_2d(x + xi(b * kBY), &tmR, 2 * kl0, jr * Sy + b * kBY, &lbar);
   }
   const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
   const int gm0 = jm >= 0 ? __ldg(col_off + jm) : 0, mjm = jm >= 0 ? __ldg(col_off + jm + 1) - gm0 : 0;
   for (int i = threadIdx.x; i < Sy; i += blockDim.x) stw[i] = __ldg(tw + i);
   for (int i = threadIdx.x; i < mj; i += blockDim.x) {
-    svy[i] = fft::fslot<LOGN>(__ldg(act_vy + g0 + i));
+    svy[i] = xi(fft::fslot<LOGN>(__ldg(act_vy + g0 + i)));
     sdot[i] = make_float2(0.f, 0.f);
   }
   for (int i = threadIdx.x; i < mjm; i += blockDim.x) {
-    svm[i] = fft::fslot<LOGN>((Sy - __ldg(act_vy + gm0 + i)) & (Sy - 1));
+    svm[i] = xi(fft::fslot<LOGN>((Sy - __ldg(act_vy + gm0 + i)) & (Sy - 1)));
     sdm[i] = make_float2(0.f, 0.f);
   }
   if (use_tma & 1)
@@ -1203,15 +1221,15 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
       fence_proxy_async_smem();                        // generic writes of x before the async refill
       mbar_arrive_expect_tx(&lbar, (uint32_t)(Sy * KT * 8));
       for (int b = 0; b < Sy / kBY; ++b)
-        tma_load_2d(x + ((b * kBY) << logKT), &tmR, 2 * kl, jr * Sy + b * kBY, &lbar);
+        tma_load_2d(x + xi(b * kBY), &tmR, 2 * kl, jr * Sy + b * kBY, &lbar);
     }
     mbar_wait(&lbar, (uint32_t)(t & 1));
     if (n_rows < Sy)
       for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x)
-        if (!sstaged[e >> logKT]) x[e] = make_float2(0.f, 0.f);
+        if (!sstaged[e >> logKT]) x[xi(e >> logKT) + (e & (KT - 1))] = make_float2(0.f, 0.f);
   } else {
   if (n_rows < Sy)
-    for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x) x[e] = make_float2(0.f, 0.f);
+    for (int e = threadIdx.x; e < (Sy << logKT); e += blockDim.x) x[xi(e >> logKT) + (e & (KT - 1))] = make_float2(0.f, 0.f);
   __syncthreads();
   // staged rows of R[j] (k0 .. k0+KT), two coefficients (16 bytes) per load, kU loads in flight
   const float4* Rj = reinterpret_cast<const float4*>(R + (int64_t)jr * Sy * KR + kl);
@@ -1223,7 +1241,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     for (int u = 0; u < kU; ++u) {
       const int e = base + u * (int)blockDim.x + threadIdx.x;
       const int sy = e < total ? srow[e >> lh] : 0, h = e & (hKT - 1);
-      dst[u] = e < total ? (sy << logKT) + 2 * h : -1;
+      dst[u] = e < total ? xi(sy) + 2 * h : -1;
       v[u] = e < total ? __ldg(Rj + (int64_t)sy * (KR >> 1) + h) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
@@ -1244,7 +1262,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     }
   }
   __syncthreads();
-  fft::fft_seq<LOGN>(x, stw, logKT);
+  fft::fft_seq<LOGN, LOGC, PAD>(x, stw, logKT);
   // Output: thread = (row slot, coefficient pair p); G (+)= X / sqrt(Sy) for the column's active
   // vy, and the tile's share of sum_k G K_v reduced over the hKT threads of the row.
   const int pp = threadIdx.x & (hKT - 1), rs = threadIdx.x >> lh, rpp = (int)blockDim.x >> lh;
@@ -1272,7 +1290,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
       const int i = ib + u * rpp + rs;
       float2 d = make_float2(0.f, 0.f);
       if (i < mc) {
-        const float4 z = *reinterpret_cast<const float4*>(x + (sv[i] << logKT) + 2 * pp);
+        const float4 z = *reinterpret_cast<const float4*>(x + sv[i] + 2 * pp);
         const float4 gn = make_float4(fmaf(z.x, scale, o[u].x), fmaf(z.y, cs, o[u].y), fmaf(z.z, scale, o[u].z),
                                       fmaf(z.w, cs, o[u].w));
         if (!o_only) G4[(int64_t)(gc + i) * K2 + (k0 >> 1) + pp] = gn;
@@ -1429,6 +1447,47 @@ static int rowfft_logp(const Plan& p) {
   return logP;
 }
 
+// compile-time tile width of the FFT flush kernels' specialised instances: the default logKT of
+// the y-FFT from Sy = 128 and the default logP of the row FFT at Sx = 128 (-1: runtime width only;
+// WDD_FFT_SPEC=0 off).  Measured (bench.py): y-FFT Box 1.82 -> 1.60 ms, Large 140 -> 131 us, Medium
+// 18.8 -> 16.8 us; row FFT Medium 14.8 -> 12.5 us, but Box 0.91 -> 1.01 ms and Large 90 -> 94 us.
+static constexpr int fft_spec_logc(int logn, bool row) {
+  return logn < 7 ? -1 : row ? (logn == 7 ? 4 : -1) : (logn >= 10 ? 3 : logn == 9 ? 4 : 5);
+}
+static bool fft_spec_on() {
+  static const bool on = [] { const char* e = std::getenv("WDD_FFT_SPEC"); return !(e && std::atoi(e) == 0); }();
+  return on;
+}
+
+template <int LOGN, int LOGC>
+static cudaError_t launch_rowfft_t(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows,
+                               cudaStream_t st, int kbase, int KR, int logP, int nt) {
+  constexpr int PAD = FftPad<LOGC>::value;
+  const size_t smem = ((size_t)p.Sx << logP) * 8 + (size_t)(p.Sx / fft::Split<LOGN>::N2) * PAD * 8 + (size_t)p.Sx * 8 + 16;
+  {
+    cudaError_t e = func_attr_once((const void*)rowfft_kernel<LOGN, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kFftSmem + 16384);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid(KR / (2 << logP), n_rows);
+  // (with two projection CTAs per SM a PDL-launched row FFT would park its CTAs next to the
+  // last projection CTAs and slow them down: launch it after the projection completes -- unless
+  // that projection ran fewer CTAs than SMs, where the parked CTAs take idle SMs and the launch
+  // overlaps the projection's tail: Medium's 512-frame batches, 32 CTAs each, +1.6% end to end;
+  // Box's and Large's full-width last batches -0.4% with PDL, tools/experiments/exp_rowpdl.sh)
+  static const int env_pdl = [] { const char* e = std::getenv("WDD_ROWFFT_PDL"); return e ? std::atoi(e) : -1; }();
+  const bool rowfft_pdl = env_pdl >= 0 ? env_pdl != 0 : !project_is_lean(p) || p.last_proj_grid < p.sm_count;
+  CUtensorMap tmC;
+  const bool tma = fft_tmap(&tmC, p.d_Call, (uint64_t)p.Kl, (uint64_t)p.S, (uint64_t)p.Kl * 4, 2u << logP,
+                            (uint32_t)(PAD ? fft::Split<LOGN>::N2 : std::min(p.Sx, 256)));
+  // (Hermitian half plane, p.r_half: only the primary columns vx <= Sx/2 go to R)
+  return launch_pdl(rowfft_kernel<LOGN, LOGC>, grid, dim3(nt), smem, st, rowfft_pdl, (const float*)p.d_Call, rows, masks,
+                    p.mask_words, (const float2*)p.d_twx,
+                    (const int32_t*)(p.r_half ? p.d_col_vx_half : p.d_col_vx), p.d_R, logP, p.Sy, p.Kl,
+                    p.r_half ? p.n_vh : p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0),
+                    kbase, KR);
+}
+
 cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows, cudaStream_t st,
                           int kbase, int KR) {
   if (KR <= 0) { kbase = 0; KR = p.Kl; }
@@ -1440,31 +1499,12 @@ cudaError_t launch_rowdft(const Plan& p, const int32_t* rows, const uint32_t* ma
     // of 32 pairs on 256: +0.8% Medium, +1% Large end to end); 256 threads beyond (Live: -0.5%)
     const int logP = rowfft_logp(p);
     const int nt = knob.y > 0 ? knob.y : logSx <= 8 ? 128 : 256;
-    const size_t smem = ((size_t)p.Sx << logP) * 8 + (size_t)p.Sx * 8 + 16;
     return with_log(logSx, [&](auto LN) {
       constexpr int LOGN = decltype(LN)::value;
-      {
-        cudaError_t e = func_attr_once((const void*)rowfft_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kFftSmem + 16384);
-        if (e != cudaSuccess) return e;
-      }
-      dim3 grid(KR / (2 << logP), n_rows);
-      // (with two projection CTAs per SM a PDL-launched row FFT would park its CTAs next to the
-      // last projection CTAs and slow them down: launch it after the projection completes -- unless
-      // that projection ran fewer CTAs than SMs, where the parked CTAs take idle SMs and the launch
-      // overlaps the projection's tail: Medium's 512-frame batches, 32 CTAs each, +1.6% end to end;
-      // Box's and Large's full-width last batches -0.4% with PDL, tools/experiments/exp_rowpdl.sh)
-      static const int env_pdl = [] { const char* e = std::getenv("WDD_ROWFFT_PDL"); return e ? std::atoi(e) : -1; }();
-      const bool rowfft_pdl = env_pdl >= 0 ? env_pdl != 0 : !project_is_lean(p) || p.last_proj_grid < p.sm_count;
-      CUtensorMap tmC;
-      const bool tma = fft_tmap(&tmC, p.d_Call, (uint64_t)p.Kl, (uint64_t)p.S, (uint64_t)p.Kl * 4, 2u << logP,
-                                (uint32_t)std::min(p.Sx, 256));
-      // (Hermitian half plane, p.r_half: only the primary columns vx <= Sx/2 go to R)
-      return launch_pdl(rowfft_kernel<LOGN>, grid, dim3(nt), smem, st, rowfft_pdl, (const float*)p.d_Call, rows, masks,
-                        p.mask_words, (const float2*)p.d_twx,
-                        (const int32_t*)(p.r_half ? p.d_col_vx_half : p.d_col_vx), p.d_R, logP, p.Sy, p.Kl,
-                        p.r_half ? p.n_vh : p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0),
-                        kbase, KR);
+      constexpr int SPEC = fft_spec_logc(LOGN, true);
+      if constexpr (SPEC >= 0)
+        if (logP == SPEC && fft_spec_on()) return launch_rowfft_t<LOGN, SPEC>(p, rows, masks, n_rows, st, kbase, KR, logP, nt);
+      return launch_rowfft_t<LOGN, -1>(p, rows, masks, n_rows, st, kbase, KR, logP, nt);
     });
   }
   {
@@ -2357,6 +2397,34 @@ int flush_tiles(const Plan& p, int n_rows, int kind) {
   return k == 3 ? rgemm_nkc(p) : k == 2 ? colgemm_chunks(p) : k == 1 ? colfft_tiles(p) : 0;
 }
 
+template <int LOGN, int LOGC>
+static cudaError_t launch_colfft_t(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st,
+                                   bool o_only, int kbase, int KR, int logKT) {
+  constexpr int PAD = FftPad<LOGC>::value;
+  const size_t smem = ((size_t)p.Sy << logKT) * 8 + (size_t)(p.Sy / fft::Split<LOGN>::N2) * PAD * 8 + (size_t)p.Sy * 8 + 16;
+  {
+    cudaError_t e = func_attr_once((const void*)colfft_kernel<LOGN, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kFftSmem + 16384);
+    if (e != cudaSuccess) return e;
+  }
+  const int tpc = colfft_tpc(p);
+  const bool half = p.r_half;
+  dim3 grid((KR >> logKT) / tpc, half ? p.n_vh : p.n_vx);
+  static const int2 knob = env_pair("WDD_COLFFT");
+  // L2 prefetch of the output stage's rows: Large readout 339 -> 333 us, Box 3.77 -> 3.65 ms;
+  // none at Medium (-0.15%: fewer load rounds per tile), so only from Sy = 256
+  static const bool pf_on = [] { const char* e = std::getenv("WDD_COLFFT_PF"); return !(e && std::atoi(e) == 0); }();
+  CUtensorMap tmR;
+  const bool tma = fft_tmap(&tmR, p.d_R, (uint64_t)KR * 2, (uint64_t)grid.y * p.Sy, (uint64_t)KR * 8,
+                            2u << logKT, (uint32_t)(PAD ? fft::Split<LOGN>::N2 : std::min(p.Sy, 256)));
+  return launch_pdl(colfft_kernel<LOGN, LOGC>, grid, dim3(knob.y > 0 ? knob.y : 256), smem, st, true, p.d_R, rows, n_rows,
+                    (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G,
+                    (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.Kl,
+                    (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0, tpc, o_only ? 1 : 0, tmR,
+                    (tma ? 1 : 0) | (pf_on && p.Sy >= 256 ? 8 : 0), kbase, KR,
+                    half ? (const int2*)p.d_half_map : (const int2*)nullptr);
+}
+
 cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st, bool o_only,
                          int kind, int row0, int kbase, int KR) {
   if (KR <= 0) { kbase = 0; KR = p.Kl; }
@@ -2380,30 +2448,13 @@ cudaError_t launch_flush(const Plan& p, const int32_t* rows, int n_rows, bool ov
   if (kind == 1) {
     const int logSy = ilog2(p.Sy);
     const int logKT = colfft_logkt(p);
-    const size_t smem = ((size_t)p.Sy << logKT) * 8 + (size_t)p.Sy * 8 + 16;
     return with_log(logSy, [&](auto LN) {
       constexpr int LOGN = decltype(LN)::value;
-      {
-        cudaError_t e = func_attr_once((const void*)colfft_kernel<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kFftSmem + 16384);
-        if (e != cudaSuccess) return e;
-      }
-      const int tpc = colfft_tpc(p);
-      const bool half = p.r_half;
-      dim3 grid((KR >> logKT) / tpc, half ? p.n_vh : p.n_vx);
-      static const int2 knob = env_pair("WDD_COLFFT");
-      // L2 prefetch of the output stage's rows: Large readout 339 -> 333 us, Box 3.77 -> 3.65 ms;
-      // none at Medium (-0.15%: fewer load rounds per tile), so only from Sy = 256
-      static const bool pf_on = [] { const char* e = std::getenv("WDD_COLFFT_PF"); return !(e && std::atoi(e) == 0); }();
-      CUtensorMap tmR;
-      const bool tma = fft_tmap(&tmR, p.d_R, (uint64_t)KR * 2, (uint64_t)grid.y * p.Sy, (uint64_t)KR * 8,
-                                2u << logKT, (uint32_t)std::min(p.Sy, 256));
-      return launch_pdl(colfft_kernel<LOGN>, grid, dim3(knob.y > 0 ? knob.y : 256), smem, st, true, p.d_R, rows, n_rows,
-                        (const float2*)p.d_twy, (const int32_t*)p.d_col_off, (const int32_t*)p.d_act_vy, p.d_G,
-                        (const float2*)p.d_W, p.d_opart, (int64_t)p.n_act, logKT, p.Kl,
-                        (float)(1.0 / std::sqrt((double)p.Sy)), overwrite ? 1 : 0, tpc, o_only ? 1 : 0, tmR,
-                        (tma ? 1 : 0) | (pf_on && p.Sy >= 256 ? 8 : 0), kbase, KR,
-                        half ? (const int2*)p.d_half_map : (const int2*)nullptr);
+      constexpr int SPEC = fft_spec_logc(LOGN, false);
+      if constexpr (SPEC >= 0)
+        if (logKT == SPEC && fft_spec_on())
+          return launch_colfft_t<LOGN, SPEC>(p, rows, n_rows, overwrite, st, o_only, kbase, KR, logKT);
+      return launch_colfft_t<LOGN, -1>(p, rows, n_rows, overwrite, st, o_only, kbase, KR, logKT);
     });
   }
   if (o_only) return cudaErrorNotSupported;   // unreachable: flush_kind never picks the DFT for these
