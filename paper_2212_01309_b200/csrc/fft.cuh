@@ -90,13 +90,14 @@ __device__ __forceinline__ int fslot(int f) {
 // second step's 8-sequence tiles conflict-free: consecutive blocks then start half a bank row
 // apart).  LOGC >= 0 fixes logc at compile time, so every shared-memory address of a thread is
 // one base register plus an immediate offset.  Input in natural order; frequency f ends at slot
-// fslot<LOGN>(f).  tw = the full table tw[m] = exp(-2 pi i m / N), m < N, in shared memory (only
-// the step-2 twiddles W_N^{n2 k1} read it).  Starts and ends with the block synchronised.
+// fslot<LOGN>(f).  tw = the full table tw[m] = exp(-2 pi i m / N), m < N, in shared memory, or in
+// global memory read through the L1 (TWG: no per-CTA copy; only the step-2 twiddles W_N^{n2 k1}
+// read it).  Starts and ends with the block synchronised.
 template <int LOGN, int PAD = 0>
 __device__ __forceinline__ int pidx(int n, int logc) {
   return (n << logc) + (n >> Split<LOGN>::L2) * PAD;
 }
-template <int LOGN, int LOGC = -1, int PAD = 0>
+template <int LOGN, int LOGC = -1, int PAD = 0, bool TWG = false>
 __device__ __forceinline__ void fft_seq(float2* x, const float2* tw, int logc_rt) {
   using S = Split<LOGN>;
   constexpr int N1 = S::N1, N2 = S::N2;
@@ -112,7 +113,7 @@ __device__ __forceinline__ void fft_seq(float2* x, const float2* tw, int logc_rt
     dft_reg<S::L1>(v);
     if (N2 > 1) {
 #pragma unroll
-      for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], tw[n2 * k1]);
+      for (int k1 = 1; k1 < N1; ++k1) v[k1] = cmul(v[k1], TWG ? __ldg(tw + n2 * k1) : tw[n2 * k1]);
     }
 #pragma unroll
     for (int k1 = 0; k1 < N1; ++k1) xb[k1 * bs] = v[k1];

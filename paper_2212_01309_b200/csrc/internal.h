@@ -78,6 +78,7 @@ struct Plan {
   // column's mirror from the same transform (colfft_kernel); r_half is set per flush (FFT flushes)
   int n_vh = 0;                       // 0: not available
   int32_t* d_col_vx_half = nullptr;   // n_vh primary vx
+  bool half_identity = false;         // d_col_vx_half[j] == j
   int2* d_half_map = nullptr;         // n_vh (accumulator column of vx, of -vx or -1)
   mutable bool r_half = false;
   float2* d_W = nullptr;              // n_act * K

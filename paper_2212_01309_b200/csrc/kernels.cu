@@ -1034,6 +1034,19 @@ __device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uin
 // a bank row (64 B) would remove the FFT's second-step bank conflicts, but the TMA tile loads need
 // 128-byte aligned shared-memory destinations (measured: misaligned-address fault).
 template <int LOGC> struct FftPad { static constexpr int value = 0; };
+// Twiddles of the FFT flush kernels read through the L1 from the plan's global table (no per-CTA
+// shared copy: its load latency sat at the head of every CTA), by scan-length threshold; and the
+// y-FFT output stage's row slots computed from act_vy loaded with the W rows instead of from a
+// shared table built in the prologue.
+#ifndef WDD_RF_TWG_MINLOG
+#define WDD_RF_TWG_MINLOG 99
+#endif
+#ifndef WDD_CF_TWG_MINLOG
+#define WDD_CF_TWG_MINLOG 9
+#endif
+#ifndef WDD_CF_LAZY_MINLOG
+#define WDD_CF_LAZY_MINLOG 9
+#endif
 template <int LOGN, int LOGC>
 __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MINB_LARGE) rowfft_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
                                                      const uint32_t* __restrict__ masks, int mask_words,
@@ -1052,8 +1065,9 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
   const int logP = LOGC >= 0 ? LOGC : logP_rt;
   const int P = 1 << logP;
   auto xi = [&](int n) { return fft::pidx<LOGN, PAD>(n, logP); };   // position n of the [Sx][P] tile
+  constexpr bool TWG = LOGN >= WDD_RF_TWG_MINLOG;
   float2* x = fsm;                       // [Sx][P] (+ PAD per block of N2 positions)
-  float2* stw = fsm + xi(Sx);            // [Sx] twiddles
+  float2* stw = fsm + xi(Sx);            // [Sx] twiddles (!TWG)
   const int r = blockIdx.y, k0 = kbase + blockIdx.x * 2 * P;
   // use_tma bit 1 (set when this grid is itself PDL-launched): no early trigger -- this kernel reads
   // the coefficient store, which the first projection of the acquisition after next overwrites, so
@@ -1074,11 +1088,13 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
       for (int b = 0; b < Sx / kBY; ++b) tma_load_2d(x + xi(b * kBY), &tmC, k0, sy0 * Sx + b * kBY, &lbar);
     }
   }
-  for (int i = threadIdx.x; i < Sx; i += blockDim.x) stw[i] = __ldg(tw + i);
-  for (int j = threadIdx.x; j < n_vx; j += blockDim.x) {
-    const int v = __ldg(col_vx + j);
-    sslot[j] = make_int2(xi(fft::fslot<LOGN>(v)), xi(fft::fslot<LOGN>((Sx - v) & (Sx - 1))));
-  }
+  if constexpr (!TWG)
+    for (int i = threadIdx.x; i < Sx; i += blockDim.x) stw[i] = __ldg(tw + i);
+  if (col_vx)   // (NULL: column j is vx = j, the half plane's primary columns; slots computed below)
+    for (int j = threadIdx.x; j < n_vx; j += blockDim.x) {
+      const int v = __ldg(col_vx + j);
+      sslot[j] = make_int2(xi(fft::fslot<LOGN>(v)), xi(fft::fslot<LOGN>((Sx - v) & (Sx - 1))));
+    }
   pdl_wait();   // C of the projection kernels (and the uploaded row list / masks)
   const int sy = rows[r];
   if (use_tma & 1) {
@@ -1123,11 +1139,11 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
   __syncthreads();
   if (use_tma & 2) pdl_trigger();   // every read of C by this CTA is complete
   }
-  fft::fft_seq<LOGN, LOGC, PAD>(x, stw, logP);
+  fft::fft_seq<LOGN, LOGC, PAD, TWG>(x, TWG ? tw : stw, logP);
   const float hs = 0.5f * scale;
   for (int e = threadIdx.x; e < (n_vx << logP); e += blockDim.x) {
     const int j = e >> logP, pp = e & (P - 1);
-    const int2 sl = sslot[j];
+    const int2 sl = col_vx ? sslot[j] : make_int2(xi(fft::fslot<LOGN>(j)), xi(fft::fslot<LOGN>((Sx - j) & (Sx - 1))));
     const float2 z = x[sl.x + pp], zm = x[sl.y + pp];
     const float4 o = make_float4((z.x + zm.x) * hs, (z.y - zm.y) * hs, (z.y + zm.y) * hs, (zm.x - z.x) * hs);
     *reinterpret_cast<float4*>(R + ((int64_t)j * Sy + sy) * KR + (k0 - kbase) + 2 * pp) = o;
@@ -1167,12 +1183,13 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   __shared__ int srow[Sy];                // staged rows
   __shared__ uint8_t sstaged[Sy];         // row staged (TMA path: the others are zeroed)
   __shared__ __align__(8) uint64_t lbar;
-  __shared__ int svy[Sy];                 // tile offset of the slot of each active vy of column j
   __shared__ float2 sdot[Sy];             // per-row readout partial over this CTA's k-tiles
-  __shared__ int svm[Sy];                 // the same for the mirror column (slot of -vy)
   __shared__ float2 sdm[Sy];
+  constexpr bool TWG = LOGN >= WDD_CF_TWG_MINLOG, LAZY = LOGN >= WDD_CF_LAZY_MINLOG;
+  __shared__ int svy[LAZY ? 1 : Sy];      // tile offset of the slot of each active vy of column j (!LAZY)
+  __shared__ int svm[LAZY ? 1 : Sy];      // the same for the mirror column (slot of -vy)
   float2* x = fsm;                       // [Sy][KT] (+ PAD per block of N2 rows)
-  float2* stw = fsm + xi(Sy);            // [Sy] twiddles
+  float2* stw = fsm + xi(Sy);            // [Sy] twiddles (!TWG)
   const int jr = blockIdx.y;              // column of R
   int j = jr, jm = -1;
   if (hmap) {
@@ -1193,19 +1210,21 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   }
   const int g0 = __ldg(col_off + j), mj = __ldg(col_off + j + 1) - g0;
   const int gm0 = jm >= 0 ? __ldg(col_off + jm) : 0, mjm = jm >= 0 ? __ldg(col_off + jm + 1) - gm0 : 0;
-  for (int i = threadIdx.x; i < Sy; i += blockDim.x) stw[i] = __ldg(tw + i);
+  if constexpr (!TWG)
+    for (int i = threadIdx.x; i < Sy; i += blockDim.x) stw[i] = __ldg(tw + i);
   for (int i = threadIdx.x; i < mj; i += blockDim.x) {
-    svy[i] = xi(fft::fslot<LOGN>(__ldg(act_vy + g0 + i)));
+    if constexpr (!LAZY) svy[i] = xi(fft::fslot<LOGN>(__ldg(act_vy + g0 + i)));
     sdot[i] = make_float2(0.f, 0.f);
   }
   for (int i = threadIdx.x; i < mjm; i += blockDim.x) {
-    svm[i] = xi(fft::fslot<LOGN>((Sy - __ldg(act_vy + gm0 + i)) & (Sy - 1)));
+    if constexpr (!LAZY) svm[i] = xi(fft::fslot<LOGN>((Sy - __ldg(act_vy + gm0 + i)) & (Sy - 1)));
     sdm[i] = make_float2(0.f, 0.f);
   }
   if (use_tma & 1)
     for (int i = threadIdx.x; i < Sy; i += blockDim.x) sstaged[i] = n_rows < Sy ? 0 : 1;
   pdl_wait();   // R (row DFT) and G of the preceding kernels (and the uploaded row list)
-  for (int i = threadIdx.x; i < n_rows; i += blockDim.x) srow[i] = __ldg(rows + i);
+  if (!(use_tma & 1) || n_rows < Sy)   // (a whole-scan TMA flush needs no row list)
+    for (int i = threadIdx.x; i < n_rows; i += blockDim.x) srow[i] = __ldg(rows + i);
   if ((use_tma & 1) && n_rows < Sy) {
     __syncthreads();
     for (int i = threadIdx.x; i < n_rows; i += blockDim.x) sstaged[srow[i]] = 1;
@@ -1262,7 +1281,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
     }
   }
   __syncthreads();
-  fft::fft_seq<LOGN, LOGC, PAD>(x, stw, logKT);
+  fft::fft_seq<LOGN, LOGC, PAD, TWG>(x, TWG ? tw : stw, logKT);
   // Output: thread = (row slot, coefficient pair p); G (+)= X / sqrt(Sy) for the column's active
   // vy, and the tile's share of sum_k G K_v reduced over the hKT threads of the row.
   const int pp = threadIdx.x & (hKT - 1), rs = threadIdx.x >> lh, rpp = (int)blockDim.x >> lh;
@@ -1272,15 +1291,16 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   // pass 0: column j; pass 1 (half plane): the mirror column, X[-vy] conjugated
   for (int pass = 0; pass < (mjm > 0 ? 2 : 1); ++pass) {
   const int gc = pass ? gm0 : g0, mc = pass ? mjm : mj;
-  const int* sv = pass ? svm : svy;
   float2* sd = pass ? sdm : sdot;
   const float cs = pass ? -scale : scale;                // imaginary parts: conjugate
   for (int ib = 0; ib < mc; ib += rpp * 4) {             // block-uniform trip count (shuffles)
     float4 o[4], w[4];
+    int vy[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int i = ib + u * rpp + rs;
       const int64_t gi = (int64_t)(gc + i) * K2 + (k0 >> 1) + pp;
+      if constexpr (LAZY) vy[u] = i < mc ? __ldg(act_vy + gc + i) : 0;   // (loaded with W: no table round)
       w[u] = i < mc ? __ldg(W4 + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
       o[u] = (i < mc && !overwrite && !o_only) ? G4[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -1290,7 +1310,9 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
       const int i = ib + u * rpp + rs;
       float2 d = make_float2(0.f, 0.f);
       if (i < mc) {
-        const float4 z = *reinterpret_cast<const float4*>(x + sv[i] + 2 * pp);
+        // row of X: vy for column j, -vy for the mirror pass (X[-vy] conjugated)
+        const int sl = !LAZY ? (pass ? svm[i] : svy[i]) : xi(fft::fslot<LOGN>(pass ? (Sy - vy[u]) & (Sy - 1) : vy[u]));
+        const float4 z = *reinterpret_cast<const float4*>(x + sl + 2 * pp);
         const float4 gn = make_float4(fmaf(z.x, scale, o[u].x), fmaf(z.y, cs, o[u].y), fmaf(z.z, scale, o[u].z),
                                       fmaf(z.w, cs, o[u].w));
         if (!o_only) G4[(int64_t)(gc + i) * K2 + (k0 >> 1) + pp] = gn;
@@ -1463,7 +1485,8 @@ template <int LOGN, int LOGC>
 static cudaError_t launch_rowfft_t(const Plan& p, const int32_t* rows, const uint32_t* masks, int n_rows,
                                cudaStream_t st, int kbase, int KR, int logP, int nt) {
   constexpr int PAD = FftPad<LOGC>::value;
-  const size_t smem = ((size_t)p.Sx << logP) * 8 + (size_t)(p.Sx / fft::Split<LOGN>::N2) * PAD * 8 + (size_t)p.Sx * 8 + 16;
+  const size_t smem = ((size_t)p.Sx << logP) * 8 + (size_t)(p.Sx / fft::Split<LOGN>::N2) * PAD * 8 +
+                      (LOGN >= WDD_RF_TWG_MINLOG ? 0 : (size_t)p.Sx * 8) + 16;
   {
     cudaError_t e = func_attr_once((const void*)rowfft_kernel<LOGN, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                kFftSmem + 16384);
@@ -1483,7 +1506,7 @@ static cudaError_t launch_rowfft_t(const Plan& p, const int32_t* rows, const uin
   // (Hermitian half plane, p.r_half: only the primary columns vx <= Sx/2 go to R)
   return launch_pdl(rowfft_kernel<LOGN, LOGC>, grid, dim3(nt), smem, st, rowfft_pdl, (const float*)p.d_Call, rows, masks,
                     p.mask_words, (const float2*)p.d_twx,
-                    (const int32_t*)(p.r_half ? p.d_col_vx_half : p.d_col_vx), p.d_R, logP, p.Sy, p.Kl,
+                    (const int32_t*)(p.r_half ? (p.half_identity ? nullptr : p.d_col_vx_half) : p.d_col_vx), p.d_R, logP, p.Sy, p.Kl,
                     p.r_half ? p.n_vh : p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0),
                     kbase, KR);
 }
@@ -2401,7 +2424,8 @@ template <int LOGN, int LOGC>
 static cudaError_t launch_colfft_t(const Plan& p, const int32_t* rows, int n_rows, bool overwrite, cudaStream_t st,
                                    bool o_only, int kbase, int KR, int logKT) {
   constexpr int PAD = FftPad<LOGC>::value;
-  const size_t smem = ((size_t)p.Sy << logKT) * 8 + (size_t)(p.Sy / fft::Split<LOGN>::N2) * PAD * 8 + (size_t)p.Sy * 8 + 16;
+  const size_t smem = ((size_t)p.Sy << logKT) * 8 + (size_t)(p.Sy / fft::Split<LOGN>::N2) * PAD * 8 +
+                      (LOGN >= WDD_CF_TWG_MINLOG ? 0 : (size_t)p.Sy * 8) + 16;
   {
     cudaError_t e = func_attr_once((const void*)colfft_kernel<LOGN, LOGC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kFftSmem + 16384);

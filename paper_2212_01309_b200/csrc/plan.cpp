@@ -796,7 +796,11 @@ wdd_status wdd_plan_create(const int32_t scan_shape[2], double step_A, const int
       half_vx.push_back(vx);
       half_map.push_back(make_int2(j, jm));
     }
-    if (sym) p->n_vh = (int)half_vx.size();
+    if (sym) {
+      p->n_vh = (int)half_vx.size();
+      p->half_identity = true;       // primary columns vx = 0 .. n_vh - 1 (the row FFT needs no column table)
+      for (int j = 0; j < p->n_vh; ++j) p->half_identity = p->half_identity && half_vx[j] == j;
+    }
   }
 
   // twiddles
