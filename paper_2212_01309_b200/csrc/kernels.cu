@@ -2372,7 +2372,11 @@ static cudaError_t launch_rgemm(const Plan& p, const int32_t* rows, int n_rows, 
            (!overwrite && !o_only) ? 1 : 0, o_only ? 0 : 1, row0};
   const int64_t work = (int64_t)p.rg_items.size() * nkc;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)std::min<int64_t>(work, p.sm_count));
+  // (WDD_RG_GRID: at most that many persistent CTAs, e.g. to leave SMs to projections running
+  // beside a pipelined readout)
+  static const int env_grid = [] { const char* e = std::getenv("WDD_RG_GRID"); return e ? std::atoi(e) : 0; }();
+  const int max_ctas = env_grid > 0 ? std::min(env_grid, p.sm_count) : p.sm_count;
+  cfg.gridDim = dim3((unsigned)std::min<int64_t>(work, max_ctas));
   cfg.blockDim = dim3(kRgThreads);
   cfg.dynamicSmemBytes = kRgSmem;
   cfg.stream = st;
