@@ -1047,6 +1047,9 @@ template <int LOGC> struct FftPad { static constexpr int value = 0; };
 #ifndef WDD_CF_LAZY_MINLOG
 #define WDD_CF_LAZY_MINLOG 9
 #endif
+#ifndef WDD_CF_U_NOG
+#define WDD_CF_U_NOG 8   // y-FFT output rows per thread per round without a G read
+#endif
 template <int LOGN, int LOGC>
 __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MINB_LARGE) rowfft_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
                                                      const uint32_t* __restrict__ masks, int mask_words,
@@ -1098,14 +1101,17 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
   pdl_wait();   // C of the projection kernels (and the uploaded row list / masks)
   const int sy = rows[r];
   if (use_tma & 1) {
-    if (threadIdx.x < mask_words) smask[threadIdx.x] = masks[(int64_t)r * mask_words + threadIdx.x];
+    // (use_tma bit 2: every position of the row is pending -- no mask to apply)
+    if (!(use_tma & 4) && threadIdx.x < mask_words) smask[threadIdx.x] = masks[(int64_t)r * mask_words + threadIdx.x];
     __syncthreads();
     mbar_wait(&lbar, 0);
-    for (int sx = threadIdx.x; sx < Sx; sx += blockDim.x)
-      if (!((smask[sx >> 5] >> (sx & 31)) & 1u))
-        for (int pp = 0; pp < P; ++pp) x[xi(sx) + pp] = make_float2(0.f, 0.f);
-    __syncthreads();
-    if (use_tma & 2) pdl_trigger();   // every read of C by this CTA is complete
+    if (!(use_tma & 4)) {
+      for (int sx = threadIdx.x; sx < Sx; sx += blockDim.x)
+        if (!((smask[sx >> 5] >> (sx & 31)) & 1u))
+          for (int pp = 0; pp < P; ++pp) x[xi(sx) + pp] = make_float2(0.f, 0.f);
+      __syncthreads();
+    }
+    if (use_tma & 2) pdl_trigger();   // every read of C by this CTA is complete (the TMA tile has landed)
   } else {
   if (threadIdx.x < mask_words) smask[threadIdx.x] = masks[(int64_t)r * mask_words + threadIdx.x];
   __syncthreads();
@@ -1288,45 +1294,59 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   float4* G4 = reinterpret_cast<float4*>(G);
   const float4* W4 = reinterpret_cast<const float4*>(W);
   const int64_t K2 = K >> 1;
-  // pass 0: column j; pass 1 (half plane): the mirror column, X[-vy] conjugated
-  for (int pass = 0; pass < (mjm > 0 ? 2 : 1); ++pass) {
-  const int gc = pass ? gm0 : g0, mc = pass ? mjm : mj;
-  float2* sd = pass ? sdm : sdot;
-  const float cs = pass ? -scale : scale;                // imaginary parts: conjugate
-  for (int ib = 0; ib < mc; ib += rpp * 4) {             // block-uniform trip count (shuffles)
-    float4 o[4], w[4];
-    int vy[4];
+  // Rows 0 .. mj-1: column j; rows mj .. mj+mjm-1 (half plane): the mirror column, X[-vy]
+  // conjugated -- one stream of rows, U rows per thread per round with their W (and G) segments in
+  // flight together: 8 on the first flush after a reset (no G read), else 4.
+  const int mt = mj + mjm;
+  auto out_rows = [&](auto UC, auto RGC) {
+    constexpr int U = decltype(UC)::value;
+    constexpr bool RG = decltype(RGC)::value;
+    for (int ib = 0; ib < mt; ib += rpp * U) {           // block-uniform trip count (shuffles)
+      float4 o[U], w[U];
+      int vy[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = ib + u * rpp + rs;
-      const int64_t gi = (int64_t)(gc + i) * K2 + (k0 >> 1) + pp;
-      if constexpr (LAZY) vy[u] = i < mc ? __ldg(act_vy + gc + i) : 0;   // (loaded with W: no table round)
-      w[u] = i < mc ? __ldg(W4 + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
-      o[u] = (i < mc && !overwrite && !o_only) ? G4[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+      for (int u = 0; u < U; ++u) {
+        const int i = ib + u * rpp + rs;
+        const int gr = i < mj ? g0 + i : gm0 + (i - mj);   // accumulator row
+        const int64_t gi = (int64_t)gr * K2 + (k0 >> 1) + pp;
+        if constexpr (LAZY) vy[u] = i < mt ? __ldg(act_vy + gr) : 0;   // (loaded with W: no table round)
+        w[u] = i < mt ? __ldg(W4 + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (RG) o[u] = i < mt ? G4[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
+        else o[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (ib + u * rpp >= mc) break;                     // block-uniform
-      const int i = ib + u * rpp + rs;
-      float2 d = make_float2(0.f, 0.f);
-      if (i < mc) {
-        // row of X: vy for column j, -vy for the mirror pass (X[-vy] conjugated)
-        const int sl = !LAZY ? (pass ? svm[i] : svy[i]) : xi(fft::fslot<LOGN>(pass ? (Sy - vy[u]) & (Sy - 1) : vy[u]));
-        const float4 z = *reinterpret_cast<const float4*>(x + sl + 2 * pp);
-        const float4 gn = make_float4(fmaf(z.x, scale, o[u].x), fmaf(z.y, cs, o[u].y), fmaf(z.z, scale, o[u].z),
-                                      fmaf(z.w, cs, o[u].w));
-        if (!o_only) G4[(int64_t)(gc + i) * K2 + (k0 >> 1) + pp] = gn;
-        d.x = fmaf(gn.x, w[u].x, fmaf(-gn.y, w[u].y, fmaf(gn.z, w[u].z, -gn.w * w[u].w)));
-        d.y = fmaf(gn.x, w[u].y, fmaf(gn.y, w[u].x, fmaf(gn.z, w[u].w, gn.w * w[u].z)));
+      for (int u = 0; u < U; ++u) {
+        if (ib + u * rpp >= mt) break;                   // block-uniform
+        const int i = ib + u * rpp + rs;
+        const bool mir = i >= mj;
+        float2 d = make_float2(0.f, 0.f);
+        if (i < mt) {
+          // row of X: vy for column j, -vy for the mirror column (X[-vy] conjugated)
+          const int sl = !LAZY ? (mir ? svm[i - mj] : svy[i])
+                               : xi(fft::fslot<LOGN>(mir ? (Sy - vy[u]) & (Sy - 1) : vy[u]));
+          const float cs = mir ? -scale : scale;
+          const float4 z = *reinterpret_cast<const float4*>(x + sl + 2 * pp);
+          const float4 gn = make_float4(fmaf(z.x, scale, o[u].x), fmaf(z.y, cs, o[u].y), fmaf(z.z, scale, o[u].z),
+                                        fmaf(z.w, cs, o[u].w));
+          const int gr = mir ? gm0 + (i - mj) : g0 + i;
+          if (!o_only) G4[(int64_t)gr * K2 + (k0 >> 1) + pp] = gn;
+          d.x = fmaf(gn.x, w[u].x, fmaf(-gn.y, w[u].y, fmaf(gn.z, w[u].z, -gn.w * w[u].w)));
+          d.y = fmaf(gn.x, w[u].y, fmaf(gn.y, w[u].x, fmaf(gn.z, w[u].w, gn.w * w[u].z)));
+        }
+        for (int off = hKT >> 1; off > 0; off >>= 1) {
+          d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
+          d.y += __shfl_xor_sync(0xffffffffu, d.y, off);
+        }
+        if (pp == 0 && i < mt) {
+          float2* sp = mir ? sdm + (i - mj) : sdot + i;
+          sp->x += d.x;
+          sp->y += d.y;
+        }
       }
-      for (int off = hKT >> 1; off > 0; off >>= 1) {
-        d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
-        d.y += __shfl_xor_sync(0xffffffffu, d.y, off);
-      }
-      if (pp == 0 && i < mc) { sd[i].x += d.x; sd[i].y += d.y; }
     }
-  }
-  }
+  };
+  if (!overwrite && !o_only) out_rows(std::integral_constant<int, 4>{}, std::true_type{});
+  else out_rows(std::integral_constant<int, WDD_CF_U_NOG>{}, std::false_type{});
   __syncthreads();   // x reused by the next k-tile; sdot settled
   }
   const int64_t orow = blockIdx.x + kbase / (KT * tpc);
@@ -1507,7 +1527,8 @@ static cudaError_t launch_rowfft_t(const Plan& p, const int32_t* rows, const uin
   return launch_pdl(rowfft_kernel<LOGN, LOGC>, grid, dim3(nt), smem, st, rowfft_pdl, (const float*)p.d_Call, rows, masks,
                     p.mask_words, (const float2*)p.d_twx,
                     (const int32_t*)(p.r_half ? (p.half_identity ? nullptr : p.d_col_vx_half) : p.d_col_vx), p.d_R, logP, p.Sy, p.Kl,
-                    p.r_half ? p.n_vh : p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC, (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0),
+                    p.r_half ? p.n_vh : p.n_vx, (float)(1.0 / std::sqrt((double)p.Sx)), tmC,
+                    (tma ? 1 : 0) | (rowfft_pdl ? 2 : 0) | (masks == p.d_ones ? 4 : 0),
                     kbase, KR);
 }
 
