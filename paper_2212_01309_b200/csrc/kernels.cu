@@ -737,11 +737,13 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
             uint32_t hw[4], lw[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const __half h0 = __float2half_rn(t[q0 + 2 * e]), h1 = __float2half_rn(t[q0 + 2 * e + 1]);
-              const __half l0 = __float2half_rn(t[q0 + 2 * e] - __half2float(h0));
-              const __half l1 = __float2half_rn(t[q0 + 2 * e + 1] - __half2float(h1));
-              hw[e] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-              lw[e] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+              // packed conversions (one F2FP per pair; the same RN values as per-element converts)
+              const float a0 = t[q0 + 2 * e], a1 = t[q0 + 2 * e + 1];
+              const __half2 h = __floats2half2_rn(a0, a1);
+              const float2 hf = __half22float2(h);
+              const __half2 l = __floats2half2_rn(a0 - hf.x, a1 - hf.y);
+              hw[e] = *reinterpret_cast<const uint32_t*>(&h);
+              lw[e] = *reinterpret_cast<const uint32_t*>(&l);
             }
             uint8_t* p = base + (q0 >> 3) * Cfg::kSBO2;
             *reinterpret_cast<uint4*>(p) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
