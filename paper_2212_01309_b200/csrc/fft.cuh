@@ -14,8 +14,16 @@
 namespace wdd {
 namespace fft {
 
+// Complex arithmetic on packed fp32 pairs (sm_100 FADD2 / FMUL2 / FFMA2: one instruction per
+// complex add, two per complex multiply; each lane rounds exactly as the scalar expression in the
+// comment, so results are bit-identical to the scalar forms).
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }   // a + b
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {                              // a - b
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+// (fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x))
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+  return __ffma2_rn(make_float2(a.x, a.x), b, __fmul2_rn(make_float2(-b.y, b.x), make_float2(a.y, a.y)));
 }
 
 __host__ __device__ constexpr int brev_c(int v, int bits) {
@@ -37,7 +45,8 @@ __device__ __forceinline__ float2 rot32(float2 v, int q) {
   if (q == 8) return make_float2(v.y, -v.x);                        // times -i
   const float c = cos32(q), sn = q < 8 ? cos32(8 - q) : cos32(q - 8);
   // exp(-i t) = cos t - i sin t; sin(2 pi q/32) = cos(2 pi (8 - q)/32) for q < 8, = cos(2 pi (q - 8)/32) for q >= 8
-  return make_float2(fmaf(v.x, c, v.y * sn), fmaf(v.y, c, -v.x * sn));
+  // (fmaf(v.x, c, v.y * sn), fmaf(v.y, c, -v.x * sn))
+  return __ffma2_rn(v, make_float2(c, c), __fmul2_rn(make_float2(v.y, -v.x), make_float2(sn, sn)));
 }
 
 // One radix-2 DIT stage (butterfly span LEN) of an in-register DFT of R <= 32 points; recursion
@@ -51,8 +60,8 @@ __device__ __forceinline__ void dft_stage(float2 (&v)[R]) {
       for (int j = 0; j < LEN / 2; ++j) {
         const float2 a = v[i + j];
         const float2 b = rot32(v[i + j + LEN / 2], j * (32 / LEN));   // W_LEN^j = W_32^{32 j / LEN}
-        v[i + j] = make_float2(a.x + b.x, a.y + b.y);
-        v[i + j + LEN / 2] = make_float2(a.x - b.x, a.y - b.y);
+        v[i + j] = cadd(a, b);
+        v[i + j + LEN / 2] = csub(a, b);
       }
     }
     dft_stage<R, 2 * LEN>(v);
