@@ -650,7 +650,18 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
       float d[Cfg::kNacc];
       tmem_ld_cols<Cfg::kNacc>(tbase + Cfg::tAcc2 + gb * Cfg::kNacc + lane_addr, d);
       // value of accumulator column b (the hi + lo sum: formed by the MMAs, or here for L = 8)
-      auto dv = [&](int b) { if constexpr (Cfg::kSplitAcc) return d[b]; else return d[b] + d[(L + b) % Cfg::kNacc]; };
+      // C values b .. b + 3 (the accumulator sum times sc2), packed arithmetic, same rounding as dv(b) * sc2
+      const float2 sc2 = make_float2(a.sc2, a.sc2);
+      auto dq = [&](int b) {
+        float2 u = make_float2(d[b], d[b + 1]), w = make_float2(d[b + 2], d[b + 3]);
+        if constexpr (!Cfg::kSplitAcc) {
+          u = __fadd2_rn(u, make_float2(d[(L + b) % Cfg::kNacc], d[(L + b + 1) % Cfg::kNacc]));
+          w = __fadd2_rn(w, make_float2(d[(L + b + 2) % Cfg::kNacc], d[(L + b + 3) % Cfg::kNacc]));
+        }
+        u = __fmul2_rn(u, sc2);
+        w = __fmul2_rn(w, sc2);
+        return make_float4(u.x, u.y, w.x, w.y);
+      };
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc2_empty[gb]);
@@ -665,7 +676,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
 #pragma unroll
           for (int b = 0; b < L; b += 4)
             *reinterpret_cast<float4*>(stg + lane * L + (((b >> 2) ^ (lane & 7)) << 2)) =
-                make_float4(dv(b) * a.sc2, dv(b + 1) * a.sc2, dv(b + 2) * a.sc2, dv(b + 3) * a.sc2);
+                dq(b);
         }
         __syncwarp();
         const int fw = (quad * 16) / L;                      // the warp's frame (warp-uniform)
@@ -686,7 +697,7 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
         float* dst = c_base + (a.idx ? (int64_t)__ldg(a.idx + fg) : a.pos0 + fg) * c_stride + c_off;
 #pragma unroll
         for (int b = 0; b < L; b += 4) {
-          float4 v = make_float4(dv(b) * a.sc2, dv(b + 1) * a.sc2, dv(b + 2) * a.sc2, dv(b + 3) * a.sc2);
+          const float4 v = dq(b);
           *reinterpret_cast<float4*>(dst + b) = v;
         }
       }
@@ -707,12 +718,16 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
         if (et == 0) TRACE(8, tile);
         tc_fence_after();
         float acc[Cfg::kNacc];
-        float t[L];
+        float2 t[L / 2];                                 // T values of this row, packed pairs
         tmem_ld_cols<Cfg::kNacc>(tbase + Cfg::tAcc1 + s1 * Cfg::kAcc1 + lane_addr, acc);
+        {
+          const float2 sc = make_float2(a.sc1, a.sc1);
 #pragma unroll
-        for (int q = 0; q < L; ++q) {
-          if constexpr (Cfg::kSplitAcc) t[q] = acc[q] * a.sc1;
-          else t[q] = (acc[q] + acc[(L + q) % Cfg::kNacc]) * a.sc1;
+          for (int q = 0; q < L; q += 2) {
+            float2 v = make_float2(acc[q], acc[q + 1]);
+            if constexpr (!Cfg::kSplitAcc) v = __fadd2_rn(v, make_float2(acc[(L + q) % Cfg::kNacc], acc[(L + q + 1) % Cfg::kNacc]));
+            t[q / 2] = __fmul2_rn(v, sc);
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -738,10 +753,11 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               // packed conversions (one F2FP per pair; the same RN values as per-element converts)
-              const float a0 = t[q0 + 2 * e], a1 = t[q0 + 2 * e + 1];
-              const __half2 h = __floats2half2_rn(a0, a1);
+              const float2 av = t[q0 / 2 + e];
+              const __half2 h = __floats2half2_rn(av.x, av.y);
               const float2 hf = __half22float2(h);
-              const __half2 l = __floats2half2_rn(a0 - hf.x, a1 - hf.y);
+              const float2 dv2 = __fadd2_rn(av, make_float2(-hf.x, -hf.y));
+              const __half2 l = __floats2half2_rn(dv2.x, dv2.y);
               hw[e] = *reinterpret_cast<const uint32_t*>(&h);
               lw[e] = *reinterpret_cast<const uint32_t*>(&l);
             }
@@ -1153,7 +1169,11 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MI
     const int j = e >> logP, pp = e & (P - 1);
     const int2 sl = col_vx ? sslot[j] : make_int2(xi(fft::fslot<LOGN>(j)), xi(fft::fslot<LOGN>((Sx - j) & (Sx - 1))));
     const float2 z = x[sl.x + pp], zm = x[sl.y + pp];
-    const float4 o = make_float4((z.x + zm.x) * hs, (z.y - zm.y) * hs, (z.y + zm.y) * hs, (zm.x - z.x) * hs);
+    // ((z.x + zm.x) hs, (z.y - zm.y) hs, (z.y + zm.y) hs, (zm.x - z.x) hs) on packed pairs
+    const float2 hs2 = make_float2(hs, hs);
+    const float2 o01 = __fmul2_rn(__fadd2_rn(z, make_float2(zm.x, -zm.y)), hs2);
+    const float2 o23 = __fmul2_rn(__fadd2_rn(make_float2(z.y, -z.x), make_float2(zm.y, zm.x)), hs2);
+    const float4 o = make_float4(o01.x, o01.y, o23.x, o23.y);
     *reinterpret_cast<float4*>(R + ((int64_t)j * Sy + sy) * KR + (k0 - kbase) + 2 * pp) = o;
   }
 }
@@ -1328,12 +1348,21 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
                                : xi(fft::fslot<LOGN>(mir ? (Sy - vy[u]) & (Sy - 1) : vy[u]));
           const float cs = mir ? -scale : scale;
           const float4 z = *reinterpret_cast<const float4*>(x + sl + 2 * pp);
-          const float4 gn = make_float4(fmaf(z.x, scale, o[u].x), fmaf(z.y, cs, o[u].y), fmaf(z.z, scale, o[u].z),
-                                        fmaf(z.w, cs, o[u].w));
+          // (fmaf(z.x, scale, o.x), fmaf(z.y, cs, o.y), ...) on packed pairs
+          const float2 s2 = make_float2(scale, cs);
+          const float2 g01 = __ffma2_rn(make_float2(z.x, z.y), s2, make_float2(o[u].x, o[u].y));
+          const float2 g23 = __ffma2_rn(make_float2(z.z, z.w), s2, make_float2(o[u].z, o[u].w));
+          const float4 gn = make_float4(g01.x, g01.y, g23.x, g23.y);
           const int gr = mir ? gm0 + (i - mj) : g0 + i;
           if (!o_only) G4[(int64_t)gr * K2 + (k0 >> 1) + pp] = gn;
-          d.x = fmaf(gn.x, w[u].x, fmaf(-gn.y, w[u].y, fmaf(gn.z, w[u].z, -gn.w * w[u].w)));
-          d.y = fmaf(gn.x, w[u].y, fmaf(gn.y, w[u].x, fmaf(gn.z, w[u].w, gn.w * w[u].z)));
+          // d = g01 w01 + g23 w23 (complex), lane by lane the scalar chain
+          // (fmaf(gn.x, w.x, fmaf(-gn.y, w.y, fmaf(gn.z, w.z, -gn.w * w.w))), fmaf(gn.x, w.y, fmaf(gn.y, w.x, ...)))
+          const float2 w01 = make_float2(w[u].x, w[u].y), w23 = make_float2(w[u].z, w[u].w);
+          float2 dd = __fmul2_rn(make_float2(-g23.y, g23.y), make_float2(w23.y, w23.x));
+          dd = __ffma2_rn(make_float2(g23.x, g23.x), w23, dd);
+          dd = __ffma2_rn(make_float2(-g01.y, g01.y), make_float2(w01.y, w01.x), dd);
+          dd = __ffma2_rn(make_float2(g01.x, g01.x), w01, dd);
+          d = dd;
         }
         for (int off = hKT >> 1; off > 0; off >>= 1) {
           d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
