@@ -2272,8 +2272,12 @@ __global__ void __launch_bounds__(kRgThreads, 1) rgemm_kernel(RgArgs a, const __
                 if (direct) Gr[q] = gv;
                 else *reinterpret_cast<float4*>(sg8 + (q ^ (m & 7)) * 16) = gv;
               }
-              dot.x = fmaf(gv.x, wv[q].x, fmaf(-gv.y, wv[q].y, fmaf(gv.z, wv[q].z, fmaf(-gv.w, wv[q].w, dot.x))));
-              dot.y = fmaf(gv.x, wv[q].y, fmaf(gv.y, wv[q].x, fmaf(gv.z, wv[q].w, fmaf(gv.w, wv[q].z, dot.y))));
+              // dot.x = fmaf(gv.x, w.x, fmaf(-gv.y, w.y, fmaf(gv.z, w.z, fmaf(-gv.w, w.w, dot.x)))),
+              // dot.y = fmaf(gv.x, w.y, fmaf(gv.y, w.x, fmaf(gv.z, w.w, fmaf(gv.w, w.z, dot.y)))): packed pairs
+              dot = __ffma2_rn(make_float2(-gv.w, gv.w), make_float2(wv[q].w, wv[q].z), dot);
+              dot = __ffma2_rn(make_float2(gv.z, gv.z), make_float2(wv[q].z, wv[q].w), dot);
+              dot = __ffma2_rn(make_float2(-gv.y, gv.y), make_float2(wv[q].y, wv[q].x), dot);
+              dot = __ffma2_rn(make_float2(gv.x, gv.x), make_float2(wv[q].x, wv[q].y), dot);
             }
           }
           if (a.write_g) fence_proxy_async_smem();           // smem G writes -> TMA store
