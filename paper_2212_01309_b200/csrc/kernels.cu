@@ -1525,7 +1525,10 @@ static int rowfft_logp(const Plan& p) {
 // WDD_FFT_SPEC=0 off).  Measured (bench.py): y-FFT Box 1.82 -> 1.60 ms, Large 140 -> 131 us, Medium
 // 18.8 -> 16.8 us; row FFT Medium 14.8 -> 12.5 us, but Box 0.91 -> 1.01 ms and Large 90 -> 94 us.
 static constexpr int fft_spec_logc(int logn, bool row) {
-  return logn < 7 ? -1 : row ? (logn == 7 ? 4 : -1) : (logn >= 10 ? 3 : logn == 9 ? 4 : 5);
+#ifndef WDD_RF_SPEC_MAXLOG
+#define WDD_RF_SPEC_MAXLOG 7
+#endif
+  return logn < 7 ? -1 : row ? (logn > WDD_RF_SPEC_MAXLOG ? -1 : logn == 10 ? 3 : 4) : (logn >= 10 ? 3 : logn == 9 ? 4 : 5);
 }
 static bool fft_spec_on() {
   static const bool on = [] { const char* e = std::getenv("WDD_FFT_SPEC"); return !(e && std::atoi(e) == 0); }();
