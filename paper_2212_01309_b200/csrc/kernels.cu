@@ -2956,11 +2956,39 @@ __global__ void __launch_bounds__(512) img_fused_kernel(const float2* __restrict
   for (int i = threadIdx.x; i < SY; i += blockDim.x) sty[i] = __ldg(twy + i);
   pdl_wait();   // the partial readouts of the preceding flush / readout kernel
   const int vy0 = r * RB;
-  for (int e = threadIdx.x; e < SX * RB; e += blockDim.x) {
-    const int c = e >> LX, vx = e & (SX - 1);
-    const int g = __ldg(gidx + (int64_t)(vy0 + c) * SX + vx);
-    const float2 v = g >= 0 ? sum_tiles(op, tiles, n_act, g) : make_float2(0.f, 0.f);
-    xr[(vx << LRB) + c] = make_float2(v.x, -v.y);    // conj(o): O = DFT2(conj o) / sqrt(S)
+  // up to 4 positions per thread per round: their accumulator rows load together, then their tile
+  // sums (two dependent load rounds per 4 positions instead of per position)
+  for (int e0 = threadIdx.x; e0 < SX * RB; e0 += 4 * blockDim.x) {
+    int g[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * (int)blockDim.x;
+      g[u] = e < SX * RB ? __ldg(gidx + (int64_t)(vy0 + (e >> LX)) * SX + (e & (SX - 1))) : -1;
+    }
+    float2 acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = make_float2(0.f, 0.f);
+    for (int t0 = 0; t0 < tiles; t0 += 8) {          // (the fixed tile order of sum_tiles)
+      float2 v[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          v[u][q] = g[u] >= 0 && t0 + q < tiles ? __ldg(op + (int64_t)(t0 + q) * n_act + g[u]) : make_float2(0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          acc[u].x += v[u][q].x;
+          acc[u].y += v[u][q].y;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * (int)blockDim.x;
+      if (e < SX * RB)
+        xr[((e & (SX - 1)) << LRB) + (e >> LX)] = make_float2(acc[u].x, -acc[u].y);   // conj(o): O = DFT2(conj o) / sqrt(S)
+    }
   }
   __syncthreads();
   fft::fft_seq<LX>(xr, stx, LRB);
