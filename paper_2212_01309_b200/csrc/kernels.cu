@@ -2785,13 +2785,13 @@ cudaError_t launch_readout(const Plan& p, const float2* G, float2* o, cudaStream
 // o_v = sum over the `tiles` partial sums (fixed order), scattered to the dense spectrum
 __device__ __forceinline__ float2 sum_tiles(const float2* __restrict__ op, int tiles, int64_t n_act, int64_t g) {
   float2 acc = make_float2(0.f, 0.f);
-  for (int t0 = 0; t0 < tiles; t0 += 8) {      // eight independent loads in flight, summed in order
-    float2 v[8];
+  for (int t0 = 0; t0 < tiles; t0 += 16) {     // sixteen independent loads in flight, summed in order
+    float2 v[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < 16; ++u)
       v[u] = t0 + u < tiles ? __ldg(op + (int64_t)(t0 + u) * n_act + g) : make_float2(0.f, 0.f);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 16; ++u) {
       acc.x += v[u].x;
       acc.y += v[u].y;
     }
