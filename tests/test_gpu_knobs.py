@@ -8,9 +8,10 @@
   written as the conjugate) against the full plane: G[-v] = conj G[v] holds bit-exactly in G, and
   G and the image agree with the full plane to float32 rounding (relative L2 <= 1e-6).
 * Pure data-movement alternatives of the two-kernel flush must give bit-identical images: the FFT
-  kernels' TMA tile loads against per-thread vector loads (WDD_FFT_TMA=0) and the y-FFT's L2
-  prefetch (WDD_COLFFT_PF=0).  Both read the same bytes into the same shared-memory layout and run
-  the same arithmetic.
+  kernels' TMA tile loads against per-thread vector loads (WDD_FFT_TMA=0), the y-FFT's L2
+  prefetch (WDD_COLFFT_PF=0) and the y-FFT's runtime tile width against its compile-time
+  specialisation (WDD_FFT_SPEC=0).  They read the same bytes into the same shared-memory layout
+  and run the same arithmetic.
 * Alternative arithmetic (image transform by cuFFT or two passes, the DFT-matrix and tensor-core
   rank-update flushes) must agree to float32 rounding of a different summation order: relative
   L2 <= 1e-5 against the default path (the oracle tolerance is 1e-4, P:815 readout).
@@ -102,7 +103,7 @@ def test_half_plane_flush(default_image, tmp_path):
     assert np.linalg.norm(img - img_f) / np.linalg.norm(img_f) <= 1e-6
 
 
-@pytest.mark.parametrize("env", [{"WDD_FFT_TMA": "0"}, {"WDD_COLFFT_PF": "0"}])
+@pytest.mark.parametrize("env", [{"WDD_FFT_TMA": "0"}, {"WDD_COLFFT_PF": "0"}, {"WDD_FFT_SPEC": "0"}])
 def test_data_movement_variants_bit_identical(default_image, tmp_path, env):
     img, _, _ = _run(tmp_path, "v", env)
     assert np.array_equal(img, default_image[0]), env
