@@ -258,7 +258,8 @@ struct ProjArgs {
   const uint4* Bpack;
   float sc1;   // acc1 -> fp16 A2 scale   (2^(eT - s))
   float sc2;   // acc2 -> C scale          (2^(-s - eT))
-  int pdl_wait_end;   // 1: complete only after the preceding grid (keeps stream order for later launches)
+  int pdl_wait_end;   // 1: complete only after the preceding grid (keeps stream order for later launches;
+                      // CTA 0 waits), 2: every CTA waits
   int pdl_wait_start; // 1: no frame load (and no dependent launch) before the preceding grid has completed --
                       // the frames may come from a caller kernel enqueued right before the ingest
   unsigned* err;      // f32 frames: bit 0 set if a value does not fit the fp16 hi/lo split (|x| > 65504 or
@@ -793,10 +794,14 @@ __global__ void __launch_bounds__(ProjCfg<Q, L, U16>::kThreads, ProjCfg<Q, L, U1
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tbase);
-  if (a.pdl_wait_end) pdl_wait();
+  // This grid completes only after the preceding grid has completed (so an ordinary launch after
+  // it also follows every earlier kernel): one CTA waiting is enough -- the grid is complete only
+  // once that CTA exits -- and the others free their SM slots for the next grid of the chain
+  // instead of idling until the predecessor's last CTA is done (WDD_PROJ_WAIT_ALL=1: every CTA).
+  if (a.pdl_wait_end && (blockIdx.x == 0 || a.pdl_wait_end > 1)) pdl_wait();
 #ifdef WDD_TRACE
   if (tid == 0) CTA_REC(cta_slot, 3);
-#endif   // this grid completes only after the preceding grid has completed
+#endif
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link needed)
@@ -882,8 +887,9 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
   static const int no_wait = [] { const char* e = std::getenv("WDD_PROJ_NO_PDLWAIT"); return e ? std::atoi(e) : 0; }();
+  static const int wait_all = [] { const char* e = std::getenv("WDD_PROJ_WAIT_ALL"); return e ? std::atoi(e) : 0; }();
   ProjArgs a{frames, n, pos0, idx, dst, g2, reinterpret_cast<const uint4*>(p.d_Bpack), (float)p.sc1, (float)p.sc2,
-             no_wait ? 0 : 1, wait_start ? 1 : 0, p.d_err};
+             no_wait ? 0 : wait_all ? 2 : 1, wait_start ? 1 : 0, p.d_err};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(Cfg::kThreads);
