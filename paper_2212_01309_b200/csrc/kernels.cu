@@ -855,13 +855,17 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
     const int64_t per_cta = (groups + p.sm_count - 1) / p.sm_count * c;
     if (per_cta <= best) { best = per_cta; g2 = c; }
   }
-  // Frames per CTA: about 1 MiB (lean: 512 KiB) of frame data per CTA, so that a small batch occupies only part
+  // Frames per CTA: about 2 MiB (lean: 512 KiB) of frame data per CTA, so that a small batch occupies only part
   // of the GPU and consecutive (PDL-chained) batches stream concurrently on the other SMs instead
   // of each batch paying its own pipeline fill and drain on every SM.  WDD_PROJ_MIN_FRAMES
   // overrides (0 = spread every batch over all SMs).
   static const int env_frames = [] { const char* e = std::getenv("WDD_PROJ_MIN_FRAMES"); return e ? std::atoi(e) : -1; }();
   int min_frames = env_frames >= 0 ? env_frames
-                                   : std::max(4, (Cfg::kLean ? (1 << 19) : (1 << 20)) / (Q * Q * (U16 ? 2 : 4)));
+                                   : std::max(4, (Cfg::kLean ? (1 << 19) : (1 << 21)) / (Q * Q * (U16 ? 2 : 4)));
+  // (full variant: 2 MiB measured best since only CTA 0 of a grid waits for the preceding grid at
+  // its end -- Live 1 / 2 / 4 MiB: 23.8 / 24.8 / 24.7 M frames/s, projection 0.96 / 1.03 / 1.05 of the
+  // copy peak; the chained per-batch time p50 34 -> 55 us, a lone batch 48 -> 70 us -- the latency
+  // grid, opts.ingest_spread, keeps 51 us)
   // the first batch after a reset finds the GPU idle: spread it over every CTA slot so the chained
   // launches of the following batches find a full machine instead of ramping up one grid at a time
   static const int wide_first = [] { const char* e = std::getenv("WDD_PROJ_WIDE_FIRST"); return e ? std::atoi(e) : 1; }();
