@@ -64,6 +64,8 @@ struct Plan {
   std::vector<uint8_t> row_staged;    // Sy: R holds this row's DFT, not yet folded into G
   int mask_words = 1;                 // ceil(Sx / 32)
   int64_t frames_ingested = 0;
+  int64_t frames_enqueued = 0;        // frames this plan projected since the reset (its own ingest calls)
+  int64_t proj_rem_after = -1;        // scan positions still to come after the projection being launched (-1: unknown)
 
   // device buffers
   void* d_Bpack = nullptr;            // fp16 [Psi_hi | Psi_lo] B operand, smem image

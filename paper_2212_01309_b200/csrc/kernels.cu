@@ -870,6 +870,16 @@ static cudaError_t launch_project_t(const Plan& p, const void* frames, int64_t n
   // launches of the following batches find a full machine instead of ramping up one grid at a time
   static const int wide_first = [] { const char* e = std::getenv("WDD_PROJ_WIDE_FIRST"); return e ? std::atoi(e) : 1; }();
   if (wide_first && p.frames_ingested == 0 && env_frames < 0) min_frames = 1;
+  // The launches that end a scan (the frames of this one and of the calls still to come fit the
+  // GPU's CTA slots at fewer than min_frames each) spread thinner: with min_frames frames per CTA
+  // the chain's last grids ran alone for a whole CTA lifetime (Medium: the last ~25 us of a
+  // 117 us acquisition at a third of the slots, tools/trace_ctas.py)
+  static const int tail_spread = [] { const char* e = std::getenv("WDD_PROJ_TAIL"); return e ? std::atoi(e) : 1; }();
+  if (tail_spread && p.proj_rem_after >= 0 && env_frames < 0 && min_frames > 1) {
+    const int64_t slots = (int64_t)p.sm_count * Cfg::kMinBlocks;
+    const int64_t per = (n + p.proj_rem_after + slots - 1) / slots;
+    if (per < min_frames) min_frames = (int)std::max<int64_t>(1, per);
+  }
   if (p.ingest_spread) min_frames = 1;                 // latency grid (opts.ingest_spread)
   if (min_frames > 0) g2 = Cfg::kG2;
   const int64_t groups = (n + g2 - 1) / g2;

@@ -369,8 +369,15 @@ wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, in
     // (frames of the first chunk of a call may come from a caller kernel enqueued right before it:
     // unless the plan was created with ingest_overlap, that launch reads them only after its
     // predecessor grid has completed; later chunks are ordered behind it)
-    CUDA_TRY(launch_project(p, frames_dev, nc, dst, d_idx, contiguous ? idx[0] : 0, st, first && !p.ingest_overlap));
+    // (a single-rank plan knows how much of the scan is still to come: the launches that end a scan
+    // spread their frames thinner, so the chain's last CTAs finish together -- see launch_project_t)
+    p.proj_rem_after = (p.nranks == 1 && p.nshard == 1) ? std::max<int64_t>(0, p.S - (p.frames_enqueued + nc)) : -1;
+    const cudaError_t e = launch_project(p, frames_dev, nc, dst, d_idx, contiguous ? idx[0] : 0, st,
+                                         first && !p.ingest_overlap);
+    p.proj_rem_after = -1;
+    CUDA_TRY(e);
   }
+  p.frames_enqueued += nc;
   p.c_fresh = false;
   // The row DFT of completed rows is deferred to the next flush (readout): launched per batch it
   // would sit between the PDL-chained projection launches and stall them (measured: 246 us vs
@@ -1217,6 +1224,7 @@ wdd_status wdd_reset(wdd_plan_t plan) {
     p.c_read_since_swap = false;
   }
   p.frames_ingested = 0;
+  p.frames_enqueued = 0;
   return WDD_OK;
 }
 
