@@ -12,9 +12,12 @@ Contents (see oracle/wdd.py for per-function citations of PAPER.md):
   * F-oracle: conventional full WDD, `eq:deconv_mat` + `eq:extract`
     (P:97-106) as drawn in `Fig:schematic_WDD` (P:107-114).
 
-Pins (tests/test_oracle_*.py) tie every function to something other than itself.
-"Parity unpinned": the reduced (HG-basis) reconstruction as a whole has no closed form;
-it is pinned piecewise (basis, projection, accumulation, bank, DFT-basis substitution
-identity with the F-oracle, phase recovery) -- see DESIGN.md §3.
+Pins (tests/test_oracle_*.py) tie every function to something other than itself; no
+function is unpinned.  `reduced_wdd` is basis-agnostic code (Psi is an argument): with the
+DFT basis it equals the F-oracle to 3e-16 (an end-to-end pin of projection, accumulation,
+bank, readout and image), and the HG basis it uses by default is pinned on its own (Gram,
+parity, DFT eigen-property, Hermite recurrence).  What has no closed form is the numerical
+VALUE of an HG-basis reconstruction (Eq. hermite_conv is not an identity); it is checked by
+phase recovery of a known object and by convergence to full WDD -- see DESIGN.md §2.
 """
 from .wdd import *  # noqa: F401,F403
