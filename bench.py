@@ -485,8 +485,11 @@ def main():
     torch.cuda.synchronize()
     lat_ing = np.array([a.elapsed_time(b) for a, b in evs["ingest"]]) * 1e3
     lat_rd = np.array([a.elapsed_time(b) for a, b in evs["readout"]]) * 1e3
-    def isolated(pl):
-        # a lone batch on an idle GPU (the second batch of an acquisition: not the wide first launch)
+    def isolated(pl, hide_host=False):
+        # a lone batch on an idle GPU (the second batch of an acquisition: not the wide first launch).
+        # hide_host: a ~0.2 ms sleep kernel on the plan stream ahead of the first event, so the host's
+        # submission of the call (Python, the C ABI, the launch) overlaps it and the events time the
+        # device work of the batch alone; otherwise the interval includes the host submission.
         t = []
         for k in range(5):
             pl.reset()
@@ -495,6 +498,9 @@ def main():
                 pl.ingest(frames_of(s0[1], len(s0[2])), s0[2], stream)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if hide_host:
+                with torch.cuda.stream(stream):
+                    torch.cuda._sleep(400_000)
             e0.record(stream)
             pl.ingest(frames_of(s[1], len(s[2])), s[2], stream)
             e1.record(stream)
@@ -503,12 +509,14 @@ def main():
         pl.reset()
         return t
     iso = isolated(plan) if not kshard else None          # (resets are collective in a shard group)
-    iso_spread = None
+    iso_dev = isolated(plan, hide_host=True) if not kshard else None
+    iso_spread = iso_spread_dev = None
     if world == 1:
         # the same on a plan with the latency grid (opts.ingest_spread = 1)
         lp = wdd.Plan.from_config(cfg, device=local, ingest_overlap=True, accumulator=args.accumulator,
                                   ingest_spread=True)
         iso_spread = isolated(lp)
+        iso_spread_dev = isolated(lp, hide_host=True)
         lp.close()
 
     # ---- per-kernel device times (eager, event pairs around every launch: isolated-launch costs)
@@ -530,6 +538,8 @@ def main():
     bytes_per_launch = n_own / n_launch * (fb + cfg.K * 4)     # frames read + C written (per launch)
     proj_ms_launch = proj_ms_step / n_launch
     achieved = bytes_per_launch / (proj_ms_launch * 1e-3) / 1e9
+    # a lone batch's frame + C bytes at the copy peak (the floor of the isolated-batch latency)
+    batch_bytes_floor_us = len(own[min(1, len(own) - 1)][2]) * (fb + cfg.K * 4) / (peaks["hbm_gbs"] * 1e9) * 1e6
     share = proj_ms_step / ms_step
     # whole-step algorithmic roofline (SURVEY §8(d) bytes per frame; every stage is HBM-bound):
     # frame + C write/read (8K) + R staging write/read (16 n_r K / Sx, n_r = the staged columns: the
@@ -614,12 +624,19 @@ def main():
                                     "max": float(lat_ing.max()), "n": int(len(lat_ing)), "frames": batch},
                 "isolated_batch_us": {"median": float(np.median(iso)) if iso else None, "n": len(iso or []),
                                       "frames": len(own[min(1, len(own) - 1)][2]),
-                                      "latency_grid_median": float(np.median(iso_spread)) if iso_spread else None},
+                                      "latency_grid_median": float(np.median(iso_spread)) if iso_spread else None,
+                                      "device_median": float(np.median(iso_dev)) if iso_dev else None,
+                                      "device_latency_grid_median":
+                                          float(np.median(iso_spread_dev)) if iso_spread_dev else None,
+                                      "floor_at_hbm": batch_bytes_floor_us},
                 "readout_us": {"p50": float(np.percentile(lat_rd, 50)), "max": float(lat_rd.max()),
                                "n": int(len(lat_rd))},
                 "how": "CUDA events around each call of one eager acquisition (ingest_batch, readout); "
                        "isolated_batch: one batch on an idle GPU after a sync (default throughput grid, "
-                       "and on a plan with the latency grid, opts.ingest_spread = 1)"},
+                       "and on a plan with the latency grid, opts.ingest_spread = 1), from the call to "
+                       "completion; device_*: the same with the host submission hidden behind a sleep "
+                       "kernel (device work of the batch alone); floor_at_hbm: the batch's frame + C "
+                       "bytes at the measured copy peak"},
             "kernels_isolated": kern,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(cfg.S * fb),
                     "d2h_bytes_per_step": int(cfg.S * 8 * n_read)},

@@ -300,7 +300,39 @@ wdd_status upload_meta(Plan& p, const void* host, size_t bytes, void** dev_out) 
 
 // Validate a whole call (range, duplicates within the call and against the seen set) before
 // anything is enqueued.  On success the indices are marked seen.
-wdd_status validate_and_mark(Plan& p, const int32_t* idx, int64_t n) {
+// idx[0 .. n) is the run idx[0], idx[0] + 1, ...  (frames arriving in scan order: the common case)
+static bool is_run(const int32_t* idx, int64_t n) {
+  for (int64_t i = 1; i < n; ++i)
+    if (idx[i] != idx[0] + i) return false;
+  return true;
+}
+
+// run: 1 / 0 if the caller already knows whether idx is a contiguous run, -1 to check here
+wdd_status validate_and_mark(Plan& p, const int32_t* idx, int64_t n, int run = -1) {
+  if (n > 0 && (run >= 0 ? run == 1 : is_run(idx, n))) {
+    // contiguous run: range by its ends, duplicates word by word over the seen bitmap, then marked
+    // (same outcome as the per-index loop below: nothing is marked unless the whole call is valid)
+    const int64_t a = idx[0], b = a + n;   // [a, b)
+    if (a < 0 || b > p.S) {
+      const int64_t i = (a < 0 || a >= p.S) ? 0 : p.S - a;   // first position outside the range
+      return fail(WDD_E_RANGE, "scan index %lld at position %lld outside [0, %lld)", (long long)(a + i),
+                  (long long)i, (long long)p.S);
+    }
+    for (int64_t w = a >> 6; w <= (b - 1) >> 6; ++w) {
+      const int64_t lo = std::max<int64_t>(a, w << 6), hi = std::min<int64_t>(b, (w + 1) << 6);   // [lo, hi)
+      const uint64_t m = (hi - lo == 64 ? ~0ull : ((1ull << (hi - lo)) - 1)) << (lo & 63);
+      if (const uint64_t d = p.seen[(size_t)w] & m) {
+        const int64_t s = (w << 6) + __builtin_ctzll(d);
+        return fail(WDD_E_DUP, "scan index %lld (position %lld) already ingested or repeated", (long long)s,
+                    (long long)(s - a));
+      }
+    }
+    for (int64_t w = a >> 6; w <= (b - 1) >> 6; ++w) {
+      const int64_t lo = std::max<int64_t>(a, w << 6), hi = std::min<int64_t>(b, (w + 1) << 6);
+      p.seen[(size_t)w] |= (hi - lo == 64 ? ~0ull : ((1ull << (hi - lo)) - 1)) << (lo & 63);
+    }
+    return WDD_OK;
+  }
   for (int64_t i = 0; i < n; ++i)
     if (idx[i] < 0 || (int64_t)idx[i] >= p.S)
       return fail(WDD_E_RANGE, "scan index %d at position %lld outside [0, %lld)", idx[i], (long long)i,
@@ -323,7 +355,22 @@ wdd_status validate_and_mark(Plan& p, const int32_t* idx, int64_t n) {
 
 // Positions whose coefficients are (or, for a peer rank's frames, will be) in the current store:
 // their rows are row-transformed at the next flush.
-void mark_pending(Plan& p, const int32_t* idx, int64_t n) {
+void mark_pending(Plan& p, const int32_t* idx, int64_t n, int run = -1) {
+  if (n > 0 && (run >= 0 ? run == 1 : is_run(idx, n))) {
+    // contiguous run: whole mask words per scan row
+    const int64_t a = idx[0], b = a + n;
+    for (int64_t sy = a / p.Sx; sy <= (b - 1) / p.Sx; ++sy) {
+      p.row_dirty[sy] = 1;
+      const int64_t x0 = std::max<int64_t>(a - sy * p.Sx, 0), x1 = std::min<int64_t>(b - sy * p.Sx, p.Sx);   // [x0, x1)
+      for (int64_t w = x0 >> 5; w <= (x1 - 1) >> 5; ++w) {
+        const int64_t lo = std::max<int64_t>(x0, w << 5), hi = std::min<int64_t>(x1, (w + 1) << 5);
+        const uint32_t m = (hi - lo == 32 ? ~0u : ((1u << (hi - lo)) - 1)) << (lo & 31);
+        p.pending[(size_t)sy * p.mask_words + w] |= m;
+        if (p.o_only) p.ingested[(size_t)sy * p.mask_words + w] |= m;
+      }
+    }
+    return;
+  }
   for (int64_t i = 0; i < n; ++i) {
     const int sy = idx[i] / p.Sx, sx = idx[i] % p.Sx;
     p.row_dirty[sy] = 1;
@@ -352,10 +399,9 @@ ProjDst proj_dst(const Plan& p) {
 
 // Enqueue the projection of one chunk of already-validated frames; its coefficients land in
 // the coefficient store(s) at their scan positions (the row DFT happens at flush time).
-wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, int64_t nc, bool first) {
+wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, int64_t nc, bool first, int run = -1) {
   cudaStream_t st = p.stream;
-  bool contiguous = true;
-  for (int64_t i = 1; i < nc && contiguous; ++i) contiguous = idx[i] == idx[0] + i;
+  const bool contiguous = run >= 0 ? run == 1 : is_run(idx, nc);
   const ProjDst dst = proj_dst(p);
   const int32_t* d_idx = nullptr;
   if (!contiguous) {
@@ -382,7 +428,7 @@ wdd_status enqueue_chunk(Plan& p, const void* frames_dev, const int32_t* idx, in
   // The row DFT of completed rows is deferred to the next flush (readout): launched per batch it
   // would sit between the PDL-chained projection launches and stall them (measured: 246 us vs
   // 162 us per Medium acquisition).
-  mark_pending(p, idx, nc);
+  mark_pending(p, idx, nc, contiguous ? 1 : 0);
   return WDD_OK;
 }
 
@@ -967,19 +1013,20 @@ wdd_status wdd_ingest(wdd_plan_t plan, const void* frames_dev, const int32_t* sc
   if (!frames_dev || !scan_idx_host) return fail(WDD_E_ARG, "NULL frames or indices");
   if (!p.peers_ready) return fail(WDD_E_STATE, "shard plan: wdd_set_shard_peers / wdd_link_shards first");
   CUDA_TRY(cudaSetDevice(p.device));
-  wdd_status s = validate_and_mark(p, scan_idx_host, n);
+  // a call over a contiguous run of scan positions is one projection launch (no index upload):
+  // each CTA then streams many frames, and its pipeline fill / drain is paid once per call
+  // (Large: 0.70 -> see DESIGN.md); scattered indices go in chunks of the metadata slot size.
+  // The host bookkeeping of a run is word-wise (validate_and_mark, mark_pending).
+  const bool contiguous = is_run(scan_idx_host, n);
+  wdd_status s = validate_and_mark(p, scan_idx_host, n, contiguous ? 1 : 0);
   if (s != WDD_OK) return s;
   use_stream(p, reinterpret_cast<cudaStream_t>(stream));
   const size_t fb = frame_bytes(p);
-  // a call over a contiguous run of scan positions is one projection launch (no index upload):
-  // each CTA then streams many frames, and its pipeline fill / drain is paid once per call
-  // (Large: 0.70 -> see DESIGN.md); scattered indices go in chunks of the metadata slot size
-  bool contiguous = true;
-  for (int64_t i = 1; i < n && contiguous; ++i) contiguous = scan_idx_host[i] == scan_idx_host[0] + i;
   const int64_t cap = contiguous ? std::max<int64_t>(p.chunk_cap, kMaxLaunchFrames) : p.chunk_cap;
   for (int64_t c0 = 0; c0 < n; c0 += cap) {
     const int64_t nc = std::min<int64_t>(cap, n - c0);
-    s = enqueue_chunk(p, static_cast<const uint8_t*>(frames_dev) + (size_t)c0 * fb, scan_idx_host + c0, nc, c0 == 0);
+    s = enqueue_chunk(p, static_cast<const uint8_t*>(frames_dev) + (size_t)c0 * fb, scan_idx_host + c0, nc, c0 == 0,
+                      contiguous ? 1 : -1);
     if (s != WDD_OK) return s;
   }
   p.frames_ingested += n;

@@ -222,6 +222,53 @@ def test_rejects_duplicates_and_range_without_effect(wdd, torch_cuda):
     plan.ingest(fr_dev[:4], np.arange(4))
 
 
+def test_contiguous_run_bookkeeping(wdd, torch_cuda):
+    # contiguous calls take word-wise host bookkeeping (seen bitmap, pending masks): runs that start
+    # and end inside 32- / 64-bit words and scan rows, a run hitting an ingested position in its
+    # middle (DUP, nothing marked), runs crossing the scan end or starting past it (RANGE); the
+    # accumulator and image must equal the same frames ingested as scattered (non-run) calls
+    torch = torch_cuda
+    cfg = CONFIGS["tiny"]   # 32 x 32: one 32-bit mask word per row, two rows per 64-bit seen word
+    idx = np.arange(cfg.S)
+    fr = _frames(cfg, idx)
+    fr_dev = _to_dev(torch, fr)
+    runs = [(0, 1), (1, 31), (31, 33), (33, 65), (65, 130), (130, 131), (131, 700), (700, cfg.S)]
+    plan = wdd.Plan.from_config(cfg)
+    plan.ingest(fr_dev[65:130], idx[65:130])
+    with pytest.raises(wdd.WddError) as e:
+        plan.ingest(fr_dev[40:100], idx[40:100])          # overlaps 65 .. 99
+    assert e.value.name == "WDD_E_DUP"
+    with pytest.raises(wdd.WddError) as e:
+        plan.ingest(fr_dev[cfg.S - 3:], np.arange(cfg.S - 3, cfg.S + 0) + 1)   # ends past the scan
+    assert e.value.name == "WDD_E_RANGE"
+    with pytest.raises(wdd.WddError) as e:
+        plan.ingest(fr_dev[:2], np.array([cfg.S, cfg.S + 1]))
+    assert e.value.name == "WDD_E_RANGE"
+    with pytest.raises(wdd.WddError) as e:
+        plan.ingest(fr_dev[:2], np.array([-1, 0]))
+    assert e.value.name == "WDD_E_RANGE"
+    for a, b in runs:
+        if (a, b) != (65, 130):
+            plan.ingest(fr_dev[a:b], idx[a:b])
+    assert plan.info()["frames_ingested"] == cfg.S
+    out = plan.readout()
+    G, _ = plan.get_accumulator()
+    # the same frames as scattered calls (every call permuted: never a run)
+    ref_plan = wdd.Plan.from_config(cfg)
+    rng = np.random.default_rng(7)
+    perm = rng.permutation(cfg.S)
+    for c in np.array_split(perm, 9):
+        c = c if len(c) < 2 or not np.all(np.diff(c) == 1) else c[::-1]
+        ref_plan.ingest(fr_dev[torch.from_numpy(c).long().cuda()].contiguous(), c)
+    out_ref = ref_plan.readout()
+    G_ref, _ = ref_plan.get_accumulator()
+    torch.cuda.synchronize()
+    assert rel(G.cpu().numpy(), G_ref.cpu().numpy()) < 1e-6
+    assert rel(out.cpu().numpy(), out_ref.cpu().numpy()) < 1e-6
+    ref = _oracle_all(cfg, fr, idx)
+    assert rel(out.cpu().numpy(), ref["O"]) < TOL
+
+
 def test_normalize_flag(wdd, torch_cuda):
     torch = torch_cuda
     cfg = CONFIGS["tiny"]
