@@ -1088,6 +1088,17 @@ template <int LOGC> struct FftPad { static constexpr int value = 0; };
 #ifndef WDD_CF_U_NOG
 #define WDD_CF_U_NOG 8   // y-FFT output rows per thread per round without a G read
 #endif
+#ifndef WDD_CF_U_NOG_KT8
+#define WDD_CF_U_NOG_KT8 16   // the same for 8-coefficient tiles (Sy = 1024: Box)
+#endif
+// y-FFT readout reduction over the hKT lanes of a row: transposed butterfly (every shuffle carries a
+// useful value) for compile-time tiles from 2^WDD_CF_BF_MINLOGC coefficients and at runtime widths,
+// a plain xor tree per row below (both bit-identical).  Measured (tools/experiments/exp_cfred*.sh):
+// Large y-FFT 136 -> 121 us; Box 1.48 ms (xor tree, 8 rows per round) -> 1.53 (xor tree, 16 rows)
+// / 1.56 (butterfly, 8 rows) / 1.46 ms (butterfly, 16 rows)
+#ifndef WDD_CF_BF_MINLOGC
+#define WDD_CF_BF_MINLOGC 3
+#endif
 template <int LOGN, int LOGC>
 __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_RF_MINB_SMALL : WDD_RF_MINB_LARGE) rowfft_kernel(const float* __restrict__ C, const int32_t* __restrict__ rows,
                                                      const uint32_t* __restrict__ masks, int mask_words,
@@ -1343,6 +1354,7 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
   auto out_rows = [&](auto UC, auto RGC) {
     constexpr int U = decltype(UC)::value;
     constexpr bool RG = decltype(RGC)::value;
+    constexpr bool BF = LOGC < 0 || LOGC >= WDD_CF_BF_MINLOGC;
     for (int ib = 0; ib < mt; ib += rpp * U) {           // block-uniform trip count (shuffles)
       float4 o[U], w[U];
       int vy[U];
@@ -1356,9 +1368,9 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
         if constexpr (RG) o[u] = i < mt ? G4[gi] : make_float4(0.f, 0.f, 0.f, 0.f);
         else o[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
+      float2 a[U];   // this thread's share of the tile's readout for each of its U rows
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (ib + u * rpp >= mt) break;                   // block-uniform
         const int i = ib + u * rpp + rs;
         const bool mir = i >= mj;
         float2 d = make_float2(0.f, 0.f);
@@ -1384,20 +1396,70 @@ __global__ void __launch_bounds__(256, LOGN <= 8 ? WDD_CF_MINB_SMALL : WDD_CF_MI
           dd = __ffma2_rn(make_float2(g01.x, g01.x), w01, dd);
           d = dd;
         }
-        for (int off = hKT >> 1; off > 0; off >>= 1) {
-          d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
-          d.y += __shfl_xor_sync(0xffffffffu, d.y, off);
-        }
-        if (pp == 0 && i < mt) {
-          float2* sp = mir ? sdm + (i - mj) : sdot + i;
-          sp->x += d.x;
-          sp->y += d.y;
+        a[u] = d;
+        if constexpr (!BF) {   // plain xor tree per row, lane 0 of the row accumulates
+          if (ib + u * rpp < mt) {                       // block-uniform
+            for (int off = hKT >> 1; off > 0; off >>= 1) {
+              d.x += __shfl_xor_sync(0xffffffffu, d.x, off);
+              d.y += __shfl_xor_sync(0xffffffffu, d.y, off);
+            }
+            if (pp == 0 && i < mt) {
+              float2* sp = mir ? sdm + (i - mj) : sdot + i;
+              sp->x += d.x;
+              sp->y += d.y;
+            }
+          }
         }
       }
+      if constexpr (BF) {
+      // Sum each row's hKT lane shares with a transposed butterfly: at offset off a lane keeps
+      // half of its rows and sends the other half to lane ^ off, so every shuffle carries a useful
+      // value (per U rows: U - U / hKT complex shuffles instead of U log2 hKT) and each lane ends
+      // with whole-row sums of U / hKT rows (a row's sum, own share + partner share at every level,
+      // is the lane-0 value of the plain xor tree bit for bit: fp addition is commutative).
+      constexpr int LU = U >= 16 ? 4 : U >= 8 ? 3 : U >= 4 ? 2 : U >= 2 ? 1 : 0;
+      int ub = 0, lv = 0;   // first row (u) of this lane's remaining values; levels done
+#pragma unroll
+      for (int L = 0; L < LU; ++L) {
+        const int off = hKT >> (L + 1);
+        if (off >= 1) {   // block-uniform
+          const bool hi = (pp & off) != 0;
+          const int h = U >> (L + 1);
+#pragma unroll
+          for (int j = 0; j < (U >> (L + 1)); ++j) {
+            const float2 send = hi ? a[j] : a[j + (U >> (L + 1))];
+            const float2 keep = hi ? a[j + (U >> (L + 1))] : a[j];
+            const float rx = __shfl_xor_sync(0xffffffffu, send.x, off);
+            const float ry = __shfl_xor_sync(0xffffffffu, send.y, off);
+            a[j] = make_float2(keep.x + rx, keep.y + ry);
+          }
+          if (hi) ub += h;
+          ++lv;
+        }
+      }
+      // lanes beyond the transposition (hKT > U): plain xor tree on the one remaining value
+      for (int off = hKT >> (LU + 1); off >= 1; off >>= 1) {
+        a[0].x += __shfl_xor_sync(0xffffffffu, a[0].x, off);
+        a[0].y += __shfl_xor_sync(0xffffffffu, a[0].y, off);
+      }
+      const int nfin = U >> lv;                            // rows per lane after the butterfly
+      const bool writer = (pp & ((hKT >> lv) - 1)) == 0;   // one lane per row when hKT > U
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        if (j < nfin && writer) {
+          const int i = ib + (ub + j) * rpp + rs;
+          if (i < mt) {
+            float2* sp = i >= mj ? sdm + (i - mj) : sdot + i;
+            sp->x += a[j].x;
+            sp->y += a[j].y;
+          }
+        }
+      }
+      }   // BF
     }
   };
   if (!overwrite && !o_only) out_rows(std::integral_constant<int, 4>{}, std::true_type{});
-  else out_rows(std::integral_constant<int, WDD_CF_U_NOG>{}, std::false_type{});
+  else out_rows(std::integral_constant<int, LOGC == 3 ? WDD_CF_U_NOG_KT8 : WDD_CF_U_NOG>{}, std::false_type{});
   __syncthreads();   // x reused by the next k-tile; sdot settled
   }
   const int64_t orow = blockIdx.x + kbase / (KT * tpc);
