@@ -29,7 +29,8 @@ def main():
         fr = np.concatenate([fr] * (n // len(fr)))
     dev = torch.from_numpy(fr).cuda()
     idx = np.arange(n, dtype=np.int32)
-    plan = wdd.Plan.from_config(cfg, ingest_overlap=True)
+    spread = os.environ.get("TRACE_SPREAD", "0") == "1"     # the latency grid (opts.ingest_spread)
+    plan = wdd.Plan.from_config(cfg, ingest_overlap=True, ingest_spread=spread)
     s = torch.cuda.Stream()
     buf = (ctypes.c_ulonglong * (8192 * 5))()
     torch.cuda.set_stream(s)
@@ -56,8 +57,14 @@ def main():
         e, x = ent[sm == k][o], ext[sm == k][o]
         gaps += list(e[1:] - x[:-1])
     gaps = np.array(gaps)
-    print(f"  SMs used {len(np.unique(sm))}; idle gap between CTAs on an SM: mean {gaps.mean():.2f} us, "
-          f"p90 {np.percentile(gaps, 90):.2f}, total {gaps.sum():.1f} SM-us")
+    if len(gaps):
+        print(f"  SMs used {len(np.unique(sm))}; idle gap between CTAs on an SM: mean {gaps.mean():.2f} us, "
+              f"p90 {np.percentile(gaps, 90):.2f}, total {gaps.sum():.1f} SM-us")
+    else:
+        print(f"  SMs used {len(np.unique(sm))}; one CTA per SM")
+    print(f"  per-CTA setup p50 / max {np.median(iss - ent):.2f} / {np.max(iss - ent):.2f} us; first landing "
+          f"-> exit p50 {np.median(ext - land):.2f}; entry spread {ent.max() - ent.min():.2f} us; exit spread "
+          f"{ext.max() - ext.min():.2f} us")
     busy = np.sum(ext - ent)
     print(f"  SM busy fraction over the span: {busy / (148 * span):.3f}; first entry->all SMs busy, "
           f"last-CTA start {ent.max():.1f} us, first exit {ext.min():.1f} us")
