@@ -9,8 +9,9 @@
 // |W_P|^2, so only the pre-modulation (-1)^(my+mx) is applied (folded into the frame load for
 // chi).  The transforms are cuFFT (this workload is not the reduced method's path); the frame
 // load, Y_v, the Wiener combine + sum and the image step are kernels here.  Memory: S x Q^2
-// complex64 twice (Gf in pixel-major and scan-frequency-major order: Medium 4.3 GB, Large 17 GB)
-// plus a batch of Y_v.
+// float32 (the frames, pixel-major) + S/2 x Q^2 complex64 (Gf's half plane, pixel-major) + n_act x Q^2
+// complex64 (the active scan frequencies' rows in scan-frequency-major order); Medium 1.1 + 1.1 +
+// 1.0 GB, Large 4.3 + 4.3 + 3.9 GB; plus a batch of Y_v.
 #include <cuda_runtime.h>
 #include <cufft.h>
 
@@ -26,10 +27,10 @@
 namespace wdd {
 namespace {
 
-// frames [s][m] -> (-1)^(my+mx) I as complex64, transposed to [m][s] (pixel-major: the scan DFT of
-// each detector pixel is then a contiguous batch), through 32 x 32 shared-memory tiles
+// frames [s][m] -> (-1)^(my+mx) I as float32, transposed to [m][s] (pixel-major: the scan DFT of
+// each detector pixel is then a contiguous real-to-complex batch), through 32 x 32 shared-memory tiles
 template <typename T>
-__global__ void fw_load_kernel(const T* __restrict__ frames, int64_t S, int QQ, int Q, float2* __restrict__ A) {
+__global__ void fw_load_kernel(const T* __restrict__ frames, int64_t S, int QQ, int Q, float* __restrict__ A) {
   __shared__ float tile[32][33];
   const int64_t s0 = (int64_t)blockIdx.y * 32;
   const int m0 = blockIdx.x * 32;
@@ -44,23 +45,82 @@ __global__ void fw_load_kernel(const T* __restrict__ frames, int64_t S, int QQ, 
     const int64_t s = s0 + threadIdx.x;
     if (m < QQ && s < S) {
       const float sg = (((m / Q) + (m % Q)) & 1) ? -1.f : 1.f;
-      A[(int64_t)m * S + s] = make_float2(tile[threadIdx.x][dy] * sg, 0.f);
+      A[(int64_t)m * S + s] = tile[threadIdx.x][dy] * sg;
     }
   }
 }
 
-// complex64 [rows][cols] -> [cols][rows], 32 x 32 tiles
-__global__ void fw_transpose_kernel(const float2* __restrict__ in, int64_t rows, int64_t cols, float2* __restrict__ out) {
+// The same with two detector pixels per thread (4-byte u16 / 8-byte f32 loads: a warp reads 128 /
+// 256 contiguous bytes of a frame instead of 64 / 128); 32 scan positions x 64 pixels per tile.
+// Needs QQ even and a frame pointer aligned to two elements (checked by the caller).
+template <typename T>
+__global__ void fw_load2_kernel(const T* __restrict__ frames, int64_t S, int QQ, int Q, float* __restrict__ A) {
+  __shared__ float tile[32][65];
+  const int64_t s0 = (int64_t)blockIdx.y * 32;
+  const int m0 = blockIdx.x * 64;
+  // (block 32 x 8: the four loads of a thread are issued together)
+  float2 ld[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t s = s0 + threadIdx.y + 8 * i;
+    const int m = m0 + 2 * threadIdx.x;
+    ld[i] = make_float2(0.f, 0.f);
+    if (s < S && m < QQ) {
+      if constexpr (sizeof(T) == 2) {
+        const ushort2 v = __ldg(reinterpret_cast<const ushort2*>(frames + s * QQ + m));
+        ld[i] = make_float2((float)v.x, (float)v.y);
+      } else {
+        ld[i] = __ldg(reinterpret_cast<const float2*>(frames + s * QQ + m));
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    tile[threadIdx.y + 8 * i][2 * threadIdx.x] = ld[i].x;
+    tile[threadIdx.y + 8 * i][2 * threadIdx.x + 1] = ld[i].y;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int dm = threadIdx.y; dm < 64; dm += 8) {
+    const int m = m0 + dm;
+    const int64_t s = s0 + threadIdx.x;
+    if (m < QQ && s < S) {
+      const float sg = (((m / Q) + (m % Q)) & 1) ? -1.f : 1.f;
+      A[(int64_t)m * S + s] = tile[threadIdx.x][dm] * sg;
+    }
+  }
+}
+
+// Gf of the real frames is Hermitian per pixel, Gf[m][-v] = conj Gf[m][v], so the scan DFT is a
+// real-to-complex transform that stores vx <= Sx/2 only: B[m][vy][vx], Sxh = Sx/2 + 1 columns.
+// B (pixel-major) -> A[b][m] = Gf[m][v_b] for the listed scan frequencies only (the inactive v have
+// Y_v = 0 and contribute nothing: their detector transforms are never needed), mirror columns read
+// as conjugates; 32 x 32 tiles; vlist ascending, so the gathered reads of a tile row are runs of
+// consecutive addresses
+__global__ void fw_gather_transpose_kernel(const float2* __restrict__ in, int64_t QQ, int Sy, int Sx,
+                                           const int32_t* __restrict__ vlist, int64_t nv, float2* __restrict__ out) {
   __shared__ float2 tile[32][33];
-  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  const int Sxh = Sx / 2 + 1;
+  const int64_t pitch = (int64_t)Sy * Sxh;
+  const int64_t m0 = (int64_t)blockIdx.y * 32, b0 = (int64_t)blockIdx.x * 32;
+  const int64_t bl = b0 + threadIdx.x;
+  int64_t off = -1;
+  float cj = 1.f;
+  if (bl < nv) {
+    const int v = vlist[bl], vy = v / Sx, vx = v % Sx;
+    if (vx <= Sx / 2) off = (int64_t)vy * Sxh + vx;
+    else { off = (int64_t)((Sy - vy) % Sy) * Sxh + (Sx - vx); cj = -1.f; }
+  }
   for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
-    const int64_t r = r0 + dy, c = c0 + threadIdx.x;
-    tile[dy][threadIdx.x] = (r < rows && c < cols) ? in[r * cols + c] : make_float2(0.f, 0.f);
+    const int64_t m = m0 + dy;
+    float2 z = (m < QQ && off >= 0) ? in[m * pitch + off] : make_float2(0.f, 0.f);
+    z.y *= cj;
+    tile[dy][threadIdx.x] = z;
   }
   __syncthreads();
   for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
-    const int64_t c = c0 + dy, r = r0 + threadIdx.x;
-    if (c < cols && r < rows) out[c * rows + r] = tile[threadIdx.x][dy];
+    const int64_t b = b0 + dy, m = m0 + threadIdx.x;
+    if (b < nv && m < QQ) out[b * QQ + m] = tile[threadIdx.x][dy];
   }
 }
 
@@ -69,14 +129,29 @@ __device__ __forceinline__ double fw_freq(int v, int S, double step) {
   return (double)sf / __dmul_rn((double)S, step);
 }
 
-// (-1)^(my+mx) Y_v for a batch of scan frequencies (flattened v = vy*Sx + vx)
-__global__ void fw_y_kernel(const int32_t* __restrict__ vlist, int nb, int Q, double dq, double qa2, double cph,
-                            int Sy, int Sx, double step, float2* __restrict__ Y) {
-  const int b = blockIdx.y;
+// (-1)^(my+mx) Y_v for a batch of scan frequencies (flattened v = vy*Sx + vx), one CTA per v.
+// Y_v = p_hat(q) conj(p_hat(q + q_hat)) with p_hat = e^{-i cph |q|^2} on the aperture, and
+// |q + q_hat|^2 - |q|^2 = 2 q.q_hat + |q_hat|^2 is linear in q: the phase factor separates into a
+// constant, a per-row and a per-column factor (2Q float64 sincos per v instead of Q^2), multiplied
+// in float64.  The aperture tests are the per-pixel float64 tests of the oracle's Y_v.
+__global__ void __launch_bounds__(256) fw_y_kernel(const int32_t* __restrict__ vlist, int nb, int Q, double dq,
+                                                   double qa2, double cph, int Sy, int Sx, double step,
+                                                   float2* __restrict__ Y) {
+  extern __shared__ double2 fw_e[];            // [Q] row factors e^{i cph 2 qy sy}, [Q] column factors
+  const int b = blockIdx.x;
   if (b >= nb) return;
   const int v = vlist[b];
   const double sy = fw_freq(v / Sx, Sy, step), sx = fw_freq(v % Sx, Sx, step);
-  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < Q * Q; m += gridDim.x * blockDim.x) {
+  for (int i = threadIdx.x; i < 2 * Q; i += blockDim.x) {
+    const double q = (double)((i < Q ? i : i - Q) - Q / 2) * dq;
+    double sn, cs;
+    sincos(cph * 2.0 * q * (i < Q ? sy : sx), &sn, &cs);
+    fw_e[i] = make_double2(cs, sn);
+  }
+  double s0, c0;
+  sincos(cph * (sy * sy + sx * sx), &s0, &c0);
+  __syncthreads();
+  for (int m = threadIdx.x; m < Q * Q; m += blockDim.x) {
     const int my = m / Q, mx = m % Q;
     const double qy = (double)(my - Q / 2) * dq, qx = (double)(mx - Q / 2) * dq;
     const double u2 = __dadd_rn(__dmul_rn(qy, qy), __dmul_rn(qx, qx));
@@ -84,10 +159,11 @@ __global__ void fw_y_kernel(const int32_t* __restrict__ vlist, int nb, int Q, do
     const double s2 = __dadd_rn(__dmul_rn(ay, ay), __dmul_rn(ax, ax));
     float2 y = make_float2(0.f, 0.f);
     if (u2 <= qa2 && s2 <= qa2) {
-      double s, c;
-      sincos(cph * (s2 - u2), &s, &c);          // p_hat(q) conj(p_hat(q + q_hat)), p_hat = e^{-i cph |q|^2}
+      const double2 ey = fw_e[my], ex = fw_e[Q + mx];
+      const double pr = ey.x * ex.x - ey.y * ex.y, pi = ey.x * ex.y + ey.y * ex.x;
+      const double c = c0 * pr - s0 * pi, sn = c0 * pi + s0 * pr;    // e^{i cph (s2 - u2)}
       const float sg = ((my + mx) & 1) ? -1.f : 1.f;
-      y = make_float2((float)c * sg, (float)s * sg);
+      y = make_float2((float)c * sg, (float)sn * sg);
     }
     Y[(int64_t)b * Q * Q + m] = y;
   }
@@ -98,17 +174,18 @@ __global__ void fw_y_kernel(const int32_t* __restrict__ vlist, int nb, int Q, do
 __global__ void fw_combine_kernel(const float2* __restrict__ A, const float2* __restrict__ Y,
                                   const int32_t* __restrict__ vlist, int Q, double chi_s, double wp_s, double eps,
                                   float2* __restrict__ spec) {
+  // (A and vlist already offset to the batch: row b of A is chi of vlist[b])
   const int b = blockIdx.x;
   const int v = vlist[b];
-  const float2* chi = A + (int64_t)v * Q * Q;
+  const float2* chi = A + (int64_t)b * Q * Q;
   const float2* wp = Y + (int64_t)b * Q * Q;
   double sr = 0.0, si = 0.0;
   for (int m = threadIdx.x; m < Q * Q; m += blockDim.x) {
     const float2 c = chi[m], w = wp[m];
     const double cr = c.x * chi_s, ci = c.y * chi_s, wr = w.x * wp_s, wi = w.y * wp_s;
-    const double den = wr * wr + wi * wi + eps;
-    sr += (cr * wr + ci * wi) / den;
-    si += (ci * wr - cr * wi) / den;
+    const double inv = 1.0 / (wr * wr + wi * wi + eps);
+    sr += (cr * wr + ci * wi) * inv;
+    si += (ci * wr - cr * wi) * inv;
   }
   __shared__ double rr[256], ri[256];
   rr[threadIdx.x] = sr;
@@ -147,6 +224,7 @@ __global__ void fw_image_kernel(float2* __restrict__ out, int64_t S, float scale
 // milliseconds to create).
 struct FullWddWork {
   float2 *A = nullptr, *B = nullptr, *Y = nullptr, *spec = nullptr;
+  float* Bf = nullptr;
   int32_t* dv = nullptr;
   cufftHandle scan = 0, det = 0, yplan = 0, img = 0;
   bool ok = false;
@@ -161,6 +239,7 @@ void full_wdd_release(Plan& p) {
   if (w->img) cufftDestroy(w->img);
   cudaFree(w->A);
   cudaFree(w->B);
+  cudaFree(w->Bf);
   cudaFree(w->Y);
   cudaFree(w->spec);
   cudaFree(w->dv);
@@ -177,20 +256,25 @@ static wdd_status fw_prepare(Plan& p, char* err, size_t errn) {
   p.fw = w;
   const int Q = p.Q;
   const int64_t S = p.S, QQ = (int64_t)Q * Q;
-  if (cudaMalloc(&w->A, (size_t)S * QQ * sizeof(float2)) != cudaSuccess ||
-      cudaMalloc(&w->B, (size_t)S * QQ * sizeof(float2)) != cudaSuccess ||
+  const int64_t nv = std::max<int64_t>(1, p.n_act);
+  if (cudaMalloc(&w->A, (size_t)nv * QQ * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc(&w->Bf, (size_t)S * QQ * sizeof(float)) != cudaSuccess ||
+      cudaMalloc(&w->B, (size_t)QQ * p.Sy * (p.Sx / 2 + 1) * sizeof(float2)) != cudaSuccess ||
       cudaMalloc(&w->Y, (size_t)kFwYBatch * QQ * sizeof(float2)) != cudaSuccess ||
       cudaMalloc(&w->spec, (size_t)S * sizeof(float2)) != cudaSuccess ||
       cudaMalloc(&w->dv, p.active_v.size() * sizeof(int32_t)) != cudaSuccess) {
-    std::snprintf(err, errn, "full WDD: %.1f GB of device scratch not available", 2.0 * S * QQ * 8 / 1e9);
+    std::snprintf(err, errn, "full WDD: %.1f GB of device scratch not available", (double)(S + nv) * QQ * 8 / 1e9);   // (Bf + B ~ S x Q^2 x 8 bytes)
     full_wdd_release(p);
     return WDD_E_NOMEM;
   }
   int sdims[2] = {p.Sy, p.Sx}, ddims[2] = {Q, Q};
-  if (cudaMemcpy(w->dv, p.active_v.data(), p.active_v.size() * sizeof(int32_t), cudaMemcpyHostToDevice) !=
+  std::vector<int32_t> vsorted(p.active_v.begin(), p.active_v.end());   // ascending v: gathers in runs of s
+  std::sort(vsorted.begin(), vsorted.end());
+  if (cudaMemcpy(w->dv, vsorted.data(), vsorted.size() * sizeof(int32_t), cudaMemcpyHostToDevice) !=
           cudaSuccess ||
-      cufftPlanMany(&w->scan, 2, sdims, nullptr, 1, (int)S, nullptr, 1, (int)S, CUFFT_C2C, (int)QQ) != CUFFT_SUCCESS ||
-      cufftPlanMany(&w->det, 2, ddims, nullptr, 1, (int)QQ, nullptr, 1, (int)QQ, CUFFT_C2C, (int)S) != CUFFT_SUCCESS ||
+      cufftPlanMany(&w->scan, 2, sdims, nullptr, 1, (int)S, nullptr, 1, p.Sy * (p.Sx / 2 + 1), CUFFT_R2C, (int)QQ) !=
+          CUFFT_SUCCESS ||
+      cufftPlanMany(&w->det, 2, ddims, nullptr, 1, (int)QQ, nullptr, 1, (int)QQ, CUFFT_C2C, (int)nv) != CUFFT_SUCCESS ||
       cufftPlanMany(&w->yplan, 2, ddims, nullptr, 1, (int)QQ, nullptr, 1, (int)QQ, CUFFT_C2C, kFwYBatch) !=
           CUFFT_SUCCESS ||
       cufftPlan2d(&w->img, p.Sy, p.Sx, CUFFT_C2C) != CUFFT_SUCCESS) {
@@ -218,30 +302,39 @@ wdd_status full_wdd(Plan& p, const void* frames_dev, void* out_dev, char* err, s
       cufftSetStream(w->yplan, st) != CUFFT_SUCCESS || cufftSetStream(w->img, st) != CUFFT_SUCCESS)
     return fail("cuFFT stream");
   if (cudaMemsetAsync(w->spec, 0, (size_t)S * sizeof(float2), st) != cudaSuccess) return fail("memset");
-  // (a) frames -> (-1)^m I transposed to pixel-major B[m][s]; scan DFT of every pixel (contiguous
-  // batches); transpose back to A[v][m] for the detector transforms
+  // (a) frames -> (-1)^m I transposed to pixel-major Bf[m][s]; real-to-complex scan DFT of every
+  // pixel (contiguous batches, half plane B[m][vy][vx <= Sx/2]); the active scan frequencies' rows
+  // gathered and transposed to A[b][m] for the detector transforms (n_act of S rows: ~45% at
+  // Medium / Large)
   const dim3 tb(32, 8);
   const dim3 tg1((unsigned)((QQ + 31) / 32), (unsigned)((S + 31) / 32));
-  if (p.dtype == 0) fw_load_kernel<uint16_t><<<tg1, tb, 0, st>>>(static_cast<const uint16_t*>(frames_dev), S, (int)QQ, Q, w->B);
-  else fw_load_kernel<float><<<tg1, tb, 0, st>>>(static_cast<const float*>(frames_dev), S, (int)QQ, Q, w->B);
-  if (cufftExecC2C(w->scan, reinterpret_cast<cufftComplex*>(w->B), reinterpret_cast<cufftComplex*>(w->B),
-                   CUFFT_FORWARD) != CUFFT_SUCCESS) return fail("scan FFT");
-  const dim3 tg2((unsigned)((S + 31) / 32), (unsigned)((QQ + 31) / 32));
-  fw_transpose_kernel<<<tg2, tb, 0, st>>>(w->B, QQ, S, w->A);
+  const dim3 tg1v((unsigned)((QQ + 63) / 64), (unsigned)((S + 31) / 32));
+  const bool pair_ok = reinterpret_cast<uintptr_t>(frames_dev) % (p.dtype == 0 ? 4 : 8) == 0;   // (QQ is even)
+  if (p.dtype == 0) {
+    if (pair_ok) fw_load2_kernel<uint16_t><<<tg1v, tb, 0, st>>>(static_cast<const uint16_t*>(frames_dev), S, (int)QQ, Q, w->Bf);
+    else fw_load_kernel<uint16_t><<<tg1, tb, 0, st>>>(static_cast<const uint16_t*>(frames_dev), S, (int)QQ, Q, w->Bf);
+  } else {
+    if (pair_ok) fw_load2_kernel<float><<<tg1v, tb, 0, st>>>(static_cast<const float*>(frames_dev), S, (int)QQ, Q, w->Bf);
+    else fw_load_kernel<float><<<tg1, tb, 0, st>>>(static_cast<const float*>(frames_dev), S, (int)QQ, Q, w->Bf);
+  }
+  if (cufftExecR2C(w->scan, w->Bf, reinterpret_cast<cufftComplex*>(w->B)) != CUFFT_SUCCESS) return fail("scan FFT");
+  const dim3 tg2((unsigned)((p.n_act + 31) / 32), (unsigned)((QQ + 31) / 32));
+  if (p.n_act > 0) fw_gather_transpose_kernel<<<tg2, tb, 0, st>>>(w->B, QQ, p.Sy, p.Sx, w->dv, p.n_act, w->A);
   // (b) chi_v for every v: inverse detector DFT of each scan-frequency row (the 1/sqrt(S) of the
   // unitary scan DFT is folded into the combine scale)
-  if (cufftExecC2C(w->det, reinterpret_cast<cufftComplex*>(w->A), reinterpret_cast<cufftComplex*>(w->A),
+  if (p.n_act > 0 &&
+      cufftExecC2C(w->det, reinterpret_cast<cufftComplex*>(w->A), reinterpret_cast<cufftComplex*>(w->A),
                    CUFFT_INVERSE) != CUFFT_SUCCESS) return fail("detector FFT");
   // (c) W_P for the active v in batches, Wiener combine and sum
   const double cph = kPi * p.lambda * p.defocus;
   const double chi_s = 1.0 / ((double)Q * std::sqrt((double)S)), wp_s = 1.0 / Q;   // unitary scales
   for (int64_t a = 0; a < p.n_act; a += kFwYBatch) {
     const int m = (int)std::min<int64_t>(kFwYBatch, p.n_act - a);
-    fw_y_kernel<<<dim3((unsigned)((QQ + 255) / 256), kFwYBatch), 256, 0, st>>>(w->dv + a, m, Q, p.dq, p.qa * p.qa, cph,
-                                                                              p.Sy, p.Sx, p.step, w->Y);
+    fw_y_kernel<<<m, 256, 2 * Q * sizeof(double2), st>>>(w->dv + a, m, Q, p.dq, p.qa * p.qa, cph, p.Sy, p.Sx,
+                                                          p.step, w->Y);
     if (cufftExecC2C(w->yplan, reinterpret_cast<cufftComplex*>(w->Y), reinterpret_cast<cufftComplex*>(w->Y),
                      CUFFT_INVERSE) != CUFFT_SUCCESS) return fail("probe FFT");
-    fw_combine_kernel<<<m, 256, 0, st>>>(w->A, w->Y, w->dv + a, Q, chi_s, wp_s, p.eps, w->spec);
+    fw_combine_kernel<<<m, 256, 0, st>>>(w->A + a * QQ, w->Y, w->dv + a, Q, chi_s, wp_s, p.eps, w->spec);
   }
   // (d) O = conj(F^-1_unitary(x)) [/ sqrt(x_0)]
   if (cufftExecC2C(w->img, reinterpret_cast<cufftComplex*>(w->spec), static_cast<cufftComplex*>(out_dev),

@@ -39,7 +39,7 @@ def main():
     r1.record()
     torch.cuda.synchronize()
     print(json.dumps({"config": cfg.name, "full_wdd_ms": ms, "full_wdd_frames_per_s": cfg.S / (ms / 1e3),
-                      "reduced_ms": r0.elapsed_time(r1), "scratch_GB": 2 * cfg.S * cfg.Q * cfg.Q * 8 / 1e9}))
+                      "reduced_ms": r0.elapsed_time(r1), "scratch_GB": (cfg.S * 4 + cfg.Sy * (cfg.Sx // 2 + 1) * 8 + plan.n_act * 8) * cfg.Q * cfg.Q / 1e9}))
 
 
 if __name__ == "__main__":
