@@ -253,7 +253,9 @@ wdd_status wdd_get_info(wdd_plan_t plan, wdd_plan_info* info);
  * chi_v conj(W_P) / (|W_P|^2 + eps) summed over r (R12), and O = conj(F^-1_unitary(x)) (R13;
  * / sqrt(x_0) if the plan normalises).  frames_dev: DEVICE, S = Sy*Sx frames of Q x Q in the
  * plan's dtype, in scan order (s = sy*Sx + sx); complex_out_dev: DEVICE, Sy*Sx complex64.
- * Stream-ordered on `stream`; the first call allocates 2*S*Q*Q*8 bytes of device scratch and the
+ * Stream-ordered on `stream`; the first call allocates about (S + n_act)*Q*Q*8 bytes of device
+ * scratch (the frames as float32 and the half-plane scan DFT, pixel-major; the active scan
+ * frequencies' rows) and the
  * cuFFT plans, kept by the plan until wdd_destroy (WDD_E_NOMEM if the scratch is not available);
  * Q must be even.  Independent of the plan's ingest state. */
 wdd_status wdd_full_wdd(wdd_plan_t plan, const void* frames_dev, void* complex_out_dev, void* stream);
