@@ -25,7 +25,8 @@ def env():
 
 
 @pytest.mark.parametrize("name,kw", [("tiny", {}), ("medium", dict(Sy=32, Sx=32, Q=64)),
-                                     ("tiny", dict(Sy=24, Sx=40)), ("medium", dict(Sy=16, Sx=16, normalize=True))])
+                                     ("tiny", dict(Sy=24, Sx=40)), ("medium", dict(Sy=16, Sx=16, normalize=True)),
+                                     ("tiny", dict(Sy=9, Sx=15))])   # (odd axes: the half-plane mirror indexing)
 def test_full_wdd_matches_f_oracle(env, name, kw):
     torch, wdd = env
     kw = dict(kw)
