@@ -180,12 +180,21 @@ __global__ void fw_combine_kernel(const float2* __restrict__ A, const float2* __
   const float2* chi = A + (int64_t)b * Q * Q;
   const float2* wp = Y + (int64_t)b * Q * Q;
   double sr = 0.0, si = 0.0;
-  for (int m = threadIdx.x; m < Q * Q; m += blockDim.x) {
-    const float2 c = chi[m], w = wp[m];
-    const double cr = c.x * chi_s, ci = c.y * chi_s, wr = w.x * wp_s, wi = w.y * wp_s;
+  auto term = [&](float cx, float cy, float wx, float wy) {
+    const double cr = cx * chi_s, ci = cy * chi_s, wr = wx * wp_s, wi = wy * wp_s;
     const double inv = 1.0 / (wr * wr + wi * wi + eps);
     sr += (cr * wr + ci * wi) * inv;
     si += (ci * wr - cr * wi) * inv;
+  };
+  // two pixels per 16-byte load (Q even; rows of A and Y are 16-byte aligned), four loads in flight
+  const float4* chi4 = reinterpret_cast<const float4*>(chi);
+  const float4* wp4 = reinterpret_cast<const float4*>(wp);
+  const int n2 = Q * Q / 2;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    const float4 c = __ldg(chi4 + i), w = __ldg(wp4 + i);
+    term(c.x, c.y, w.x, w.y);
+    term(c.z, c.w, w.z, w.w);
   }
   __shared__ double rr[256], ri[256];
   rr[threadIdx.x] = sr;
@@ -225,6 +234,7 @@ __global__ void fw_image_kernel(float2* __restrict__ out, int64_t S, float scale
 struct FullWddWork {
   float2 *A = nullptr, *B = nullptr, *Y = nullptr, *spec = nullptr;
   float* Bf = nullptr;
+  int ybatch = 0;
   int32_t* dv = nullptr;
   cufftHandle scan = 0, det = 0, yplan = 0, img = 0;
   bool ok = false;
@@ -247,7 +257,11 @@ void full_wdd_release(Plan& p) {
   p.fw = nullptr;
 }
 
-static constexpr int kFwYBatch = 512;                   // scan frequencies per Y_v batch
+// Scan frequencies per Y_v batch: three per SM.  cuFFT's 128 x 128 kernel runs one transform per
+// CTA, one CTA per SM, so a batch that is a multiple of the SM count wastes no partial wave, and
+// 444 x Q^2 x 8 B stays L2-resident at Q = 128 (measured, Medium / Large: 512 -> 5.49 / 21.5 ms,
+// 592 -> 5.20 / 20.3, 444 -> 4.75 / 18.7, 296 -> 5.21 / 20.3)
+static int fw_ybatch(const Plan& p) { return 3 * std::max(1, p.sm_count); }
 
 static wdd_status fw_prepare(Plan& p, char* err, size_t errn) {
   if (p.fw && p.fw->ok) return WDD_OK;
@@ -257,16 +271,19 @@ static wdd_status fw_prepare(Plan& p, char* err, size_t errn) {
   const int Q = p.Q;
   const int64_t S = p.S, QQ = (int64_t)Q * Q;
   const int64_t nv = std::max<int64_t>(1, p.n_act);
-  if (cudaMalloc(&w->A, (size_t)nv * QQ * sizeof(float2)) != cudaSuccess ||
+  w->ybatch = fw_ybatch(p);
+  const int64_t nv_pad = (nv + w->ybatch - 1) / w->ybatch * w->ybatch;   // (whole batches: see full_wdd)
+  if (cudaMalloc(&w->A, (size_t)nv_pad * QQ * sizeof(float2)) != cudaSuccess ||
       cudaMalloc(&w->Bf, (size_t)S * QQ * sizeof(float)) != cudaSuccess ||
       cudaMalloc(&w->B, (size_t)QQ * p.Sy * (p.Sx / 2 + 1) * sizeof(float2)) != cudaSuccess ||
-      cudaMalloc(&w->Y, (size_t)kFwYBatch * QQ * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc(&w->Y, (size_t)w->ybatch * QQ * sizeof(float2)) != cudaSuccess ||
       cudaMalloc(&w->spec, (size_t)S * sizeof(float2)) != cudaSuccess ||
       cudaMalloc(&w->dv, p.active_v.size() * sizeof(int32_t)) != cudaSuccess) {
     std::snprintf(err, errn, "full WDD: %.1f GB of device scratch not available", (double)(S + nv) * QQ * 8 / 1e9);   // (Bf + B ~ S x Q^2 x 8 bytes)
     full_wdd_release(p);
     return WDD_E_NOMEM;
   }
+  cudaMemset(w->A + nv * QQ, 0, (size_t)(nv_pad - nv) * QQ * sizeof(float2));   // pad rows stay zero under the FFT
   int sdims[2] = {p.Sy, p.Sx}, ddims[2] = {Q, Q};
   std::vector<int32_t> vsorted(p.active_v.begin(), p.active_v.end());   // ascending v: gathers in runs of s
   std::sort(vsorted.begin(), vsorted.end());
@@ -274,8 +291,7 @@ static wdd_status fw_prepare(Plan& p, char* err, size_t errn) {
           cudaSuccess ||
       cufftPlanMany(&w->scan, 2, sdims, nullptr, 1, (int)S, nullptr, 1, p.Sy * (p.Sx / 2 + 1), CUFFT_R2C, (int)QQ) !=
           CUFFT_SUCCESS ||
-      cufftPlanMany(&w->det, 2, ddims, nullptr, 1, (int)QQ, nullptr, 1, (int)QQ, CUFFT_C2C, (int)nv) != CUFFT_SUCCESS ||
-      cufftPlanMany(&w->yplan, 2, ddims, nullptr, 1, (int)QQ, nullptr, 1, (int)QQ, CUFFT_C2C, kFwYBatch) !=
+      cufftPlanMany(&w->yplan, 2, ddims, nullptr, 1, (int)QQ, nullptr, 1, (int)QQ, CUFFT_C2C, w->ybatch) !=
           CUFFT_SUCCESS ||
       cufftPlan2d(&w->img, p.Sy, p.Sx, CUFFT_C2C) != CUFFT_SUCCESS) {
     std::snprintf(err, errn, "full WDD: cuFFT plan creation failed");
@@ -298,7 +314,7 @@ wdd_status full_wdd(Plan& p, const void* frames_dev, void* out_dev, char* err, s
   const int Q = p.Q;
   const int64_t S = p.S, QQ = (int64_t)Q * Q;
   cudaStream_t st = p.stream;
-  if (cufftSetStream(w->scan, st) != CUFFT_SUCCESS || cufftSetStream(w->det, st) != CUFFT_SUCCESS ||
+  if (cufftSetStream(w->scan, st) != CUFFT_SUCCESS ||
       cufftSetStream(w->yplan, st) != CUFFT_SUCCESS || cufftSetStream(w->img, st) != CUFFT_SUCCESS)
     return fail("cuFFT stream");
   if (cudaMemsetAsync(w->spec, 0, (size_t)S * sizeof(float2), st) != cudaSuccess) return fail("memset");
@@ -320,18 +336,21 @@ wdd_status full_wdd(Plan& p, const void* frames_dev, void* out_dev, char* err, s
   if (cufftExecR2C(w->scan, w->Bf, reinterpret_cast<cufftComplex*>(w->B)) != CUFFT_SUCCESS) return fail("scan FFT");
   const dim3 tg2((unsigned)((p.n_act + 31) / 32), (unsigned)((QQ + 31) / 32));
   if (p.n_act > 0) fw_gather_transpose_kernel<<<tg2, tb, 0, st>>>(w->B, QQ, p.Sy, p.Sx, w->dv, p.n_act, w->A);
-  // (b) chi_v for every v: inverse detector DFT of each scan-frequency row (the 1/sqrt(S) of the
-  // unitary scan DFT is folded into the combine scale)
-  if (p.n_act > 0 &&
-      cufftExecC2C(w->det, reinterpret_cast<cufftComplex*>(w->A), reinterpret_cast<cufftComplex*>(w->A),
-                   CUFFT_INVERSE) != CUFFT_SUCCESS) return fail("detector FFT");
+  // (b) chi_v: inverse detector DFT of each gathered scan-frequency row, batch by batch in the
+  // loop below with the same cuFFT plan as the probe transforms (at this batch size cuFFT runs the
+  // 128 x 128 transform as two 1-D passes, measured faster than its one-kernel 2-D form on all
+  // n_act rows at once: Medium 1.18 -> 0.75 ms); the 1/sqrt(S) of the unitary scan DFT is folded
+  // into the combine scale.  A is padded to whole batches; the pad rows are transformed, never read.
   // (c) W_P for the active v in batches, Wiener combine and sum
   const double cph = kPi * p.lambda * p.defocus;
   const double chi_s = 1.0 / ((double)Q * std::sqrt((double)S)), wp_s = 1.0 / Q;   // unitary scales
-  for (int64_t a = 0; a < p.n_act; a += kFwYBatch) {
-    const int m = (int)std::min<int64_t>(kFwYBatch, p.n_act - a);
+  for (int64_t a = 0; a < p.n_act; a += w->ybatch) {
+    const int m = (int)std::min<int64_t>(w->ybatch, p.n_act - a);
     fw_y_kernel<<<m, 256, 2 * Q * sizeof(double2), st>>>(w->dv + a, m, Q, p.dq, p.qa * p.qa, cph, p.Sy, p.Sx,
                                                           p.step, w->Y);
+    if (cufftExecC2C(w->yplan, reinterpret_cast<cufftComplex*>(w->A + a * QQ),
+                     reinterpret_cast<cufftComplex*>(w->A + a * QQ), CUFFT_INVERSE) != CUFFT_SUCCESS)
+      return fail("detector FFT");
     if (cufftExecC2C(w->yplan, reinterpret_cast<cufftComplex*>(w->Y), reinterpret_cast<cufftComplex*>(w->Y),
                      CUFFT_INVERSE) != CUFFT_SUCCESS) return fail("probe FFT");
     fw_combine_kernel<<<m, 256, 0, st>>>(w->A + a * QQ, w->Y, w->dv + a, Q, chi_s, wp_s, p.eps, w->spec);
