@@ -50,18 +50,19 @@ __global__ void fw_load_kernel(const T* __restrict__ frames, int64_t S, int QQ, 
   }
 }
 
-// The same with two detector pixels per thread (4-byte u16 / 8-byte f32 loads: a warp reads 128 /
-// 256 contiguous bytes of a frame instead of 64 / 128); 32 scan positions x 64 pixels per tile.
-// Needs QQ even and a frame pointer aligned to two elements (checked by the caller).
+// The same with two detector pixels per load and two scan positions per store (4-byte u16 / 8-byte
+// f32 loads: a warp reads 128 / 256 contiguous bytes of a frame; 8-byte stores: 256 contiguous
+// bytes of a pixel's scan row); 64 scan positions x 64 pixels per tile, block 32 x 8, the eight
+// loads of a thread issued together.  Needs QQ and S even and a frame pointer aligned to two
+// elements (checked by the caller).
 template <typename T>
 __global__ void fw_load2_kernel(const T* __restrict__ frames, int64_t S, int QQ, int Q, float* __restrict__ A) {
-  __shared__ float tile[32][65];
-  const int64_t s0 = (int64_t)blockIdx.y * 32;
+  __shared__ float tile[64][65];
+  const int64_t s0 = (int64_t)blockIdx.y * 64;
   const int m0 = blockIdx.x * 64;
-  // (block 32 x 8: the four loads of a thread are issued together)
-  float2 ld[4];
+  float2 ld[8];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 8; ++i) {
     const int64_t s = s0 + threadIdx.y + 8 * i;
     const int m = m0 + 2 * threadIdx.x;
     ld[i] = make_float2(0.f, 0.f);
@@ -75,7 +76,7 @@ __global__ void fw_load2_kernel(const T* __restrict__ frames, int64_t S, int QQ,
     }
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 8; ++i) {
     tile[threadIdx.y + 8 * i][2 * threadIdx.x] = ld[i].x;
     tile[threadIdx.y + 8 * i][2 * threadIdx.x + 1] = ld[i].y;
   }
@@ -83,10 +84,11 @@ __global__ void fw_load2_kernel(const T* __restrict__ frames, int64_t S, int QQ,
 #pragma unroll
   for (int dm = threadIdx.y; dm < 64; dm += 8) {
     const int m = m0 + dm;
-    const int64_t s = s0 + threadIdx.x;
+    const int64_t s = s0 + 2 * threadIdx.x;
     if (m < QQ && s < S) {
       const float sg = (((m / Q) + (m % Q)) & 1) ? -1.f : 1.f;
-      A[(int64_t)m * S + s] = tile[threadIdx.x][dm] * sg;
+      *reinterpret_cast<float2*>(A + (int64_t)m * S + s) =
+          make_float2(tile[2 * threadIdx.x][dm] * sg, tile[2 * threadIdx.x + 1][dm] * sg);
     }
   }
 }
@@ -137,35 +139,42 @@ __device__ __forceinline__ double fw_freq(int v, int S, double step) {
 __global__ void __launch_bounds__(256) fw_y_kernel(const int32_t* __restrict__ vlist, int nb, int Q, double dq,
                                                    double qa2, double cph, int Sy, int Sx, double step,
                                                    float2* __restrict__ Y) {
-  extern __shared__ double2 fw_e[];            // [Q] row factors e^{i cph 2 qy sy}, [Q] column factors
+  // per row my / column mx: the phase factor (the rows' carrying the constant e^{i cph |q_hat|^2}),
+  // q^2 and (q + q_hat)^2, each rounded as in the per-pixel sums u2 = qy^2 + qx^2, s2 = ay^2 + ax^2
+  extern __shared__ double2 fw_e[];            // [2Q] factors, then [2Q] (q^2, (q + q_hat)^2)
+  double2* fw_q = fw_e + 2 * Q;
   const int b = blockIdx.x;
   if (b >= nb) return;
   const int v = vlist[b];
   const double sy = fw_freq(v / Sx, Sy, step), sx = fw_freq(v % Sx, Sx, step);
-  for (int i = threadIdx.x; i < 2 * Q; i += blockDim.x) {
-    const double q = (double)((i < Q ? i : i - Q) - Q / 2) * dq;
-    double sn, cs;
-    sincos(cph * 2.0 * q * (i < Q ? sy : sx), &sn, &cs);
-    fw_e[i] = make_double2(cs, sn);
-  }
   double s0, c0;
   sincos(cph * (sy * sy + sx * sx), &s0, &c0);
+  for (int i = threadIdx.x; i < 2 * Q; i += blockDim.x) {
+    const bool row = i < Q;
+    const double q = (double)((row ? i : i - Q) - Q / 2) * dq;
+    const double sh = row ? sy : sx;
+    double sn, cs;
+    sincos(cph * 2.0 * q * sh, &sn, &cs);
+    fw_e[i] = row ? make_double2(c0 * cs - s0 * sn, c0 * sn + s0 * cs) : make_double2(cs, sn);
+    const double a = __dadd_rn(q, sh);
+    fw_q[i] = make_double2(__dmul_rn(q, q), __dmul_rn(a, a));
+  }
   __syncthreads();
-  for (int m = threadIdx.x; m < Q * Q; m += blockDim.x) {
-    const int my = m / Q, mx = m % Q;
-    const double qy = (double)(my - Q / 2) * dq, qx = (double)(mx - Q / 2) * dq;
-    const double u2 = __dadd_rn(__dmul_rn(qy, qy), __dmul_rn(qx, qx));
-    const double ay = __dadd_rn(qy, sy), ax = __dadd_rn(qx, sx);
-    const double s2 = __dadd_rn(__dmul_rn(ay, ay), __dmul_rn(ax, ax));
-    float2 y = make_float2(0.f, 0.f);
-    if (u2 <= qa2 && s2 <= qa2) {
-      const double2 ey = fw_e[my], ex = fw_e[Q + mx];
-      const double pr = ey.x * ex.x - ey.y * ex.y, pi = ey.x * ex.y + ey.y * ex.x;
-      const double c = c0 * pr - s0 * pi, sn = c0 * pi + s0 * pr;    // e^{i cph (s2 - u2)}
-      const float sg = ((my + mx) & 1) ? -1.f : 1.f;
-      y = make_float2((float)c * sg, (float)sn * sg);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int my = warp; my < Q; my += nw) {
+    const double2 ey = fw_e[my], qy = fw_q[my];
+    float2* Yr = Y + (int64_t)b * Q * Q + (int64_t)my * Q;
+    for (int mx = lane; mx < Q; mx += 32) {
+      const double2 qx = fw_q[Q + mx];
+      float2 y = make_float2(0.f, 0.f);
+      if (__dadd_rn(qy.x, qx.x) <= qa2 && __dadd_rn(qy.y, qx.y) <= qa2) {
+        const double2 ex = fw_e[Q + mx];
+        const double c = ey.x * ex.x - ey.y * ex.y, sn = ey.x * ex.y + ey.y * ex.x;   // e^{i cph (s2 - u2)}
+        const float sg = ((my + mx) & 1) ? -1.f : 1.f;
+        y = make_float2((float)c * sg, (float)sn * sg);
+      }
+      Yr[mx] = y;
     }
-    Y[(int64_t)b * Q * Q + m] = y;
   }
 }
 
@@ -324,8 +333,8 @@ wdd_status full_wdd(Plan& p, const void* frames_dev, void* out_dev, char* err, s
   // Medium / Large)
   const dim3 tb(32, 8);
   const dim3 tg1((unsigned)((QQ + 31) / 32), (unsigned)((S + 31) / 32));
-  const dim3 tg1v((unsigned)((QQ + 63) / 64), (unsigned)((S + 31) / 32));
-  const bool pair_ok = reinterpret_cast<uintptr_t>(frames_dev) % (p.dtype == 0 ? 4 : 8) == 0;   // (QQ is even)
+  const dim3 tg1v((unsigned)((QQ + 63) / 64), (unsigned)((S + 63) / 64));
+  const bool pair_ok = reinterpret_cast<uintptr_t>(frames_dev) % (p.dtype == 0 ? 4 : 8) == 0 && S % 2 == 0;   // (QQ is even)
   if (p.dtype == 0) {
     if (pair_ok) fw_load2_kernel<uint16_t><<<tg1v, tb, 0, st>>>(static_cast<const uint16_t*>(frames_dev), S, (int)QQ, Q, w->Bf);
     else fw_load_kernel<uint16_t><<<tg1, tb, 0, st>>>(static_cast<const uint16_t*>(frames_dev), S, (int)QQ, Q, w->Bf);
@@ -346,7 +355,7 @@ wdd_status full_wdd(Plan& p, const void* frames_dev, void* out_dev, char* err, s
   const double chi_s = 1.0 / ((double)Q * std::sqrt((double)S)), wp_s = 1.0 / Q;   // unitary scales
   for (int64_t a = 0; a < p.n_act; a += w->ybatch) {
     const int m = (int)std::min<int64_t>(w->ybatch, p.n_act - a);
-    fw_y_kernel<<<m, 256, 2 * Q * sizeof(double2), st>>>(w->dv + a, m, Q, p.dq, p.qa * p.qa, cph, p.Sy, p.Sx,
+    fw_y_kernel<<<m, 256, 4 * Q * sizeof(double2), st>>>(w->dv + a, m, Q, p.dq, p.qa * p.qa, cph, p.Sy, p.Sx,
                                                           p.step, w->Y);
     if (cufftExecC2C(w->yplan, reinterpret_cast<cufftComplex*>(w->A + a * QQ),
                      reinterpret_cast<cufftComplex*>(w->A + a * QQ), CUFFT_INVERSE) != CUFFT_SUCCESS)
