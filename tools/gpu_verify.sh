@@ -1,3 +1,5 @@
+# Verification of a build (under gpurun, from the repo root): smoke, the -m gpu suite, the default bench
+# line and the reference arm, the conventional-WDD comparison; outputs in gpurun_out/r02h_*.
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r02h_build.log 2>&1 || { echo BUILD FAILED; exit 1; }
 timeout 600 python __graft_entry__.py smoke > gpurun_out/r02h_smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/r02h_smoke.log
